@@ -1,0 +1,426 @@
+"""Benchmark of the B200 ECC engine (driver contract: one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Headline workload (BASELINE.json configs[1], the metric's 1-GPU config):
+discrete ECC of a 3D 512^3 float32 volume with 1024 uniform thresholds.
+Under torchrun with N ranks the volume is z-slab sharded (weak scaling: each
+rank owns 512 planes of 512x512, a one-plane halo is exchanged with the
+z-neighbours over NCCL and the (B+1) int64 histogram is all-reduced), i.e.
+the C5 pipeline at 512 planes per GPU.
+
+A step = one pass of the hot path over the volume: halo exchange (N>1) +
+fused stencil/bin/histogram sweep + all-reduce (N>1) + prefix scan.  Inputs
+are resident in HBM and larger than L2 (512 MiB per rank vs 126 MB), so no
+flush is needed between steps.  `e2e` repeats the measurement through the
+public API with the volume copied host->device from pinned memory every step
+and the curve copied back.  `soft` reports the C3 soft-ECC forward+backward
+(128 x 1024^2, 256 thresholds, lambda 50, learnable tau/u/alpha).
+
+--impl reference times the reference algorithm's CPU port (oracle/, all host
+threads) on a bounded sample of the same workload (the reference is pure
+Python/numpy and cannot travel to the GPU box; its C restatement is pinned
+to the reference's golden vectors, see tests/test_oracle_golden.py).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "ECC Gvoxels/s (discrete, 3D f32, 1024 bins)"
+UNIT = "Gvoxel/s"
+NB = 1024
+SEED = 20261018
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={','.join(self.FIELDS)}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.3)
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.2)
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) != 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def _dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the CPU port on a bounded sample
+# ---------------------------------------------------------------------------
+
+def cpu_port_sample(planes: int = 32, reps: int = 1):
+    """Time oracle/ (the C restatement of ecckit's compute_ecc, all host
+    threads) on `planes` planes of the 512^3 workload.  Returns Gvox/s."""
+    from oracle import oracle
+
+    dims = (planes + 2, 512, 512)
+    x = oracle.counter_grid(SEED, dims).reshape(dims)
+    taus = np.linspace(0.0, 1.0, NB + 1)[1:]
+    oracle.histogram_rows(x, 1, planes + 1, taus)  # warm-up (thread pool)
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        oracle.histogram_rows(x, 1, planes + 1, taus)
+        ts.append(time.perf_counter() - t0)
+    vox = planes * 512 * 512
+    return vox / min(ts) / 1e9, oracle.num_threads(), f"{planes}x512x512 f32 planes of the 512^3 volume, {NB} bins"
+
+
+def run_reference(args):
+    world, rank, _ = _dist_env()
+    if rank != 0:
+        return
+    vals = []
+    sample = ""
+    cores = 1
+    for _ in range(args.warmup):
+        cpu_port_sample(planes=16)
+    for _ in range(args.steps):
+        v, cores, sample = cpu_port_sample(planes=32)
+        vals.append(v)
+    value = statistics.median(vals)
+    vox_per_step = 512 * 512 * 512 * world
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": vox_per_step / (value * 1e9) * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "C2: 3D 512^3 float32 volume, discrete ECC, 1024 uniform thresholds "
+                   "(sampled: 32 planes per step)", "volume": [512 * world, 512, 512], "bins": NB,
+                   "parallelism": f"zslab{world}"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2510_20271_b200 as E
+    from paper_2510_20271_b200 import _lib
+    from paper_2510_20271_b200 import distributed as D
+
+    world, rank, local = _dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    L = _lib.lib()
+    stream = torch.cuda.current_stream(dev)
+
+    # --- synthetic volume: this rank's 512 planes (+ halos) --------------------
+    P, H, W = args.planes, 512, 512
+    padded = D.alloc_padded_slab(P, (H, W), torch.float32, dev)
+    own = padded[1:-1]
+    start = rank * P * H * W
+    _lib.check(L.ecc_counter_grid(SEED, start, own.numel(), _lib.ptr(own), _lib.stream_ptr(own)))
+    if world == 1:
+        padded[0].fill_(float("nan"))
+        padded[-1].fill_(float("nan"))
+
+    # thresholds: uniform over the global range (device min/max, grid.py:183-196)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    if world > 1:
+        lo, hi = D.global_range(own)
+    else:
+        lo, hi, _ = E.device_minmax(own)
+    torch.cuda.synchronize()
+    minmax_ms = (time.perf_counter() - t0) * 1e3
+    taus = E.thresholds_from_range(lo, hi, NB)
+    table, binning = taus.device_table(_lib.DTYPE_F32, dev)
+    hist = torch.empty(NB + 1, dtype=torch.int64, device=dev)
+    curve = torch.empty(NB, dtype=torch.int64, device=dev)
+    view, z0, z1 = (padded, 1, P + 1) if world == 1 else D.slab_view(padded)
+    dims = _lib.dims_arg(view.shape)
+    kstart = torch.cuda.Event(enable_timing=True)
+    kend = torch.cuda.Event(enable_timing=True)
+    kernel_ms = []
+
+    def step(record=False):
+        if world > 1:
+            D.exchange_halos(padded)
+        if record:
+            kstart.record(stream)
+        _lib.check(L.ecc_histogram_range(_lib.ptr(view), _lib.DTYPE_F32, 3, _lib.ptr(dims), 1, z0, z1,
+                                         _lib.ptr(table), _lib.ctypes.byref(binning), _lib.ptr(hist),
+                                         _lib.ctypes.c_void_p(stream.cuda_stream)))
+        if record:
+            kend.record(stream)
+        if world > 1:
+            dist.all_reduce(hist)
+        _lib.check(L.ecc_scan(_lib.ptr(hist), 1, NB, _lib.ptr(curve), _lib.ctypes.c_void_p(stream.cuda_stream)))
+
+    # correctness gate on the real workload (size-independent properties):
+    # the full-volume curve ends at chi(box) = 1 and sums of c are 1.
+    step()
+    h = hist.cpu().numpy()
+    c = curve.cpu().numpy()
+    assert int(h.sum()) == 1 and int(c[-1]) == 1, "ECC invariant violated (sum c != 1)"
+    checksum = int(np.bitwise_xor.reduce(c.view(np.uint64)))
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        barrier()
+    total_ms = ev0.elapsed_time(ev1)
+    # kernel-only timing of the dominant kernel (same stream, separate pass)
+    for _ in range(args.steps):
+        step(record=True)
+        kend.synchronize()
+        kernel_ms.append(kstart.elapsed_time(kend))
+    if world > 1:
+        t = torch.tensor([total_ms, statistics.mean(kernel_ms)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, kmean = float(t[0]), float(t[1])
+    else:
+        kmean = statistics.mean(kernel_ms)
+    ms_per_step = total_ms / args.steps
+    vox_rank = P * H * W
+    vox_total = vox_rank * world
+    value = vox_total / (ms_per_step * 1e-3) / 1e9
+
+    peak, peak_kind = _peaks()
+    achieved = 4.0 * vox_rank / (kmean * 1e-3) / 1e9
+    traffic = None
+    tfile = ROOT / "profiles" / "ncu_traffic.json"
+    if tfile.exists():
+        try:
+            traffic = json.loads(tfile.read_text()).get("bytes_per_launch")
+        except (ValueError, OSError):
+            traffic = None
+
+    # --- e2e through the public API: pinned H2D + compute + D2H -------------
+    e2e = None
+    if world == 1 and not args.no_e2e:
+        host = torch.empty((P, H, W), dtype=torch.float32, pin_memory=True)
+        host.copy_(own.cpu())
+        xdev = torch.empty((P, H, W), dtype=torch.float32, device=dev)
+
+        def e2e_step():
+            xdev.copy_(host, non_blocking=True)
+            cv = E.ecc_discrete(xdev, taus)
+            return cv.cpu()
+
+        got = e2e_step()
+        assert int(got[-1]) == 1
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        reps = max(3, min(args.steps, 10))
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            e2e_step()
+        torch.cuda.synchronize()
+        e_ms = (time.perf_counter() - t0) * 1e3 / reps
+        e2e = {"value": vox_rank / (e_ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": e_ms,
+               "h2d_bytes_per_step": int(host.numel() * 4), "d2h_bytes_per_step": int(NB * 8),
+               "api": "paper_2510_20271_b200.ecc_discrete (pinned host -> HBM copy inside the timed region)"}
+        del host, xdev
+
+    # --- soft ECC C3 (forward + backward) -------------------------------------
+    soft = None
+    if not args.no_soft:
+        soft = bench_soft(args, dev, world, rank)
+
+    # --- CPU baseline (rank 0, N = 1) ----------------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v, cores, sample = cpu_port_sample(planes=32)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "C2: 3D 512^3 float32 volume, discrete ECC, 1024 uniform thresholds"
+                       + (" (z-slab per GPU, halo exchange + NCCL histogram all-reduce)" if world > 1 else ""),
+                       "volume": [P * world, H, W], "bins": NB, "parallelism": f"zslab{world}",
+                       "l2": "input larger than L2 (512 MiB per GPU), no flush",
+                       "thresholds": "given (uniform over the device min/max, computed once)",
+                       "minmax_pass_ms": minmax_ms, "seed": SEED, "curve_xor_checksum": checksum},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
+                         "kernel": "ecc_sweep_kernel<RawSrc<float>,HistSink<float>>",
+                         "kernel_ms": kmean, "algorithmic_bytes_per_launch": 4 * vox_rank},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": 2 * args.steps,
+            "clocks": clocks.summary(),
+            "soft": soft,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def bench_soft(args, dev, world, rank):
+    import torch
+
+    import paper_2510_20271_b200 as E
+
+    N, H, W, B, lam, alpha = args.soft_batch, 1024, 1024, 256, 50.0, 0.3
+    g = torch.Generator(device=dev)
+    g.manual_seed(SEED + rank)
+    x = torch.rand((N, H, W), device=dev, generator=g, dtype=torch.float32)
+    v = np.array([1.0, 2.0])
+    u = v / np.linalg.norm(v)
+    span = alpha * np.abs(u).sum()
+    taus = np.linspace(-span, 1.0 + span, B + 1)[1:]
+    m = E.SoftECC(taus, v, alpha=alpha, lam=lam).to(dev)
+    up = torch.ones((N, B), dtype=torch.float64, device=dev)
+
+    def step():
+        m.zero_grad(set_to_none=True)
+        chi = m(x)
+        chi.backward(up)
+        if world > 1:
+            from paper_2510_20271_b200 import distributed as D
+
+            D.allreduce_soft_grads(m)
+
+    step()
+    torch.cuda.synchronize()
+    steps = max(2, min(args.steps, 5))
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t[0])
+    vox = N * H * W * world
+    pairs = vox * B * 2
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    mufu_peak = 16 * sms * 1.965e9 * world
+    return {"metric": "soft-ECC fwd+bwd voxels/s", "value": vox / (ms * 1e-3), "unit": "voxel/s",
+            "ms_per_step": ms, "steps": steps,
+            "config": {"workload": "C3: batched 2D 128x1024x1024 f32, soft ECC fwd+bwd, learnable tau/u/alpha",
+                       "batch_per_gpu": N, "bins": B, "lambda": lam, "alpha": alpha, "parallelism": f"batch{world}"},
+            "roofline": {"bound": "sfu", "unit": "pairs/s (one MUFU op per (voxel, threshold) pair per pass)",
+                         "achieved": pairs / (ms * 1e-3), "peak": mufu_peak, "frac": pairs / (ms * 1e-3) / mufu_peak,
+                         "note": "pairs counted over all voxels; voxels with c = 0 are skipped by the kernels"}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--planes", type=int, default=512, help="planes per GPU (512 = C2)")
+    ap.add_argument("--soft-batch", type=int, default=128)
+    ap.add_argument("--no-soft", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,151 @@
+/*
+ * ecc_b200.h -- C ABI of the B200 Euler Characteristic Curve engine
+ * (libecc_b200.so, built from paper_2510_20271_b200/csrc/).
+ *
+ * The reference (ecckit 0.1.0, /root/reference/pkg/src/ecckit) is pure
+ * Python and has no FFI; its hot path sits behind the Python functions
+ * re-exported by ecckit/__init__.py:11-117.  Each entry point below replaces
+ * the numpy kernel of one of those functions; the Python shim in
+ * paper_2510_20271_b200/ keeps the reference's names, argument meaning and
+ * exceptions and calls these through ctypes (INTEGRATION.md shows the
+ * binding).
+ *
+ * Conventions
+ *   - every array argument is a caller-owned DEVICE pointer unless the name
+ *     ends in _host; nothing is allocated inside a launcher;
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream); launches are
+ *     asynchronous on it;
+ *   - grids are row-major, last axis fastest (grid.py:5-9); `dims` is a HOST
+ *     array of `ndim` (2 or 3) extents; `batch` grids of that shape are
+ *     stored back to back;
+ *   - return 0 on success, a negative errno-style code on failure, with a
+ *     thread-local message in ecc_last_error().
+ */
+#ifndef ECC_B200_H
+#define ECC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ECC_OK 0
+#define ECC_EINVAL (-22)   /* the reference raises ValueError here */
+#define ECC_ECUDA (-5)     /* CUDA runtime / launch failure */
+
+#define ECC_DTYPE_U8 0
+#define ECC_DTYPE_F32 1
+#define ECC_DTYPE_F64 2
+
+#define ECC_MAX_BINS (1 << 20)
+
+/* Binning parameters produced by ecc_threshold_table(). */
+typedef struct {
+  double t0;      /* first threshold, in the compare type's precision       */
+  double inv_w;   /* (nbins-1)/(t_last-t0) or 0                              */
+  int64_t nbins;  /* B                                                       */
+  int32_t mode;   /* 0 affine guess + exact correction, 1 binary search      */
+  int32_t max_correction; /* largest guess error seen at the breakpoints    */
+} ecc_binning;
+
+/* Version string and thread-local description of the last failure. */
+const char *ecc_version(void);
+const char *ecc_last_error(void);
+
+/* HOST.  Validates a threshold set exactly like ThresholdSet.__init__
+ * (grid.py:129-139: non-empty, finite, strictly increasing) and writes the
+ * device compare table into table_host (nbins+2 entries of float32 for
+ * ECC_DTYPE_U8/F32 -- t32_j = the largest float32 <= tau_j -- or float64 for
+ * ECC_DTYPE_F64, with -inf/+inf sentinels), plus the binning parameters.
+ * Replaces ThresholdSet._certify_affine / bin_indices (grid.py:147-180). */
+int ecc_threshold_table(const double *taus_host, int64_t nbins, int dtype, void *table_host,
+                        ecc_binning *binning_host);
+
+/* Fused stencil + coefficient + bin + histogram sweep.
+ * hist: int64 [batch][nbins+1], the last entry of each row is the overflow
+ * bucket (HistogramBins.bins / .overflow, hard.py:75-86).  Zeroed here.
+ * Replaces accumulate_histogram (hard.py:184-212) with FullSweep semantics. */
+int ecc_histogram(const void *x, int dtype, int ndim, const int64_t *dims, int64_t batch, const void *table,
+                  const ecc_binning *binning_host, int64_t *hist, void *stream);
+
+/* As ecc_histogram, but only voxels in planes [plane_begin, plane_end) of
+ * axis 0 are deposited; the planes outside act as halo (coefficients.py:
+ * 141-152 _coefficient_rows).  A halo plane filled with NaN behaves exactly
+ * like "outside the grid".  This is the z-slab entry point of the multi-GPU
+ * path (one rank = one slab plus a one-plane halo on each side).  3D only. */
+int ecc_histogram_range(const void *x, int dtype, int ndim, const int64_t *dims, int64_t batch,
+                        int64_t plane_begin, int64_t plane_end, const void *table,
+                        const ecc_binning *binning_host, int64_t *hist, void *stream);
+
+/* Inclusive prefix sum of bins[0..nbins) per batch item -> int64 curve
+ * [batch][nbins] (compute_ecc, hard.py:226). */
+int ecc_scan(const int64_t *hist, int64_t batch, int64_t nbins, int64_t *curve, void *stream);
+
+/* Lower-star coefficients, int8 [batch][dims] (compute_coefficients,
+ * coefficients.py:163-175). */
+int ecc_coefficients(const void *x, int dtype, int ndim, const int64_t *dims, int64_t batch, int8_t *out,
+                     void *stream);
+
+/* Min / max / non-finite count of n values, as order-preserving uint64 keys
+ * out3[0] (min), out3[1] (max), out3[2] (count of NaN/Inf); decode with
+ * ecc_key_to_double().  Feeds uniform_thresholds (grid.py:183-196) and the
+ * ScalarGrid finiteness check (grid.py:63-64). */
+int ecc_minmax(const void *x, int dtype, int64_t n, uint64_t *out3, void *stream);
+double ecc_key_to_double(uint64_t key);
+
+/* Soft ECC (soft.py).  Parameters shared by forward and backward. */
+typedef struct {
+  double lam;          /* sharpness lambda > 0                                  */
+  double alpha;        /* direction scale                                       */
+  double u[3];         /* direction (first ndim used); any vector, not forced unit */
+  double center;       /* m: taus and field are centred on m before fp32 math   */
+  int32_t factorized;  /* 1: sigma = 1/(1 + a_j b_p) with a_j = e^{-lam(tau_j-m)},
+                          b_p = e^{lam(f_p-m)}; 0: direct ex2 per pair           */
+  int32_t pad;
+} ecc_soft_params;
+
+/* effective_field (soft.py:97-101): out = X + alpha * <u, pos> in float64
+ * with the reference's rounding sequence.  u_host: ndim doubles (HOST). */
+int ecc_effective_field(const void *x, int dtype, int ndim, const int64_t *dims, int64_t batch, double alpha,
+                        const double *u_host, double *out, void *stream);
+
+/* Workspace bytes for ecc_soft_forward/backward partials. */
+size_t ecc_soft_workspace_bytes(int ndim, const int64_t *dims, int64_t batch, int64_t nbins);
+
+/* Effective-field coefficients (the coefficients callers feed to soft_ecc:
+ * compute_coefficients(effective_field(grid, alpha, u)), cli.py:201,
+ * soft.py:292) computed from a float64 effective field built on the fly with
+ * the reference's rounding sequence; also writes the centred float32 field
+ * fc = f - m used by the sigma kernels.  x: float32 or float64 grid. */
+int ecc_soft_prepare(const void *x, int dtype, int ndim, const int64_t *dims, int64_t batch,
+                     const ecc_soft_params *params_host, int8_t *coeffs, float *field_c, void *stream);
+
+/* Forward: chi[batch][nbins] (float64) = sum_p c_p sigmoid(lam (tau_j - f_p))
+ * (soft.py:154-196).  coeffs may be any int8 grid (e.g. the reference's).
+ * taus: float64 [nbins] device.  workspace: ecc_soft_workspace_bytes. */
+int ecc_soft_forward(const int8_t *coeffs, const float *field_c, int ndim, const int64_t *dims, int64_t batch,
+                     const double *taus, int64_t nbins, const ecc_soft_params *params_host, double *chi,
+                     void *workspace, void *stream);
+
+/* Backward (soft.py:199-257 plus the alpha gradient):
+ *   d_values[b][p] = -c_p w_p,  w_p = sum_j up[b][j] lam s(1-s)   (float32)
+ *   d_tau[b][j]    = up[b][j] sum_p c_p lam s(1-s)                (float64)
+ *   G[b][0..ndim)  = sum_p c_p w_p pos_p                          (float64)
+ * from which d_u = -alpha G (then tangent-projected by the caller) and
+ * d_alpha = -G.u.  upstream: float64 [batch][nbins]. */
+int ecc_soft_backward(const int8_t *coeffs, const float *field_c, int ndim, const int64_t *dims, int64_t batch,
+                      const double *taus, int64_t nbins, const ecc_soft_params *params_host,
+                      const double *upstream, float *d_values, double *d_tau, double *G, void *workspace,
+                      void *stream);
+
+/* Counter-based synthetic float32 grid: out[i] = top-24-bits(splitmix64(
+ * seed * K + start + i)) * 2^-24 (identical to the oracle's
+ * generator so 2048^3 slabs are reproducible on both sides). */
+int ecc_counter_grid(uint64_t seed, int64_t start, int64_t count, float *out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ECC_B200_H */

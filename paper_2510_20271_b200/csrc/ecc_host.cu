@@ -1,0 +1,150 @@
+// ecc_host.cu -- host-side pieces of the C ABI: errors, threshold tables,
+// key decoding, and the counter-based synthetic generator kernel.
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <cmath>
+#include <limits>
+
+#include "ecc_common.cuh"
+#include "ecc_internal.h"
+
+namespace ecc {
+static thread_local char g_err[512] = "";
+
+int set_error(int code, const char* msg) {
+  snprintf(g_err, sizeof(g_err), "%s", msg);
+  return code;
+}
+int set_cuda_error(cudaError_t e, const char* what) {
+  snprintf(g_err, sizeof(g_err), "%s: %s", what, cudaGetErrorString(e));
+  return ECC_ECUDA;
+}
+void clear_error() { g_err[0] = 0; }
+
+// largest float32 <= t (round toward -inf), the t32 of DESIGN.md
+static float round_down_f32(double t) {
+  float f = (float)t;
+  if ((double)f > t) f = std::nextafter(f, -std::numeric_limits<float>::infinity());
+  return f;
+}
+
+template <typename V>
+static int64_t true_bin(V x, const V* tab, int64_t nb) {
+  // tab has sentinels: tab[j+1] = tau_j
+  int64_t lo = 0, hi = nb;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (tab[mid + 1] < x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+template <typename V>
+static int64_t guess_bin(V x, V t0, V inv_w, int64_t nb) {
+  volatile V d = x - t0;  // volatile: no contraction, matches the device's two roundings
+  V g = d * inv_w;
+  if (g < V(0)) g = V(0);
+  if (g > V(nb)) g = V(nb);
+  return (int64_t)g;
+}
+
+template <typename V>
+static void certify(const V* tab, int64_t nb, ecc_binning* b) {
+  const V t0 = tab[1], tl = tab[nb];
+  b->t0 = (double)t0;
+  b->inv_w = 0.0;
+  b->mode = 1;
+  b->max_correction = -1;
+  if (nb < 2) {
+    b->mode = 0;  // guess 0 then correct: at most one step
+    b->max_correction = 1;
+    return;
+  }
+  if (!std::isfinite((double)t0) || !std::isfinite((double)tl) || !(tl > t0)) return;
+  const V span = tl - t0;
+  if (!std::isfinite((double)span)) return;
+  const V inv_w = V(nb - 1) / span;
+  if (!std::isfinite((double)inv_w) || !(inv_w > V(0))) return;
+  int64_t worst = 0;
+  for (int64_t j = 0; j < nb; ++j) {
+    const V at = tab[j + 1];
+    const V above = std::nextafter(at, std::numeric_limits<V>::infinity());
+    const V probes[2] = {at, above};
+    for (V x : probes) {
+      int64_t t = true_bin<V>(x, tab, nb), gg = guess_bin<V>(x, t0, inv_w, nb);
+      int64_t e = t > gg ? t - gg : gg - t;
+      if (e > worst) worst = e;
+    }
+  }
+  b->inv_w = (double)inv_w;
+  b->max_correction = (int32_t)(worst > 0x7fffffff ? 0x7fffffff : worst);
+  // a guess off by a few bins costs a few smem reads; beyond that binary
+  // search is cheaper (grid.py:147-166 makes the same choice on the CPU)
+  b->mode = worst <= 4 ? 0 : 1;
+}
+
+__global__ void counter_grid_kernel(uint64_t seed, int64_t start, int64_t count, float* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t z = seed * 0xD1B54A32D192ED03ull + (uint64_t)(start + i);
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    out[i] = (float)(z >> 40) * (1.0f / 16777216.0f);
+  }
+}
+}  // namespace ecc
+
+using namespace ecc;
+
+extern "C" const char* ecc_version(void) { return "ecc_b200 0.1.0 (sm_100a)"; }
+extern "C" const char* ecc_last_error(void) { return g_err; }
+
+extern "C" double ecc_key_to_double(uint64_t k) {
+  uint64_t b = (k & 0x8000000000000000ull) ? (k & 0x7fffffffffffffffull) : ~k;
+  double d;
+  memcpy(&d, &b, sizeof d);
+  return d;
+}
+
+extern "C" int ecc_threshold_table(const double* taus, int64_t nb, int dtype, void* table_host,
+                                   ecc_binning* b) {
+  clear_error();
+  if (!taus || !table_host || !b) return set_error(ECC_EINVAL, "null pointer argument");
+  if (nb < 1) return set_error(ECC_EINVAL, "threshold set must contain at least one value");
+  if (nb > ECC_MAX_BINS) return set_error(ECC_EINVAL, "too many thresholds");
+  for (int64_t j = 0; j < nb; ++j)
+    if (!std::isfinite(taus[j])) return set_error(ECC_EINVAL, "thresholds must be finite");
+  for (int64_t j = 1; j < nb; ++j)
+    if (!(taus[j] > taus[j - 1])) return set_error(ECC_EINVAL, "thresholds must be strictly increasing");
+  b->nbins = nb;
+  if (dtype == ECC_DTYPE_U8 || dtype == ECC_DTYPE_F32) {
+    float* t = (float*)table_host;
+    t[0] = -std::numeric_limits<float>::infinity();
+    for (int64_t j = 0; j < nb; ++j) t[j + 1] = round_down_f32(taus[j]);
+    t[nb + 1] = std::numeric_limits<float>::infinity();
+    certify<float>(t, nb, b);
+  } else if (dtype == ECC_DTYPE_F64) {
+    double* t = (double*)table_host;
+    t[0] = -std::numeric_limits<double>::infinity();
+    for (int64_t j = 0; j < nb; ++j) t[j + 1] = taus[j];
+    t[nb + 1] = std::numeric_limits<double>::infinity();
+    certify<double>(t, nb, b);
+  } else {
+    return set_error(ECC_EINVAL, "unsupported dtype");
+  }
+  return ECC_OK;
+}
+
+extern "C" int ecc_counter_grid(uint64_t seed, int64_t start, int64_t count, float* out, void* stream) {
+  clear_error();
+  if (!out) return set_error(ECC_EINVAL, "null pointer argument");
+  if (count <= 0) return ECC_OK;
+  int64_t blocks = (count + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  counter_grid_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(seed, start, count, out);
+  return check_launch("counter_grid_kernel");
+}

@@ -1,0 +1,190 @@
+"""Exact Euler characteristic curves -- the API of ecckit/hard.py on the GPU.
+
+``compute_ecc`` / ``accumulate_histogram`` keep the reference's signatures
+(hard.py:184-226).  The reference's two strategies (FullSweep, Chunked) and
+its worker count are accepted for compatibility; the device always runs one
+fused sweep (ecc_histogram) whose integer result equals both strategies'
+(strategy equivalence) at every worker count.
+
+``ecc_discrete`` is the torch-native batched entry point: a CUDA tensor of
+shape [N?, (D,) H, W] in, int64 curves [N?, B] out, no host round trip.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .grid import EulerCurve, ScalarGrid, ThresholdSet
+
+
+@dataclass(frozen=True)
+class FullSweep:
+    """Single pass over the grid (hard.py:41-46)."""
+
+    def __str__(self):
+        return "fullsweep"
+
+
+@dataclass(frozen=True)
+class Chunked:
+    """Sequential fixed-size chunks (hard.py:49-60).  Accepted for API
+    compatibility; results are identical to FullSweep by construction."""
+
+    chunk_len: int
+
+    def __post_init__(self):
+        if self.chunk_len < 1:
+            raise ValueError(f"chunk_len must be >= 1, got {self.chunk_len}")
+
+    def __str__(self):
+        return f"chunked:{self.chunk_len}"
+
+
+Strategy = FullSweep | Chunked
+
+
+def parse_strategy(text: str) -> Strategy:
+    """Parse ``fullsweep`` or ``chunked:<k>`` (hard.py:66-72)."""
+    if text == "fullsweep":
+        return FullSweep()
+    if text.startswith("chunked:"):
+        return Chunked(int(text.split(":", 1)[1]))
+    raise ValueError(f"unknown strategy {text!r}; expected 'fullsweep' or 'chunked:<k>'")
+
+
+@dataclass(frozen=True)
+class HistogramBins:
+    """Integer coefficient totals per threshold bin (hard.py:75-86)."""
+
+    taus: np.ndarray
+    bins: np.ndarray
+    overflow: int
+
+
+def bin_index(x: float, taus: ThresholdSet) -> int | None:
+    """Smallest j with x <= taus[j], or None beyond the last (hard.py:89-96)."""
+    j = int(np.searchsorted(taus.taus, x, side="left"))
+    return j if j < len(taus) else None
+
+
+def merge_histograms(parts) -> HistogramBins:
+    """Element-wise int64 sum over identical threshold sets (hard.py:99-118)."""
+    parts = list(parts)
+    if not parts:
+        raise ValueError("cannot merge zero histograms")
+    first = parts[0]
+    for p in parts[1:]:
+        if p.bins.shape != first.bins.shape:
+            raise ValueError(f"histogram bin counts differ: {p.bins.size} vs {first.bins.size}")
+        if not np.array_equal(p.taus, first.taus):
+            raise ValueError("histograms were accumulated over different thresholds")
+    bins = np.sum([p.bins for p in parts], axis=0, dtype=np.int64)
+    overflow = int(sum(p.overflow for p in parts))
+    return HistogramBins(first.taus, bins, overflow)
+
+
+# ---------------------------------------------------------------------------
+# device primitives
+# ---------------------------------------------------------------------------
+
+def device_minmax(t: torch.Tensor) -> tuple[float, float, int]:
+    """(min, max, #non-finite) of a CUDA tensor via ecc_minmax (one pass)."""
+    L = _lib.lib()
+    t = t.contiguous()
+    out = torch.empty(3, dtype=torch.int64, device=t.device)
+    _lib.check(L.ecc_minmax(_lib.ptr(t), _lib.dtype_code(t), t.numel(), _lib.ptr(out), _lib.stream_ptr(t)))
+    k = out.cpu().numpy().view(np.uint64)
+    return float(L.ecc_key_to_double(int(k[0]))), float(L.ecc_key_to_double(int(k[1]))), int(k[2])
+
+
+def _split_batch(x: torch.Tensor, ndim: int | None):
+    """(batch, grid dims) of a [N?, (D,) H, W] tensor."""
+    if ndim is None:
+        ndim = x.ndim if x.ndim in (2, 3) else None
+        if ndim is None:
+            raise ValueError(f"pass ndim for a {x.ndim}-D tensor (batched grids)")
+    if ndim not in (2, 3):
+        raise ValueError(f"grid must be 2D or 3D, got ndim={ndim}")
+    if x.ndim == ndim:
+        return 1, tuple(x.shape), False
+    if x.ndim == ndim + 1:
+        return int(x.shape[0]), tuple(x.shape[1:]), True
+    raise ValueError(f"expected a {ndim}-D grid or a batch of them, got shape {tuple(x.shape)}")
+
+
+def histogram_device(x: torch.Tensor, taus: ThresholdSet, ndim: int | None = None) -> torch.Tensor:
+    """int64 [N, B+1] coefficient histograms (last column = overflow) of CUDA
+    grids x [N?, (D,) H, W] (uint8 / float32 / float64)."""
+    if not x.is_cuda:
+        raise ValueError("histogram_device takes a CUDA tensor")
+    x = x.contiguous()
+    batch, dims, _ = _split_batch(x, ndim)
+    code = _lib.dtype_code(x)
+    table, binning = taus.device_table(code, x.device)
+    hist = torch.empty((batch, len(taus) + 1), dtype=torch.int64, device=x.device)
+    d = _lib.dims_arg(dims)
+    _lib.check(_lib.lib().ecc_histogram(_lib.ptr(x), code, len(dims), _lib.ptr(d), batch, _lib.ptr(table),
+                                        _lib.ctypes.byref(binning), _lib.ptr(hist), _lib.stream_ptr(x)))
+    return hist
+
+
+def scan_device(hist: torch.Tensor, nbins: int) -> torch.Tensor:
+    """Inclusive prefix over the first nbins columns -> int64 [N, B] curves."""
+    batch = hist.shape[0]
+    curve = torch.empty((batch, nbins), dtype=torch.int64, device=hist.device)
+    _lib.check(_lib.lib().ecc_scan(_lib.ptr(hist), batch, nbins, _lib.ptr(curve), _lib.stream_ptr(hist)))
+    return curve
+
+
+def ecc_discrete(x: torch.Tensor, taus, ndim: int | None = None, return_hist: bool = False):
+    """Torch-native batched exact ECC.
+
+    x: CUDA tensor [N?, (D,) H, W] of uint8 / float32 / float64 (float32
+    values are compared exactly as the reference's float64 would be).
+    taus: ThresholdSet or 1-D array of strictly increasing thresholds.
+    Returns int64 curves [N?, B] on the device (and the [N?, B+1] histogram).
+    Non-finite inputs are the caller's responsibility on this path (validate
+    with ScalarGrid or device_minmax).
+    """
+    ts = taus if isinstance(taus, ThresholdSet) else ThresholdSet(taus)
+    _, _, batched = _split_batch(x, ndim)
+    hist = histogram_device(x, ts, ndim)
+    curve = scan_device(hist, len(ts))
+    if not batched:
+        curve, hist = curve[0], hist[0]
+    return (curve, hist) if return_hist else curve
+
+
+def _check_strategy(strategy, workers):
+    if workers < 1:
+        raise ValueError(f"workers must be >= 1, got {workers}")
+    if not isinstance(strategy, (FullSweep, Chunked)):
+        raise TypeError(f"unknown strategy {strategy!r}")
+
+
+def accumulate_histogram(
+    grid: ScalarGrid,
+    taus: ThresholdSet,
+    strategy: Strategy = FullSweep(),
+    workers: int = 1,
+) -> HistogramBins:
+    """Coefficient histogram of a grid (hard.py:184-212), on the GPU."""
+    _check_strategy(strategy, workers)
+    h = histogram_device(grid.device_tensor(), taus)[0].cpu().numpy()
+    return HistogramBins(taus.taus, h[:-1].copy(), int(h[-1]))
+
+
+def compute_ecc(
+    grid: ScalarGrid,
+    taus: ThresholdSet,
+    strategy: Strategy = FullSweep(),
+    workers: int = 1,
+) -> EulerCurve:
+    """Exact Euler characteristic curve at every threshold (hard.py:215-226)."""
+    _check_strategy(strategy, workers)
+    curve = ecc_discrete(grid.device_tensor(), taus)
+    return EulerCurve(taus.taus, curve.cpu().numpy())

@@ -1,0 +1,313 @@
+"""Differentiable (soft) ECC with one learnable direction -- ecckit/soft.py on the GPU.
+
+Reference-compatible functions (soft.py:41-257): ``SoftEccParams``,
+``SoftGradients``, ``pixel_coordinates``, ``effective_field``,
+``reparametrize_direction[_jvp]``, ``soft_ecc``, ``soft_ecc_backward``.
+
+PyTorch surface (the north star's module): ``SoftECCFunction`` (autograd)
+and ``SoftECC`` (nn.Module with learnable thresholds tau, direction v -> u =
+v/|v| and scale alpha; sharpness lambda is a buffer).  The kernels return
+the raw direction gradient -alpha*G; autograd through u = v/|v| supplies the
+tangent projection and 1/|v|, i.e. reparametrize_direction_jvp (soft.py:113-121).
+
+Numerics: the reference evaluates in float64.  The engine evaluates the
+sigmoid arguments in float32 around a centre m (fp32 accumulation within a
+lane, fp64 across lanes and CTAs, fixed order), and the coefficients of the
+effective field from a float64 field with the reference's rounding sequence.
+Parity contract: normwise relative error <= 1e-4 (max|a-b| / max|b|).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .coefficients import CoefficientGrid
+from .grid import EulerCurve, ScalarGrid, ThresholdSet
+
+UNIT_NORM_TOL = 1e-12
+_LOG2E = 1.4426950408889634
+_FACTOR_LIMIT = 63.0  # |log2 a_j| bound for the factorised sigmoid (a_j b_p <= 2^126)
+
+
+@dataclass(frozen=True)
+class SoftEccParams:
+    """Sharpness, direction scale, unit direction and thresholds (soft.py:41-63)."""
+
+    lam: float
+    alpha: float
+    u: np.ndarray
+    taus: ThresholdSet
+
+    def __post_init__(self):
+        if not self.lam > 0:
+            raise ValueError(f"sharpness must be positive, got {self.lam}")
+        u = np.asarray(self.u, dtype=np.float64).ravel()
+        if u.size not in (2, 3):
+            raise ValueError(f"direction must have 2 or 3 components, got {u.size}")
+        if not np.isfinite(u).all():
+            raise ValueError("direction must be finite")
+        if abs(np.linalg.norm(u) - 1.0) > UNIT_NORM_TOL:
+            raise ValueError(
+                f"direction must be unit length within {UNIT_NORM_TOL}, "
+                f"got norm {np.linalg.norm(u)!r}"
+            )
+        object.__setattr__(self, "u", u)
+
+
+@dataclass(frozen=True)
+class SoftGradients:
+    """Cotangent-weighted gradients (soft.py:66-76), plus d_alpha (north star)."""
+
+    d_values: np.ndarray
+    d_tau: np.ndarray
+    d_u: np.ndarray
+    d_alpha: float = field(default=float("nan"))
+
+
+def pixel_coordinates(dims, start: int = 0, stop: int | None = None) -> np.ndarray:
+    """Positions of pixels [start, stop) mapped per axis into [-1, 1] (soft.py:79-94)."""
+    dims = tuple(dims)
+    n = 1
+    for d in dims:
+        n *= d
+    if stop is None:
+        stop = n
+    coords = np.unravel_index(np.arange(start, stop), dims)
+    out = np.empty((stop - start, len(dims)))
+    for a, (idx, d) in enumerate(zip(coords, dims)):
+        out[:, a] = 0.0 if d == 1 else idx * (2.0 / (d - 1)) - 1.0
+    return out
+
+
+def reparametrize_direction(v) -> np.ndarray:
+    """Map an unconstrained vector onto the unit sphere (soft.py:104-110)."""
+    v = np.asarray(v, dtype=np.float64).ravel()
+    norm = float(np.linalg.norm(v))
+    if norm <= 1e-12:
+        raise ValueError(f"direction vector too close to zero (norm {norm!r})")
+    return v / norm
+
+
+def reparametrize_direction_jvp(v, dv) -> np.ndarray:
+    """Jacobian-vector product of :func:`reparametrize_direction` (soft.py:113-121)."""
+    v = np.asarray(v, dtype=np.float64).ravel()
+    dv = np.asarray(dv, dtype=np.float64).ravel()
+    norm = float(np.linalg.norm(v))
+    if norm <= 1e-12:
+        raise ValueError(f"direction vector too close to zero (norm {norm!r})")
+    u = v / norm
+    return (dv - u * (u @ dv)) / norm
+
+
+# ---------------------------------------------------------------------------
+# device plumbing
+# ---------------------------------------------------------------------------
+
+def _soft_tensor(x: torch.Tensor) -> torch.Tensor:
+    if x.dtype not in (torch.float32, torch.float64):
+        x = x.to(torch.float32)
+    return x.contiguous()
+
+
+def _params(lam: float, alpha: float, u, tau_lo: float, tau_hi: float, ndim: int) -> _lib.SoftParams:
+    p = _lib.SoftParams()
+    p.lam = float(lam)
+    p.alpha = float(alpha)
+    uu = np.zeros(3)
+    uu[:ndim] = np.asarray(u, dtype=np.float64).ravel()[:ndim]
+    for i in range(3):
+        p.u[i] = float(uu[i])
+    m = 0.5 * (tau_lo + tau_hi)
+    p.center = m
+    p.factorized = int(lam * _LOG2E * max(abs(tau_hi - m), abs(tau_lo - m)) <= _FACTOR_LIMIT)
+    return p
+
+
+def soft_prepare_device(x: torch.Tensor, dims, batch: int, p: _lib.SoftParams):
+    """(int8 coefficients of the effective field, centred fp32 field) on device."""
+    code = _lib.dtype_code(x)
+    c = torch.empty(x.shape, dtype=torch.int8, device=x.device)
+    fc = torch.empty(x.shape, dtype=torch.float32, device=x.device)
+    d = _lib.dims_arg(dims)
+    _lib.check(_lib.lib().ecc_soft_prepare(_lib.ptr(x), code, len(dims), _lib.ptr(d), batch, _lib.ctypes.byref(p),
+                                           _lib.ptr(c), _lib.ptr(fc), _lib.stream_ptr(x)))
+    return c, fc
+
+
+def _workspace(dims, batch: int, nb: int, device) -> torch.Tensor:
+    d = _lib.dims_arg(dims)
+    nbytes = int(_lib.lib().ecc_soft_workspace_bytes(len(dims), _lib.ptr(d), batch, nb))
+    return torch.empty(max(nbytes, 8) // 8 + 1, dtype=torch.float64, device=device)
+
+
+def soft_forward_device(c, fc, dims, batch: int, taus_dev: torch.Tensor, p: _lib.SoftParams) -> torch.Tensor:
+    nb = taus_dev.numel()
+    chi = torch.empty((batch, nb), dtype=torch.float64, device=fc.device)
+    ws = _workspace(dims, batch, nb, fc.device)
+    d = _lib.dims_arg(dims)
+    _lib.check(_lib.lib().ecc_soft_forward(_lib.ptr(c), _lib.ptr(fc), len(dims), _lib.ptr(d), batch,
+                                           _lib.ptr(taus_dev), nb, _lib.ctypes.byref(p), _lib.ptr(chi), _lib.ptr(ws),
+                                           _lib.stream_ptr(fc)))
+    return chi
+
+
+def soft_backward_device(c, fc, dims, batch: int, taus_dev, p, upstream: torch.Tensor):
+    """(d_values fp32 like fc, d_tau [N,B] fp64, G [N,ndim] fp64)."""
+    nb = taus_dev.numel()
+    up = upstream.to(torch.float64).contiguous()
+    dX = torch.empty(fc.shape, dtype=torch.float32, device=fc.device)
+    dtau = torch.empty((batch, nb), dtype=torch.float64, device=fc.device)
+    G = torch.empty((batch, len(dims)), dtype=torch.float64, device=fc.device)
+    ws = _workspace(dims, batch, nb, fc.device)
+    d = _lib.dims_arg(dims)
+    _lib.check(_lib.lib().ecc_soft_backward(_lib.ptr(c), _lib.ptr(fc), len(dims), _lib.ptr(d), batch,
+                                            _lib.ptr(taus_dev), nb, _lib.ctypes.byref(p), _lib.ptr(up), _lib.ptr(dX),
+                                            _lib.ptr(dtau), _lib.ptr(G), _lib.ptr(ws), _lib.stream_ptr(fc)))
+    return dX, dtau, G
+
+
+def effective_field(grid: ScalarGrid, alpha: float, u) -> ScalarGrid:
+    """The field X + alpha <u, p> (soft.py:97-101), float64, on the device."""
+    x = _soft_tensor(grid.device_tensor())
+    u = np.ascontiguousarray(np.asarray(u, dtype=np.float64).ravel())
+    if u.size != grid.ndim:
+        raise ValueError(f"direction has {u.size} components for a {grid.ndim}D grid")
+    out = torch.empty(x.shape, dtype=torch.float64, device=x.device)
+    d = _lib.dims_arg(grid.dims)
+    _lib.check(_lib.lib().ecc_effective_field(_lib.ptr(x), _lib.dtype_code(x), grid.ndim, _lib.ptr(d), 1,
+                                              float(alpha), _lib.ptr(u), _lib.ptr(out), _lib.stream_ptr(x)))
+    return ScalarGrid(out)
+
+
+def _check_shapes(grid: ScalarGrid, coeffs: CoefficientGrid, u: np.ndarray):
+    if tuple(coeffs.dims) != tuple(grid.dims):
+        raise ValueError(f"coefficient dims {coeffs.dims} != grid dims {grid.dims}")
+    if u.size != grid.ndim:
+        raise ValueError(f"direction has {u.size} components for a {grid.ndim}D grid")
+
+
+def _coeff_tensor(coeffs: CoefficientGrid, device) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(coeffs.coeffs, dtype=np.int8)).to(device)
+
+
+def _prepared(grid, coeffs, params):
+    x = _soft_tensor(grid.device_tensor())
+    taus = params.taus.taus
+    p = _params(params.lam, params.alpha, params.u, float(taus[0]), float(taus[-1]), grid.ndim)
+    _, fc = soft_prepare_device(x, grid.dims, 1, p)
+    c = _coeff_tensor(coeffs, x.device)
+    taus_dev = torch.from_numpy(np.ascontiguousarray(taus)).to(x.device)
+    return c, fc, taus_dev, p
+
+
+def soft_ecc(grid: ScalarGrid, coeffs: CoefficientGrid, params: SoftEccParams, workers: int = 1) -> EulerCurve:
+    """Smoothed Euler characteristic curve (soft.py:182-196), on the GPU.
+
+    ``coeffs`` is expected to come from the effective field; it is taken as
+    given (e.g. the reference's own), exactly like the reference.
+    """
+    _check_shapes(grid, coeffs, params.u)
+    c, fc, taus_dev, p = _prepared(grid, coeffs, params)
+    chi = soft_forward_device(c, fc, grid.dims, 1, taus_dev, p)
+    return EulerCurve(params.taus.taus, chi[0].cpu().numpy())
+
+
+def soft_ecc_backward(grid: ScalarGrid, coeffs: CoefficientGrid, params: SoftEccParams, upstream,
+                      workers: int = 1) -> SoftGradients:
+    """Cotangent-weighted gradients (soft.py:199-257), on the GPU; also d_alpha."""
+    _check_shapes(grid, coeffs, params.u)
+    upstream = np.asarray(upstream, dtype=np.float64).ravel()
+    ntau = len(params.taus)
+    if upstream.size != ntau:
+        raise ValueError(f"upstream has {upstream.size} weights for {ntau} thresholds")
+    c, fc, taus_dev, p = _prepared(grid, coeffs, params)
+    up = torch.from_numpy(upstream).to(fc.device).reshape(1, ntau)
+    dX, dtau, G = soft_backward_device(c, fc, grid.dims, 1, taus_dev, p, up)
+    G = G[0].cpu().numpy()
+    u = params.u
+    d_u = -params.alpha * G
+    d_u = d_u - (d_u @ u) * u
+    d_alpha = -float(G @ u)
+    return SoftGradients(dX.to(torch.float64).cpu().numpy().reshape(grid.dims), dtau[0].cpu().numpy(), d_u,
+                         d_alpha)
+
+
+# ---------------------------------------------------------------------------
+# PyTorch autograd surface
+# ---------------------------------------------------------------------------
+
+class SoftECCFunction(torch.autograd.Function):
+    """chi[N, B] = sum_p c_p sigmoid(lam (tau_j - X_np - alpha <u, pos_p>)).
+
+    x: CUDA [N, (D,) H, W] float32/float64; taus: [B]; u: [ndim] (any norm;
+    the module normalises); alpha: scalar tensor; lam: python float.
+    Coefficients come from the effective field and carry no gradient
+    (soft.py:14-19).
+    """
+
+    @staticmethod
+    def forward(ctx, x, taus, u, alpha, lam: float, ndim: int):
+        from .hard import _split_batch
+
+        xs = _soft_tensor(x.detach())
+        batch, dims, batched = _split_batch(xs, ndim)
+        taus_d = taus.detach().to(torch.float64).contiguous()
+        lo, hi = torch.aminmax(taus_d)
+        uh = u.detach().to(torch.float64).cpu().numpy()
+        a = float(alpha.detach())
+        p = _params(lam, a, uh, float(lo), float(hi), ndim)
+        c, fc = soft_prepare_device(xs, dims, batch, p)
+        chi = soft_forward_device(c, fc, dims, batch, taus_d, p)
+        ctx.save_for_backward(c, fc, taus_d, u.detach(), alpha.detach())
+        ctx.meta = (dims, batch, batched, p, x.dtype, taus.dtype)
+        return chi if batched else chi[0]
+
+    @staticmethod
+    def backward(ctx, grad_chi):
+        c, fc, taus_d, u, alpha = ctx.saved_tensors
+        dims, batch, batched, p, xdtype, tdtype = ctx.meta
+        up = grad_chi.reshape(batch, -1)
+        dX, dtau, G = soft_backward_device(c, fc, dims, batch, taus_d, p, up)
+        Gs = G.sum(0)
+        gx = dX.to(xdtype) if ctx.needs_input_grad[0] else None
+        gt = dtau.sum(0).to(tdtype) if ctx.needs_input_grad[1] else None
+        gu = (-alpha.to(torch.float64) * Gs).to(u.dtype) if ctx.needs_input_grad[2] else None
+        ga = (-(Gs * u.to(torch.float64)).sum()).to(alpha.dtype) if ctx.needs_input_grad[3] else None
+        return gx, gt, gu, ga, None, None
+
+
+class SoftECC(torch.nn.Module):
+    """Single-direction differentiable ECC layer (the paper's PyTorch module).
+
+    Learnable: thresholds ``taus`` [B], direction ``v`` [ndim] (u = v/|v|,
+    soft.py:104-110), scale ``alpha``.  Buffer: sharpness ``lam``.
+    forward(x [N?, (D,) H, W]) -> chi [N?, B] (float64).
+    """
+
+    def __init__(self, taus, direction, alpha: float = 0.0, lam: float = 50.0, ndim: int | None = None,
+                 learn_taus: bool = True, learn_direction: bool = True, learn_alpha: bool = True):
+        super().__init__()
+        taus = torch.as_tensor(np.asarray(taus, dtype=np.float64))
+        v = torch.as_tensor(np.asarray(direction, dtype=np.float64).ravel())
+        if v.numel() not in (2, 3):
+            raise ValueError(f"direction must have 2 or 3 components, got {v.numel()}")
+        if float(v.norm()) <= 1e-12:
+            raise ValueError("direction vector too close to zero")
+        if not lam > 0:
+            raise ValueError(f"sharpness must be positive, got {lam}")
+        self.ndim = int(v.numel()) if ndim is None else int(ndim)
+        self.taus = torch.nn.Parameter(taus, requires_grad=learn_taus)
+        self.v = torch.nn.Parameter(v, requires_grad=learn_direction)
+        self.alpha = torch.nn.Parameter(torch.tensor(float(alpha), dtype=torch.float64), requires_grad=learn_alpha)
+        self.register_buffer("lam", torch.tensor(float(lam), dtype=torch.float64))
+
+    def direction(self) -> torch.Tensor:
+        return self.v / self.v.norm()
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        return SoftECCFunction.apply(x, self.taus, self.direction(), self.alpha, float(self.lam), self.ndim)

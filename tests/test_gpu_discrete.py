@@ -1,0 +1,211 @@
+"""Discrete ECC on the GPU: bit-exact parity with the reference (golden vectors)
+and with the CPU oracle, through the reference-shaped API and the C ABI.
+
+Mirrors the reference's tests/test_hard.py, test_coefficients.py and
+acceptance criteria 1/3/6 (test_acceptance.py:51-209) with the CUDA engine
+in place of ecckit's numpy kernels.
+"""
+
+import numpy as np
+import pytest
+import torch
+from hypothesis import given, settings
+from hypothesis import strategies as st
+
+from conftest import golden_cases, random_f32_grid, random_int_grid
+from oracle import oracle
+
+pytestmark = pytest.mark.gpu
+
+E = pytest.importorskip("paper_2510_20271_b200")
+
+
+def _grid(vals):
+    return E.ScalarGrid(vals)
+
+
+class TestGoldenParity:
+    def test_coefficients(self, golden):
+        for k in golden_cases(golden, "coeff"):
+            x = golden[f"coeff{k}_x"]
+            got = E.compute_coefficients(_grid(x)).coeffs
+            assert np.array_equal(got, golden[f"coeff{k}_c"]), f"case {k} dims {x.shape}"
+
+    def test_coefficients_all_dtypes(self, golden):
+        dev = torch.device("cuda")
+        for k in golden_cases(golden, "coeff"):
+            x = golden[f"coeff{k}_x"]
+            want = golden[f"coeff{k}_c"]
+            for dt in (torch.float64, torch.float32):
+                t = torch.from_numpy(x).to(dev, dt)
+                if dt == torch.float32 and not np.array_equal(t.double().cpu().numpy(), x):
+                    continue
+                assert np.array_equal(E.coefficients_device(t).cpu().numpy(), want), (k, dt)
+
+    def test_histograms_and_curves(self, golden):
+        for k in golden_cases(golden, "hist"):
+            x = golden[f"hist{k}_x"]
+            ts = E.ThresholdSet(golden[f"hist{k}_taus"])
+            g = _grid(x)
+            h = E.accumulate_histogram(g, ts)
+            assert np.array_equal(h.bins, golden[f"hist{k}_bins"]), f"case {k} {x.shape}"
+            assert h.overflow == int(golden[f"hist{k}_overflow"][0]), f"case {k}"
+            curve = E.compute_ecc(g, ts)
+            assert curve.values.dtype == np.int64
+            assert np.array_equal(curve.values, golden[f"hist{k}_curve"]), f"case {k}"
+
+    def test_histograms_every_dtype(self, golden):
+        """float64 and float32 device tensors (and uint8 when exact) agree."""
+        dev = torch.device("cuda")
+        for k in golden_cases(golden, "hist"):
+            x = golden[f"hist{k}_x"]
+            ts = E.ThresholdSet(golden[f"hist{k}_taus"])
+            want = np.concatenate([golden[f"hist{k}_bins"], golden[f"hist{k}_overflow"]])
+            variants = [torch.from_numpy(x).to(dev)]
+            if np.array_equal(x.astype(np.float32).astype(np.float64), x):
+                variants.append(torch.from_numpy(x.astype(np.float32)).to(dev))
+            if x.min() >= 0 and x.max() <= 255 and np.array_equal(np.floor(x), x):
+                variants.append(torch.from_numpy(x.astype(np.uint8)).to(dev))
+            for t in variants:
+                got = E.histogram_device(t, ts)[0].cpu().numpy()
+                assert np.array_equal(got, want), (k, t.dtype)
+
+    def test_uniform_thresholds(self, golden):
+        for k in golden_cases(golden, "uthr"):
+            x = golden[f"uthr{k}_x"]
+            bins = int(golden[f"uthr{k}_bins"][0])
+            got = E.uniform_thresholds(_grid(x), bins).taus
+            assert np.array_equal(got, golden[f"uthr{k}_taus"]), k
+
+
+class TestFixtures:
+    """test_hard.py:27-50, test_coefficients.py:29-69."""
+
+    def test_center_peak_2d(self):
+        vals = np.zeros((3, 3))
+        vals[1, 1] = 1.0
+        assert np.array_equal(E.compute_ecc(_grid(vals), E.ThresholdSet([0.0, 1.0])).values, [0, 1])
+
+    def test_center_peak_3d_shell(self):
+        vals = np.zeros((3, 3, 3))
+        vals[1, 1, 1] = 1.0
+        assert np.array_equal(E.compute_ecc(_grid(vals), E.ThresholdSet([0.0, 1.0])).values, [2, 1])
+
+    def test_threshold_below_min_gives_zero(self, rng):
+        x = random_f32_grid(rng, 2, 8)
+        curve = E.compute_ecc(_grid(x), E.ThresholdSet([x.min() - 1.0, x.max()]))
+        assert curve.values[0] == 0 and curve.values[-1] == 1
+
+    def test_tail_is_one_at_max(self, rng):
+        for _ in range(10):
+            x = random_int_grid(rng, 2, 10)
+            g = _grid(x)
+            assert E.compute_ecc(g, E.uniform_thresholds(g, 7)).values[-1] == 1
+
+    def test_single_pixel_and_2x2(self):
+        assert np.array_equal(E.compute_coefficients(_grid([[5.0]])).coeffs, [[1]])
+        assert np.array_equal(E.compute_coefficients(_grid(np.zeros((2, 2)))).coeffs.ravel(), [1, 0, 0, 0])
+
+
+class TestOracleEquivalence:
+    def test_random_int_grids(self, rng):
+        """acceptance criterion 1 (test_acceptance.py:51-68): 200 grids, every distinct value."""
+        for ndim, max_extent in ((2, 32), (3, 8)):
+            for _ in range(100):
+                x = random_int_grid(rng, ndim, max_extent)
+                taus = np.unique(x)
+                got = E.compute_ecc(_grid(x), E.ThresholdSet(taus)).values
+                assert np.array_equal(got, oracle.curve(x, taus)), x.shape
+
+    def test_float_plateaus(self, rng):
+        vals = rng.random((9, 9)).astype(np.float32).astype(np.float64)
+        vals[vals < 0.4] = 0.25
+        taus = np.unique(vals)
+        assert np.array_equal(E.compute_ecc(_grid(vals), E.ThresholdSet(taus)).values, oracle.curve(vals, taus))
+
+    @given(st.lists(st.integers(1, 4), min_size=2, max_size=3), st.data())
+    @settings(max_examples=200, deadline=None)
+    def test_arbitrary_float32_property(self, dims, data):
+        """test_hard.py:169-188: arbitrary float32 values incl. +-0 and subnormals."""
+        n = int(np.prod(dims))
+        values = data.draw(st.lists(st.floats(allow_nan=False, allow_infinity=False, width=32),
+                                     min_size=n, max_size=n))
+        x = np.array(values, dtype=np.float64).reshape(dims)
+        taus = np.unique(x)
+        got = E.compute_ecc(_grid(x), E.ThresholdSet(taus)).values
+        assert np.array_equal(got, oracle.curve(x, taus))
+
+    def test_odd_shapes_and_sizes(self, rng):
+        """Tile edges: extents around multiples of the 32x16 tile and z-chunks."""
+        for dims in [(37, 23), (9, 8, 7), (1, 1), (1, 200), (200, 1), (33, 17), (31, 65), (3, 1, 1), (1, 1, 50),
+                     (70, 33, 17), (130, 5, 40), (2, 300, 3)]:
+            x = rng.random(dims).astype(np.float32).astype(np.float64)
+            g = _grid(x)
+            ts = E.uniform_thresholds(g, 97)
+            assert np.array_equal(E.compute_ecc(g, ts).values, oracle.curve(x, ts.taus)), dims
+            assert np.array_equal(E.compute_coefficients(g).coeffs, oracle.coefficients(x)), dims
+
+    def test_mass_is_one_with_overflow(self, rng):
+        for trial in range(20):
+            x = random_int_grid(rng, 2 if trial % 2 else 3, 10 if trial % 2 else 5)
+            hi = float(x.max())
+            ts = E.ThresholdSet([hi / 3, hi / 2]) if hi > 0 else E.ThresholdSet([0.0])
+            h = E.accumulate_histogram(_grid(x), ts)
+            assert int(h.bins.sum()) + h.overflow == 1
+
+    def test_medium_volume_vs_oracle(self):
+        """uniform-random 3D with 1024 bins, several z-chunks and tiles."""
+        x = oracle.counter_grid(7, (96, 80, 72)).reshape(96, 80, 72)
+        t = torch.from_numpy(x).cuda()
+        lo, hi, bad = E.device_minmax(t)
+        assert bad == 0 and lo == float(x.min()) and hi == float(x.max())
+        ts = E.thresholds_from_range(lo, hi, 1024)
+        curve, hist = E.ecc_discrete(t, ts, return_hist=True)
+        bins, ovf = oracle.histogram(x, ts.taus)
+        assert np.array_equal(hist.cpu().numpy(), np.append(bins, ovf))
+        assert np.array_equal(curve.cpu().numpy(), np.cumsum(bins))
+
+
+class TestBatchedAndValidation:
+    def test_batched_matches_individual(self, rng):
+        xs = rng.random((5, 19, 23, 11)).astype(np.float32)
+        ts = E.ThresholdSet(np.linspace(0.05, 0.95, 33))
+        curves = E.ecc_discrete(torch.from_numpy(xs).cuda(), ts, ndim=3).cpu().numpy()
+        for i in range(5):
+            assert np.array_equal(curves[i], oracle.curve(xs[i], ts.taus))
+        xs2 = rng.integers(0, 256, (4, 40, 50)).astype(np.uint8)
+        taus2 = np.arange(0.0, 256.0, 3.0)
+        curves2 = E.ecc_discrete(torch.from_numpy(xs2).cuda(), E.ThresholdSet(taus2), ndim=2).cpu().numpy()
+        for i in range(4):
+            assert np.array_equal(curves2[i], oracle.curve(xs2[i].astype(np.float64), taus2))
+
+    def test_bad_workers_and_strategy(self, rng):
+        g = _grid(random_int_grid(rng, 2, 4))
+        with pytest.raises(ValueError):
+            E.compute_ecc(g, E.uniform_thresholds(g, 2), E.FullSweep(), 0)
+        with pytest.raises(TypeError):
+            E.compute_ecc(g, E.uniform_thresholds(g, 2), "sideways")
+
+    def test_strategies_and_workers_identical(self, rng):
+        x = random_int_grid(rng, 3, 6)
+        g = _grid(x)
+        ts = E.uniform_thresholds(g, 9)
+        ref = E.compute_ecc(g, ts).values
+        for strategy in (E.FullSweep(), E.Chunked(1), E.Chunked(7)):
+            for workers in (1, 2, 8):
+                assert E.compute_ecc(g, ts, strategy, workers).values.tobytes() == ref.tobytes()
+
+    def test_nonfinite_device_grid_rejected(self):
+        t = torch.zeros((4, 4), device="cuda")
+        t[1, 2] = float("nan")
+        with pytest.raises(ValueError):
+            E.ScalarGrid(t)
+
+    def test_c1_uint8(self):
+        """BASELINE configs[0]: 256x256 uint8, 256 thresholds, bit-exact."""
+        x = np.random.default_rng(1).integers(0, 256, (256, 256), np.uint8)
+        t = torch.from_numpy(x).cuda()
+        lo, hi, _ = E.device_minmax(t)
+        ts = E.thresholds_from_range(lo, hi, 256)
+        got = E.ecc_discrete(t, ts).cpu().numpy()
+        assert np.array_equal(got, oracle.curve(x.astype(np.float64), ts.taus))

@@ -1,0 +1,185 @@
+"""Soft ECC on the GPU against the reference (golden vectors) and the oracle.
+
+Tolerance (north star: 1e-4 relative, fp32): normwise, i.e.
+max|gpu - ref| / max|ref| <= 1e-4, for chi, d_tau, d_u, d_values; d_alpha
+against the reference's 4th-order finite difference of _forward_raw
+(soft.py:308-315) with the gradient_check floor (soft.py:303-306).
+Coefficients of the effective field must match the reference exactly.
+Mirrors tests/test_soft.py of the reference.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden_cases, normwise
+from oracle import oracle
+
+pytestmark = pytest.mark.gpu
+
+E = pytest.importorskip("paper_2510_20271_b200")
+
+TOL = 1e-4
+
+
+def _params(golden, k):
+    alpha, lam = golden[f"soft{k}_params"]
+    return E.SoftEccParams(lam=float(lam), alpha=float(alpha), u=golden[f"soft{k}_u"],
+                           taus=E.ThresholdSet(golden[f"soft{k}_taus"]))
+
+
+class TestGoldenParity:
+    def test_effective_field_bit_exact(self, golden):
+        for k in golden_cases(golden, "soft"):
+            x = golden[f"soft{k}_x"]
+            alpha, _ = golden[f"soft{k}_params"]
+            eff = E.effective_field(E.ScalarGrid(x), float(alpha), golden[f"soft{k}_u"]).values
+            assert np.array_equal(eff, golden[f"soft{k}_eff"]), k
+
+    def test_effective_field_coefficients_exact(self, golden):
+        for k in golden_cases(golden, "soft"):
+            x = golden[f"soft{k}_x"]
+            alpha, lam = golden[f"soft{k}_params"]
+            taus = golden[f"soft{k}_taus"]
+            p = E.soft._params(float(lam), float(alpha), golden[f"soft{k}_u"], taus[0], taus[-1], x.ndim)
+            t = torch.from_numpy(x).cuda()
+            c, _ = E.soft.soft_prepare_device(t, x.shape, 1, p)
+            assert np.array_equal(c.cpu().numpy(), golden[f"soft{k}_coeffs"]), k
+
+    def test_forward(self, golden):
+        for k in golden_cases(golden, "soft"):
+            g = E.ScalarGrid(golden[f"soft{k}_x"])
+            cg = E.CoefficientGrid(golden[f"soft{k}_coeffs"])
+            chi = E.soft_ecc(g, cg, _params(golden, k)).values
+            assert chi.dtype == np.float64
+            err = normwise(chi, golden[f"soft{k}_chi"])
+            assert err <= TOL, (k, err)
+
+    def test_backward(self, golden):
+        for k in golden_cases(golden, "soft"):
+            g = E.ScalarGrid(golden[f"soft{k}_x"])
+            cg = E.CoefficientGrid(golden[f"soft{k}_coeffs"])
+            params = _params(golden, k)
+            gr = E.soft_ecc_backward(g, cg, params, golden[f"soft{k}_upstream"])
+            for name, got in (("dvalues", gr.d_values), ("dtau", gr.d_tau), ("du", gr.d_u)):
+                want = golden[f"soft{k}_{name}"]
+                if np.abs(want).max() == 0:
+                    assert np.abs(got).max() <= 1e-12, (k, name)
+                    continue
+                err = normwise(got, want)
+                assert err <= TOL, (k, name, err)
+            assert abs(gr.d_u @ params.u) <= 1e-8
+            fd = float(golden[f"soft{k}_dalpha_fd"][0])
+            rel = abs(gr.d_alpha - fd) / max(abs(gr.d_alpha), abs(fd), 1e-4)
+            assert rel <= TOL, (k, gr.d_alpha, fd)
+
+    def test_closed_forms(self):
+        """test_soft.py:39-50, 160-174."""
+        g = E.ScalarGrid([[0.0]])
+        c = E.compute_coefficients(g)
+        u = E.reparametrize_direction([1.0, 0.0])
+        for lam in (0.5, 4.0, 100.0):
+            p = E.SoftEccParams(lam=lam, alpha=0.0, u=u, taus=E.ThresholdSet([0.0]))
+            assert abs(E.soft_ecc(g, c, p).values[0] - 0.5) <= 1e-6
+        p = E.SoftEccParams(lam=100.0, alpha=0.0, u=u, taus=E.ThresholdSet([1.0]))
+        assert abs(E.soft_ecc(g, c, p).values[0] - 1.0) <= 1e-6
+        p = E.SoftEccParams(lam=4.0, alpha=0.0, u=u, taus=E.ThresholdSet([0.0]))
+        gr = E.soft_ecc_backward(g, c, p, np.ones(1))
+        assert abs(gr.d_tau[0] - 1.0) <= 1e-6 and abs(gr.d_values.ravel()[0] + 1.0) <= 1e-6
+
+    def test_alpha_zero_kills_direction_gradient(self, rng):
+        x = rng.integers(0, 10, (6, 7)).astype(np.float64)
+        g = E.ScalarGrid(x)
+        c = E.compute_coefficients(g)
+        p = E.SoftEccParams(lam=3.0, alpha=0.0, u=E.reparametrize_direction([3.0, 4.0]),
+                            taus=E.uniform_thresholds(g, 5))
+        gr = E.soft_ecc_backward(g, c, p, rng.normal(size=5))
+        assert np.array_equal(gr.d_u, np.zeros(2))
+
+    def test_upstream_length_checked(self, rng):
+        g = E.ScalarGrid(rng.integers(0, 10, (4, 4)).astype(np.float64))
+        p = E.SoftEccParams(lam=1.0, alpha=0.0, u=np.array([1.0, 0.0]), taus=E.uniform_thresholds(g, 4))
+        with pytest.raises(ValueError):
+            E.soft_ecc_backward(g, E.compute_coefficients(g), p, np.ones(3))
+
+
+def _oracle_case(rng, dims, B, lam, alpha, u):
+    x = rng.random(dims).astype(np.float32).astype(np.float64)
+    eff = oracle.effective_field(x, alpha, u)
+    c = oracle.coefficients(eff)
+    taus = E.uniform_thresholds(E.ScalarGrid(eff), B).taus
+    return x, c, taus
+
+
+class TestOracleParity:
+    @pytest.mark.parametrize("dims,B,lam", [((128, 96), 256, 50.0), ((24, 20, 16), 256, 50.0),
+                                           ((64, 64), 1024, 50.0), ((40, 40), 37, 1e4), ((50, 30), 7, 0.5)])
+    def test_forward_backward(self, rng, dims, B, lam):
+        alpha = 0.3
+        u = E.reparametrize_direction([1.0, 2.0, -0.5][: len(dims)])
+        x, c, taus = _oracle_case(rng, dims, B, lam, alpha, u)
+        params = E.SoftEccParams(lam=lam, alpha=alpha, u=u, taus=E.ThresholdSet(taus))
+        g, cg = E.ScalarGrid(x), E.CoefficientGrid(c)
+        chi = E.soft_ecc(g, cg, params).values
+        want = oracle.soft_forward(x, c, lam, alpha, u, taus)
+        assert normwise(chi, want) <= TOL
+        up = rng.uniform(0.5, 1.5, taus.size)
+        gr = E.soft_ecc_backward(g, cg, params, up)
+        dv, dt, du, da, _ = oracle.soft_backward(x, c, lam, alpha, u, taus, up)
+        assert normwise(gr.d_values, dv) <= TOL
+        assert normwise(gr.d_tau, dt) <= TOL
+        assert normwise(gr.d_u, du) <= TOL
+        assert abs(gr.d_alpha - da) <= TOL * max(abs(da), 1e-4)
+
+    def test_determinism(self, rng):
+        """Bit-identical repeated runs (test_soft.py:296-306)."""
+        x = rng.random((96, 96))
+        g = E.ScalarGrid(x)
+        c = E.compute_coefficients(g)
+        p = E.SoftEccParams(lam=8.0, alpha=0.2, u=E.reparametrize_direction([2.0, -1.0]),
+                            taus=E.uniform_thresholds(g, 32))
+        a = E.soft_ecc(g, c, p).values
+        b = E.soft_ecc(g, c, p).values
+        assert a.tobytes() == b.tobytes()
+
+
+class TestModule:
+    def test_module_gradients_vs_oracle(self, rng):
+        N, H, W, B = 3, 40, 36, 64
+        x = rng.random((N, H, W)).astype(np.float32)
+        v = np.array([1.0, 2.0])
+        alpha, lam = 0.3, 50.0
+        u = v / np.linalg.norm(v)
+        taus0 = np.linspace(-0.4, 1.4, B)
+        m = E.SoftECC(taus0, v, alpha=alpha, lam=lam).cuda()
+        xt = torch.from_numpy(x).cuda().requires_grad_(True)
+        chi = m(xt)
+        assert chi.shape == (N, B)
+        up = torch.from_numpy(rng.uniform(0.5, 1.5, (N, B))).cuda()
+        (chi * up).sum().backward()
+        gtau = np.zeros(B)
+        G = np.zeros(2)
+        for i in range(N):
+            xi = x[i].astype(np.float64)
+            c = oracle.coefficients(oracle.effective_field(xi, alpha, u))
+            want = oracle.soft_forward(xi, c, lam, alpha, u, taus0)
+            assert normwise(chi[i].detach().cpu().numpy(), want) <= TOL
+            dv, dt, _, _, Gi = oracle.soft_backward(xi, c, lam, alpha, u, taus0, up[i].cpu().numpy())
+            assert normwise(xt.grad[i].cpu().numpy(), dv) <= TOL
+            gtau += dt
+            G += Gi
+        assert normwise(m.taus.grad.cpu().numpy(), gtau) <= TOL
+        # u = v/|v|: dL/dv = jvp^T(-alpha G) ; dL/dalpha = -G.u
+        du_raw = -alpha * G
+        dv_want = (du_raw - u * (u @ du_raw)) / np.linalg.norm(v)
+        assert normwise(m.v.grad.cpu().numpy(), dv_want) <= TOL
+        da = -(G @ u)
+        assert abs(float(m.alpha.grad) - da) <= TOL * max(abs(da), 1e-4)
+
+    def test_module_3d_batch(self, rng):
+        x = torch.from_numpy(rng.random((2, 12, 10, 9)).astype(np.float32)).cuda()
+        m = E.SoftECC(np.linspace(0, 1, 16), [1.0, 2.0, -0.5], alpha=0.25, lam=10.0).cuda()
+        chi = m(x)
+        assert chi.shape == (2, 16)
+        chi.sum().backward()
+        assert m.taus.grad is not None and m.v.grad is not None and m.alpha.grad is not None
