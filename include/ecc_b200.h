@@ -48,6 +48,13 @@ typedef struct {
   int64_t nbins;  /* B                                                       */
   int32_t mode;   /* 0 affine guess + exact correction, 1 binary search      */
   int32_t max_correction; /* largest guess error seen at the breakpoints    */
+  /* cell table of the float32 fast path: cell(x) = trunc(sat((x - lut_lo) *
+   * lut_scale) * lut_cells); every cell holds at most one threshold, so
+   * bin(x) = b[cell] + (x > t[cell]) exactly (verified at build time). */
+  float lut_lo;
+  float lut_scale;
+  int32_t lut_cells;
+  int32_t lut_ok;
 } ecc_binning;
 
 /* Version string and thread-local description of the last failure. */
@@ -58,10 +65,15 @@ const char *ecc_last_error(void);
  * (grid.py:129-139: non-empty, finite, strictly increasing) and writes the
  * device compare table into table_host (nbins+2 entries of float32 for
  * ECC_DTYPE_U8/F32 -- t32_j = the largest float32 <= tau_j -- or float64 for
- * ECC_DTYPE_F64, with -inf/+inf sentinels), plus the binning parameters.
+ * ECC_DTYPE_F64, with -inf/+inf sentinels), followed for float32/uint8 by
+ * the cell table of the fast path (8-byte aligned, lut_cells+1 entries of
+ * {float t, int32 b}); size: ecc_threshold_table_bytes().
  * Replaces ThresholdSet._certify_affine / bin_indices (grid.py:147-180). */
 int ecc_threshold_table(const double *taus_host, int64_t nbins, int dtype, void *table_host,
                         ecc_binning *binning_host);
+
+/* Bytes of the table ecc_threshold_table writes (sentinel table + cell table). */
+size_t ecc_threshold_table_bytes(int64_t nbins, int dtype);
 
 /* Fused stencil + coefficient + bin + histogram sweep.
  * hist: int64 [batch][nbins+1], the last entry of each row is the overflow

@@ -30,7 +30,8 @@ class EngineUnavailable(RuntimeError):
 
 class Binning(ctypes.Structure):
     _fields_ = [("t0", ctypes.c_double), ("inv_w", ctypes.c_double), ("nbins", ctypes.c_int64),
-                ("mode", ctypes.c_int32), ("max_correction", ctypes.c_int32)]
+                ("mode", ctypes.c_int32), ("max_correction", ctypes.c_int32), ("lut_lo", ctypes.c_float),
+                ("lut_scale", ctypes.c_float), ("lut_cells", ctypes.c_int32), ("lut_ok", ctypes.c_int32)]
 
 
 class SoftParams(ctypes.Structure):
@@ -49,6 +50,8 @@ def lib():
         L.ecc_version.restype = ctypes.c_char_p
         L.ecc_last_error.restype = ctypes.c_char_p
         L.ecc_threshold_table.argtypes = [vp, i64, i32, vp, ctypes.POINTER(Binning)]
+        L.ecc_threshold_table_bytes.argtypes = [i64, i32]
+        L.ecc_threshold_table_bytes.restype = ctypes.c_size_t
         L.ecc_histogram.argtypes = [vp, i32, i32, vp, i64, vp, ctypes.POINTER(Binning), vp, vp]
         L.ecc_histogram_range.argtypes = [vp, i32, i32, vp, i64, i64, i64, vp, ctypes.POINTER(Binning), vp, vp]
         L.ecc_scan.argtypes = [vp, i64, i64, vp, vp]

@@ -10,6 +10,7 @@
 // subnormal comparisons (the reference's hypothesis test draws subnormals).
 #include "ecc_common.cuh"
 #include "ecc_internal.h"
+#include <stdlib.h>
 
 namespace ecc {
 
@@ -477,6 +478,9 @@ extern "C" int ecc_histogram_range(const void* x, int dtype, int ndim, const int
                           plane_begin, plane_end);
     }
     case ECC_DTYPE_F32: {
+      if (fast3d_eligible(x, d3[0], d3[1], d3[2], batch, nb) && !getenv("ECC_B200_GENERIC"))
+        return fast3d_launch((const float*)x, d3[0], d3[1], d3[2], batch, plane_begin, plane_end, table, binning, h,
+                             s);
       HistSink<float> sk{(const float*)table, h, bp};
       return launch_sweep(RawSrc<float>{(const float*)x}, sk, d3, batch, HistSink<float>::smem_bytes(nb), s,
                           plane_begin, plane_end);

@@ -1,0 +1,537 @@
+// ecc_fast3d.cu -- bit-sliced, TMA-fed discrete ECC sweep (the sm_100a fast path).
+//
+// Same contract as the generic sweep in ecc_discrete.cu (histogram of the
+// lower-star coefficients, hard.py:134-143 / coefficients.py:74-138) for
+// float32 grids whose row pitch is 16-byte aligned; bit-exact with it.
+//
+// Layout.  A CTA owns a tile of 128 (x) by 32 (y) columns and sweeps a
+// chunk of z planes.  Warp w owns x-segment [x0 + 32w, x0 + 32w + 32); lane
+// r owns row y0 - 1 + r of that segment: lanes 0 and 31 are halo rows, so a
+// tile emits 30 rows.  One thread therefore holds the 32 voxels of a row
+// segment as BITS of 32-bit words ("bit-sliced"): bit i of a word is voxel
+// x0 + i.
+//
+// Per plane a thread computes the 13 "lower" words of the lexicographically
+// negative offsets of its voxels (q <= p), with one FSUB.RD + one funnel
+// shift per bit: RD(X(q) - X(p)) is negative or -0 exactly when X(q) <= X(p)
+// (p canonicalised to +0), and NaN (out-of-grid, TMA OOB fill) gives +NaN.
+// The 13 positive-offset words are the complements of neighbours' negative
+// words (order antisymmetry, coefficients.py:97-105), fetched with warp
+// shuffles (rows y+-1) and from the next plane (one-plane lag), shifted by
+// one bit for dx = +-1; the bit that crosses the segment edge is compared
+// directly.  The cell logic (12 squares, 8 cubes) and the signed count
+// c = 1 - E + S - C run on whole words (32 voxels per LOP3) through a
+// carry-save adder tree into 4 bit-planes of c + 5.  Only then does the
+// kernel go per voxel: c, a branch-free table lookup for the bin, and one
+// shared-memory atomic.
+//
+// Planes arrive by TMA (cp.async.bulk.tensor, 4-D map W x H x D x N, NaN
+// out-of-bounds fill) into a 3-stage shared-memory ring guarded by
+// mbarriers; one thread issues, all threads wait on the stage's parity.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <stdint.h>
+
+#include "ecc_common.cuh"
+#include "ecc_internal.h"
+
+namespace ecc {
+namespace fast {
+
+constexpr int NW = 4;                  // warps per CTA, side by side along x
+constexpr int NT = 32 * NW;            // threads per CTA
+constexpr int SEG = 32;                // voxels per thread (bits per word)
+constexpr int TXW = NW * SEG;          // tile width (x)
+constexpr int OUTR = 30;               // output rows per tile (32 lanes - 2 halo)
+constexpr int PITCH = 140;             // staged row: x0-4 .. x0+135 (== 12 mod 32 words: LDS.128 conflict-free)
+constexpr int PLANE = PITCH * 32;      // floats per staged plane
+constexpr int NSTAGE = 3;
+constexpr uint32_t PLANE_BYTES = PLANE * 4;
+
+struct Geom {
+  int W, H, D;
+  int tiles_x, tiles_y, zchunks, zc;
+  int zb, ze;          // deposit planes [zb, ze)
+  int64_t items;
+};
+
+struct LutEntry {
+  float t;   // split threshold: bin = b + (x > t)
+  int b;
+};
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void tma_load_4d(float* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
+                                            int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
+      "%5}], [%6];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// sign bit of RD(q - p) is 1  <=>  q <= p  (p canonical, both finite or q NaN)
+__device__ __forceinline__ uint32_t le_bit(float q, float p) { return __float_as_uint(__fsub_rd(q, p)); }
+__device__ __forceinline__ uint32_t push(uint32_t w, uint32_t d) { return __funnelshift_l(d, w, 1); }
+
+// Load a staged row segment: 32 values + left/right halo
+struct Row {
+  float v[32];
+  float l, r;
+};
+__device__ __forceinline__ void load_row(Row& R, const float* plane, int row, int col0) {
+  const float* p = plane + row * PITCH + col0;
+  const float4* p4 = reinterpret_cast<const float4*>(p);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    float4 t = p4[k];
+    R.v[4 * k] = t.x;
+    R.v[4 * k + 1] = t.y;
+    R.v[4 * k + 2] = t.z;
+    R.v[4 * k + 3] = t.w;
+  }
+  R.l = p[-1];
+  R.r = p[32];
+}
+__device__ __forceinline__ float qat(const Row& A, int j) { return j < 0 ? A.l : (j > 31 ? A.r : A.v[j]); }
+
+// three words (dx = -1, 0, +1) comparing row A (the q's) against own canonical values pc
+__device__ __forceinline__ void words3(const Row& A, const float (&pc)[32], uint32_t& wm, uint32_t& w0, uint32_t& wp) {
+  wm = 0;
+  w0 = 0;
+  wp = 0;
+#pragma unroll
+  for (int i = 31; i >= 0; --i) {
+    wm = push(wm, le_bit(qat(A, i - 1), pc[i]));
+    w0 = push(w0, le_bit(A.v[i], pc[i]));
+    wp = push(wp, le_bit(qat(A, i + 1), pc[i]));
+  }
+}
+
+// full adder on bit-planes
+__device__ __forceinline__ void fa(uint32_t a, uint32_t b, uint32_t c, uint32_t& s, uint32_t& co) {
+  s = a ^ b ^ c;
+  co = (a & b) | (c & (a ^ b));
+}
+
+// word indices of the 13 negative offsets
+enum { NX = 0, NYM_XM, NYM_X0, NYM_XP, NZ_YM_XM, NZ_YM_X0, NZ_YM_XP, NZ_Y0_XM, NZ_Y0_X0, NZ_Y0_XP, NZ_YP_XM, NZ_YP_X0,
+       NZ_YP_XP, NNEG };
+
+// ---------------------------------------------------------------- the kernel
+__global__ void __launch_bounds__(NT, 3)
+ecc_fast3d_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* __restrict__ table_g, int nb,
+                  int cells, float lut_lo, float lut_scale, int lut_ok, unsigned long long* __restrict__ hist) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* planes = reinterpret_cast<float*>(smem_raw);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + (size_t)NSTAGE * PLANE_BYTES);
+  int* s_hist = reinterpret_cast<int*>(bars + NSTAGE);
+  float* s_tab = reinterpret_cast<float*>(s_hist + ((nb + 1 + 3) & ~3));        // nb+2 (sentinels)
+  LutEntry* s_lut = reinterpret_cast<LutEntry*>(s_tab + ((nb + 2 + 3) & ~3));   // cells+1
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const float* tab_g = reinterpret_cast<const float*>(table_g);
+  const LutEntry* lut_g = reinterpret_cast<const LutEntry*>(tab_g + ((nb + 2 + 1) & ~1));
+  for (int i = threadIdx.x; i <= nb; i += NT) s_hist[i] = 0;
+  for (int i = threadIdx.x; i < nb + 2; i += NT) s_tab[i] = tab_g[i];
+  if (lut_ok)
+    for (int i = threadIdx.x; i <= cells; i += NT) s_lut[i] = lut_g[i];
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < NSTAGE; ++b) mbar_init(&bars[b], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+  }
+  __syncthreads();
+
+  uint32_t phase = 0;           // parity bit per stage
+  int64_t cur_n = -1;
+  const int col0 = 4 + SEG * warp;
+  const int rm = lane > 0 ? lane - 1 : 0, rp = lane < 31 ? lane + 1 : 31;
+  const float cellsf = (float)cells;
+
+  auto stage_of = [](int p) { return ((p % NSTAGE) + NSTAGE) % NSTAGE; };
+
+  for (int64_t item = blockIdx.x; item < g.items; item += gridDim.x) {
+    int64_t rr = item;
+    const int tx = (int)(rr % g.tiles_x); rr /= g.tiles_x;
+    const int ty = (int)(rr % g.tiles_y); rr /= g.tiles_y;
+    const int zk = (int)(rr % g.zchunks); rr /= g.zchunks;
+    const int64_t n = rr;
+    const int x0 = tx * TXW, y0 = ty * OUTR;
+    const int zs = g.zb + zk * g.zc;
+    const int ze = min(zs + g.zc, g.ze);   // own planes [zs, ze), halo plane ze
+
+    if (n != cur_n) {
+      // flush the CTA histogram of the previous batch item (one int64 atomic per bin)
+      if (cur_n >= 0) {
+        __syncthreads();
+        unsigned long long* h = hist + cur_n * (nb + 1);
+        for (int i = threadIdx.x; i <= nb; i += NT) {
+          const int v = s_hist[i];
+          if (v) { atomicAdd(h + i, (unsigned long long)(long long)v); s_hist[i] = 0; }
+        }
+        __syncthreads();
+      }
+      cur_n = n;
+    }
+
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int k = -1; k <= 1; ++k) {
+        const int p = zs + k;
+        uint64_t* bar = &bars[stage_of(p)];
+        mbar_expect_tx(bar, PLANE_BYTES);
+        tma_load_4d(planes + stage_of(p) * PLANE, &tmap, bar, x0 - 4, y0 - 1, p, (int)n);
+      }
+    }
+    {
+      const int b = stage_of(zs - 1);
+      mbar_wait(&bars[b], (phase >> b) & 1u);
+      phase ^= 1u << b;
+    }
+
+    // per-thread validity (rows / columns of this tile)
+    const int y = y0 - 1 + lane;
+    const bool lane_out = lane >= 1 && lane <= 30 && y < g.H;
+    const bool row_up_ok = (y + 1) < g.H;      // row y+1 exists
+    const bool row_dn_ok = (y - 1) >= 0;       // row y-1 exists
+    const int xs = x0 + SEG * warp;
+    const int nvalid = max(0, min(32, g.W - xs));
+    const uint32_t xmask = nvalid >= 32 ? 0xffffffffu : ((1u << nvalid) - 1u);
+    // dx = +1: bit i needs x+1 < W (bit 31 is compared directly)
+    const uint32_t xm_p1 = (nvalid >= 32 ? 0xffffffffu : ((1u << max(nvalid - 1, 0)) - 1u)) | 0x80000000u;
+    const uint32_t outmask = lane_out ? xmask : 0u;
+
+    uint32_t N1[NNEG];
+#pragma unroll
+    for (int k = 0; k < NNEG; ++k) N1[k] = 0;
+
+    for (int s = zs; s <= ze; ++s) {
+      const int bs = stage_of(s);
+      mbar_wait(&bars[bs], (phase >> bs) & 1u);
+      phase ^= 1u << bs;
+      const float* P0 = planes + bs * PLANE;               // plane s
+      const float* P1 = planes + stage_of(s - 1) * PLANE;  // plane s-1
+
+      // ---- the 13 negative-offset words of plane s ------------------------
+      uint32_t N0[NNEG];
+      {
+        float pc[32];
+        Row A;
+        load_row(A, P0, lane, col0);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) pc[i] = A.v[i] + 0.0f;   // -0 -> +0
+        uint32_t w = 0;
+#pragma unroll
+        for (int i = 31; i >= 0; --i) w = push(w, le_bit(i ? A.v[i - 1] : A.l, pc[i]));
+        N0[NX] = w;
+        load_row(A, P0, rm, col0);
+        words3(A, pc, N0[NYM_XM], N0[NYM_X0], N0[NYM_XP]);
+        load_row(A, P1, rm, col0);
+        words3(A, pc, N0[NZ_YM_XM], N0[NZ_YM_X0], N0[NZ_YM_XP]);
+        load_row(A, P1, lane, col0);
+        words3(A, pc, N0[NZ_Y0_XM], N0[NZ_Y0_X0], N0[NZ_Y0_XP]);
+        load_row(A, P1, rp, col0);
+        words3(A, pc, N0[NZ_YP_XM], N0[NZ_YP_X0], N0[NZ_YP_XP]);
+      }
+
+      if (s > zs) {
+        // ---- finalize plane s-1 ---------------------------------------------
+        const uint32_t FULL = 0xffffffffu;
+        // row y+1 of plane s-1: its (0,-1,dx) words
+        const uint32_t u_m = __shfl_down_sync(FULL, N1[NYM_XM], 1);
+        const uint32_t u_0 = __shfl_down_sync(FULL, N1[NYM_X0], 1);
+        const uint32_t u_p = __shfl_down_sync(FULL, N1[NYM_XP], 1);
+        // plane s rows y-1 / y+1: their (-1,+1,dx) / (-1,-1,dx) words
+        const uint32_t d_m = __shfl_up_sync(FULL, N0[NZ_YP_XM], 1);
+        const uint32_t d_0 = __shfl_up_sync(FULL, N0[NZ_YP_X0], 1);
+        const uint32_t d_p = __shfl_up_sync(FULL, N0[NZ_YP_XP], 1);
+        const uint32_t e_m = __shfl_down_sync(FULL, N0[NZ_YM_XM], 1);
+        const uint32_t e_0 = __shfl_down_sync(FULL, N0[NZ_YM_X0], 1);
+        const uint32_t e_p = __shfl_down_sync(FULL, N0[NZ_YM_XP], 1);
+
+        // edge bits (segment boundary) by direct comparison q < p
+        const float* r1 = P1 + lane * PITCH + col0;   // own row, plane s-1
+        const float p0v = r1[0], p31 = r1[31];
+        const float* r1u = P1 + rp * PITCH + col0;    // row y+1, plane s-1
+        const float* r0d = P0 + rm * PITCH + col0;    // row y-1, plane s
+        const float* r0c = P0 + lane * PITCH + col0;  // row y,   plane s
+        const float* r0u = P0 + rp * PITCH + col0;    // row y+1, plane s
+        const uint32_t E_x = (uint32_t)(r1[32] < p31) << 31;
+        const uint32_t E_yp_xp = (uint32_t)(r1u[32] < p31) << 31;
+        const uint32_t E_yp_xm = (uint32_t)(r1u[-1] < p0v);
+        const uint32_t E_zp_ym_xp = (uint32_t)(r0d[32] < p31) << 31, E_zp_ym_xm = (uint32_t)(r0d[-1] < p0v);
+        const uint32_t E_zp_y0_xp = (uint32_t)(r0c[32] < p31) << 31, E_zp_y0_xm = (uint32_t)(r0c[-1] < p0v);
+        const uint32_t E_zp_yp_xp = (uint32_t)(r0u[32] < p31) << 31, E_zp_yp_xm = (uint32_t)(r0u[-1] < p0v);
+
+        const uint32_t mz = (s < g.D) ? FULL : 0u;             // plane s exists
+        const uint32_t myu = row_up_ok ? FULL : 0u;
+        const uint32_t myd = row_dn_ok ? FULL : 0u;
+
+        // L[dz+1][dy+1][dx+1]
+        uint32_t L[3][3][3];
+        // negative offsets: computed directly (out-of-grid q gave 0)
+        L[1][1][0] = N1[NX];
+        L[1][0][0] = N1[NYM_XM];
+        L[1][0][1] = N1[NYM_X0];
+        L[1][0][2] = N1[NYM_XP];
+        L[0][0][0] = N1[NZ_YM_XM];
+        L[0][0][1] = N1[NZ_YM_X0];
+        L[0][0][2] = N1[NZ_YM_XP];
+        L[0][1][0] = N1[NZ_Y0_XM];
+        L[0][1][1] = N1[NZ_Y0_X0];
+        L[0][1][2] = N1[NZ_Y0_XP];
+        L[0][2][0] = N1[NZ_YP_XM];
+        L[0][2][1] = N1[NZ_YP_X0];
+        L[0][2][2] = N1[NZ_YP_XP];
+        // positive offsets: complement of the neighbour's negative word, moved by dx
+        // (0,0,+1): voxel x+1's (0,0,-1) word
+        L[1][1][2] = (((~N1[NX]) >> 1) & 0x7fffffffu & xm_p1) | E_x;
+        // (0,+1,dx): row y+1's (0,-1,-dx) words
+        L[1][2][1] = (~u_0) & myu;
+        L[1][2][2] = ((((~u_m) >> 1) & 0x7fffffffu & xm_p1) | E_yp_xp) & myu;
+        L[1][2][0] = ((~u_p) << 1 | E_yp_xm) & myu;
+        // (+1,dy,dx): plane s row y+dy's (-1,-dy,-dx) words
+        L[2][0][1] = (~d_0) & myd & mz;
+        L[2][0][2] = ((((~d_m) >> 1) & 0x7fffffffu & xm_p1) | E_zp_ym_xp) & myd & mz;
+        L[2][0][0] = ((~d_p) << 1 | E_zp_ym_xm) & myd & mz;
+        L[2][1][1] = (~N0[NZ_Y0_X0]) & mz;
+        L[2][1][2] = ((((~N0[NZ_Y0_XM]) >> 1) & 0x7fffffffu & xm_p1) | E_zp_y0_xp) & mz;
+        L[2][1][0] = ((~N0[NZ_Y0_XP]) << 1 | E_zp_y0_xm) & mz;
+        L[2][2][1] = (~e_0) & myu & mz;
+        L[2][2][2] = ((((~e_m) >> 1) & 0x7fffffffu & xm_p1) | E_zp_yp_xp) & myu & mz;
+        L[2][2][0] = ((~e_p) << 1 | E_zp_yp_xm) & myu & mz;
+
+        // squares (coefficients.py:119-126) and cubes (128-136) on words
+        uint32_t Sxy[2][2], Szx[2][2], Szy[2][2];
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+          for (int b = 0; b < 2; ++b) {
+            const int A = 2 * a, B = 2 * b;
+            Sxy[a][b] = L[1][A][1] & L[1][1][B] & L[1][A][B];   // (y=a, x=b)
+            Szx[a][b] = L[A][1][1] & L[1][1][B] & L[A][1][B];   // (z=a, x=b)
+          }
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+          for (int b = 0; b < 2; ++b) Szy[a][b] = L[2 * a][1][1] & L[1][2 * b][1] & L[2 * a][2 * b][1];  // (z=a, y=b)
+        uint32_t C[8];
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+          for (int b = 0; b < 2; ++b)
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+              C[4 * a + 2 * b + c] = Szy[a][b] & Szx[a][c] & Sxy[b][c] & L[2 * a][2 * b][2 * c];
+
+        // c + 13 = sum of 26 bits: ~E (6), S (12), ~C (8); carry-save adder tree
+        uint32_t in[26];
+        in[0] = ~L[1][1][0]; in[1] = ~L[1][1][2]; in[2] = ~L[1][0][1];
+        in[3] = ~L[1][2][1]; in[4] = ~L[0][1][1]; in[5] = ~L[2][1][1];
+        in[6] = Sxy[0][0]; in[7] = Sxy[0][1]; in[8] = Sxy[1][0]; in[9] = Sxy[1][1];
+        in[10] = Szx[0][0]; in[11] = Szx[0][1]; in[12] = Szx[1][0]; in[13] = Szx[1][1];
+        in[14] = Szy[0][0]; in[15] = Szy[0][1]; in[16] = Szy[1][0]; in[17] = Szy[1][1];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) in[18 + k] = ~C[k];
+        // weight 1: 26 -> ...
+        uint32_t s1[9], c2[9];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) fa(in[3 * k], in[3 * k + 1], in[3 * k + 2], s1[k], c2[k]);
+        // s1[0..7], in[24], in[25] at weight 1 (10 bits)
+        uint32_t t1a, t1b, t1c, k2a, k2b, k2c;
+        fa(s1[0], s1[1], s1[2], t1a, k2a);
+        fa(s1[3], s1[4], s1[5], t1b, k2b);
+        fa(s1[6], s1[7], in[24], t1c, k2c);
+        uint32_t t1d, k2d;
+        fa(t1a, t1b, t1c, t1d, k2d);
+        // weight 1 left: t1d, in[25]
+        const uint32_t b0 = t1d ^ in[25];
+        const uint32_t k2e = t1d & in[25];
+        // weight 2: c2[0..7], k2a..k2e (13 bits)
+        uint32_t u2[4], c4[4];
+        fa(c2[0], c2[1], c2[2], u2[0], c4[0]);
+        fa(c2[3], c2[4], c2[5], u2[1], c4[1]);
+        fa(c2[6], c2[7], k2a, u2[2], c4[2]);
+        fa(k2b, k2c, k2d, u2[3], c4[3]);
+        // weight 2 left: u2[0..3], k2e (5)
+        uint32_t v2a, c4e, v2b, c4f;
+        fa(u2[0], u2[1], u2[2], v2a, c4e);
+        fa(u2[3], k2e, v2a, v2b, c4f);
+        const uint32_t b1 = v2b;
+        // weight 4: c4[0..3], c4e, c4f (6)
+        uint32_t w4a, c8a, w4b, c8b;
+        fa(c4[0], c4[1], c4[2], w4a, c8a);
+        fa(c4[3], c4e, c4f, w4b, c8b);
+        const uint32_t b2 = w4a ^ w4b;
+        const uint32_t c8c = w4a & w4b;
+        // weight 8: c8a, c8b, c8c -> bit 3 and bit 4
+        uint32_t b3, b4;
+        fa(c8a, c8b, c8c, b3, b4);
+        // sum in [8, 20]: c + 5 = sum - 8 has planes (b4, b2, b1, b0)  (b3 = !b4)
+        const uint32_t v0 = b0, v1 = b1, v2 = b2, v3 = b4;
+        // c != 0  <=>  c + 5 != 0101b
+        const uint32_t nz = ~(v0 & ~v1 & v2 & ~v3) & outmask;
+
+        // ---- per voxel: bin + shared-memory atomic -------------------------
+        if (nz) {
+          const float4* r14 = reinterpret_cast<const float4*>(r1);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const float4 xv4 = r14[k];
+            const float xs4[4] = {xv4.x, xv4.y, xv4.z, xv4.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int i = 4 * k + j;
+              if ((nz >> i) & 1u) {
+                const int cc = (int)(((v0 >> i) & 1u) | (((v1 >> i) & 1u) << 1) | (((v2 >> i) & 1u) << 2) |
+                                     (((v3 >> i) & 1u) << 3)) - 5;
+                const float xv = xs4[j];
+                int bin;
+                if (lut_ok) {
+                  const float gg = __saturatef(__fmul_rn(__fsub_rn(xv, lut_lo), lut_scale));
+                  const int cell = __float2int_rz(__fmul_rn(gg, cellsf));
+                  const LutEntry e = s_lut[cell];
+                  bin = e.b + (xv > e.t ? 1 : 0);
+                } else {
+                  int lo = 0, hi = nb;
+                  while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (s_tab[mid + 1] < xv) lo = mid + 1; else hi = mid;
+                  }
+                  bin = lo;
+                }
+                atomicAdd(&s_hist[bin], cc);
+              }
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < NNEG; ++k) N1[k] = N0[k];
+
+      __syncthreads();   // everyone is done with plane s-1's buffer
+      if (threadIdx.x == 0 && s + 2 <= ze) {
+        const int p = s + 2;
+        uint64_t* bar = &bars[stage_of(p)];
+        mbar_expect_tx(bar, PLANE_BYTES);
+        tma_load_4d(planes + stage_of(p) * PLANE, &tmap, bar, x0 - 4, y0 - 1, p, (int)n);
+      }
+    }
+  }
+  __syncthreads();
+  if (cur_n >= 0) {
+    unsigned long long* h = hist + cur_n * (nb + 1);
+    for (int i = threadIdx.x; i <= nb; i += NT) {
+      const int v = s_hist[i];
+      if (v) atomicAdd(h + i, (unsigned long long)(long long)v);
+    }
+  }
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+static int num_sms_fast() {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms > 0 ? sms : 148;
+}
+
+}  // namespace fast
+
+// Eligibility: float32, 16-byte aligned base and row pitch, extents that fit int.
+bool fast3d_eligible(const void* x, int64_t D, int64_t H, int64_t W, int64_t batch, int64_t nb) {
+  if (((uintptr_t)x & 15u) != 0) return false;
+  if (W % 4 != 0) return false;
+  if (W > (1 << 30) || H > (1 << 30) || D > (1 << 30) || batch > (1 << 30)) return false;
+  if (nb > 16384) return false;
+  return fast::encode_fn() != nullptr;
+}
+
+int fast3d_launch(const float* x, int64_t D, int64_t H, int64_t W, int64_t batch, int64_t zb, int64_t ze,
+                  const void* table, const ecc_binning* b, unsigned long long* hist, cudaStream_t stream) {
+  using namespace fast;
+  CUtensorMap map;
+  const cuuint64_t gdim[4] = {(cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)D, (cuuint64_t)batch};
+  const cuuint64_t gstride[3] = {(cuuint64_t)W * 4, (cuuint64_t)(W * H) * 4, (cuuint64_t)(W * H * D) * 4};
+  const cuuint32_t box[4] = {PITCH, 32, 1, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(x), gdim, gstride, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NAN_REQUEST_ZERO_FMA);
+  if (r != CUDA_SUCCESS) return set_error(ECC_ECUDA, "cuTensorMapEncodeTiled failed");
+  const int nb = (int)b->nbins;
+  const int cells = b->lut_ok ? b->lut_cells : 0;
+  const size_t smem = (size_t)NSTAGE * PLANE_BYTES + NSTAGE * 8 + (size_t)((nb + 1 + 3) & ~3) * 4 +
+                      (size_t)((nb + 2 + 3) & ~3) * 4 + (size_t)(cells + 1) * sizeof(LutEntry);
+  cudaError_t e = cudaFuncSetAttribute(ecc_fast3d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(fast3d)");
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ecc_fast3d_kernel, NT, smem);
+  if (occ < 1) return set_error(ECC_EINVAL, "fast3d kernel does not fit on an SM");
+  const int64_t max_ctas = (int64_t)num_sms_fast() * occ;
+
+  Geom g;
+  g.W = (int)W;
+  g.H = (int)H;
+  g.D = (int)D;
+  g.zb = (int)zb;
+  g.ze = (int)ze;
+  g.tiles_x = (int)((W + TXW - 1) / TXW);
+  g.tiles_y = (int)((H + OUTR - 1) / OUTR);
+  const int64_t tiles = (int64_t)g.tiles_x * g.tiles_y * batch;
+  const int64_t Dw = ze - zb;
+  // z-chunk: long enough to amortise the halo plane, short enough for >= ~6
+  // items per CTA so the persistent grid balances
+  int64_t zc = 64;
+  while (zc > 8 && tiles * ((Dw + zc - 1) / zc) < 6 * max_ctas) zc >>= 1;
+  if (zc > Dw) zc = Dw;
+  if (zc < 1) zc = 1;
+  g.zc = (int)zc;
+  g.zchunks = (int)((Dw + zc - 1) / zc);
+  g.items = tiles * g.zchunks;
+  const int64_t grid = g.items < max_ctas ? g.items : max_ctas;
+  if (grid < 1) return ECC_OK;
+  ecc_fast3d_kernel<<<(unsigned)grid, NT, smem, stream>>>(map, g, table, nb, cells, b->lut_lo, b->lut_scale,
+                                                            b->lut_ok, hist);
+  return check_launch("ecc_fast3d_kernel");
+}
+
+}  // namespace ecc

@@ -6,6 +6,7 @@
 
 #include <cmath>
 #include <limits>
+#include <vector>
 
 #include "ecc_common.cuh"
 #include "ecc_internal.h"
@@ -85,6 +86,84 @@ static void certify(const V* tab, int64_t nb, ecc_binning* b) {
   b->mode = worst <= 4 ? 0 : 1;
 }
 
+// ---- cell table of the float32 fast path (see ecc_binning in ecc_b200.h) ----
+struct LutEntryH {
+  float t;
+  int32_t b;
+};
+
+// the device's cell computation, operation for operation (no contraction)
+static int cell_of(float x, float lo, float scale, float cellsf) {
+  volatile float d = x - lo;
+  volatile float g = d * scale;
+  float gs = g;
+  if (!(gs > 0.0f)) gs = 0.0f;  // __saturatef: NaN -> 0
+  if (gs > 1.0f) gs = 1.0f;
+  volatile float m = gs * cellsf;
+  return (int)(float)m;  // __float2int_rz
+}
+
+static uint32_t fkey(float f) {
+  uint32_t b;
+  memcpy(&b, &f, 4);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+static float keyf(uint32_t k) {
+  uint32_t b = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
+  float f;
+  memcpy(&f, &b, 4);
+  return f;
+}
+
+static int64_t bin32(float x, const float* t32, int64_t nb) {
+  int64_t lo = 0, hi = nb;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (t32[mid] < x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// Build the cell table for thresholds t32 (non-decreasing); returns cells or 0.
+static int build_lut(const float* t32, int64_t nb, int cells, float* lo_out, float* scale_out, LutEntryH* lut) {
+  if (nb < 2) return 0;
+  const float lo = t32[0], hi = t32[nb - 1];
+  if (!std::isfinite(lo) || !std::isfinite(hi) || !(hi > lo)) return 0;
+  volatile float span = hi - lo;
+  if (!std::isfinite((float)span)) return 0;
+  volatile float scale = 1.0f / span;
+  if (!std::isfinite((float)scale) || !(scale > 0.0f)) return 0;
+  const float cellsf = (float)cells;
+  const uint32_t kmin = fkey(-std::numeric_limits<float>::max());
+  const uint32_t kmax = fkey(std::numeric_limits<float>::max());
+  // first key with cell >= k, for k = 0..cells+1
+  std::vector<uint32_t> first((size_t)cells + 2);
+  for (int k = 0; k <= cells + 1; ++k) {
+    uint32_t a = kmin, b = kmax + 1;  // search in [a, b)
+    while (a < b) {
+      uint32_t mid = a + (b - a) / 2;
+      if (cell_of(keyf(mid), lo, scale, cellsf) >= k) b = mid; else a = mid + 1;
+    }
+    first[k] = a;  // == kmax + 1 if no finite float reaches cell k
+  }
+  for (int k = 0; k <= cells; ++k) {
+    if (first[k] >= first[k + 1]) {  // empty cell: never indexed
+      lut[k].t = std::numeric_limits<float>::infinity();
+      lut[k].b = (int32_t)nb;
+      continue;
+    }
+    const float xlo = keyf(first[k]);
+    const float xhi = keyf(first[k + 1] - 1);
+    const int64_t b = bin32(xlo, t32, nb);
+    if (bin32(xhi, t32, nb) > b + 1) return 0;  // two thresholds inside one cell
+    lut[k].b = (int32_t)b;
+    lut[k].t = b < nb ? t32[b] : std::numeric_limits<float>::infinity();
+  }
+  *lo_out = lo;
+  *scale_out = scale;
+  return cells;
+}
+
 __global__ void counter_grid_kernel(uint64_t seed, int64_t start, int64_t count, float* out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -121,12 +200,28 @@ extern "C" int ecc_threshold_table(const double* taus, int64_t nb, int dtype, vo
   for (int64_t j = 1; j < nb; ++j)
     if (!(taus[j] > taus[j - 1])) return set_error(ECC_EINVAL, "thresholds must be strictly increasing");
   b->nbins = nb;
+  b->lut_ok = 0;
+  b->lut_cells = 0;
+  b->lut_lo = 0.0f;
+  b->lut_scale = 0.0f;
   if (dtype == ECC_DTYPE_U8 || dtype == ECC_DTYPE_F32) {
     float* t = (float*)table_host;
     t[0] = -std::numeric_limits<float>::infinity();
     for (int64_t j = 0; j < nb; ++j) t[j + 1] = round_down_f32(taus[j]);
     t[nb + 1] = std::numeric_limits<float>::infinity();
     certify<float>(t, nb, b);
+    LutEntryH* lut = reinterpret_cast<LutEntryH*>(t + ((nb + 2 + 1) & ~int64_t(1)));
+    for (int mult = 2; mult <= 4 && !b->lut_ok; mult *= 2) {
+      const int64_t cells = mult * nb;
+      if (cells > (1 << 16)) break;
+      float lo = 0.f, sc = 0.f;
+      if (build_lut(t + 1, nb, (int)cells, &lo, &sc, lut)) {
+        b->lut_ok = 1;
+        b->lut_cells = (int32_t)cells;
+        b->lut_lo = lo;
+        b->lut_scale = sc;
+      }
+    }
   } else if (dtype == ECC_DTYPE_F64) {
     double* t = (double*)table_host;
     t[0] = -std::numeric_limits<double>::infinity();
@@ -147,4 +242,11 @@ extern "C" int ecc_counter_grid(uint64_t seed, int64_t start, int64_t count, flo
   if (blocks > 148 * 16) blocks = 148 * 16;
   counter_grid_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(seed, start, count, out);
   return check_launch("counter_grid_kernel");
+}
+
+extern "C" size_t ecc_threshold_table_bytes(int64_t nb, int dtype) {
+  if (nb < 1) return 0;
+  if (dtype == ECC_DTYPE_F64) return sizeof(double) * (size_t)(nb + 2);
+  const int64_t cells = 4 * nb <= (1 << 16) ? 4 * nb : (1 << 16);
+  return sizeof(float) * (size_t)((nb + 2 + 1) & ~int64_t(1)) + sizeof(LutEntryH) * (size_t)(cells + 1);
 }

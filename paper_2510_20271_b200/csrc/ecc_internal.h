@@ -12,4 +12,8 @@ inline int check_launch(const char* what) {
   if (e != cudaSuccess) return set_cuda_error(e, what);
   return ECC_OK;
 }
+// float32 fast path (ecc_fast3d.cu)
+bool fast3d_eligible(const void* x, int64_t D, int64_t H, int64_t W, int64_t batch, int64_t nb);
+int fast3d_launch(const float* x, int64_t D, int64_t H, int64_t W, int64_t batch, int64_t zb, int64_t ze,
+                  const void* table, const ecc_binning* b, unsigned long long* hist, cudaStream_t stream);
 }  // namespace ecc

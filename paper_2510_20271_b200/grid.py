@@ -165,7 +165,10 @@ class ThresholdSet:
         hit = self._tables.get(key)
         if hit is None:
             nb = self.taus.size
-            host = np.empty(nb + 2, dtype=np.float64 if dtype_code == _lib.DTYPE_F64 else np.float32)
+            nbytes = int(_lib.lib().ecc_threshold_table_bytes(nb, dtype_code))
+            host = np.zeros(nbytes // 4 + 1, dtype=np.float32)
+            if dtype_code == _lib.DTYPE_F64:
+                host = np.zeros(nbytes // 8 + 1, dtype=np.float64)
             b = _lib.Binning()
             taus = np.ascontiguousarray(self.taus)
             _lib.check(_lib.lib().ecc_threshold_table(_lib.ptr(taus), nb, dtype_code, _lib.ptr(host),

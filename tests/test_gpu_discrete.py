@@ -209,3 +209,104 @@ class TestBatchedAndValidation:
         ts = E.thresholds_from_range(lo, hi, 256)
         got = E.ecc_discrete(t, ts).cpu().numpy()
         assert np.array_equal(got, oracle.curve(x.astype(np.float64), ts.taus))
+
+
+class TestFastPath:
+    """The bit-sliced TMA kernel (float32, W % 4 == 0) against the oracle and
+    against the generic sweep, on shapes that hit every tile/segment edge."""
+
+    SHAPES = [(1, 4, 4), (3, 5, 8), (7, 31, 32), (9, 30, 36), (5, 61, 100), (33, 33, 128), (2, 64, 132),
+              (17, 90, 260), (64, 31, 4), (1, 1, 64), (40, 1, 40), (65, 47, 68)]
+
+    @staticmethod
+    def _both(t, ts, **kw):
+        import os
+
+        fast = E.histogram_device(t, ts, **kw).cpu().numpy()
+        os.environ["ECC_B200_GENERIC"] = "1"
+        try:
+            gen = E.histogram_device(t, ts, **kw).cpu().numpy()
+        finally:
+            del os.environ["ECC_B200_GENERIC"]
+        return fast, gen
+
+    def test_random_volumes(self, rng):
+        for dims in self.SHAPES:
+            x = rng.random(dims).astype(np.float32)
+            t = torch.from_numpy(x).cuda()
+            for nb in (1, 7, 256, 1024):
+                lo, hi = float(x.min()), float(x.max())
+                ts = E.thresholds_from_range(lo, hi, nb)
+                fast, gen = self._both(t, ts)
+                want = np.append(*oracle.histogram(x, ts.taus))
+                assert np.array_equal(fast[0], want), (dims, nb)
+                assert np.array_equal(gen[0], want), (dims, nb)
+
+    def test_ties_signed_zeros_subnormals(self, rng):
+        specials = np.array([0.0, -0.0, 1e-45, -1e-45, 1.17549435e-38, -1.4e-45, 3.4e38, -3.4e38, 1.0, -1.0, 0.5],
+                            dtype=np.float32)
+        for dims in [(6, 9, 12), (11, 40, 36), (4, 33, 64)]:
+            for pool in (specials, np.array([0.0, 1.0, 2.0], np.float32)):
+                x = rng.choice(pool, size=dims).astype(np.float32)
+                t = torch.from_numpy(x).cuda()
+                taus = np.unique(x.astype(np.float64))
+                ts = E.ThresholdSet(taus)
+                fast, _ = self._both(t, ts)
+                want = np.append(*oracle.histogram(x, taus))
+                assert np.array_equal(fast[0], want), dims
+                c = np.cumsum(want[:-1])
+                assert c[-1] == 1
+
+    def test_hostile_thresholds_binary_search_path(self, rng):
+        x = (rng.normal(0, 3, (9, 20, 24))).astype(np.float32)
+        t = torch.from_numpy(x).cuda()
+        for taus in (np.unique(rng.normal(0, 2, 300)), np.array([-1e300, 0.0, 1e300]),
+                     np.array([-1.0, -1e-45, 0.0, 1e-45, 0.5])):
+            ts = E.ThresholdSet(taus)
+            fast, gen = self._both(t, ts)
+            want = np.append(*oracle.histogram(x, taus))
+            assert np.array_equal(fast[0], want) and np.array_equal(gen[0], want)
+
+    def test_batched(self, rng):
+        xs = rng.random((3, 10, 37, 44)).astype(np.float32)
+        ts = E.ThresholdSet(np.linspace(0.01, 0.99, 129))
+        h = E.histogram_device(torch.from_numpy(xs).cuda(), ts, ndim=3).cpu().numpy()
+        for i in range(3):
+            assert np.array_equal(h[i], np.append(*oracle.histogram(xs[i], ts.taus)))
+
+    def test_plane_range_slabs(self, rng):
+        """ecc_histogram_range: slabs with halos sum to the whole volume (C5 path)."""
+        from paper_2510_20271_b200 import _lib
+
+        D, H, W = 23, 35, 72
+        x = rng.random((D, H, W)).astype(np.float32)
+        ts = E.ThresholdSet(np.linspace(0.0, 1.0, 65)[1:])
+        t = torch.from_numpy(x).cuda()
+        table, binning = ts.device_table(_lib.DTYPE_F32, t.device)
+        total = np.zeros(65, np.int64)
+        for z0, z1 in [(0, 7), (7, 8), (8, 16), (16, 23)]:
+            lo, hi = max(0, z0 - 1), min(D, z1 + 1)
+            view = t[lo:hi]
+            hist = torch.empty(65, dtype=torch.int64, device="cuda")
+            d = _lib.dims_arg(view.shape)
+            _lib.check(_lib.lib().ecc_histogram_range(_lib.ptr(view), _lib.DTYPE_F32, 3, _lib.ptr(d), 1, z0 - lo,
+                                                      z1 - lo, _lib.ptr(table), _lib.ctypes.byref(binning),
+                                                      _lib.ptr(hist), _lib.stream_ptr(view)))
+            total += hist.cpu().numpy()
+        assert np.array_equal(total, np.append(*oracle.histogram(x, ts.taus)))
+
+    def test_large_volume_invariants(self):
+        """256^3 counter grid: bit-exact vs oracle, sum c = 1, tail = 1."""
+        dims = (256, 256, 256)
+        from paper_2510_20271_b200 import _lib
+
+        t = torch.empty(dims, dtype=torch.float32, device="cuda")
+        _lib.check(_lib.lib().ecc_counter_grid(9, 0, t.numel(), _lib.ptr(t), _lib.stream_ptr(t)))
+        x = t.cpu().numpy()
+        assert np.array_equal(x.ravel(), oracle.counter_grid(9, dims))
+        lo, hi, _ = E.device_minmax(t)
+        ts = E.thresholds_from_range(lo, hi, 1024)
+        curve, hist = E.ecc_discrete(t, ts, return_hist=True)
+        h = hist.cpu().numpy()
+        assert int(h.sum()) == 1 and int(curve[-1]) == 1
+        assert np.array_equal(h, np.append(*oracle.histogram(x, ts.taus)))
