@@ -48,11 +48,12 @@ typedef struct {
   int64_t nbins;  /* B                                                       */
   int32_t mode;   /* 0 affine guess + exact correction, 1 binary search      */
   int32_t max_correction; /* largest guess error seen at the breakpoints    */
-  /* cell table of the float32 fast path: cell(x) = trunc(sat((x - lut_lo) *
-   * lut_scale) * lut_cells); every cell holds at most one threshold, so
-   * bin(x) = b[cell] + (x > t[cell]) exactly (verified at build time). */
-  float lut_lo;
+  /* cell table of the float32 fast path: cell(x) = floor(sat(fma(x,
+   * lut_scale, lut_bias)) * lut_cells), lut_cells a power of two; every
+   * cell holds at most one threshold, so bin(x) = b[cell] + (x > t[cell])
+   * exactly (verified for every float32 when the table is built). */
   float lut_scale;
+  float lut_bias;
   int32_t lut_cells;
   int32_t lut_ok;
 } ecc_binning;

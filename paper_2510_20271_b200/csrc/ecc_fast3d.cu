@@ -143,35 +143,62 @@ enum { NX = 0, NYM_XM, NYM_X0, NYM_XP, NZ_YM_XM, NZ_YM_X0, NZ_YM_XP, NZ_Y0_XM, N
        NZ_YP_XP, NNEG };
 
 // ---------------------------------------------------------------- the kernel
+__device__ __forceinline__ void lds_entry(uint32_t addr, float& t, uint32_t& b) {
+  asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=f"(t), "=r"(b) : "r"(addr));
+}
+__device__ __forceinline__ float f4get(const float4& v, int j) {
+  return j == 0 ? v.x : (j == 1 ? v.y : (j == 2 ? v.z : v.w));
+}
+__device__ __forceinline__ void red_add_shared(uint32_t addr, int v) {
+  asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
+// word of 32 "q <= p" bits, two independent 16-step chains
+template <typename QF>
+__device__ __forceinline__ uint32_t word1(QF q, const float (&pc)[32]) {
+  uint32_t lo = 0, hi = 0;
+#pragma unroll
+  for (int i = 15; i >= 0; --i) {
+    hi = push(hi, le_bit(q(i + 16), pc[i + 16]));
+    lo = push(lo, le_bit(q(i), pc[i]));
+  }
+  return (hi << 16) | lo;
+}
+
 __global__ void __launch_bounds__(NT, 3)
 ecc_fast3d_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* __restrict__ table_g, int nb,
-                  int cells, float lut_lo, float lut_scale, int lut_ok, unsigned long long* __restrict__ hist) {
+                  int cells, int cell_shift, float lut_scale, float lut_bias, int lut_ok,
+                  unsigned long long* __restrict__ hist) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* planes = reinterpret_cast<float*>(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + (size_t)NSTAGE * PLANE_BYTES);
-  int* s_hist = reinterpret_cast<int*>(bars + NSTAGE);
-  float* s_tab = reinterpret_cast<float*>(s_hist + ((nb + 1 + 3) & ~3));        // nb+2 (sentinels)
-  LutEntry* s_lut = reinterpret_cast<LutEntry*>(s_tab + ((nb + 2 + 3) & ~3));   // cells+1
+  LutEntry* s_lut = reinterpret_cast<LutEntry*>(bars + 4);                      // cells+1 (lut_ok)
+  int* s_hist = reinterpret_cast<int*>(s_lut + (lut_ok ? cells + 1 : 0));       // nb+1
+  float* s_tab = reinterpret_cast<float*>(s_hist + ((nb + 1 + 3) & ~3));        // nb+2 (!lut_ok)
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const float* tab_g = reinterpret_cast<const float*>(table_g);
   const LutEntry* lut_g = reinterpret_cast<const LutEntry*>(tab_g + ((nb + 2 + 1) & ~1));
   for (int i = threadIdx.x; i <= nb; i += NT) s_hist[i] = 0;
-  for (int i = threadIdx.x; i < nb + 2; i += NT) s_tab[i] = tab_g[i];
-  if (lut_ok)
+  if (lut_ok) {
     for (int i = threadIdx.x; i <= cells; i += NT) s_lut[i] = lut_g[i];
+  } else {
+    for (int i = threadIdx.x; i < nb + 2; i += NT) s_tab[i] = tab_g[i];
+  }
   if (threadIdx.x == 0) {
     for (int b = 0; b < NSTAGE; ++b) mbar_init(&bars[b], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
   }
   __syncthreads();
+  // lut biased so that the cell index is (bits(RZ(g + 1)) >> shift):
+  // bits(1 + g) = 0x3F800000 + floor(g 2^23), and 0x3F800000 >> shift = 127 cells
+  const LutEntry* lut_b = s_lut - 127 * cells;
 
   uint32_t phase = 0;           // parity bit per stage
   int64_t cur_n = -1;
   const int col0 = 4 + SEG * warp;
   const int rm = lane > 0 ? lane - 1 : 0, rp = lane < 31 ? lane + 1 : 31;
-  const float cellsf = (float)cells;
 
   auto stage_of = [](int p) { return ((p % NSTAGE) + NSTAGE) % NSTAGE; };
 
@@ -237,25 +264,22 @@ ecc_fast3d_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* 
       const float* P0 = planes + bs * PLANE;               // plane s
       const float* P1 = planes + stage_of(s - 1) * PLANE;  // plane s-1
 
-      // ---- the 13 negative-offset words of plane s ------------------------
+      // ---- the 13 negative-offset words of plane s (rows double-buffered) ----
       uint32_t N0[NNEG];
       {
         float pc[32];
-        Row A;
+        Row A, B;
         load_row(A, P0, lane, col0);
+        load_row(B, P0, rm, col0);
 #pragma unroll
         for (int i = 0; i < 32; ++i) pc[i] = A.v[i] + 0.0f;   // -0 -> +0
-        uint32_t w = 0;
-#pragma unroll
-        for (int i = 31; i >= 0; --i) w = push(w, le_bit(i ? A.v[i - 1] : A.l, pc[i]));
-        N0[NX] = w;
-        load_row(A, P0, rm, col0);
-        words3(A, pc, N0[NYM_XM], N0[NYM_X0], N0[NYM_XP]);
+        N0[NX] = word1([&](int i) { return i ? A.v[i - 1] : A.l; }, pc);
         load_row(A, P1, rm, col0);
+        words3(B, pc, N0[NYM_XM], N0[NYM_X0], N0[NYM_XP]);
+        load_row(B, P1, lane, col0);
         words3(A, pc, N0[NZ_YM_XM], N0[NZ_YM_X0], N0[NZ_YM_XP]);
-        load_row(A, P1, lane, col0);
-        words3(A, pc, N0[NZ_Y0_XM], N0[NZ_Y0_X0], N0[NZ_Y0_XP]);
         load_row(A, P1, rp, col0);
+        words3(B, pc, N0[NZ_Y0_XM], N0[NZ_Y0_X0], N0[NZ_Y0_XP]);
         words3(A, pc, N0[NZ_YP_XM], N0[NZ_YP_X0], N0[NZ_YP_XP]);
       }
 
@@ -309,13 +333,10 @@ ecc_fast3d_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* 
         L[0][2][1] = N1[NZ_YP_X0];
         L[0][2][2] = N1[NZ_YP_XP];
         // positive offsets: complement of the neighbour's negative word, moved by dx
-        // (0,0,+1): voxel x+1's (0,0,-1) word
         L[1][1][2] = (((~N1[NX]) >> 1) & 0x7fffffffu & xm_p1) | E_x;
-        // (0,+1,dx): row y+1's (0,-1,-dx) words
         L[1][2][1] = (~u_0) & myu;
         L[1][2][2] = ((((~u_m) >> 1) & 0x7fffffffu & xm_p1) | E_yp_xp) & myu;
         L[1][2][0] = ((~u_p) << 1 | E_yp_xm) & myu;
-        // (+1,dy,dx): plane s row y+dy's (-1,-dy,-dx) words
         L[2][0][1] = (~d_0) & myd & mz;
         L[2][0][2] = ((((~d_m) >> 1) & 0x7fffffffu & xm_p1) | E_zp_ym_xp) & myd & mz;
         L[2][0][0] = ((~d_p) << 1 | E_zp_ym_xm) & myd & mz;
@@ -332,14 +353,10 @@ ecc_fast3d_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* 
         for (int a = 0; a < 2; ++a)
 #pragma unroll
           for (int b = 0; b < 2; ++b) {
-            const int A = 2 * a, B = 2 * b;
-            Sxy[a][b] = L[1][A][1] & L[1][1][B] & L[1][A][B];   // (y=a, x=b)
-            Szx[a][b] = L[A][1][1] & L[1][1][B] & L[A][1][B];   // (z=a, x=b)
+            Sxy[a][b] = L[1][2 * a][1] & L[1][1][2 * b] & L[1][2 * a][2 * b];   // (y=a, x=b)
+            Szx[a][b] = L[2 * a][1][1] & L[1][1][2 * b] & L[2 * a][1][2 * b];   // (z=a, x=b)
+            Szy[a][b] = L[2 * a][1][1] & L[1][2 * b][1] & L[2 * a][2 * b][1];   // (z=a, y=b)
           }
-#pragma unroll
-        for (int a = 0; a < 2; ++a)
-#pragma unroll
-          for (int b = 0; b < 2; ++b) Szy[a][b] = L[2 * a][1][1] & L[1][2 * b][1] & L[2 * a][2 * b][1];  // (z=a, y=b)
         uint32_t C[8];
 #pragma unroll
         for (int a = 0; a < 2; ++a)
@@ -358,74 +375,94 @@ ecc_fast3d_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* 
         in[14] = Szy[0][0]; in[15] = Szy[0][1]; in[16] = Szy[1][0]; in[17] = Szy[1][1];
 #pragma unroll
         for (int k = 0; k < 8; ++k) in[18 + k] = ~C[k];
-        // weight 1: 26 -> ...
-        uint32_t s1[9], c2[9];
+        uint32_t s1[8], c2[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) fa(in[3 * k], in[3 * k + 1], in[3 * k + 2], s1[k], c2[k]);
-        // s1[0..7], in[24], in[25] at weight 1 (10 bits)
         uint32_t t1a, t1b, t1c, k2a, k2b, k2c;
         fa(s1[0], s1[1], s1[2], t1a, k2a);
         fa(s1[3], s1[4], s1[5], t1b, k2b);
         fa(s1[6], s1[7], in[24], t1c, k2c);
         uint32_t t1d, k2d;
         fa(t1a, t1b, t1c, t1d, k2d);
-        // weight 1 left: t1d, in[25]
         const uint32_t b0 = t1d ^ in[25];
         const uint32_t k2e = t1d & in[25];
-        // weight 2: c2[0..7], k2a..k2e (13 bits)
         uint32_t u2[4], c4[4];
         fa(c2[0], c2[1], c2[2], u2[0], c4[0]);
         fa(c2[3], c2[4], c2[5], u2[1], c4[1]);
         fa(c2[6], c2[7], k2a, u2[2], c4[2]);
         fa(k2b, k2c, k2d, u2[3], c4[3]);
-        // weight 2 left: u2[0..3], k2e (5)
         uint32_t v2a, c4e, v2b, c4f;
         fa(u2[0], u2[1], u2[2], v2a, c4e);
         fa(u2[3], k2e, v2a, v2b, c4f);
         const uint32_t b1 = v2b;
-        // weight 4: c4[0..3], c4e, c4f (6)
         uint32_t w4a, c8a, w4b, c8b;
         fa(c4[0], c4[1], c4[2], w4a, c8a);
         fa(c4[3], c4e, c4f, w4b, c8b);
         const uint32_t b2 = w4a ^ w4b;
         const uint32_t c8c = w4a & w4b;
-        // weight 8: c8a, c8b, c8c -> bit 3 and bit 4
         uint32_t b3, b4;
         fa(c8a, c8b, c8c, b3, b4);
-        // sum in [8, 20]: c + 5 = sum - 8 has planes (b4, b2, b1, b0)  (b3 = !b4)
-        const uint32_t v0 = b0, v1 = b1, v2 = b2, v3 = b4;
-        // c != 0  <=>  c + 5 != 0101b
-        const uint32_t nz = ~(v0 & ~v1 & v2 & ~v3) & outmask;
+        (void)b4;
+        // c = sum - 13 as 4-bit two's complement: (sum + 3) mod 16 (c in [-5, 7]);
+        // voxels outside the tile's output get c = 0
+        const uint32_t r0 = ~b0 & outmask;
+        const uint32_t r1b = ~(b1 ^ b0) & outmask;
+        const uint32_t cy1 = b1 | b0;
+        const uint32_t r2 = (b2 ^ cy1) & outmask;
+        const uint32_t r3 = (b3 ^ (b2 & cy1)) & outmask;
 
-        // ---- per voxel: bin + shared-memory atomic -------------------------
-        if (nz) {
+        // ---- bit-planes -> nibbles: Q[k] nibble j = c of voxel 8k + j --------
+        uint32_t Q[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t sel = (uint32_t)k | ((uint32_t)(4 + k) << 4);
+          uint32_t gq = __byte_perm(__byte_perm(r0, r2, sel), __byte_perm(r1b, r3, sel), 0x5410);
+          uint32_t t = ((gq >> 12) ^ gq) & 0x0000F0F0u;
+          gq ^= t ^ (t << 12);
+          t = ((gq >> 6) ^ gq) & 0x00CC00CCu;
+          gq ^= t ^ (t << 6);
+          t = ((gq >> 3) ^ gq) & 0x0A0A0A0Au;
+          gq ^= t ^ (t << 3);
+          Q[k] = gq;
+        }
+
+        // ---- per voxel: bin (cell table) + shared-memory reduction ----------
+        if (__any_sync(FULL, (r0 | r1b | r2 | r3) != 0u)) {
           const float4* r14 = reinterpret_cast<const float4*>(r1);
+          if (lut_ok) {
+            // 8 voxels at a time: cells, table entries, then the reductions
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const float4 xv4 = r14[k];
-            const float xs4[4] = {xv4.x, xv4.y, xv4.z, xv4.w};
+            for (int h = 0; h < 4; ++h) {
+              const float4 xa = r14[2 * h], xb = r14[2 * h + 1];
+              const float xv[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+              uint32_t cell[8];
+              LutEntry e[8];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const int i = 4 * k + j;
-              if ((nz >> i) & 1u) {
-                const int cc = (int)(((v0 >> i) & 1u) | (((v1 >> i) & 1u) << 1) | (((v2 >> i) & 1u) << 2) |
-                                     (((v3 >> i) & 1u) << 3)) - 5;
-                const float xv = xs4[j];
-                int bin;
-                if (lut_ok) {
-                  const float gg = __saturatef(__fmul_rn(__fsub_rn(xv, lut_lo), lut_scale));
-                  const int cell = __float2int_rz(__fmul_rn(gg, cellsf));
-                  const LutEntry e = s_lut[cell];
-                  bin = e.b + (xv > e.t ? 1 : 0);
-                } else {
-                  int lo = 0, hi = nb;
-                  while (lo < hi) {
-                    const int mid = (lo + hi) >> 1;
-                    if (s_tab[mid + 1] < xv) lo = mid + 1; else hi = mid;
-                  }
-                  bin = lo;
+              for (int j = 0; j < 8; ++j) {
+                const float gg = __saturatef(__fmaf_rn(xv[j], lut_scale, lut_bias));
+                cell[j] = __float_as_uint(__fadd_rz(gg, 1.0f)) >> cell_shift;
+              }
+#pragma unroll
+              for (int j = 0; j < 8; ++j) e[j] = lut_b[cell[j]];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const int cc = ((int)(Q[h] << (28 - 4 * j))) >> 28;
+                const int bin = e[j].b + (xv[j] > e[j].t ? 1 : 0);
+                atomicAdd(&s_hist[bin], cc);   // c == 0 adds nothing
+              }
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const int cc = ((int)(Q[i >> 3] << (28 - 4 * (i & 7)))) >> 28;
+              if (cc) {
+                const float xv = r1[i];
+                int lo = 0, hi = nb;
+                while (lo < hi) {
+                  const int mid = (lo + hi) >> 1;
+                  if (s_tab[mid + 1] < xv) lo = mid + 1; else hi = mid;
                 }
-                atomicAdd(&s_hist[bin], cc);
+                atomicAdd(&s_hist[lo], cc);
               }
             }
           }
@@ -499,8 +536,11 @@ int fast3d_launch(const float* x, int64_t D, int64_t H, int64_t W, int64_t batch
   if (r != CUDA_SUCCESS) return set_error(ECC_ECUDA, "cuTensorMapEncodeTiled failed");
   const int nb = (int)b->nbins;
   const int cells = b->lut_ok ? b->lut_cells : 0;
-  const size_t smem = (size_t)NSTAGE * PLANE_BYTES + NSTAGE * 8 + (size_t)((nb + 1 + 3) & ~3) * 4 +
-                      (size_t)((nb + 2 + 3) & ~3) * 4 + (size_t)(cells + 1) * sizeof(LutEntry);
+  int log2c = 0;
+  while ((1 << log2c) < cells) ++log2c;
+  const int cell_shift = 23 - log2c;
+  const size_t smem = (size_t)NSTAGE * PLANE_BYTES + 4 * 8 + (size_t)(b->lut_ok ? cells + 1 : 0) * sizeof(LutEntry) +
+                      (size_t)((nb + 1 + 3) & ~3) * 4 + (size_t)(b->lut_ok ? 0 : nb + 2) * 4;
   cudaError_t e = cudaFuncSetAttribute(ecc_fast3d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(fast3d)");
   int occ = 0;
@@ -529,8 +569,8 @@ int fast3d_launch(const float* x, int64_t D, int64_t H, int64_t W, int64_t batch
   g.items = tiles * g.zchunks;
   const int64_t grid = g.items < max_ctas ? g.items : max_ctas;
   if (grid < 1) return ECC_OK;
-  ecc_fast3d_kernel<<<(unsigned)grid, NT, smem, stream>>>(map, g, table, nb, cells, b->lut_lo, b->lut_scale,
-                                                            b->lut_ok, hist);
+  ecc_fast3d_kernel<<<(unsigned)grid, NT, smem, stream>>>(map, g, table, nb, cells, cell_shift, b->lut_scale,
+                                                            b->lut_bias, b->lut_ok, hist);
   return check_launch("ecc_fast3d_kernel");
 }
 

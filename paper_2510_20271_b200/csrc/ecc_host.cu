@@ -92,15 +92,14 @@ struct LutEntryH {
   int32_t b;
 };
 
-// the device's cell computation, operation for operation (no contraction)
-static int cell_of(float x, float lo, float scale, float cellsf) {
-  volatile float d = x - lo;
-  volatile float g = d * scale;
-  float gs = g;
-  if (!(gs > 0.0f)) gs = 0.0f;  // __saturatef: NaN -> 0
-  if (gs > 1.0f) gs = 1.0f;
-  volatile float m = gs * cellsf;
-  return (int)(float)m;  // __float2int_rz
+// the device's cell computation, operation for operation:
+//   g = sat(fma(x, scale, bias));  cell = floor(g * cells)   (cells = 2^k)
+// (the device gets the floor from the mantissa of RZ(g + 1), exact for 2^k cells)
+static int cell_of(float x, float scale, float bias, int cells) {
+  float g = fmaf(x, scale, bias);
+  if (!(g > 0.0f)) g = 0.0f;  // __saturatef: NaN -> 0
+  if (g > 1.0f) g = 1.0f;
+  return (int)floor((double)g * (double)cells);
 }
 
 static uint32_t fkey(float f) {
@@ -125,7 +124,7 @@ static int64_t bin32(float x, const float* t32, int64_t nb) {
 }
 
 // Build the cell table for thresholds t32 (non-decreasing); returns cells or 0.
-static int build_lut(const float* t32, int64_t nb, int cells, float* lo_out, float* scale_out, LutEntryH* lut) {
+static int build_lut(const float* t32, int64_t nb, int cells, float* scale_out, float* bias_out, LutEntryH* lut) {
   if (nb < 2) return 0;
   const float lo = t32[0], hi = t32[nb - 1];
   if (!std::isfinite(lo) || !std::isfinite(hi) || !(hi > lo)) return 0;
@@ -133,7 +132,7 @@ static int build_lut(const float* t32, int64_t nb, int cells, float* lo_out, flo
   if (!std::isfinite((float)span)) return 0;
   volatile float scale = 1.0f / span;
   if (!std::isfinite((float)scale) || !(scale > 0.0f)) return 0;
-  const float cellsf = (float)cells;
+  volatile float bias = -(lo * scale);
   const uint32_t kmin = fkey(-std::numeric_limits<float>::max());
   const uint32_t kmax = fkey(std::numeric_limits<float>::max());
   // first key with cell >= k, for k = 0..cells+1
@@ -142,7 +141,7 @@ static int build_lut(const float* t32, int64_t nb, int cells, float* lo_out, flo
     uint32_t a = kmin, b = kmax + 1;  // search in [a, b)
     while (a < b) {
       uint32_t mid = a + (b - a) / 2;
-      if (cell_of(keyf(mid), lo, scale, cellsf) >= k) b = mid; else a = mid + 1;
+      if (cell_of(keyf(mid), scale, bias, cells) >= k) b = mid; else a = mid + 1;
     }
     first[k] = a;  // == kmax + 1 if no finite float reaches cell k
   }
@@ -159,8 +158,8 @@ static int build_lut(const float* t32, int64_t nb, int cells, float* lo_out, flo
     lut[k].b = (int32_t)b;
     lut[k].t = b < nb ? t32[b] : std::numeric_limits<float>::infinity();
   }
-  *lo_out = lo;
   *scale_out = scale;
+  *bias_out = bias;
   return cells;
 }
 
@@ -202,8 +201,8 @@ extern "C" int ecc_threshold_table(const double* taus, int64_t nb, int dtype, vo
   b->nbins = nb;
   b->lut_ok = 0;
   b->lut_cells = 0;
-  b->lut_lo = 0.0f;
   b->lut_scale = 0.0f;
+  b->lut_bias = 0.0f;
   if (dtype == ECC_DTYPE_U8 || dtype == ECC_DTYPE_F32) {
     float* t = (float*)table_host;
     t[0] = -std::numeric_limits<float>::infinity();
@@ -211,15 +210,15 @@ extern "C" int ecc_threshold_table(const double* taus, int64_t nb, int dtype, vo
     t[nb + 1] = std::numeric_limits<float>::infinity();
     certify<float>(t, nb, b);
     LutEntryH* lut = reinterpret_cast<LutEntryH*>(t + ((nb + 2 + 1) & ~int64_t(1)));
-    for (int mult = 2; mult <= 4 && !b->lut_ok; mult *= 2) {
-      const int64_t cells = mult * nb;
-      if (cells > (1 << 16)) break;
-      float lo = 0.f, sc = 0.f;
-      if (build_lut(t + 1, nb, (int)cells, &lo, &sc, lut)) {
+    int64_t cells = 1;
+    while (cells < nb) cells <<= 1;
+    for (; cells <= 4 * nb && cells <= (1 << 16) && !b->lut_ok; cells <<= 1) {
+      float sc = 0.f, bi = 0.f;
+      if (build_lut(t + 1, nb, (int)cells, &sc, &bi, lut)) {
         b->lut_ok = 1;
         b->lut_cells = (int32_t)cells;
-        b->lut_lo = lo;
         b->lut_scale = sc;
+        b->lut_bias = bi;
       }
     }
   } else if (dtype == ECC_DTYPE_F64) {
@@ -247,6 +246,9 @@ extern "C" int ecc_counter_grid(uint64_t seed, int64_t start, int64_t count, flo
 extern "C" size_t ecc_threshold_table_bytes(int64_t nb, int dtype) {
   if (nb < 1) return 0;
   if (dtype == ECC_DTYPE_F64) return sizeof(double) * (size_t)(nb + 2);
-  const int64_t cells = 4 * nb <= (1 << 16) ? 4 * nb : (1 << 16);
+  int64_t cells = 1;
+  while (cells < nb) cells <<= 1;
+  cells *= 4;
+  if (cells > (1 << 16)) cells = 1 << 16;
   return sizeof(float) * (size_t)((nb + 2 + 1) & ~int64_t(1)) + sizeof(LutEntryH) * (size_t)(cells + 1);
 }
