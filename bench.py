@@ -194,24 +194,22 @@ def run_b200(args):
     own = padded[1:-1]
     start = rank * P * H * W
     _lib.check(L.ecc_counter_grid(SEED, start, own.numel(), _lib.ptr(own), _lib.stream_ptr(own)))
-    if world == 1:
-        padded[0].fill_(float("nan"))
-        padded[-1].fill_(float("nan"))
 
     # thresholds: uniform over the global range (device min/max, grid.py:183-196)
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    if world > 1:
-        lo, hi = D.global_range(own)
-    else:
-        lo, hi, _ = E.device_minmax(own)
-    torch.cuda.synchronize()
-    minmax_ms = (time.perf_counter() - t0) * 1e3
+    for _ in range(2):  # second call timed (first pays lazy init)
+        t0 = time.perf_counter()
+        if world > 1:
+            lo, hi = D.global_range(own)
+        else:
+            lo, hi, _ = E.device_minmax(own)
+        torch.cuda.synchronize()
+        minmax_ms = (time.perf_counter() - t0) * 1e3
     taus = E.thresholds_from_range(lo, hi, NB)
     table, binning = taus.device_table(_lib.DTYPE_F32, dev)
     hist = torch.empty(NB + 1, dtype=torch.int64, device=dev)
     curve = torch.empty(NB, dtype=torch.int64, device=dev)
-    view, z0, z1 = (padded, 1, P + 1) if world == 1 else D.slab_view(padded)
+    view, z0, z1 = (own, 0, P) if world == 1 else D.slab_view(padded)
     dims = _lib.dims_arg(view.shape)
     kstart = torch.cuda.Event(enable_timing=True)
     kend = torch.cuda.Event(enable_timing=True)
@@ -334,7 +332,7 @@ def run_b200(args):
                        "minmax_pass_ms": minmax_ms, "seed": SEED, "curve_xor_checksum": checksum},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
-                         "kernel": "ecc_sweep_kernel<RawSrc<float>,HistSink<float>>",
+                         "kernel": "ecc_fast3d_kernel" if W % 4 == 0 else "ecc_sweep_kernel<RawSrc<float>,HistSink<float>>",
                          "kernel_ms": kmean, "algorithmic_bytes_per_launch": 4 * vox_rank},
             "cpu_baseline": cpu,
             "e2e": e2e,

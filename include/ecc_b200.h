@@ -85,9 +85,10 @@ int ecc_histogram(const void *x, int dtype, int ndim, const int64_t *dims, int64
 
 /* As ecc_histogram, but only voxels in planes [plane_begin, plane_end) of
  * axis 0 are deposited; the planes outside act as halo (coefficients.py:
- * 141-152 _coefficient_rows).  A halo plane filled with NaN behaves exactly
- * like "outside the grid".  This is the z-slab entry point of the multi-GPU
- * path (one rank = one slab plus a one-plane halo on each side).  3D only. */
+ * 141-152 _coefficient_rows); they must hold the neighbouring slab's real
+ * values (at the volume's ends, pass a view without the halo plane instead).
+ * This is the z-slab entry point of the multi-GPU path (one rank = one slab
+ * plus a one-plane halo on each interior side).  3D only. */
 int ecc_histogram_range(const void *x, int dtype, int ndim, const int64_t *dims, int64_t batch,
                         int64_t plane_begin, int64_t plane_end, const void *table,
                         const ecc_binning *binning_host, int64_t *hist, void *stream);
