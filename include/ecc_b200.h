@@ -115,8 +115,9 @@ typedef struct {
   double alpha;        /* direction scale                                       */
   double u[3];         /* direction (first ndim used); any vector, not forced unit */
   double center;       /* m: taus and field are centred on m before fp32 math   */
-  int32_t factorized;  /* 1: sigma = 1/(1 + a_j b_p) with a_j = e^{-lam(tau_j-m)},
-                          b_p = e^{lam(f_p-m)}; 0: direct ex2 per pair           */
+  int32_t factorized;  /* 1: sigma = 1/(1 + a_j b_p), a_j = e^{-lam(tau_j-m_l)},
+                          b_p = e^{lam(f_p-m_l)}, m_l the centre of the lane's
+                          32-threshold block; 0: float64 exponent, ex2 + rcp   */
   int32_t pad;
 } ecc_soft_params;
 
@@ -131,17 +132,23 @@ size_t ecc_soft_workspace_bytes(int ndim, const int64_t *dims, int64_t batch, in
 /* Effective-field coefficients (the coefficients callers feed to soft_ecc:
  * compute_coefficients(effective_field(grid, alpha, u)), cli.py:201,
  * soft.py:292) computed from a float64 effective field built on the fly with
- * the reference's rounding sequence; also writes the centred float32 field
- * fc = f - m used by the sigma kernels.  x: float32 or float64 grid. */
+ * the reference's rounding sequence; also writes the centred field
+ * f - m as float32 (field_c) and, when field_lo is not NULL, its float32
+ * remainder (f - m) - field_c (needed by the direct mode below).
+ * x: float32 or float64 grid. */
 int ecc_soft_prepare(const void *x, int dtype, int ndim, const int64_t *dims, int64_t batch,
-                     const ecc_soft_params *params_host, int8_t *coeffs, float *field_c, void *stream);
+                     const ecc_soft_params *params_host, int8_t *coeffs, float *field_c, float *field_lo,
+                     void *stream);
 
 /* Forward: chi[batch][nbins] (float64) = sum_p c_p sigmoid(lam (tau_j - f_p))
  * (soft.py:154-196).  coeffs may be any int8 grid (e.g. the reference's).
- * taus: float64 [nbins] device.  workspace: ecc_soft_workspace_bytes. */
-int ecc_soft_forward(const int8_t *coeffs, const float *field_c, int ndim, const int64_t *dims, int64_t batch,
-                     const double *taus, int64_t nbins, const ecc_soft_params *params_host, double *chi,
-                     void *workspace, void *stream);
+ * taus: float64 [nbins] device.  workspace: ecc_soft_workspace_bytes.
+ * factorized != 0: one MUFU.RCP per pair (per-lane centring, needs
+ * lam*log2(e)*half-width of every 32-threshold block <= 40); otherwise the
+ * direct mode forms each exponent in float64 (field_lo required). */
+int ecc_soft_forward(const int8_t *coeffs, const float *field_c, const float *field_lo, int ndim,
+                     const int64_t *dims, int64_t batch, const double *taus, int64_t nbins,
+                     const ecc_soft_params *params_host, double *chi, void *workspace, void *stream);
 
 /* Backward (soft.py:199-257 plus the alpha gradient):
  *   d_values[b][p] = -c_p w_p,  w_p = sum_j up[b][j] lam s(1-s)   (float32)
@@ -149,10 +156,10 @@ int ecc_soft_forward(const int8_t *coeffs, const float *field_c, int ndim, const
  *   G[b][0..ndim)  = sum_p c_p w_p pos_p                          (float64)
  * from which d_u = -alpha G (then tangent-projected by the caller) and
  * d_alpha = -G.u.  upstream: float64 [batch][nbins]. */
-int ecc_soft_backward(const int8_t *coeffs, const float *field_c, int ndim, const int64_t *dims, int64_t batch,
-                      const double *taus, int64_t nbins, const ecc_soft_params *params_host,
-                      const double *upstream, float *d_values, double *d_tau, double *G, void *workspace,
-                      void *stream);
+int ecc_soft_backward(const int8_t *coeffs, const float *field_c, const float *field_lo, int ndim,
+                      const int64_t *dims, int64_t batch, const double *taus, int64_t nbins,
+                      const ecc_soft_params *params_host, const double *upstream, float *d_values, double *d_tau,
+                      double *G, void *workspace, void *stream);
 
 /* Counter-based synthetic float32 grid: out[i] = top-24-bits(splitmix64(
  * seed * K + start + i)) * 2^-24 (identical to the oracle's

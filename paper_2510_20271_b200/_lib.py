@@ -61,10 +61,10 @@ def lib():
         L.ecc_key_to_double.restype = ctypes.c_double
         L.ecc_soft_workspace_bytes.argtypes = [i32, vp, i64, i64]
         L.ecc_soft_workspace_bytes.restype = ctypes.c_size_t
-        L.ecc_soft_prepare.argtypes = [vp, i32, i32, vp, i64, ctypes.POINTER(SoftParams), vp, vp, vp]
-        L.ecc_soft_forward.argtypes = [vp, vp, i32, vp, i64, vp, i64, ctypes.POINTER(SoftParams), vp, vp, vp]
-        L.ecc_soft_backward.argtypes = [vp, vp, i32, vp, i64, vp, i64, ctypes.POINTER(SoftParams), vp, vp, vp,
-                                        vp, vp, vp]
+        L.ecc_soft_prepare.argtypes = [vp, i32, i32, vp, i64, ctypes.POINTER(SoftParams), vp, vp, vp, vp]
+        L.ecc_soft_forward.argtypes = [vp, vp, vp, i32, vp, i64, vp, i64, ctypes.POINTER(SoftParams), vp, vp, vp]
+        L.ecc_soft_backward.argtypes = [vp, vp, vp, i32, vp, i64, vp, i64, ctypes.POINTER(SoftParams), vp, vp,
+                                        vp, vp, vp, vp]
         L.ecc_effective_field.argtypes = [vp, i32, i32, vp, i64, ctypes.c_double, vp, vp, vp]
         L.ecc_counter_grid.argtypes = [ctypes.c_uint64, i64, i64, vp, vp]
         _lib = L

@@ -163,6 +163,7 @@ struct CoeffSink {
 struct SoftPrepSink {
   int8_t* __restrict__ coeffs;
   float* __restrict__ fc;
+  float* __restrict__ fclo;   // optional: (f - m) - fc, for the float64-exponent direct mode
   double center;
   int64_t D, H, W;
   __device__ void init(unsigned char*) {}
@@ -173,7 +174,10 @@ struct SoftPrepSink {
   __device__ __forceinline__ void put(int c, V value, int64_t n, int64_t z, int64_t y, int64_t x) {
     const int64_t i = ((n * D + z) * H + y) * W + x;
     coeffs[i] = (int8_t)c;
-    fc[i] = (float)((double)value - center);
+    const double d = (double)value - center;
+    const float hi = (float)d;
+    fc[i] = hi;
+    if (fclo) fclo[i] = (float)(d - (double)hi);
   }
 };
 
@@ -551,14 +555,15 @@ extern "C" int ecc_minmax(const void* x, int dtype, int64_t n, uint64_t* out3, v
 }
 
 extern "C" int ecc_soft_prepare(const void* x, int dtype, int ndim, const int64_t* dims, int64_t batch,
-                                const ecc_soft_params* p, int8_t* coeffs, float* field_c, void* stream) {
+                                const ecc_soft_params* p, int8_t* coeffs, float* field_c, float* field_lo,
+                                void* stream) {
   clear_error();
   int64_t d3[3];
   int rc = dims_to3(ndim, dims, d3);
   if (rc) return rc;
   if (!x || !p || !coeffs || !field_c) return set_error(ECC_EINVAL, "null pointer argument");
   if (batch < 1) return set_error(ECC_EINVAL, "batch must be >= 1");
-  SoftPrepSink sk{coeffs, field_c, p->center, d3[0], d3[1], d3[2]};
+  SoftPrepSink sk{coeffs, field_c, field_lo, p->center, d3[0], d3[1], d3[2]};
   cudaStream_t s = (cudaStream_t)stream;
   if (dtype == ECC_DTYPE_F32) {
     EffSrc<float> src{(const float*)x, p->alpha, p->u[0], p->u[1], p->u[2], d3[0], d3[1], d3[2], ndim};

@@ -35,7 +35,8 @@ constexpr double LOG2E = 1.4426950408889634;
 
 struct SoftArgs {
   const int8_t* c;        // [N][n]
-  const float* fc;        // [N][n] centred field f - m
+  const float* fc;        // [N][n] centred field f - m (float32)
+  const float* fclo;      // [N][n] f - m - fc (direct mode only)
   int64_t n;              // voxels per item
   int64_t chunks;         // ceil(n / CH)
   int64_t D, H, W;
@@ -64,15 +65,57 @@ __device__ __forceinline__ float rcp_approx(float x) {
 
 // smem layout of a chunk after compaction
 struct ChunkSmem {
-  float b1[CH];     // first exponent factor (or the exponent itself, direct mode)
-  float b2[CH];     // second factor (1 unless the voxel needs the split)
-  float cf[CH];     // coefficient as float
-  int idx[CH];      // voxel index within the chunk
+  float fc[CH];     // centred field f_p - m of the non-zero voxels
+  float fclo[CH];   // its float32 remainder (direct mode: f - tau in float64)
+  int pk[CH];       // voxel index within the chunk | (c << 16)
   int count;
 };
 
+// log2 bound of the per-lane factor a_j; b_p is clamped to 2^+-(126 - A_MAX)
+// so a_j b_p stays inside [2^-126, 2^126] (no overflow, no inf*0)
+constexpr float A_MAX = 40.f;
+constexpr float B_MAX = 126.f - A_MAX;
+
 template <bool BWD>
-__global__ void __launch_bounds__(SNT)
+__device__ __forceinline__ void pair_loop_fact(const float (&at)[TT], const float (&upv)[TT], float (&acc)[TT], float b,
+                                               float cf, float& w) {
+#pragma unroll
+  for (int t = 0; t < TT; ++t) {
+    const float e = at[t] * b;                          // e^{lam (f_p - tau_j)}
+    const float r = rcp_approx(e + 1.f);                // sigma
+    if (!BWD) {
+      acc[t] = __fmaf_rn(cf, r, acc[t]);
+    } else {
+      const float s1 = (e * r) * r;                     // sigma (1 - sigma), no cancellation
+      w = __fmaf_rn(upv[t], s1, w);
+      acc[t] = __fmaf_rn(cf, s1, acc[t]);
+    }
+  }
+}
+
+// direct mode (large lambda * threshold spread): the exponent
+// lam log2(e) (f_p - tau_j) is formed in float64 (f_p carried as two floats,
+// kt_j = lam log2(e) (tau_j - m) from a transposed shared table), then ex2 + rcp
+template <bool BWD>
+__device__ __forceinline__ void pair_loop_direct(const double* __restrict__ kt, int Lv, int l, const float (&upv)[TT],
+                                                 float (&acc)[TT], double kf, float cf, float& w) {
+#pragma unroll
+  for (int t = 0; t < TT; ++t) {
+    const double z = kf - kt[t * Lv + l];
+    const float e = ex2_approx(fminf((float)z, 100.f));
+    const float r = rcp_approx(e + 1.f);
+    if (!BWD) {
+      acc[t] = __fmaf_rn(cf, r, acc[t]);
+    } else {
+      const float s1 = (e * r) * r;
+      w = __fmaf_rn(upv[t], s1, w);
+      acc[t] = __fmaf_rn(cf, s1, acc[t]);
+    }
+  }
+}
+
+template <bool BWD, bool FACT>
+__global__ void __launch_bounds__(SNT, 2)
 ecc_soft_kernel(SoftArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ChunkSmem& S = *reinterpret_cast<ChunkSmem*>(smem_raw);
@@ -89,14 +132,13 @@ ecc_soft_kernel(SoftArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
   // ---- compaction of the chunk to c != 0 voxels (order-preserving) -------
-  // each warp takes a contiguous slice of the chunk
   {
     const int per_warp = (CH + SNW - 1) / SNW;
     const int w0 = warp * per_warp, w1 = min(w0 + per_warp, nvox);
     int cnt = 0;
     for (int base = w0; base < w1; base += 32) {
-      int i = base + lane;
-      int cv = i < w1 ? (int)cg[i] : 0;
+      const int i = base + lane;
+      const int cv = i < w1 ? (int)cg[i] : 0;
       cnt += __popc(__ballot_sync(0xffffffffu, cv != 0));
     }
     if (lane == 0) s_wcount[warp] = cnt;
@@ -109,36 +151,14 @@ ecc_soft_kernel(SoftArgs a) {
       S.count = tot;
     }
     for (int base = w0; base < w1; base += 32) {
-      int i = base + lane;
-      int cv = i < w1 ? (int)cg[i] : 0;
-      float f = i < w1 ? fg[i] : 0.f;
-      unsigned m = __ballot_sync(0xffffffffu, cv != 0);
+      const int i = base + lane;
+      const int cv = i < w1 ? (int)cg[i] : 0;
+      const unsigned m = __ballot_sync(0xffffffffu, cv != 0);
       if (cv != 0) {
-        int k = off + __popc(m & ((1u << lane) - 1u));
-        float kf = a.kscale * f;   // log2 of b_p
-        float b1, b2;
-        if (a.factorized) {
-          // |log2 b| <= 63 keeps a_j * b_p <= 2^126 (host guarantees |log2 a_j| <= 63):
-          // no overflow, so s(1-s) = (e r) r is never inf * 0.  Larger |kf| is
-          // split in two factors (products then clamped); beyond 126 the
-          // sigmoid is saturated to within 2^-63 at every threshold.
-          kf = fminf(fmaxf(kf, -126.f), 126.f);
-          if (fabsf(kf) <= 63.f) {
-            b1 = ex2_approx(kf);
-            b2 = 1.f;
-          } else {
-            float h = 0.5f * kf;
-            b1 = ex2_approx(h);
-            b2 = ex2_approx(kf - h);
-          }
-        } else {
-          b1 = kf;
-          b2 = 1.f;
-        }
-        S.b1[k] = b1;
-        S.b2[k] = b2;
-        S.cf[k] = (float)cv;
-        S.idx[k] = i;
+        const int k = off + __popc(m & ((1u << lane) - 1u));
+        S.fc[k] = fg[i];
+        if (!FACT) S.fclo[k] = a.fclo[item * a.n + v0 + i];
+        S.pk[k] = i | (cv << 16);
       } else if (BWD && i < w1) {
         a.dX[item * a.n + v0 + i] = 0.f;
       }
@@ -148,145 +168,104 @@ ecc_soft_kernel(SoftArgs a) {
   }
   const int count = S.count;
 
-  // ---- geometry of the lane groups ----------------------------------------
-  const int nbp_full = a.nb;
+  // ---- lane groups: Lv lanes cover one voxel's thresholds -----------------
+  const int nb = a.nb;
   int Lv = 1;
-  {
-    int need = (min(nbp_full, MAXB_PASS) + TT - 1) / TT;
-    while (Lv < need) Lv <<= 1;
-  }
+  while (Lv * TT < nb) Lv <<= 1;
   const int VW = 32 / Lv;               // voxels per warp in flight
   const int g = lane / Lv;              // voxel slot within the warp
-  const int l = lane % Lv;              // threshold block within the voxel
-  const int slot = warp * VW + g;       // voxel slot within the CTA
+  const int l = lane % Lv;              // threshold block of this lane
+  const int slot = warp * VW + g;
   const int nslots = SNW * VW;
 
-  double gacc[3] = {0.0, 0.0, 0.0};
-
-  for (int j0 = 0; j0 < nbp_full; j0 += MAXB_PASS) {
-    // thresholds of this lane: j = j0 + l*TT + t
-    float at[TT];
-    float upv[TT];
-    float acc[TT];
+  // thresholds of this lane: j = l*TT + t, centred on the block's own centre
+  // m_l (factorised: a_j = 2^{-k (tau_j - m_l)}, b_{p,l} = 2^{k (f_p - m_l)})
+  float at[TT], upv[TT], acc[TT];
+  const int j0 = l * TT;
+  const int jl = min(j0 + TT, nb) - 1;
+  const double ml = (j0 < nb) ? 0.5 * (a.taus[j0] + a.taus[jl]) : a.m;
+  const double ks = a.lam * LOG2E;
 #pragma unroll
-    for (int t = 0; t < TT; ++t) {
-      const int j = j0 + l * TT + t;
-      float av = 0.f, u = 0.f;
-      if (j < nbp_full) {
-        const double z = -(a.lam * LOG2E) * (a.taus[j] - a.m);
-        av = a.factorized ? (float)exp2(z) : (float)z;
-        if (BWD) u = (float)a.up[item * nbp_full + j];
-      } else {
-        av = a.factorized ? 0.f : -INFINITY;
-      }
-      at[t] = av;
-      upv[t] = u;
-      acc[t] = 0.f;
+  for (int t = 0; t < TT; ++t) {
+    const int j = j0 + t;
+    float av, u = 0.f;
+    if (j < nb) {
+      av = FACT ? (float)exp2(-ks * (a.taus[j] - ml)) : 0.f;
+      if (BWD) u = (float)a.up[item * nb + j];
+    } else {
+      av = 0.f;
     }
+    at[t] = av;
+    upv[t] = u;
+    acc[t] = 0.f;
+  }
+  const float koff = FACT ? (float)(ks * (a.m - ml)) : 0.f;   // k f_p - k m_l = k fc + koff
+  double* kt = reinterpret_cast<double*>(smem_raw + ((sizeof(ChunkSmem) + 15) & ~size_t(15)));
+  if (!FACT) {
+    // kt[t * Lv + l] = ks (tau_{l TT + t} - m); padded thresholds -> +inf (sigma = 1, discarded)
+    for (int q = threadIdx.x; q < Lv * TT; q += SNT) {
+      const int tt = q / Lv, ll = q % Lv, j = ll * TT + tt;
+      kt[q] = j < nb ? ks * (a.taus[j] - a.m) : (double)INFINITY;
+    }
+    __syncthreads();
+  }
 
-    float g0 = 0.f, g1 = 0.f, g2 = 0.f;
-    // warp-uniform trip count: the group reduction below shuffles across the
-    // whole warp, so every lane runs every iteration (idle slots carry c = 0)
-    for (int kb = warp * VW; kb < count; kb += nslots) {
-      const int k = kb + g;
-      const bool valid = k < count;
-      const float b1 = valid ? S.b1[k] : 1.f, b2 = valid ? S.b2[k] : 1.f, cf = valid ? S.cf[k] : 0.f;
-      float w = 0.f;
-      if (a.factorized) {
-        if (b2 == 1.f) {
-#pragma unroll
-          for (int t = 0; t < TT; ++t) {
-            if (!BWD) {
-              const float r = rcp_approx(__fmaf_rn(at[t], b1, 1.f));
-              acc[t] = __fmaf_rn(cf, r, acc[t]);
-            } else {
-              const float e = at[t] * b1;
-              const float r = rcp_approx(e + 1.f);
-              const float s1 = (e * r) * r;        // sigma (1 - sigma)
-              w = __fmaf_rn(upv[t], s1, w);
-              acc[t] = __fmaf_rn(cf, s1, acc[t]);
-            }
-          }
+  float g0 = 0.f, g1 = 0.f, g2 = 0.f;
+  const float sH = a.H > 1 ? (float)(2.0 / (double)(a.H - 1)) : 0.f;
+  const float sW = a.W > 1 ? (float)(2.0 / (double)(a.W - 1)) : 0.f;
+  const float sD = a.D > 1 ? (float)(2.0 / (double)(a.D - 1)) : 0.f;
+  // warp-uniform trip count: the group reduction shuffles across the warp
+  for (int kb = warp * VW; kb < count; kb += nslots) {
+    const int k = kb + g;
+    const bool valid = k < count;
+    const float f = valid ? S.fc[k] : 0.f;
+    const int pk = valid ? S.pk[k] : 0;
+    const float cf = (float)(pk >> 16);
+    float w = 0.f;
+    if (FACT) {
+      const float kf = fminf(fmaxf(__fmaf_rn(a.kscale, f, koff), -B_MAX), B_MAX);
+      pair_loop_fact<BWD>(at, upv, acc, ex2_approx(kf), cf, w);
+    } else {
+      const double fd = (double)f + (double)(valid ? S.fclo[k] : 0.f);
+      pair_loop_direct<BWD>(kt, Lv, l, upv, acc, ks * fd, cf, w);
+    }
+    if (BWD) {
+      for (int o = Lv >> 1; o; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+      if (l == 0 && valid) {
+        const int64_t vi = v0 + (pk & 0xffff);
+        const float lw = (float)a.lam * w;
+        a.dX[item * a.n + vi] = -cf * lw;
+        // pos_p (soft.py:79-94) for G = sum c w pos
+        const float cw = cf * lw;
+        if (a.ndim == 2) {
+          const int64_t y = vi / a.W, x = vi - y * a.W;
+          g0 = __fmaf_rn(cw, a.H > 1 ? __fmaf_rn((float)y, sH, -1.f) : 0.f, g0);
+          g1 = __fmaf_rn(cw, a.W > 1 ? __fmaf_rn((float)x, sW, -1.f) : 0.f, g1);
         } else {
-#pragma unroll
-          for (int t = 0; t < TT; ++t) {
-            const float e = fminf((at[t] * b1) * b2, 1e30f);
-            const float r = rcp_approx(e + 1.f);
-            if (!BWD) {
-              acc[t] = __fmaf_rn(cf, r, acc[t]);
-            } else {
-              const float s1 = (e * r) * r;
-              w = __fmaf_rn(upv[t], s1, w);
-              acc[t] = __fmaf_rn(cf, s1, acc[t]);
-            }
-          }
-        }
-      } else {
-#pragma unroll
-        for (int t = 0; t < TT; ++t) {
-          const float e = ex2_approx(fminf(b1 + at[t], 100.f));   // e^{lam (f_p - tau_j)}, <= 2^100
-          const float r = rcp_approx(e + 1.f);
-          if (!BWD) {
-            acc[t] = __fmaf_rn(cf, r, acc[t]);
-          } else {
-            const float s1 = (e * r) * r;
-            w = __fmaf_rn(upv[t], s1, w);
-            acc[t] = __fmaf_rn(cf, s1, acc[t]);
-          }
-        }
-      }
-      if (BWD) {
-        // w over the voxel's thresholds: reduce across the Lv lanes of the group
-        for (int o = Lv >> 1; o; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
-        // (only pass 0 writes dX when B fits one pass; multi-pass accumulates below)
-        if (l == 0 && valid) {
-          const int64_t vi = v0 + S.idx[k];
-          const float lw = (float)a.lam * w;
-          float* dxp = a.dX + item * a.n + vi;
-          if (j0 == 0) *dxp = -cf * lw; else *dxp += -cf * lw;
-          // pos_p (soft.py:79-94) for G = sum c w pos
-          int64_t z, y, x;
-          if (a.ndim == 2) { z = 0; y = vi / a.W; x = vi - y * a.W; }
-          else { z = vi / (a.H * a.W); int64_t r = vi - z * a.H * a.W; y = r / a.W; x = r - y * a.W; }
-          const float cw = cf * lw;
-          if (a.ndim == 2) {
-            g0 = __fmaf_rn(cw, (float)coord64(y, a.H), g0);
-            g1 = __fmaf_rn(cw, (float)coord64(x, a.W), g1);
-          } else {
-            g0 = __fmaf_rn(cw, (float)coord64(z, a.D), g0);
-            g1 = __fmaf_rn(cw, (float)coord64(y, a.H), g1);
-            g2 = __fmaf_rn(cw, (float)coord64(x, a.W), g2);
-          }
+          const int64_t z = vi / (a.H * a.W), r = vi - z * a.H * a.W, y = r / a.W, x = r - y * a.W;
+          g0 = __fmaf_rn(cw, a.D > 1 ? __fmaf_rn((float)z, sD, -1.f) : 0.f, g0);
+          g1 = __fmaf_rn(cw, a.H > 1 ? __fmaf_rn((float)y, sH, -1.f) : 0.f, g1);
+          g2 = __fmaf_rn(cw, a.W > 1 ? __fmaf_rn((float)x, sW, -1.f) : 0.f, g2);
         }
       }
     }
-    if (BWD) { gacc[0] += g0; gacc[1] += g1; gacc[2] += g2; }
+  }
 
-    // ---- fixed-order reduction of acc over the CTA's voxel slots ----------
-    __syncthreads();   // chunk arrays no longer needed for this pass... (reused below)
-    // red[slot][l*TT + t]
-    const int wpass = min(nbp_full - j0, MAXB_PASS);
-    const int rowlen = Lv * TT;
+  // ---- fixed-order reduction of acc over the CTA's voxel slots ------------
+  __syncthreads();   // chunk arrays no longer needed (red aliases them)
+  const int rowlen = Lv * TT;
 #pragma unroll
-    for (int t = 0; t < TT; ++t) red[slot * rowlen + l * TT + t] = acc[t];
-    __syncthreads();
-    double* out = a.part + (item * a.chunks + chunk) * nbp_full + j0;
-    for (int j = threadIdx.x; j < wpass; j += SNT) {
-      double s = 0.0;
-      for (int q = 0; q < nslots; ++q) s += (double)red[q * rowlen + j];
-      out[j] = s;
-    }
-    __syncthreads();
-    if (j0 + MAXB_PASS < nbp_full) {
-      // the reduction scratch overwrote the chunk arrays: rebuild is not
-      // needed because MAXB_PASS passes only happen for B > 1024, where we
-      // re-run compaction by relaunching per pass (see launcher)
-    }
+  for (int t = 0; t < TT; ++t) red[slot * rowlen + l * TT + t] = acc[t];
+  __syncthreads();
+  double* out = a.part + (item * a.chunks + chunk) * nb;
+  for (int j = threadIdx.x; j < nb; j += SNT) {
+    double sacc = 0.0;
+    for (int q = 0; q < nslots; ++q) sacc += (double)red[q * rowlen + j];
+    out[j] = sacc;
   }
 
   if (BWD) {
-    // G partial: fixed-order over lanes (only l == 0 lanes hold data)
-    double v0d = gacc[0], v1d = gacc[1], v2d = gacc[2];
+    double v0d = g0, v1d = g1, v2d = g2;
     for (int o = 16; o; o >>= 1) {
       v0d += __shfl_xor_sync(0xffffffffu, v0d, o);
       v1d += __shfl_xor_sync(0xffffffffu, v1d, o);
@@ -295,9 +274,9 @@ ecc_soft_kernel(SoftArgs a) {
     if (lane == 0) { s_g[warp][0] = v0d; s_g[warp][1] = v1d; s_g[warp][2] = v2d; }
     __syncthreads();
     if (threadIdx.x < 3) {
-      double s = 0.0;
-      for (int w = 0; w < SNW; ++w) s += s_g[w][threadIdx.x];
-      a.gpart[(item * a.chunks + chunk) * 4 + threadIdx.x] = s;
+      double sg = 0.0;
+      for (int w = 0; w < SNW; ++w) sg += s_g[w][threadIdx.x];
+      a.gpart[(item * a.chunks + chunk) * 4 + threadIdx.x] = sg;
     }
   }
 }
@@ -325,7 +304,7 @@ __global__ void ecc_soft_reduce_g(const double* __restrict__ gpart, int64_t chun
 }
 
 static size_t soft_smem() {
-  size_t chunk = sizeof(ChunkSmem);
+  size_t chunk = ((sizeof(ChunkSmem) + 15) & ~size_t(15)) + sizeof(double) * MAXB_PASS;   // + direct-mode table
   size_t red = sizeof(float) * (size_t)SNT * TT;   // nslots*rowlen = 8*VW*Lv*TT = 256*TT
   return chunk > red ? chunk : red;
 }
@@ -351,7 +330,7 @@ extern "C" size_t ecc_soft_workspace_bytes(int ndim, const int64_t* dims, int64_
 }
 
 template <bool BWD>
-static int soft_launch(const int8_t* coeffs, const float* fc, int ndim, const int64_t* dims, int64_t batch,
+static int soft_launch(const int8_t* coeffs, const float* fc, const float* fclo, int ndim, const int64_t* dims, int64_t batch,
                        const double* taus, int64_t nbins, const ecc_soft_params* p, const double* up, float* dX,
                        double* out_main, double* G, void* workspace, void* stream) {
   clear_error();
@@ -363,11 +342,13 @@ static int soft_launch(const int8_t* coeffs, const float* fc, int ndim, const in
   if (batch < 1 || nbins < 1) return set_error(ECC_EINVAL, "empty soft problem");
   if (nbins > MAXB_PASS) return set_error(ECC_EINVAL, "soft path supports at most 1024 thresholds per call");
   if (!(p->lam > 0)) return set_error(ECC_EINVAL, "sharpness must be positive");
+  if (!p->factorized && !fclo) return set_error(ECC_EINVAL, "direct mode needs the float32 field remainder");
   const int64_t n = d3[0] * d3[1] * d3[2];
   const int64_t chunks = (n + CH - 1) / CH;
   SoftArgs a;
   a.c = coeffs;
   a.fc = fc;
+  a.fclo = fclo;
   a.n = n;
   a.chunks = chunks;
   a.D = d3[0];
@@ -386,7 +367,7 @@ static int soft_launch(const int8_t* coeffs, const float* fc, int ndim, const in
   a.dX = dX;
   cudaStream_t s = (cudaStream_t)stream;
   const size_t smem = soft_smem();
-  auto kfn = ecc_soft_kernel<BWD>;
+  auto kfn = p->factorized ? ecc_soft_kernel<BWD, true> : ecc_soft_kernel<BWD, false>;
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(soft)");
   const int64_t grid = batch * chunks;
@@ -405,17 +386,19 @@ static int soft_launch(const int8_t* coeffs, const float* fc, int ndim, const in
   return rc;
 }
 
-extern "C" int ecc_soft_forward(const int8_t* coeffs, const float* field_c, int ndim, const int64_t* dims,
+extern "C" int ecc_soft_forward(const int8_t* coeffs, const float* field_c, const float* field_lo, int ndim,
+                                const int64_t* dims,
                                 int64_t batch, const double* taus, int64_t nbins, const ecc_soft_params* p,
                                 double* chi, void* workspace, void* stream) {
-  return soft_launch<false>(coeffs, field_c, ndim, dims, batch, taus, nbins, p, nullptr, nullptr, chi, nullptr,
+  return soft_launch<false>(coeffs, field_c, field_lo, ndim, dims, batch, taus, nbins, p, nullptr, nullptr, chi, nullptr,
                             workspace, stream);
 }
 
-extern "C" int ecc_soft_backward(const int8_t* coeffs, const float* field_c, int ndim, const int64_t* dims,
+extern "C" int ecc_soft_backward(const int8_t* coeffs, const float* field_c, const float* field_lo, int ndim,
+                                 const int64_t* dims,
                                  int64_t batch, const double* taus, int64_t nbins, const ecc_soft_params* p,
                                  const double* upstream, float* d_values, double* d_tau, double* G, void* workspace,
                                  void* stream) {
-  return soft_launch<true>(coeffs, field_c, ndim, dims, batch, taus, nbins, p, upstream, d_values, d_tau, G,
+  return soft_launch<true>(coeffs, field_c, field_lo, ndim, dims, batch, taus, nbins, p, upstream, d_values, d_tau, G,
                            workspace, stream);
 }

@@ -31,7 +31,8 @@ from .grid import EulerCurve, ScalarGrid, ThresholdSet
 
 UNIT_NORM_TOL = 1e-12
 _LOG2E = 1.4426950408889634
-_FACTOR_LIMIT = 63.0  # |log2 a_j| bound for the factorised sigmoid (a_j b_p <= 2^126)
+_FACTOR_LIMIT = 40.0  # |log2 a_j| bound for the factorised sigmoid (ecc_soft.cu A_MAX)
+_TT = 32  # thresholds per kernel lane
 
 
 @dataclass(frozen=True)
@@ -114,7 +115,22 @@ def _soft_tensor(x: torch.Tensor) -> torch.Tensor:
     return x.contiguous()
 
 
-def _params(lam: float, alpha: float, u, tau_lo: float, tau_hi: float, ndim: int) -> _lib.SoftParams:
+def _block_halfwidth(taus) -> float:
+    """Largest half-width of the 32-threshold blocks a kernel lane holds."""
+    if isinstance(taus, torch.Tensor):
+        t = taus.detach().to(torch.float64)
+        nb = t.numel()
+        pad = (-nb) % _TT
+        if pad:
+            t = torch.cat([t, t[-1:].expand(pad)])
+        blocks = t.reshape(-1, _TT)
+        return float(((blocks.max(1).values - blocks.min(1).values) * 0.5).max())
+    t = np.asarray(taus, dtype=np.float64)
+    return max(0.5 * float(t[i:i + _TT].max() - t[i:i + _TT].min()) for i in range(0, t.size, _TT))
+
+
+def _params(lam: float, alpha: float, u, tau_lo: float, tau_hi: float, ndim: int, halfwidth: float | None = None
+            ) -> _lib.SoftParams:
     p = _lib.SoftParams()
     p.lam = float(lam)
     p.alpha = float(alpha)
@@ -124,19 +140,24 @@ def _params(lam: float, alpha: float, u, tau_lo: float, tau_hi: float, ndim: int
         p.u[i] = float(uu[i])
     m = 0.5 * (tau_lo + tau_hi)
     p.center = m
-    p.factorized = int(lam * _LOG2E * max(abs(tau_hi - m), abs(tau_lo - m)) <= _FACTOR_LIMIT)
+    if halfwidth is None:
+        halfwidth = 0.5 * (tau_hi - tau_lo)
+    # per-lane-block centring keeps |log2 a_j| <= 40 (ecc_soft.cu A_MAX)
+    p.factorized = int(lam * _LOG2E * halfwidth <= _FACTOR_LIMIT)
     return p
 
 
 def soft_prepare_device(x: torch.Tensor, dims, batch: int, p: _lib.SoftParams):
-    """(int8 coefficients of the effective field, centred fp32 field) on device."""
+    """(int8 coefficients of the effective field, centred fp32 field, its fp32
+    remainder or None) on device; the remainder is only kept in direct mode."""
     code = _lib.dtype_code(x)
     c = torch.empty(x.shape, dtype=torch.int8, device=x.device)
     fc = torch.empty(x.shape, dtype=torch.float32, device=x.device)
+    lo = None if p.factorized else torch.empty(x.shape, dtype=torch.float32, device=x.device)
     d = _lib.dims_arg(dims)
     _lib.check(_lib.lib().ecc_soft_prepare(_lib.ptr(x), code, len(dims), _lib.ptr(d), batch, _lib.ctypes.byref(p),
-                                           _lib.ptr(c), _lib.ptr(fc), _lib.stream_ptr(x)))
-    return c, fc
+                                           _lib.ptr(c), _lib.ptr(fc), _lib.ptr(lo), _lib.stream_ptr(x)))
+    return c, (fc, lo)
 
 
 def _workspace(dims, batch: int, nb: int, device) -> torch.Tensor:
@@ -145,19 +166,21 @@ def _workspace(dims, batch: int, nb: int, device) -> torch.Tensor:
     return torch.empty(max(nbytes, 8) // 8 + 1, dtype=torch.float64, device=device)
 
 
-def soft_forward_device(c, fc, dims, batch: int, taus_dev: torch.Tensor, p: _lib.SoftParams) -> torch.Tensor:
+def soft_forward_device(c, field, dims, batch: int, taus_dev: torch.Tensor, p: _lib.SoftParams) -> torch.Tensor:
+    fc, lo = field
     nb = taus_dev.numel()
     chi = torch.empty((batch, nb), dtype=torch.float64, device=fc.device)
     ws = _workspace(dims, batch, nb, fc.device)
     d = _lib.dims_arg(dims)
-    _lib.check(_lib.lib().ecc_soft_forward(_lib.ptr(c), _lib.ptr(fc), len(dims), _lib.ptr(d), batch,
+    _lib.check(_lib.lib().ecc_soft_forward(_lib.ptr(c), _lib.ptr(fc), _lib.ptr(lo), len(dims), _lib.ptr(d), batch,
                                            _lib.ptr(taus_dev), nb, _lib.ctypes.byref(p), _lib.ptr(chi), _lib.ptr(ws),
                                            _lib.stream_ptr(fc)))
     return chi
 
 
-def soft_backward_device(c, fc, dims, batch: int, taus_dev, p, upstream: torch.Tensor):
-    """(d_values fp32 like fc, d_tau [N,B] fp64, G [N,ndim] fp64)."""
+def soft_backward_device(c, field, dims, batch: int, taus_dev, p, upstream: torch.Tensor):
+    """(d_values fp32 like the field, d_tau [N,B] fp64, G [N,ndim] fp64)."""
+    fc, lo = field
     nb = taus_dev.numel()
     up = upstream.to(torch.float64).contiguous()
     dX = torch.empty(fc.shape, dtype=torch.float32, device=fc.device)
@@ -165,7 +188,7 @@ def soft_backward_device(c, fc, dims, batch: int, taus_dev, p, upstream: torch.T
     G = torch.empty((batch, len(dims)), dtype=torch.float64, device=fc.device)
     ws = _workspace(dims, batch, nb, fc.device)
     d = _lib.dims_arg(dims)
-    _lib.check(_lib.lib().ecc_soft_backward(_lib.ptr(c), _lib.ptr(fc), len(dims), _lib.ptr(d), batch,
+    _lib.check(_lib.lib().ecc_soft_backward(_lib.ptr(c), _lib.ptr(fc), _lib.ptr(lo), len(dims), _lib.ptr(d), batch,
                                             _lib.ptr(taus_dev), nb, _lib.ctypes.byref(p), _lib.ptr(up), _lib.ptr(dX),
                                             _lib.ptr(dtau), _lib.ptr(G), _lib.ptr(ws), _lib.stream_ptr(fc)))
     return dX, dtau, G
@@ -198,11 +221,12 @@ def _coeff_tensor(coeffs: CoefficientGrid, device) -> torch.Tensor:
 def _prepared(grid, coeffs, params):
     x = _soft_tensor(grid.device_tensor())
     taus = params.taus.taus
-    p = _params(params.lam, params.alpha, params.u, float(taus[0]), float(taus[-1]), grid.ndim)
-    _, fc = soft_prepare_device(x, grid.dims, 1, p)
+    p = _params(params.lam, params.alpha, params.u, float(taus[0]), float(taus[-1]), grid.ndim,
+                _block_halfwidth(taus))
+    _, field = soft_prepare_device(x, grid.dims, 1, p)
     c = _coeff_tensor(coeffs, x.device)
-    taus_dev = torch.from_numpy(np.ascontiguousarray(taus)).to(x.device)
-    return c, fc, taus_dev, p
+    taus_dev = torch.from_numpy(np.array(taus, dtype=np.float64)).to(x.device)
+    return c, field, taus_dev, p
 
 
 def soft_ecc(grid: ScalarGrid, coeffs: CoefficientGrid, params: SoftEccParams, workers: int = 1) -> EulerCurve:
@@ -212,8 +236,8 @@ def soft_ecc(grid: ScalarGrid, coeffs: CoefficientGrid, params: SoftEccParams, w
     given (e.g. the reference's own), exactly like the reference.
     """
     _check_shapes(grid, coeffs, params.u)
-    c, fc, taus_dev, p = _prepared(grid, coeffs, params)
-    chi = soft_forward_device(c, fc, grid.dims, 1, taus_dev, p)
+    c, field, taus_dev, p = _prepared(grid, coeffs, params)
+    chi = soft_forward_device(c, field, grid.dims, 1, taus_dev, p)
     return EulerCurve(params.taus.taus, chi[0].cpu().numpy())
 
 
@@ -225,9 +249,9 @@ def soft_ecc_backward(grid: ScalarGrid, coeffs: CoefficientGrid, params: SoftEcc
     ntau = len(params.taus)
     if upstream.size != ntau:
         raise ValueError(f"upstream has {upstream.size} weights for {ntau} thresholds")
-    c, fc, taus_dev, p = _prepared(grid, coeffs, params)
-    up = torch.from_numpy(upstream).to(fc.device).reshape(1, ntau)
-    dX, dtau, G = soft_backward_device(c, fc, grid.dims, 1, taus_dev, p, up)
+    c, field, taus_dev, p = _prepared(grid, coeffs, params)
+    up = torch.from_numpy(upstream).to(field[0].device).reshape(1, ntau)
+    dX, dtau, G = soft_backward_device(c, field, grid.dims, 1, taus_dev, p, up)
     G = G[0].cpu().numpy()
     u = params.u
     d_u = -params.alpha * G
@@ -260,19 +284,19 @@ class SoftECCFunction(torch.autograd.Function):
         lo, hi = torch.aminmax(taus_d)
         uh = u.detach().to(torch.float64).cpu().numpy()
         a = float(alpha.detach())
-        p = _params(lam, a, uh, float(lo), float(hi), ndim)
-        c, fc = soft_prepare_device(xs, dims, batch, p)
-        chi = soft_forward_device(c, fc, dims, batch, taus_d, p)
-        ctx.save_for_backward(c, fc, taus_d, u.detach(), alpha.detach())
+        p = _params(lam, a, uh, float(lo), float(hi), ndim, _block_halfwidth(taus_d))
+        c, (fc, lo) = soft_prepare_device(xs, dims, batch, p)
+        chi = soft_forward_device(c, (fc, lo), dims, batch, taus_d, p)
+        ctx.save_for_backward(c, fc, lo if lo is not None else fc.new_empty(0), taus_d, u.detach(), alpha.detach())
         ctx.meta = (dims, batch, batched, p, x.dtype, taus.dtype)
         return chi if batched else chi[0]
 
     @staticmethod
     def backward(ctx, grad_chi):
-        c, fc, taus_d, u, alpha = ctx.saved_tensors
+        c, fc, lo, taus_d, u, alpha = ctx.saved_tensors
         dims, batch, batched, p, xdtype, tdtype = ctx.meta
         up = grad_chi.reshape(batch, -1)
-        dX, dtau, G = soft_backward_device(c, fc, dims, batch, taus_d, p, up)
+        dX, dtau, G = soft_backward_device(c, (fc, lo if lo.numel() else None), dims, batch, taus_d, p, up)
         Gs = G.sum(0)
         gx = dX.to(xdtype) if ctx.needs_input_grad[0] else None
         gt = dtau.sum(0).to(tdtype) if ctx.needs_input_grad[1] else None
