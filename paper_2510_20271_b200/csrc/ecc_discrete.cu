@@ -50,20 +50,27 @@ struct EffSrc {
   double alpha, u0, u1, u2;
   int64_t D, H, W;
   int ndim;
+  double sD, sH, sW;   // 2.0 / (d - 1) in float64 (host-computed like numpy), 0 when d == 1
+  // pixel_coordinates (soft.py:79-94): idx * (2/(d-1)) - 1 with two roundings; 0 for d == 1
+  __device__ __forceinline__ static double crd(int64_t idx, int64_t d, double s) {
+    return d == 1 ? 0.0 : __dadd_rn(__dmul_rn((double)idx, s), -1.0);
+  }
   __device__ __forceinline__ V at(int64_t lin, int64_t z, int64_t y, int64_t xx) const {
     double v = (double)x[lin];
     if (alpha == 0.0) return v;
     double dot;
     if (ndim == 2) {
-      double p0 = coord64(y, H), p1 = coord64(xx, W);
+      double p0 = crd(y, H, sH), p1 = crd(xx, W, sW);
       dot = __fma_rn(p0, u0, __dmul_rn(p1, u1));
     } else {
-      double p0 = coord64(z, D), p1 = coord64(y, H), p2 = coord64(xx, W);
+      double p0 = crd(z, D, sD), p1 = crd(y, H, sH), p2 = crd(xx, W, sW);
       dot = __fma_rn(p2, u2, __fma_rn(p0, u0, __dmul_rn(p1, u1)));
     }
     return __dadd_rn(v, __dmul_rn(alpha, dot));
   }
 };
+
+static inline double coord_scale(int64_t d) { return d > 1 ? 2.0 / (double)(d - 1) : 0.0; }
 
 // ---------------------------------------------------------------------------
 // Sweep geometry
@@ -566,10 +573,12 @@ extern "C" int ecc_soft_prepare(const void* x, int dtype, int ndim, const int64_
   SoftPrepSink sk{coeffs, field_c, field_lo, p->center, d3[0], d3[1], d3[2]};
   cudaStream_t s = (cudaStream_t)stream;
   if (dtype == ECC_DTYPE_F32) {
-    EffSrc<float> src{(const float*)x, p->alpha, p->u[0], p->u[1], p->u[2], d3[0], d3[1], d3[2], ndim};
+    EffSrc<float> src{(const float*)x, p->alpha, p->u[0], p->u[1], p->u[2], d3[0], d3[1], d3[2], ndim,
+                      coord_scale(d3[0]), coord_scale(d3[1]), coord_scale(d3[2])};
     return launch_sweep(src, sk, d3, batch, 0, s);
   } else if (dtype == ECC_DTYPE_F64) {
-    EffSrc<double> src{(const double*)x, p->alpha, p->u[0], p->u[1], p->u[2], d3[0], d3[1], d3[2], ndim};
+    EffSrc<double> src{(const double*)x, p->alpha, p->u[0], p->u[1], p->u[2], d3[0], d3[1], d3[2], ndim,
+                       coord_scale(d3[0]), coord_scale(d3[1]), coord_scale(d3[2])};
     return launch_sweep(src, sk, d3, batch, 0, s);
   }
   return set_error(ECC_EINVAL, "soft path takes float32 or float64 grids");
@@ -602,10 +611,12 @@ extern "C" int ecc_effective_field(const void* x, int dtype, int ndim, const int
   if (blocks < 1) return ECC_OK;
   cudaStream_t s = (cudaStream_t)stream;
   if (dtype == ECC_DTYPE_F32) {
-    EffSrc<float> src{(const float*)x, alpha, u[0], u[1], ndim == 3 ? u[2] : 0.0, d3[0], d3[1], d3[2], ndim};
+    EffSrc<float> src{(const float*)x, alpha, u[0], u[1], ndim == 3 ? u[2] : 0.0, d3[0], d3[1], d3[2], ndim,
+                      coord_scale(d3[0]), coord_scale(d3[1]), coord_scale(d3[2])};
     effective_field_kernel<float><<<(unsigned)blocks, 256, 0, s>>>(src, total, out);
   } else if (dtype == ECC_DTYPE_F64) {
-    EffSrc<double> src{(const double*)x, alpha, u[0], u[1], ndim == 3 ? u[2] : 0.0, d3[0], d3[1], d3[2], ndim};
+    EffSrc<double> src{(const double*)x, alpha, u[0], u[1], ndim == 3 ? u[2] : 0.0, d3[0], d3[1], d3[2], ndim,
+                       coord_scale(d3[0]), coord_scale(d3[1]), coord_scale(d3[2])};
     effective_field_kernel<double><<<(unsigned)blocks, 256, 0, s>>>(src, total, out);
   } else {
     return set_error(ECC_EINVAL, "effective field takes float32 or float64 grids");

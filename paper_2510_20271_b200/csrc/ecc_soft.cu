@@ -79,18 +79,22 @@ constexpr float B_MAX = 126.f - A_MAX;
 template <bool BWD>
 __device__ __forceinline__ void pair_loop_fact(const float (&at)[TT], const float (&upv)[TT], float (&acc)[TT], float b,
                                                float cf, float& w) {
+  // sigma = r = 1 / (1 + a_j b_p): one FFMA + one MUFU.RCP; sigma (1 - sigma)
+  // = r - r^2 (one FFMA; its absolute error ~1 ulp(1) is far below the
+  // normwise tolerance).  Two partial sums break the w dependency chain.
+  float w0 = 0.f, w1 = 0.f;
 #pragma unroll
   for (int t = 0; t < TT; ++t) {
-    const float e = at[t] * b;                          // e^{lam (f_p - tau_j)}
-    const float r = rcp_approx(e + 1.f);                // sigma
+    const float r = rcp_approx(__fmaf_rn(at[t], b, 1.f));
     if (!BWD) {
       acc[t] = __fmaf_rn(cf, r, acc[t]);
     } else {
-      const float s1 = (e * r) * r;                     // sigma (1 - sigma), no cancellation
-      w = __fmaf_rn(upv[t], s1, w);
+      const float s1 = __fmaf_rn(-r, r, r);
+      if (t & 1) w1 = __fmaf_rn(upv[t], s1, w1); else w0 = __fmaf_rn(upv[t], s1, w0);
       acc[t] = __fmaf_rn(cf, s1, acc[t]);
     }
   }
+  w = w0 + w1;
 }
 
 // direct mode (large lambda * threshold spread): the exponent
@@ -179,41 +183,41 @@ ecc_soft_kernel(SoftArgs a) {
   const int nslots = SNW * VW;
 
   // thresholds of this lane: j = l*TT + t, centred on the block's own centre
-  // m_l (factorised: a_j = 2^{-k (tau_j - m_l)}, b_{p,l} = 2^{k (f_p - m_l)})
-  float at[TT], upv[TT], acc[TT];
-  const int j0 = l * TT;
-  const int jl = min(j0 + TT, nb) - 1;
-  const double ml = (j0 < nb) ? 0.5 * (a.taus[j0] + a.taus[jl]) : a.m;
+  // m_l (factorised: a_j = 2^{-k (tau_j - m_l)}, b_{p,l} = 2^{k (f_p - m_l)}).
+  // The per-threshold factors are computed once per CTA into shared memory.
   const double ks = a.lam * LOG2E;
-#pragma unroll
-  for (int t = 0; t < TT; ++t) {
-    const int j = j0 + t;
-    float av, u = 0.f;
-    if (j < nb) {
-      av = FACT ? (float)exp2(-ks * (a.taus[j] - ml)) : 0.f;
-      if (BWD) u = (float)a.up[item * nb + j];
-    } else {
-      av = 0.f;
+  unsigned char* tail = smem_raw + ((sizeof(ChunkSmem) + 15) & ~size_t(15));
+  double* kt = reinterpret_cast<double*>(tail);                               // direct mode
+  float* atab = reinterpret_cast<float*>(tail + sizeof(double) * MAXB_PASS);  // factorised
+  if (FACT) {
+    for (int j = threadIdx.x; j < Lv * TT; j += SNT) {
+      float av = 0.f;
+      if (j < nb) {
+        const int b0 = (j / TT) * TT, b1 = min(b0 + TT, nb) - 1;
+        av = (float)exp2(-ks * (a.taus[j] - 0.5 * (a.taus[b0] + a.taus[b1])));
+      }
+      atab[j] = av;
     }
-    at[t] = av;
-    upv[t] = u;
-    acc[t] = 0.f;
-  }
-  const float koff = FACT ? (float)(ks * (a.m - ml)) : 0.f;   // k f_p - k m_l = k fc + koff
-  double* kt = reinterpret_cast<double*>(smem_raw + ((sizeof(ChunkSmem) + 15) & ~size_t(15)));
-  if (!FACT) {
+  } else {
     // kt[t * Lv + l] = ks (tau_{l TT + t} - m); padded thresholds -> +inf (sigma = 1, discarded)
     for (int q = threadIdx.x; q < Lv * TT; q += SNT) {
       const int tt = q / Lv, ll = q % Lv, j = ll * TT + tt;
       kt[q] = j < nb ? ks * (a.taus[j] - a.m) : (double)INFINITY;
     }
-    __syncthreads();
   }
+  __syncthreads();
+  float at[TT], upv[TT], acc[TT];
+  const int j0 = l * TT;
+  const int jl = min(j0 + TT, nb) - 1;
+  const double ml = (j0 < nb) ? 0.5 * (a.taus[j0] + a.taus[jl]) : a.m;
+#pragma unroll
+  for (int t = 0; t < TT; ++t) {
+    at[t] = FACT ? atab[j0 + t] : 0.f;
+    upv[t] = (BWD && j0 + t < nb) ? (float)a.up[item * nb + j0 + t] : 0.f;
+    acc[t] = 0.f;
+  }
+  const float koff = FACT ? (float)(ks * (a.m - ml)) : 0.f;   // k f_p - k m_l = k fc + koff
 
-  float g0 = 0.f, g1 = 0.f, g2 = 0.f;
-  const float sH = a.H > 1 ? (float)(2.0 / (double)(a.H - 1)) : 0.f;
-  const float sW = a.W > 1 ? (float)(2.0 / (double)(a.W - 1)) : 0.f;
-  const float sD = a.D > 1 ? (float)(2.0 / (double)(a.D - 1)) : 0.f;
   // warp-uniform trip count: the group reduction shuffles across the warp
   for (int kb = warp * VW; kb < count; kb += nslots) {
     const int k = kb + g;
@@ -231,23 +235,7 @@ ecc_soft_kernel(SoftArgs a) {
     }
     if (BWD) {
       for (int o = Lv >> 1; o; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
-      if (l == 0 && valid) {
-        const int64_t vi = v0 + (pk & 0xffff);
-        const float lw = (float)a.lam * w;
-        a.dX[item * a.n + vi] = -cf * lw;
-        // pos_p (soft.py:79-94) for G = sum c w pos
-        const float cw = cf * lw;
-        if (a.ndim == 2) {
-          const int64_t y = vi / a.W, x = vi - y * a.W;
-          g0 = __fmaf_rn(cw, a.H > 1 ? __fmaf_rn((float)y, sH, -1.f) : 0.f, g0);
-          g1 = __fmaf_rn(cw, a.W > 1 ? __fmaf_rn((float)x, sW, -1.f) : 0.f, g1);
-        } else {
-          const int64_t z = vi / (a.H * a.W), r = vi - z * a.H * a.W, y = r / a.W, x = r - y * a.W;
-          g0 = __fmaf_rn(cw, a.D > 1 ? __fmaf_rn((float)z, sD, -1.f) : 0.f, g0);
-          g1 = __fmaf_rn(cw, a.H > 1 ? __fmaf_rn((float)y, sH, -1.f) : 0.f, g1);
-          g2 = __fmaf_rn(cw, a.W > 1 ? __fmaf_rn((float)x, sW, -1.f) : 0.f, g2);
-        }
-      }
+      if (l == 0 && valid) a.dX[item * a.n + v0 + (pk & 0xffff)] = -cf * ((float)a.lam * w);
     }
   }
 
@@ -265,6 +253,40 @@ ecc_soft_kernel(SoftArgs a) {
   }
 
   if (BWD) {
+    // G = sum_p c_p w_p pos_p = -sum_p dX_p pos_p over this chunk (dX was
+    // just written by this CTA; zero-coefficient voxels hold 0).  Each thread
+    // takes a contiguous run of voxels and walks their coordinates.
+    const int per = (CH + SNT - 1) / SNT;
+    const int i0 = threadIdx.x * per, i1 = min(i0 + per, nvox);
+    float g0 = 0.f, g1 = 0.f, g2 = 0.f;
+    if (i0 < i1) {
+      const float sH = a.H > 1 ? (float)(2.0 / (double)(a.H - 1)) : 0.f;
+      const float sW = a.W > 1 ? (float)(2.0 / (double)(a.W - 1)) : 0.f;
+      const float sD = a.D > 1 ? (float)(2.0 / (double)(a.D - 1)) : 0.f;
+      const int64_t vi = v0 + i0;
+      int64_t z = vi / (a.H * a.W), r = vi - z * a.H * a.W, y = r / a.W, x = r - y * a.W;
+      const float* dxp = a.dX + item * a.n + v0;
+      for (int i = i0; i < i1; ++i) {
+        const float d = dxp[i];
+        if (d != 0.f) {
+          const float pz = a.D > 1 ? __fmaf_rn((float)z, sD, -1.f) : 0.f;
+          const float py = a.H > 1 ? __fmaf_rn((float)y, sH, -1.f) : 0.f;
+          const float px = a.W > 1 ? __fmaf_rn((float)x, sW, -1.f) : 0.f;
+          if (a.ndim == 2) {
+            g0 = __fmaf_rn(-d, py, g0);
+            g1 = __fmaf_rn(-d, px, g1);
+          } else {
+            g0 = __fmaf_rn(-d, pz, g0);
+            g1 = __fmaf_rn(-d, py, g1);
+            g2 = __fmaf_rn(-d, px, g2);
+          }
+        }
+        if (++x == a.W) {
+          x = 0;
+          if (++y == a.H) { y = 0; ++z; }
+        }
+      }
+    }
     double v0d = g0, v1d = g1, v2d = g2;
     for (int o = 16; o; o >>= 1) {
       v0d += __shfl_xor_sync(0xffffffffu, v0d, o);
@@ -304,7 +326,7 @@ __global__ void ecc_soft_reduce_g(const double* __restrict__ gpart, int64_t chun
 }
 
 static size_t soft_smem() {
-  size_t chunk = ((sizeof(ChunkSmem) + 15) & ~size_t(15)) + sizeof(double) * MAXB_PASS;   // + direct-mode table
+  size_t chunk = ((sizeof(ChunkSmem) + 15) & ~size_t(15)) + (sizeof(double) + sizeof(float)) * MAXB_PASS;
   size_t red = sizeof(float) * (size_t)SNT * TT;   // nslots*rowlen = 8*VW*Lv*TT = 256*TT
   return chunk > red ? chunk : red;
 }
