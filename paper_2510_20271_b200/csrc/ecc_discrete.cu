@@ -364,6 +364,38 @@ __global__ void ecc_minmax_kernel(const T* __restrict__ x, int64_t n, unsigned l
   }
 }
 
+// float32 specialisation: 16-byte loads, float min/max, one key conversion per thread
+__global__ void ecc_minmax_f32v_kernel(const float4* __restrict__ x4, int64_t n4, const float* __restrict__ tail,
+                                       int ntail, unsigned long long* out) {
+  float mn = INFINITY, mx = -INFINITY;
+  unsigned long long bad = 0;
+  auto take = [&](float v) {
+    if (!(fabsf(v) <= 3.402823466e38f)) { ++bad; return; }
+    mn = fminf(mn, v);
+    mx = fmaxf(mx, v);
+  };
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 v = __ldcs(x4 + i);
+    take(v.x); take(v.y); take(v.z); take(v.w);
+  }
+  if (blockIdx.x == 0 && threadIdx.x < ntail) take(tail[threadIdx.x]);
+  unsigned long long kmn = mn <= mx ? f64_key((double)mn) : ~0ull;
+  unsigned long long kmx = mn <= mx ? f64_key((double)mx) : 0ull;
+  for (int o = 16; o; o >>= 1) {
+    unsigned long long a = __shfl_xor_sync(0xffffffffu, kmn, o);
+    unsigned long long b = __shfl_xor_sync(0xffffffffu, kmx, o);
+    unsigned long long c = __shfl_xor_sync(0xffffffffu, bad, o);
+    kmn = a < kmn ? a : kmn;
+    kmx = b > kmx ? b : kmx;
+    bad += c;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(out + 0, kmn);
+    atomicMax(out + 1, kmx);
+    if (bad) atomicAdd(out + 2, bad);
+  }
+}
+
 __global__ void ecc_minmax_init(unsigned long long* out) {
   out[0] = ~0ull;
   out[1] = 0ull;
@@ -554,7 +586,18 @@ extern "C" int ecc_minmax(const void* x, int dtype, int64_t n, uint64_t* out3, v
   if (blocks < 1) blocks = 1;
   switch (dtype) {
     case ECC_DTYPE_U8: ecc_minmax_kernel<uint8_t><<<(unsigned)blocks, 256, 0, s>>>((const uint8_t*)x, n, o); break;
-    case ECC_DTYPE_F32: ecc_minmax_kernel<float><<<(unsigned)blocks, 256, 0, s>>>((const float*)x, n, o); break;
+    case ECC_DTYPE_F32:
+      if (((uintptr_t)x & 15u) == 0) {
+        const int64_t n4 = n / 4;
+        int64_t b4 = (n4 + 255) / 256;
+        if (b4 > cap) b4 = cap;
+        if (b4 < 1) b4 = 1;
+        ecc_minmax_f32v_kernel<<<(unsigned)b4, 256, 0, s>>>((const float4*)x, n4, (const float*)x + 4 * n4,
+                                                              (int)(n - 4 * n4), o);
+      } else {
+        ecc_minmax_kernel<float><<<(unsigned)blocks, 256, 0, s>>>((const float*)x, n, o);
+      }
+      break;
     case ECC_DTYPE_F64: ecc_minmax_kernel<double><<<(unsigned)blocks, 256, 0, s>>>((const double*)x, n, o); break;
     default: return set_error(ECC_EINVAL, "unsupported dtype");
   }

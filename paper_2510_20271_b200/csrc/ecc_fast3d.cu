@@ -300,7 +300,18 @@ ecc_fast3d_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* 
 
         // edge bits (segment boundary) by direct comparison q < p
         const float* r1 = P1 + lane * PITCH + col0;   // own row, plane s-1
-        const float p0v = r1[0], p31 = r1[31];
+        // the 32 values of the voxels being finalised, loaded early: they are
+        // consumed by the per-voxel stage after the word logic below
+        float xrow[32];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float4 t4 = reinterpret_cast<const float4*>(r1)[k];
+          xrow[4 * k] = t4.x;
+          xrow[4 * k + 1] = t4.y;
+          xrow[4 * k + 2] = t4.z;
+          xrow[4 * k + 3] = t4.w;
+        }
+        const float p0v = xrow[0], p31 = xrow[31];
         const float* r1u = P1 + rp * PITCH + col0;    // row y+1, plane s-1
         const float* r0d = P0 + rm * PITCH + col0;    // row y-1, plane s
         const float* r0c = P0 + lane * PITCH + col0;  // row y,   plane s
@@ -428,26 +439,29 @@ ecc_fast3d_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* 
 
         // ---- per voxel: bin (cell table) + shared-memory reduction ----------
         if (__any_sync(FULL, (r0 | r1b | r2 | r3) != 0u)) {
-          const float4* r14 = reinterpret_cast<const float4*>(r1);
           if (lut_ok) {
-            // 8 voxels at a time: cells, table entries, then the reductions
+            // groups of 8 voxels, software-pipelined: the table entries of
+            // group h+1 are in flight while group h is binned and reduced
+            LutEntry e[2][8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float gg = __saturatef(__fmaf_rn(xrow[j], lut_scale, lut_bias));
+              e[0][j] = lut_b[__float_as_uint(__fadd_rz(gg, 1.0f)) >> cell_shift];
+            }
 #pragma unroll
             for (int h = 0; h < 4; ++h) {
-              const float4 xa = r14[2 * h], xb = r14[2 * h + 1];
-              const float xv[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
-              uint32_t cell[8];
-              LutEntry e[8];
+              if (h < 3) {
 #pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                const float gg = __saturatef(__fmaf_rn(xv[j], lut_scale, lut_bias));
-                cell[j] = __float_as_uint(__fadd_rz(gg, 1.0f)) >> cell_shift;
+                for (int j = 0; j < 8; ++j) {
+                  const float gg = __saturatef(__fmaf_rn(xrow[8 * (h + 1) + j], lut_scale, lut_bias));
+                  e[(h + 1) & 1][j] = lut_b[__float_as_uint(__fadd_rz(gg, 1.0f)) >> cell_shift];
+                }
               }
-#pragma unroll
-              for (int j = 0; j < 8; ++j) e[j] = lut_b[cell[j]];
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
                 const int cc = ((int)(Q[h] << (28 - 4 * j))) >> 28;
-                const int bin = e[j].b + (xv[j] > e[j].t ? 1 : 0);
+                const LutEntry ee = e[h & 1][j];
+                const int bin = ee.b + (xrow[8 * h + j] > ee.t ? 1 : 0);
                 atomicAdd(&s_hist[bin], cc);   // c == 0 adds nothing
               }
             }
@@ -456,7 +470,7 @@ ecc_fast3d_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* 
             for (int i = 0; i < 32; ++i) {
               const int cc = ((int)(Q[i >> 3] << (28 - 4 * (i & 7)))) >> 28;
               if (cc) {
-                const float xv = r1[i];
+                const float xv = xrow[i];
                 int lo = 0, hi = nb;
                 while (lo < hi) {
                   const int mid = (lo + hi) >> 1;
