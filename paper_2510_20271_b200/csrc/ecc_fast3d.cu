@@ -149,6 +149,17 @@ __device__ __forceinline__ void lds_entry(uint32_t addr, float& t, uint32_t& b) 
 __device__ __forceinline__ float f4get(const float4& v, int j) {
   return j == 0 ? v.x : (j == 1 ? v.y : (j == 2 ? v.z : v.w));
 }
+// predicated shared-memory reduction: lanes with v == 0 do not touch the bank
+__device__ __forceinline__ void red_add_shared_nz(uint32_t addr, int v) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.s32 p, %1, 0;\n"
+      "@p red.shared.add.s32 [%0], %1;\n"
+      "}\n" ::"r"(addr),
+      "r"(v)
+      : "memory");
+}
 __device__ __forceinline__ void red_add_shared(uint32_t addr, int v) {
   asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
@@ -181,7 +192,13 @@ ecc_fast3d_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* 
   const LutEntry* lut_g = reinterpret_cast<const LutEntry*>(tab_g + ((nb + 2 + 1) & ~1));
   for (int i = threadIdx.x; i <= nb; i += NT) s_hist[i] = 0;
   if (lut_ok) {
-    for (int i = threadIdx.x; i <= cells; i += NT) s_lut[i] = lut_g[i];
+    // entries carry the shared-memory byte address of their histogram bin
+    const uint32_t hbase = smem_u32(s_hist);
+    for (int i = threadIdx.x; i <= cells; i += NT) {
+      LutEntry e = lut_g[i];
+      e.b = (int)(hbase + 4u * (uint32_t)e.b);
+      s_lut[i] = e;
+    }
   } else {
     for (int i = threadIdx.x; i < nb + 2; i += NT) s_tab[i] = tab_g[i];
   }
@@ -265,7 +282,11 @@ ecc_fast3d_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* 
       const float* P1 = planes + stage_of(s - 1) * PLANE;  // plane s-1
 
       // ---- the 13 negative-offset words of plane s (rows double-buffered) ----
+      // The own row of plane s-1 (Ro) stays live: its values are the voxels
+      // finalised below; the rows' halo values feed the segment-edge bits.
       uint32_t N0[NNEG];
+      Row Ro;
+      float h0l, h0r, hml, hmr, hpl, hpr;   // halos: own(s), row y-1 (s), row y+1 (s-1)
       {
         float pc[32];
         Row A, B;
@@ -274,13 +295,19 @@ ecc_fast3d_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* 
 #pragma unroll
         for (int i = 0; i < 32; ++i) pc[i] = A.v[i] + 0.0f;   // -0 -> +0
         N0[NX] = word1([&](int i) { return i ? A.v[i - 1] : A.l; }, pc);
+        h0l = A.l;
+        h0r = A.r;
         load_row(A, P1, rm, col0);
         words3(B, pc, N0[NYM_XM], N0[NYM_X0], N0[NYM_XP]);
-        load_row(B, P1, lane, col0);
+        hml = B.l;
+        hmr = B.r;
+        load_row(B, P1, rp, col0);
         words3(A, pc, N0[NZ_YM_XM], N0[NZ_YM_X0], N0[NZ_YM_XP]);
-        load_row(A, P1, rp, col0);
-        words3(B, pc, N0[NZ_Y0_XM], N0[NZ_Y0_X0], N0[NZ_Y0_XP]);
-        words3(A, pc, N0[NZ_YP_XM], N0[NZ_YP_X0], N0[NZ_YP_XP]);
+        load_row(Ro, P1, lane, col0);
+        words3(B, pc, N0[NZ_YP_XM], N0[NZ_YP_X0], N0[NZ_YP_XP]);
+        hpl = B.l;
+        hpr = B.r;
+        words3(Ro, pc, N0[NZ_Y0_XM], N0[NZ_Y0_X0], N0[NZ_Y0_XP]);
       }
 
       if (s > zs) {
@@ -298,30 +325,16 @@ ecc_fast3d_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* 
         const uint32_t e_0 = __shfl_down_sync(FULL, N0[NZ_YM_X0], 1);
         const uint32_t e_p = __shfl_down_sync(FULL, N0[NZ_YM_XP], 1);
 
-        // edge bits (segment boundary) by direct comparison q < p
-        const float* r1 = P1 + lane * PITCH + col0;   // own row, plane s-1
-        // the 32 values of the voxels being finalised, loaded early: they are
-        // consumed by the per-voxel stage after the word logic below
-        float xrow[32];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const float4 t4 = reinterpret_cast<const float4*>(r1)[k];
-          xrow[4 * k] = t4.x;
-          xrow[4 * k + 1] = t4.y;
-          xrow[4 * k + 2] = t4.z;
-          xrow[4 * k + 3] = t4.w;
-        }
-        const float p0v = xrow[0], p31 = xrow[31];
-        const float* r1u = P1 + rp * PITCH + col0;    // row y+1, plane s-1
-        const float* r0d = P0 + rm * PITCH + col0;    // row y-1, plane s
-        const float* r0c = P0 + lane * PITCH + col0;  // row y,   plane s
-        const float* r0u = P0 + rp * PITCH + col0;    // row y+1, plane s
-        const uint32_t E_x = (uint32_t)(r1[32] < p31) << 31;
-        const uint32_t E_yp_xp = (uint32_t)(r1u[32] < p31) << 31;
-        const uint32_t E_yp_xm = (uint32_t)(r1u[-1] < p0v);
-        const uint32_t E_zp_ym_xp = (uint32_t)(r0d[32] < p31) << 31, E_zp_ym_xm = (uint32_t)(r0d[-1] < p0v);
-        const uint32_t E_zp_y0_xp = (uint32_t)(r0c[32] < p31) << 31, E_zp_y0_xm = (uint32_t)(r0c[-1] < p0v);
-        const uint32_t E_zp_yp_xp = (uint32_t)(r0u[32] < p31) << 31, E_zp_yp_xm = (uint32_t)(r0u[-1] < p0v);
+        // edge bits (segment boundary) by direct comparison q < p; the q's are
+        // halo values of rows already loaded (row y+1 of plane s via shuffle)
+        const float p0v = Ro.v[0], p31 = Ro.v[31];
+        const float hul = __shfl_down_sync(FULL, h0l, 1), hur = __shfl_down_sync(FULL, h0r, 1);
+        const uint32_t E_x = (uint32_t)(Ro.r < p31) << 31;
+        const uint32_t E_yp_xp = (uint32_t)(hpr < p31) << 31;
+        const uint32_t E_yp_xm = (uint32_t)(hpl < p0v);
+        const uint32_t E_zp_ym_xp = (uint32_t)(hmr < p31) << 31, E_zp_ym_xm = (uint32_t)(hml < p0v);
+        const uint32_t E_zp_y0_xp = (uint32_t)(h0r < p31) << 31, E_zp_y0_xm = (uint32_t)(h0l < p0v);
+        const uint32_t E_zp_yp_xp = (uint32_t)(hur < p31) << 31, E_zp_yp_xm = (uint32_t)(hul < p0v);
 
         const uint32_t mz = (s < g.D) ? FULL : 0u;             // plane s exists
         const uint32_t myu = row_up_ok ? FULL : 0u;
@@ -445,7 +458,7 @@ ecc_fast3d_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* 
             LutEntry e[2][8];
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-              const float gg = __saturatef(__fmaf_rn(xrow[j], lut_scale, lut_bias));
+              const float gg = __saturatef(__fmaf_rn(Ro.v[j], lut_scale, lut_bias));
               e[0][j] = lut_b[__float_as_uint(__fadd_rz(gg, 1.0f)) >> cell_shift];
             }
 #pragma unroll
@@ -453,7 +466,7 @@ ecc_fast3d_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* 
               if (h < 3) {
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
-                  const float gg = __saturatef(__fmaf_rn(xrow[8 * (h + 1) + j], lut_scale, lut_bias));
+                  const float gg = __saturatef(__fmaf_rn(Ro.v[8 * (h + 1) + j], lut_scale, lut_bias));
                   e[(h + 1) & 1][j] = lut_b[__float_as_uint(__fadd_rz(gg, 1.0f)) >> cell_shift];
                 }
               }
@@ -461,8 +474,8 @@ ecc_fast3d_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* 
               for (int j = 0; j < 8; ++j) {
                 const int cc = ((int)(Q[h] << (28 - 4 * j))) >> 28;
                 const LutEntry ee = e[h & 1][j];
-                const int bin = ee.b + (xrow[8 * h + j] > ee.t ? 1 : 0);
-                atomicAdd(&s_hist[bin], cc);   // c == 0 adds nothing
+                const uint32_t addr = (uint32_t)ee.b + (Ro.v[8 * h + j] > ee.t ? 4u : 0u);
+                red_add_shared_nz(addr, cc);
               }
             }
           } else {
@@ -470,7 +483,7 @@ ecc_fast3d_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* 
             for (int i = 0; i < 32; ++i) {
               const int cc = ((int)(Q[i >> 3] << (28 - 4 * (i & 7)))) >> 28;
               if (cc) {
-                const float xv = xrow[i];
+                const float xv = Ro.v[i];
                 int lo = 0, hi = nb;
                 while (lo < hi) {
                   const int mid = (lo + hi) >> 1;
