@@ -67,6 +67,20 @@ __device__ __forceinline__ int coeff3(const V (&v)[3][3][3]) {
   return __popc(pos | ((~neg & EVA) << 1) | ((Lm ^ 1u) << 28) | ((Lp ^ 1u) << 29)) - 13;
 }
 
+// 2D coefficient (coefficients.py:109-126 on a 3x3 window v[dy][dx]):
+// c2(P) = 1 - #lower axis neighbours + #lower quadrant triples.
+template <typename V>
+__device__ __forceinline__ int coeff2(const V (&v)[3][3]) {
+  const V p = v[1][1];
+  const uint32_t P = (uint32_t)(v[1][2] < p) | ((uint32_t)(v[2][2] < p) << 1) | ((uint32_t)(v[2][1] < p) << 2) |
+                     ((uint32_t)(v[2][0] < p) << 3) | ((uint32_t)(v[1][0] <= p) << 4) |
+                     ((uint32_t)(v[0][0] <= p) << 5) | ((uint32_t)(v[0][1] <= p) << 6) |
+                     ((uint32_t)(v[0][2] <= p) << 7);
+  const uint32_t P9 = P | ((P & 1u) << 8);
+  const uint32_t sq = P9 & (P9 >> 1) & (P9 >> 2);
+  return __popc((sq & 0x55u) | ((~P & 0x55u) << 1)) - 3;
+}
+
 // ---------------------------------------------------------------------------
 // Binning: smallest j with x <= tau_j (grid.py:168-180, searchsorted-left).
 // The table holds the thresholds in the compare type with sentinels:

@@ -604,6 +604,45 @@ extern "C" int ecc_minmax(const void* x, int dtype, int64_t n, uint64_t* out3, v
   return check_launch("ecc_minmax_kernel");
 }
 
+namespace ecc {
+// 2D soft prepare: one CTA per 32x8 pixel tile; the float64 effective field of
+// the tile and its one-pixel halo is built once in shared memory (NaN outside
+// the grid), then each thread writes its pixel's coefficient and centred field.
+template <typename T>
+__global__ void __launch_bounds__(256) soft_prep2d_kernel(EffSrc<T> src, double center, int8_t* __restrict__ coeffs,
+                                                          float* __restrict__ fc, float* __restrict__ fclo) {
+  __shared__ double tile[10][34];
+  const int64_t n = blockIdx.z;
+  const int64_t y0 = (int64_t)blockIdx.y * 8, x0 = (int64_t)blockIdx.x * 32;
+  const int64_t H = src.H, W = src.W;
+  const int64_t base = n * H * W;
+  const double nanv = __longlong_as_double(0x7ff8000000000000ll);
+  for (int e = threadIdx.x; e < 340; e += 256) {
+    const int ry = e / 34, rx = e - ry * 34;
+    const int64_t yy = y0 - 1 + ry, xx = x0 - 1 + rx;
+    double v = nanv;
+    if (yy >= 0 && yy < H && xx >= 0 && xx < W) v = src.at(base + yy * W + xx, 0, yy, xx);
+    tile[ry][rx] = v;
+  }
+  __syncthreads();
+  const int ty = threadIdx.x >> 5, tx = threadIdx.x & 31;
+  const int64_t y = y0 + ty, x = x0 + tx;
+  if (y < H && x < W) {
+    double v[3][3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) v[a][b] = tile[ty + a][tx + b];
+    const int64_t i = base + y * W + x;
+    coeffs[i] = (int8_t)coeff2<double>(v);
+    const double d = v[1][1] - center;
+    const float hi = (float)d;
+    fc[i] = hi;
+    if (fclo) fclo[i] = (float)(d - (double)hi);
+  }
+}
+}  // namespace ecc
+
 extern "C" int ecc_soft_prepare(const void* x, int dtype, int ndim, const int64_t* dims, int64_t batch,
                                 const ecc_soft_params* p, int8_t* coeffs, float* field_c, float* field_lo,
                                 void* stream) {
@@ -615,6 +654,21 @@ extern "C" int ecc_soft_prepare(const void* x, int dtype, int ndim, const int64_
   if (batch < 1) return set_error(ECC_EINVAL, "batch must be >= 1");
   SoftPrepSink sk{coeffs, field_c, field_lo, p->center, d3[0], d3[1], d3[2]};
   cudaStream_t s = (cudaStream_t)stream;
+  if (ndim == 2 && batch <= 65535 && (dtype == ECC_DTYPE_F32 || dtype == ECC_DTYPE_F64)) {
+    dim3 grid((unsigned)((d3[2] + 31) / 32), (unsigned)((d3[1] + 7) / 8), (unsigned)batch);
+    if (grid.y > 65535) goto generic;
+    if (dtype == ECC_DTYPE_F32) {
+      EffSrc<float> src{(const float*)x, p->alpha, p->u[0], p->u[1], 0.0, 1, d3[1], d3[2], 2,
+                        0.0, coord_scale(d3[1]), coord_scale(d3[2])};
+      soft_prep2d_kernel<float><<<grid, 256, 0, s>>>(src, p->center, coeffs, field_c, field_lo);
+    } else {
+      EffSrc<double> src{(const double*)x, p->alpha, p->u[0], p->u[1], 0.0, 1, d3[1], d3[2], 2,
+                         0.0, coord_scale(d3[1]), coord_scale(d3[2])};
+      soft_prep2d_kernel<double><<<grid, 256, 0, s>>>(src, p->center, coeffs, field_c, field_lo);
+    }
+    return check_launch("soft_prep2d_kernel");
+  }
+generic:
   if (dtype == ECC_DTYPE_F32) {
     EffSrc<float> src{(const float*)x, p->alpha, p->u[0], p->u[1], p->u[2], d3[0], d3[1], d3[2], ndim,
                       coord_scale(d3[0]), coord_scale(d3[1]), coord_scale(d3[2])};

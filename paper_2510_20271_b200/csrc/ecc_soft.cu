@@ -20,6 +20,7 @@
 // Partials are reduced in a fixed order (deterministic, bit-reproducible
 // across runs), fp32 within a lane over its voxels, fp64 across lanes/CTAs.
 #include <math.h>
+#include <stdlib.h>
 
 #include "ecc_common.cuh"
 #include "ecc_internal.h"
@@ -76,20 +77,23 @@ struct ChunkSmem {
 constexpr float A_MAX = 40.f;
 constexpr float B_MAX = 126.f - A_MAX;
 
-template <bool BWD>
-__device__ __forceinline__ void pair_loop_fact(const float (&at)[TT], const float (&upv)[TT], float (&acc)[TT], float b,
+template <bool BWD, int T>
+__device__ __forceinline__ void pair_loop_fact(const float (&at)[T], const float (&upv)[T], float (&acc)[T], float b,
                                                float cf, float& w) {
   // sigma = r = 1 / (1 + a_j b_p): one FFMA + one MUFU.RCP; sigma (1 - sigma)
   // = r - r^2 (one FFMA; its absolute error ~1 ulp(1) is far below the
-  // normwise tolerance).  Two partial sums break the w dependency chain.
+  // normwise tolerance).  All reciprocals are issued before any is consumed
+  // so the MUFU latency overlaps; two partial sums break the w chain.
+  float r[T];
+#pragma unroll
+  for (int t = 0; t < T; ++t) r[t] = rcp_approx(__fmaf_rn(at[t], b, 1.f));
   float w0 = 0.f, w1 = 0.f;
 #pragma unroll
-  for (int t = 0; t < TT; ++t) {
-    const float r = rcp_approx(__fmaf_rn(at[t], b, 1.f));
+  for (int t = 0; t < T; ++t) {
     if (!BWD) {
-      acc[t] = __fmaf_rn(cf, r, acc[t]);
+      acc[t] = __fmaf_rn(cf, r[t], acc[t]);
     } else {
-      const float s1 = __fmaf_rn(-r, r, r);
+      const float s1 = __fmaf_rn(-r[t], r[t], r[t]);
       if (t & 1) w1 = __fmaf_rn(upv[t], s1, w1); else w0 = __fmaf_rn(upv[t], s1, w0);
       acc[t] = __fmaf_rn(cf, s1, acc[t]);
     }
@@ -100,11 +104,11 @@ __device__ __forceinline__ void pair_loop_fact(const float (&at)[TT], const floa
 // direct mode (large lambda * threshold spread): the exponent
 // lam log2(e) (f_p - tau_j) is formed in float64 (f_p carried as two floats,
 // kt_j = lam log2(e) (tau_j - m) from a transposed shared table), then ex2 + rcp
-template <bool BWD>
-__device__ __forceinline__ void pair_loop_direct(const double* __restrict__ kt, int Lv, int l, const float (&upv)[TT],
-                                                 float (&acc)[TT], double kf, float cf, float& w) {
+template <bool BWD, int T>
+__device__ __forceinline__ void pair_loop_direct(const double* __restrict__ kt, int Lv, int l, const float (&upv)[T],
+                                                 float (&acc)[T], double kf, float cf, float& w) {
 #pragma unroll
-  for (int t = 0; t < TT; ++t) {
+  for (int t = 0; t < T; ++t) {
     const double z = kf - kt[t * Lv + l];
     const float e = ex2_approx(fminf((float)z, 100.f));
     const float r = rcp_approx(e + 1.f);
@@ -118,8 +122,8 @@ __device__ __forceinline__ void pair_loop_direct(const double* __restrict__ kt, 
   }
 }
 
-template <bool BWD, bool FACT>
-__global__ void __launch_bounds__(SNT, 2)
+template <bool BWD, bool FACT, int T>
+__global__ void __launch_bounds__(SNT, (T == 16 ? 3 : 2))
 ecc_soft_kernel(SoftArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ChunkSmem& S = *reinterpret_cast<ChunkSmem*>(smem_raw);
@@ -175,14 +179,14 @@ ecc_soft_kernel(SoftArgs a) {
   // ---- lane groups: Lv lanes cover one voxel's thresholds -----------------
   const int nb = a.nb;
   int Lv = 1;
-  while (Lv * TT < nb) Lv <<= 1;
+  while (Lv * T < nb) Lv <<= 1;
   const int VW = 32 / Lv;               // voxels per warp in flight
   const int g = lane / Lv;              // voxel slot within the warp
   const int l = lane % Lv;              // threshold block of this lane
   const int slot = warp * VW + g;
   const int nslots = SNW * VW;
 
-  // thresholds of this lane: j = l*TT + t, centred on the block's own centre
+  // thresholds of this lane: j = l*T + t, centred on the block's own centre
   // m_l (factorised: a_j = 2^{-k (tau_j - m_l)}, b_{p,l} = 2^{k (f_p - m_l)}).
   // The per-threshold factors are computed once per CTA into shared memory.
   const double ks = a.lam * LOG2E;
@@ -190,28 +194,28 @@ ecc_soft_kernel(SoftArgs a) {
   double* kt = reinterpret_cast<double*>(tail);                               // direct mode
   float* atab = reinterpret_cast<float*>(tail + sizeof(double) * MAXB_PASS);  // factorised
   if (FACT) {
-    for (int j = threadIdx.x; j < Lv * TT; j += SNT) {
+    for (int j = threadIdx.x; j < Lv * T; j += SNT) {
       float av = 0.f;
       if (j < nb) {
-        const int b0 = (j / TT) * TT, b1 = min(b0 + TT, nb) - 1;
+        const int b0 = (j / T) * T, b1 = min(b0 + T, nb) - 1;
         av = (float)exp2(-ks * (a.taus[j] - 0.5 * (a.taus[b0] + a.taus[b1])));
       }
       atab[j] = av;
     }
   } else {
-    // kt[t * Lv + l] = ks (tau_{l TT + t} - m); padded thresholds -> +inf (sigma = 1, discarded)
-    for (int q = threadIdx.x; q < Lv * TT; q += SNT) {
-      const int tt = q / Lv, ll = q % Lv, j = ll * TT + tt;
+    // kt[t * Lv + l] = ks (tau_{l T + t} - m); padded thresholds -> +inf (sigma = 1, discarded)
+    for (int q = threadIdx.x; q < Lv * T; q += SNT) {
+      const int tt = q / Lv, ll = q % Lv, j = ll * T + tt;
       kt[q] = j < nb ? ks * (a.taus[j] - a.m) : (double)INFINITY;
     }
   }
   __syncthreads();
-  float at[TT], upv[TT], acc[TT];
-  const int j0 = l * TT;
-  const int jl = min(j0 + TT, nb) - 1;
+  float at[T], upv[T], acc[T];
+  const int j0 = l * T;
+  const int jl = min(j0 + T, nb) - 1;
   const double ml = (j0 < nb) ? 0.5 * (a.taus[j0] + a.taus[jl]) : a.m;
 #pragma unroll
-  for (int t = 0; t < TT; ++t) {
+  for (int t = 0; t < T; ++t) {
     at[t] = FACT ? atab[j0 + t] : 0.f;
     upv[t] = (BWD && j0 + t < nb) ? (float)a.up[item * nb + j0 + t] : 0.f;
     acc[t] = 0.f;
@@ -228,22 +232,24 @@ ecc_soft_kernel(SoftArgs a) {
     float w = 0.f;
     if (FACT) {
       const float kf = fminf(fmaxf(__fmaf_rn(a.kscale, f, koff), -B_MAX), B_MAX);
-      pair_loop_fact<BWD>(at, upv, acc, ex2_approx(kf), cf, w);
+      pair_loop_fact<BWD, T>(at, upv, acc, ex2_approx(kf), cf, w);
     } else {
       const double fd = (double)f + (double)(valid ? S.fclo[k] : 0.f);
-      pair_loop_direct<BWD>(kt, Lv, l, upv, acc, ks * fd, cf, w);
+      pair_loop_direct<BWD, T>(kt, Lv, l, upv, acc, ks * fd, cf, w);
     }
     if (BWD) {
-      for (int o = Lv >> 1; o; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+#pragma unroll
+      for (int o = 16; o; o >>= 1)
+        if (o < Lv) w += __shfl_xor_sync(0xffffffffu, w, o);   // Lv is warp-uniform
       if (l == 0 && valid) a.dX[item * a.n + v0 + (pk & 0xffff)] = -cf * ((float)a.lam * w);
     }
   }
 
   // ---- fixed-order reduction of acc over the CTA's voxel slots ------------
   __syncthreads();   // chunk arrays no longer needed (red aliases them)
-  const int rowlen = Lv * TT;
+  const int rowlen = Lv * T;
 #pragma unroll
-  for (int t = 0; t < TT; ++t) red[slot * rowlen + l * TT + t] = acc[t];
+  for (int t = 0; t < T; ++t) red[slot * rowlen + l * T + t] = acc[t];
   __syncthreads();
   double* out = a.part + (item * a.chunks + chunk) * nb;
   for (int j = threadIdx.x; j < nb; j += SNT) {
@@ -389,7 +395,12 @@ static int soft_launch(const int8_t* coeffs, const float* fc, const float* fclo,
   a.dX = dX;
   cudaStream_t s = (cudaStream_t)stream;
   const size_t smem = soft_smem();
-  auto kfn = p->factorized ? ecc_soft_kernel<BWD, true> : ecc_soft_kernel<BWD, false>;
+  // 32 thresholds per lane (fewer w shuffles per pair); ECC_SOFT_BWD_T=16
+  // selects the half-register backward variant (measured equal on B200)
+  const char* tenv = getenv("ECC_SOFT_BWD_T");
+  const bool t16 = BWD && nbins <= 16 * 32 && (tenv && tenv[0] == '1');
+  auto kfn = p->factorized ? (t16 ? ecc_soft_kernel<BWD, true, 16> : ecc_soft_kernel<BWD, true, 32>)
+                           : (t16 ? ecc_soft_kernel<BWD, false, 16> : ecc_soft_kernel<BWD, false, 32>);
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(soft)");
   const int64_t grid = batch * chunks;

@@ -107,7 +107,7 @@ class ScalarGrid:
         """Contiguous CUDA tensor (uint8/float32/float64) holding the values exactly."""
         if self._dev is None:
             dev = _lib.device()
-            self._dev = torch.from_numpy(np.ascontiguousarray(_narrowest_exact(self._host))).to(dev)
+            self._dev = torch.from_numpy(np.array(_narrowest_exact(self._host), order="C", copy=True)).to(dev)
         return self._dev
 
 
