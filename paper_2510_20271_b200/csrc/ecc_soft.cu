@@ -309,26 +309,50 @@ ecc_soft_kernel(SoftArgs a) {
   }
 }
 
-// K7: out[b][j] = scale_j * sum_c part[b][c][j] (fixed order over c)
-__global__ void ecc_soft_reduce(const double* __restrict__ part, int64_t chunks, int nb, const double* __restrict__ up,
-                                double lam, double* __restrict__ out) {
-  const int64_t item = blockIdx.y;
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < nb; j += gridDim.x * blockDim.x) {
-    const double* p = part + item * chunks * nb + j;
-    double s = 0.0;
-    for (int64_t c = 0; c < chunks; ++c) s += p[c * nb];
-    if (up) s *= up[item * nb + j] * lam;
-    out[item * nb + j] = s;
-  }
+// K7: out[b][j] = scale_j * sum_c part[b][c][j] in a fixed order: stage 1
+// sums contiguous groups of chunks (grid over bins x groups x items), stage 2
+// sums the group partials; both orders are fixed, so runs are bit-identical.
+constexpr int RGROUPS = 128;
+__global__ void ecc_soft_reduce1(const double* __restrict__ part, int64_t chunks, int nb, int64_t per_group,
+                                 double* __restrict__ gpart) {
+  const int64_t item = blockIdx.z, grp = blockIdx.y;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= nb) return;
+  const int64_t c0 = grp * per_group, c1 = min(c0 + per_group, chunks);
+  const double* p = part + item * chunks * nb + j;
+  double s = 0.0;
+  for (int64_t c = c0; c < c1; ++c) s += p[c * nb];
+  gpart[(item * gridDim.y + grp) * nb + j] = s;
 }
 
+__global__ void ecc_soft_reduce2(const double* __restrict__ gpart, int groups, int nb, const double* __restrict__ up,
+                                 double lam, double* __restrict__ out) {
+  const int64_t item = blockIdx.y;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= nb) return;
+  const double* p = gpart + item * groups * nb + j;
+  double s = 0.0;
+  for (int g = 0; g < groups; ++g) s += p[(int64_t)g * nb];
+  if (up) s *= up[item * nb + j] * lam;
+  out[item * nb + j] = s;
+}
+
+// G[item][0..ndim) = sum over chunks of gpart[item][chunk][0..ndim), fixed order:
+// strided per-thread sums, then a fixed shared-memory tree
 __global__ void ecc_soft_reduce_g(const double* __restrict__ gpart, int64_t chunks, int ndim, double* __restrict__ G) {
+  __shared__ double sm[256][3];
   const int64_t item = blockIdx.x;
-  if (threadIdx.x < ndim) {
-    double s = 0.0;
-    for (int64_t c = 0; c < chunks; ++c) s += gpart[(item * chunks + c) * 4 + threadIdx.x];
-    G[item * ndim + threadIdx.x] = s;
+  double a[3] = {0.0, 0.0, 0.0};
+  for (int64_t c = threadIdx.x; c < chunks; c += blockDim.x)
+    for (int d = 0; d < 3; ++d) a[d] += gpart[(item * chunks + c) * 4 + d];
+  for (int d = 0; d < 3; ++d) sm[threadIdx.x][d] = a[d];
+  __syncthreads();
+  for (int o = blockDim.x >> 1; o; o >>= 1) {
+    if (threadIdx.x < o)
+      for (int d = 0; d < 3; ++d) sm[threadIdx.x][d] += sm[threadIdx.x + o][d];
+    __syncthreads();
   }
+  if (threadIdx.x < ndim) G[item * ndim + threadIdx.x] = sm[0][threadIdx.x];
 }
 
 static size_t soft_smem() {
@@ -354,7 +378,9 @@ extern "C" size_t ecc_soft_workspace_bytes(int ndim, const int64_t* dims, int64_
   if (soft_dims(ndim, dims, d3)) return 0;
   const int64_t n = d3[0] * d3[1] * d3[2];
   const int64_t chunks = (n + CH - 1) / CH;
-  return sizeof(double) * (size_t)(batch * chunks) * (size_t)(nbins + 4);
+  // per-CTA partials [batch][chunks][B], G partials [batch][chunks][4],
+  // group partials [batch][RGROUPS][B]
+  return sizeof(double) * ((size_t)(batch * chunks) * (size_t)(nbins + 4) + (size_t)batch * RGROUPS * (size_t)nbins);
 }
 
 template <bool BWD>
@@ -408,12 +434,19 @@ static int soft_launch(const int8_t* coeffs, const float* fc, const float* fclo,
   kfn<<<(unsigned)grid, SNT, smem, s>>>(a);
   rc = check_launch(BWD ? "ecc_soft_kernel<bwd>" : "ecc_soft_kernel<fwd>");
   if (rc) return rc;
-  dim3 rg((unsigned)((nbins + 255) / 256), (unsigned)batch);
-  ecc_soft_reduce<<<rg, 256, 0, s>>>(a.part, chunks, (int)nbins, BWD ? up : nullptr, p->lam, out_main);
-  rc = check_launch("ecc_soft_reduce");
+  const int groups = (int)(chunks < RGROUPS ? chunks : RGROUPS);
+  const int64_t per_group = (chunks + groups - 1) / groups;
+  double* grp = a.gpart + (size_t)(batch * chunks) * 4;
+  dim3 g1((unsigned)((nbins + 127) / 128), (unsigned)groups, (unsigned)batch);
+  ecc_soft_reduce1<<<g1, 128, 0, s>>>(a.part, chunks, (int)nbins, per_group, grp);
+  rc = check_launch("ecc_soft_reduce1");
+  if (rc) return rc;
+  dim3 g2((unsigned)((nbins + 127) / 128), (unsigned)batch);
+  ecc_soft_reduce2<<<g2, 128, 0, s>>>(grp, groups, (int)nbins, BWD ? up : nullptr, p->lam, out_main);
+  rc = check_launch("ecc_soft_reduce2");
   if (rc) return rc;
   if (BWD) {
-    ecc_soft_reduce_g<<<(unsigned)batch, 32, 0, s>>>(a.gpart, chunks, ndim, G);
+    ecc_soft_reduce_g<<<(unsigned)batch, 256, 0, s>>>(a.gpart, chunks, ndim, G);
     rc = check_launch("ecc_soft_reduce_g");
   }
   return rc;
