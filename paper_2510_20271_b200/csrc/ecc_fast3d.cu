@@ -219,18 +219,30 @@ ecc_fast3d_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* 
 
   auto stage_of = [](int p) { return ((p % NSTAGE) + NSTAGE) % NSTAGE; };
 
-  for (int64_t item = blockIdx.x; item < g.items; item += gridDim.x) {
-    int64_t rr = item;
+  // Balanced static partition: the (tile, plane) steps are laid out tile by
+  // tile and every CTA takes one contiguous share, i.e. one or two z-segments
+  // of tile columns (one halo step per segment, no tail imbalance).
+  const int64_t Dw = (int64_t)(g.ze - g.zb);
+  const int64_t total = g.items * Dw;   // g.items = tiles (x * y * batch)
+  const int64_t w_end = total * ((int64_t)blockIdx.x + 1) / gridDim.x;
+  int64_t pending = 0;                  // voxels deposited since the last flush (int32 guard)
+  for (int64_t w = total * (int64_t)blockIdx.x / gridDim.x; w < w_end;) {
+    const int64_t tile = w / Dw;
+    const int64_t z0 = w - tile * Dw;
+    const int64_t seg = min(Dw - z0, w_end - w);
+    w += seg;
+    int64_t rr = tile;
     const int tx = (int)(rr % g.tiles_x); rr /= g.tiles_x;
     const int ty = (int)(rr % g.tiles_y); rr /= g.tiles_y;
-    const int zk = (int)(rr % g.zchunks); rr /= g.zchunks;
     const int64_t n = rr;
     const int x0 = tx * TXW, y0 = ty * OUTR;
-    const int zs = g.zb + zk * g.zc;
-    const int ze = min(zs + g.zc, g.ze);   // own planes [zs, ze), halo plane ze
+    const int zs = g.zb + (int)z0;
+    const int ze = zs + (int)seg;          // own planes [zs, ze), halo plane ze
 
-    if (n != cur_n) {
-      // flush the CTA histogram of the previous batch item (one int64 atomic per bin)
+    pending += seg * (TXW * OUTR);
+    if (n != cur_n || pending > (int64_t(1) << 28)) {
+      // flush the CTA histogram (one int64 atomic per bin): new batch item, or
+      // the int32 counters could overflow (|c| <= 7 per voxel)
       if (cur_n >= 0) {
         __syncthreads();
         unsigned long long* h = hist + cur_n * (nb + 1);
@@ -241,6 +253,7 @@ ecc_fast3d_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* 
         __syncthreads();
       }
       cur_n = n;
+      pending = seg * (TXW * OUTR);
     }
 
     if (threadIdx.x == 0) {
@@ -584,17 +597,11 @@ int fast3d_launch(const float* x, int64_t D, int64_t H, int64_t W, int64_t batch
   g.tiles_x = (int)((W + TXW - 1) / TXW);
   g.tiles_y = (int)((H + OUTR - 1) / OUTR);
   const int64_t tiles = (int64_t)g.tiles_x * g.tiles_y * batch;
-  const int64_t Dw = ze - zb;
-  // z-chunk: long enough to amortise the halo plane, short enough for >= ~6
-  // items per CTA so the persistent grid balances
-  int64_t zc = 64;
-  while (zc > 8 && tiles * ((Dw + zc - 1) / zc) < 6 * max_ctas) zc >>= 1;
-  if (zc > Dw) zc = Dw;
-  if (zc < 1) zc = 1;
-  g.zc = (int)zc;
-  g.zchunks = (int)((Dw + zc - 1) / zc);
-  g.items = tiles * g.zchunks;
-  const int64_t grid = g.items < max_ctas ? g.items : max_ctas;
+  g.zc = 0;
+  g.zchunks = 1;
+  g.items = tiles;   // the kernel splits tiles x planes evenly over the grid
+  const int64_t total = tiles * (ze - zb);
+  const int64_t grid = total < max_ctas ? total : max_ctas;
   if (grid < 1) return ECC_OK;
   ecc_fast3d_kernel<<<(unsigned)grid, NT, smem, stream>>>(map, g, table, nb, cells, cell_shift, b->lut_scale,
                                                             b->lut_bias, b->lut_ok, hist);
