@@ -63,6 +63,16 @@ __device__ __forceinline__ float rcp_approx(float x) {
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// 1/x on the FMA pipe for x in [1, 2^126] (the sigmoid denominators): bit-trick
+// seed (relative error < 12.5%) and three Newton steps (< 1e-7 relative).
+// Issuing a share of the reciprocals here instead of on MUFU balances the
+// SFU against the FMA pipe (the pair loop is otherwise MUFU-bound).
+__device__ __forceinline__ float rcp_fma(float x) {
+  float r = __int_as_float(0x7EF311C3 - __float_as_int(x));
+#pragma unroll
+  for (int k = 0; k < 3; ++k) r = r * __fmaf_rn(-x, r, 2.f);
+  return r;
+}
 
 // smem layout of a chunk after compaction
 struct ChunkSmem {
@@ -77,7 +87,7 @@ struct ChunkSmem {
 constexpr float A_MAX = 40.f;
 constexpr float B_MAX = 126.f - A_MAX;
 
-template <bool BWD, int T>
+template <bool BWD, int T, int EMU_EVERY>
 __device__ __forceinline__ void pair_loop_fact(const float (&at)[T], const float (&upv)[T], float (&acc)[T], float b,
                                                float cf, float& w) {
   // sigma = r = 1 / (1 + a_j b_p): one FFMA + one MUFU.RCP; sigma (1 - sigma)
@@ -86,7 +96,10 @@ __device__ __forceinline__ void pair_loop_fact(const float (&at)[T], const float
   // so the MUFU latency overlaps; two partial sums break the w chain.
   float r[T];
 #pragma unroll
-  for (int t = 0; t < T; ++t) r[t] = rcp_approx(__fmaf_rn(at[t], b, 1.f));
+  for (int t = 0; t < T; ++t) {
+    const float den = __fmaf_rn(at[t], b, 1.f);
+    r[t] = (t % EMU_EVERY == EMU_EVERY - 1) ? rcp_fma(den) : rcp_approx(den);
+  }
   float w0 = 0.f, w1 = 0.f;
 #pragma unroll
   for (int t = 0; t < T; ++t) {
@@ -232,7 +245,7 @@ ecc_soft_kernel(SoftArgs a) {
     float w = 0.f;
     if (FACT) {
       const float kf = fminf(fmaxf(__fmaf_rn(a.kscale, f, koff), -B_MAX), B_MAX);
-      pair_loop_fact<BWD, T>(at, upv, acc, ex2_approx(kf), cf, w);
+      pair_loop_fact<BWD, T, (BWD ? 1024 : 3)>(at, upv, acc, ex2_approx(kf), cf, w);
     } else {
       const double fd = (double)f + (double)(valid ? S.fclo[k] : 0.f);
       pair_loop_direct<BWD, T>(kt, Lv, l, upv, acc, ks * fd, cf, w);
