@@ -310,3 +310,19 @@ class TestFastPath:
         h = hist.cpu().numpy()
         assert int(h.sum()) == 1 and int(curve[-1]) == 1
         assert np.array_equal(h, np.append(*oracle.histogram(x, ts.taus)))
+
+
+class TestFastPath2D:
+    def test_2d_images_fast_path(self, rng):
+        """2D float32 images take the TMA kernel with D = 1 (W % 4 == 0)."""
+        xs = rng.random((3, 70, 132)).astype(np.float32)
+        ts = E.ThresholdSet(np.linspace(0.0, 1.0, 257)[1:])
+        curves = E.ecc_discrete(torch.from_numpy(xs).cuda(), ts, ndim=2).cpu().numpy()
+        for i in range(3):
+            assert np.array_equal(curves[i], oracle.curve(xs[i], ts.taus))
+
+    def test_large_uint8_volume_generic_path(self, rng):
+        x = rng.integers(0, 256, (40, 64, 61), dtype=np.uint8)
+        ts = E.ThresholdSet(np.arange(0.0, 256.0, 5.0))
+        got = E.ecc_discrete(torch.from_numpy(x).cuda(), ts).cpu().numpy()
+        assert np.array_equal(got, oracle.curve(x.astype(np.float64), ts.taus))

@@ -183,3 +183,46 @@ class TestModule:
         assert chi.shape == (2, 16)
         chi.sum().backward()
         assert m.taus.grad is not None and m.v.grad is not None and m.alpha.grad is not None
+
+
+class TestModule3D:
+    def test_3d_batch_vs_oracle(self, rng):
+        N, D, H, W, B = 2, 10, 12, 9, 40
+        x = rng.random((N, D, H, W)).astype(np.float32)
+        v = np.array([1.0, 2.0, -0.5])
+        u = v / np.linalg.norm(v)
+        alpha, lam = 0.25, 20.0
+        taus0 = np.linspace(-0.4, 1.4, B)
+        m = E.SoftECC(taus0, v, alpha=alpha, lam=lam).cuda()
+        xt = torch.from_numpy(x).cuda().requires_grad_(True)
+        chi = m(xt)
+        up = torch.from_numpy(rng.uniform(0.5, 1.5, (N, B))).cuda()
+        (chi * up).sum().backward()
+        gtau = np.zeros(B)
+        G = np.zeros(3)
+        for i in range(N):
+            xi = x[i].astype(np.float64)
+            c = oracle.coefficients(oracle.effective_field(xi, alpha, u))
+            assert normwise(chi[i].detach().cpu().numpy(), oracle.soft_forward(xi, c, lam, alpha, u, taus0)) <= TOL
+            dv, dt, _, _, Gi = oracle.soft_backward(xi, c, lam, alpha, u, taus0, up[i].cpu().numpy())
+            assert normwise(xt.grad[i].cpu().numpy(), dv) <= TOL
+            gtau += dt
+            G += Gi
+        assert normwise(m.taus.grad.cpu().numpy(), gtau) <= TOL
+        da = -(G @ u)
+        assert abs(float(m.alpha.grad) - da) <= TOL * max(abs(da), 1e-4)
+
+    def test_sharp_lambda_direct_mode_module(self, rng):
+        """lam * threshold spread too large for the factorised sigmoid: float64-exponent mode."""
+        x = rng.random((24, 20)).astype(np.float32)
+        taus0 = np.linspace(0.0, 1.0, 16)
+        m = E.SoftECC(taus0, [1.0, 0.0], alpha=0.0, lam=2000.0).cuda()
+        xt = torch.from_numpy(x).cuda().requires_grad_(True)
+        chi = m(xt)
+        chi.sum().backward()
+        xi = x.astype(np.float64)
+        c = oracle.coefficients(xi)
+        assert normwise(chi.detach().cpu().numpy(), oracle.soft_forward(xi, c, 2000.0, 0.0, [1.0, 0.0], taus0)) <= TOL
+        dv, dt, _, _, _ = oracle.soft_backward(xi, c, 2000.0, 0.0, [1.0, 0.0], taus0, np.ones(16))
+        assert normwise(xt.grad.cpu().numpy(), dv) <= TOL
+        assert normwise(m.taus.grad.cpu().numpy(), dt) <= TOL
