@@ -45,7 +45,7 @@ constexpr int TXW = NW * SEG;          // tile width (x)
 constexpr int OUTR = 30;               // output rows per tile (32 lanes - 2 halo)
 constexpr int PITCH = 140;             // staged row: x0-4 .. x0+135 (== 12 mod 32 words: LDS.128 conflict-free)
 constexpr int PLANE = PITCH * 32;      // floats per staged plane
-constexpr int NSTAGE = 3;
+constexpr int NSTAGE = 2;   // planes s-1 and s; s+1 is loaded into s-1's buffer mid-step
 constexpr uint32_t PLANE_BYTES = PLANE * 4;
 
 struct Geom {
@@ -176,7 +176,7 @@ __device__ __forceinline__ uint32_t word1(QF q, const float (&pc)[32]) {
   return (hi << 16) | lo;
 }
 
-__global__ void __launch_bounds__(NT, 3)
+__global__ void __launch_bounds__(NT, 4)
 ecc_fast3d_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* __restrict__ table_g, int nb,
                   int cells, int cell_shift, float lut_scale, float lut_bias, int lut_ok,
                   unsigned long long* __restrict__ hist) {
@@ -258,7 +258,7 @@ ecc_fast3d_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* 
 
     if (threadIdx.x == 0) {
 #pragma unroll
-      for (int k = -1; k <= 1; ++k) {
+      for (int k = -1; k <= 0; ++k) {
         const int p = zs + k;
         uint64_t* bar = &bars[stage_of(p)];
         mbar_expect_tx(bar, PLANE_BYTES);
@@ -321,6 +321,16 @@ ecc_fast3d_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* 
         hpl = B.l;
         hpr = B.r;
         words3(Ro, pc, N0[NZ_Y0_XM], N0[NZ_Y0_X0], N0[NZ_Y0_XP]);
+      }
+
+      // plane s-1 is no longer read from shared memory (its row and halo
+      // values needed below are in registers): release its buffer to plane s+1
+      __syncthreads();
+      if (threadIdx.x == 0 && s + 1 <= ze) {
+        const int p = s + 1;
+        uint64_t* bar = &bars[stage_of(p)];
+        mbar_expect_tx(bar, PLANE_BYTES);
+        tma_load_4d(planes + stage_of(p) * PLANE, &tmap, bar, x0 - 4, y0 - 1, p, (int)n);
       }
 
       if (s > zs) {
@@ -511,13 +521,6 @@ ecc_fast3d_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* 
 #pragma unroll
       for (int k = 0; k < NNEG; ++k) N1[k] = N0[k];
 
-      __syncthreads();   // everyone is done with plane s-1's buffer
-      if (threadIdx.x == 0 && s + 2 <= ze) {
-        const int p = s + 2;
-        uint64_t* bar = &bars[stage_of(p)];
-        mbar_expect_tx(bar, PLANE_BYTES);
-        tma_load_4d(planes + stage_of(p) * PLANE, &tmap, bar, x0 - 4, y0 - 1, p, (int)n);
-      }
     }
   }
   __syncthreads();
