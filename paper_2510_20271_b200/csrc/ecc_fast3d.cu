@@ -497,7 +497,9 @@ ecc_fast3d_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* 
               for (int j = 0; j < 8; ++j) {
                 const int cc = ((int)(Q[h] << (28 - 4 * j))) >> 28;
                 const LutEntry ee = e[h & 1][j];
-                const uint32_t addr = (uint32_t)ee.b + (Ro.v[8 * h + j] > ee.t ? 4u : 0u);
+                uint32_t addr = (uint32_t)ee.b;
+                asm("{\n.reg .pred p;\nsetp.gt.f32 p, %1, %2;\n@p add.u32 %0, %0, 4;\n}\n"
+                    : "+r"(addr) : "f"(Ro.v[8 * h + j]), "f"(ee.t));
                 red_add_shared_nz(addr, cc);
               }
             }
