@@ -219,18 +219,49 @@ ecc_fast3d_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* 
 
   auto stage_of = [](int p) { return ((p % NSTAGE) + NSTAGE) % NSTAGE; };
 
-  // Balanced static partition: the (tile, plane) steps are laid out tile by
-  // tile and every CTA takes one contiguous share, i.e. one or two z-segments
-  // of tile columns (one halo step per segment, no tail imbalance).
+  // Balanced static partition, z-aligned for L2 reuse.  Every CTA gets the
+  // same share S = T*Dw/G of the (tile, plane) steps (no tail imbalance).
+  // When the T tiles fit the grid G, k = g.zchunks = floor(G/T) CTAs per tile
+  // sweep the planes [0, K), K = k*S, in k aligned segments (CTA b: tile b % T,
+  // segment b / T), so CTAs running together sit on neighbouring tiles at the
+  // same depth and share their halo rows and columns in L2; the remaining
+  // G - k*T CTAs split the leftover planes [K, Dw) of all tiles evenly.
+  // Otherwise (T > G) the steps are laid out tile by tile and split evenly.
+  // A CTA's work is the index range [u, u_end) over (tile, plane) steps of
+  // L planes per tile starting at plane zbase: tile = u / L, plane = u % L.
   const int64_t Dw = (int64_t)(g.ze - g.zb);
-  const int64_t total = g.items * Dw;   // g.items = tiles (x * y * batch)
-  const int64_t w_end = total * ((int64_t)blockIdx.x + 1) / gridDim.x;
+  const int64_t T = g.items;            // tiles (x * y * batch)
+  const int64_t G = gridDim.x, b = blockIdx.x;
+  int64_t u, u_end, L, zbase;
+  if (g.zchunks > 0) {
+    const int64_t k = g.zchunks;
+    const int64_t K = k * T * Dw / G;
+    if (b < k * T) {
+      const int64_t sg = b / T, t = b % T;
+      zbase = K * sg / k;
+      L = K * (sg + 1) / k - zbase;
+      u = t * L;
+      u_end = u + L;
+    } else {
+      const int64_t r = b - k * T, R = G - k * T;
+      zbase = K;
+      L = Dw - K;
+      u = T * L * r / R;
+      u_end = T * L * (r + 1) / R;
+    }
+  } else {
+    zbase = 0;
+    L = Dw;
+    u = T * Dw * b / G;
+    u_end = T * Dw * (b + 1) / G;
+  }
   int64_t pending = 0;                  // voxels deposited since the last flush (int32 guard)
-  for (int64_t w = total * (int64_t)blockIdx.x / gridDim.x; w < w_end;) {
-    const int64_t tile = w / Dw;
-    const int64_t z0 = w - tile * Dw;
-    const int64_t seg = min(Dw - z0, w_end - w);
-    w += seg;
+  while (u < u_end) {
+    const int64_t tile = u / L;
+    const int64_t zr = u - tile * L;
+    const int64_t seg = min(L - zr, u_end - u);
+    const int64_t z0 = zbase + zr;
+    u += seg;
     int64_t rr = tile;
     const int tx = (int)(rr % g.tiles_x); rr /= g.tiles_x;
     const int ty = (int)(rr % g.tiles_y); rr /= g.tiles_y;
@@ -603,10 +634,11 @@ int fast3d_launch(const float* x, int64_t D, int64_t H, int64_t W, int64_t batch
   g.tiles_y = (int)((H + OUTR - 1) / OUTR);
   const int64_t tiles = (int64_t)g.tiles_x * g.tiles_y * batch;
   g.zc = 0;
-  g.zchunks = 1;
   g.items = tiles;   // the kernel splits tiles x planes evenly over the grid
   const int64_t total = tiles * (ze - zb);
   const int64_t grid = total < max_ctas ? total : max_ctas;
+  // z-aligned partition when every tile gets at least one CTA (see kernel)
+  g.zchunks = (tiles <= grid && grid <= tiles * (ze - zb)) ? (int)(grid / tiles) : 0;
   if (grid < 1) return ECC_OK;
   ecc_fast3d_kernel<<<(unsigned)grid, NT, smem, stream>>>(map, g, table, nb, cells, cell_shift, b->lut_scale,
                                                             b->lut_bias, b->lut_ok, hist);
