@@ -31,6 +31,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
 
 #include "ecc_common.cuh"
 #include "ecc_internal.h"
@@ -174,6 +176,92 @@ __device__ __forceinline__ uint32_t word1(QF q, const float (&pc)[32]) {
     lo = push(lo, le_bit(q(i), pc[i]));
   }
   return (hi << 16) | lo;
+}
+
+// c of the 32 voxels from the 26 lower-neighbour words L[dz+1][dy+1][dx+1]:
+// squares, cubes, signed count by a carry-save adder tree, then nibbles
+// Q[k] (nibble j = c of voxel 8k + j, 4-bit two's complement); returns the
+// OR of the bit-planes (0 when every c is 0)
+__device__ __forceinline__ uint32_t coeff_nibbles(const uint32_t (&L)[3][3][3], uint32_t outmask, uint32_t (&Q)[4]) {
+  // squares (coefficients.py:119-126) and cubes (128-136) on words
+  uint32_t Sxy[2][2], Szx[2][2], Szy[2][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      Sxy[a][b] = L[1][2 * a][1] & L[1][1][2 * b] & L[1][2 * a][2 * b];   // (y=a, x=b)
+      Szx[a][b] = L[2 * a][1][1] & L[1][1][2 * b] & L[2 * a][1][2 * b];   // (z=a, x=b)
+      Szy[a][b] = L[2 * a][1][1] & L[1][2 * b][1] & L[2 * a][2 * b][1];   // (z=a, y=b)
+    }
+  uint32_t C[8];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+        C[4 * a + 2 * b + c] = Szy[a][b] & Szx[a][c] & Sxy[b][c] & L[2 * a][2 * b][2 * c];
+
+  // c + 13 = sum of 26 bits: ~E (6), S (12), ~C (8); carry-save adder tree
+  uint32_t in[26];
+  in[0] = ~L[1][1][0]; in[1] = ~L[1][1][2]; in[2] = ~L[1][0][1];
+  in[3] = ~L[1][2][1]; in[4] = ~L[0][1][1]; in[5] = ~L[2][1][1];
+  in[6] = Sxy[0][0]; in[7] = Sxy[0][1]; in[8] = Sxy[1][0]; in[9] = Sxy[1][1];
+  in[10] = Szx[0][0]; in[11] = Szx[0][1]; in[12] = Szx[1][0]; in[13] = Szx[1][1];
+  in[14] = Szy[0][0]; in[15] = Szy[0][1]; in[16] = Szy[1][0]; in[17] = Szy[1][1];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) in[18 + k] = ~C[k];
+  uint32_t s1[8], c2[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) fa(in[3 * k], in[3 * k + 1], in[3 * k + 2], s1[k], c2[k]);
+  uint32_t t1a, t1b, t1c, k2a, k2b, k2c;
+  fa(s1[0], s1[1], s1[2], t1a, k2a);
+  fa(s1[3], s1[4], s1[5], t1b, k2b);
+  fa(s1[6], s1[7], in[24], t1c, k2c);
+  uint32_t t1d, k2d;
+  fa(t1a, t1b, t1c, t1d, k2d);
+  const uint32_t b0 = t1d ^ in[25];
+  const uint32_t k2e = t1d & in[25];
+  uint32_t u2[4], c4[4];
+  fa(c2[0], c2[1], c2[2], u2[0], c4[0]);
+  fa(c2[3], c2[4], c2[5], u2[1], c4[1]);
+  fa(c2[6], c2[7], k2a, u2[2], c4[2]);
+  fa(k2b, k2c, k2d, u2[3], c4[3]);
+  uint32_t v2a, c4e, v2b, c4f;
+  fa(u2[0], u2[1], u2[2], v2a, c4e);
+  fa(u2[3], k2e, v2a, v2b, c4f);
+  const uint32_t b1 = v2b;
+  uint32_t w4a, c8a, w4b, c8b;
+  fa(c4[0], c4[1], c4[2], w4a, c8a);
+  fa(c4[3], c4e, c4f, w4b, c8b);
+  const uint32_t b2 = w4a ^ w4b;
+  const uint32_t c8c = w4a & w4b;
+  uint32_t b3, b4;
+  fa(c8a, c8b, c8c, b3, b4);
+  (void)b4;
+  // c = sum - 13 as 4-bit two's complement: (sum + 3) mod 16 (c in [-5, 7]);
+  // voxels outside the tile's output get c = 0
+  const uint32_t r0 = ~b0 & outmask;
+  const uint32_t r1b = ~(b1 ^ b0) & outmask;
+  const uint32_t cy1 = b1 | b0;
+  const uint32_t r2 = (b2 ^ cy1) & outmask;
+  const uint32_t r3 = (b3 ^ (b2 & cy1)) & outmask;
+
+  // ---- bit-planes -> nibbles: Q[k] nibble j = c of voxel 8k + j --------
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint32_t sel = (uint32_t)k | ((uint32_t)(4 + k) << 4);
+    uint32_t gq = __byte_perm(__byte_perm(r0, r2, sel), __byte_perm(r1b, r3, sel), 0x5410);
+    uint32_t t = ((gq >> 12) ^ gq) & 0x0000F0F0u;
+    gq ^= t ^ (t << 12);
+    t = ((gq >> 6) ^ gq) & 0x00CC00CCu;
+    gq ^= t ^ (t << 6);
+    t = ((gq >> 3) ^ gq) & 0x0A0A0A0Au;
+    gq ^= t ^ (t << 3);
+    Q[k] = gq;
+  }
+
+  return r0 | r1b | r2 | r3;
 }
 
 __global__ void __launch_bounds__(NT, 4)
@@ -425,87 +513,11 @@ ecc_fast3d_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* 
         L[2][2][2] = ((((~e_m) >> 1) & 0x7fffffffu & xm_p1) | E_zp_yp_xp) & myu & mz;
         L[2][2][0] = ((~e_p) << 1 | E_zp_yp_xm) & myu & mz;
 
-        // squares (coefficients.py:119-126) and cubes (128-136) on words
-        uint32_t Sxy[2][2], Szx[2][2], Szy[2][2];
-#pragma unroll
-        for (int a = 0; a < 2; ++a)
-#pragma unroll
-          for (int b = 0; b < 2; ++b) {
-            Sxy[a][b] = L[1][2 * a][1] & L[1][1][2 * b] & L[1][2 * a][2 * b];   // (y=a, x=b)
-            Szx[a][b] = L[2 * a][1][1] & L[1][1][2 * b] & L[2 * a][1][2 * b];   // (z=a, x=b)
-            Szy[a][b] = L[2 * a][1][1] & L[1][2 * b][1] & L[2 * a][2 * b][1];   // (z=a, y=b)
-          }
-        uint32_t C[8];
-#pragma unroll
-        for (int a = 0; a < 2; ++a)
-#pragma unroll
-          for (int b = 0; b < 2; ++b)
-#pragma unroll
-            for (int c = 0; c < 2; ++c)
-              C[4 * a + 2 * b + c] = Szy[a][b] & Szx[a][c] & Sxy[b][c] & L[2 * a][2 * b][2 * c];
-
-        // c + 13 = sum of 26 bits: ~E (6), S (12), ~C (8); carry-save adder tree
-        uint32_t in[26];
-        in[0] = ~L[1][1][0]; in[1] = ~L[1][1][2]; in[2] = ~L[1][0][1];
-        in[3] = ~L[1][2][1]; in[4] = ~L[0][1][1]; in[5] = ~L[2][1][1];
-        in[6] = Sxy[0][0]; in[7] = Sxy[0][1]; in[8] = Sxy[1][0]; in[9] = Sxy[1][1];
-        in[10] = Szx[0][0]; in[11] = Szx[0][1]; in[12] = Szx[1][0]; in[13] = Szx[1][1];
-        in[14] = Szy[0][0]; in[15] = Szy[0][1]; in[16] = Szy[1][0]; in[17] = Szy[1][1];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) in[18 + k] = ~C[k];
-        uint32_t s1[8], c2[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) fa(in[3 * k], in[3 * k + 1], in[3 * k + 2], s1[k], c2[k]);
-        uint32_t t1a, t1b, t1c, k2a, k2b, k2c;
-        fa(s1[0], s1[1], s1[2], t1a, k2a);
-        fa(s1[3], s1[4], s1[5], t1b, k2b);
-        fa(s1[6], s1[7], in[24], t1c, k2c);
-        uint32_t t1d, k2d;
-        fa(t1a, t1b, t1c, t1d, k2d);
-        const uint32_t b0 = t1d ^ in[25];
-        const uint32_t k2e = t1d & in[25];
-        uint32_t u2[4], c4[4];
-        fa(c2[0], c2[1], c2[2], u2[0], c4[0]);
-        fa(c2[3], c2[4], c2[5], u2[1], c4[1]);
-        fa(c2[6], c2[7], k2a, u2[2], c4[2]);
-        fa(k2b, k2c, k2d, u2[3], c4[3]);
-        uint32_t v2a, c4e, v2b, c4f;
-        fa(u2[0], u2[1], u2[2], v2a, c4e);
-        fa(u2[3], k2e, v2a, v2b, c4f);
-        const uint32_t b1 = v2b;
-        uint32_t w4a, c8a, w4b, c8b;
-        fa(c4[0], c4[1], c4[2], w4a, c8a);
-        fa(c4[3], c4e, c4f, w4b, c8b);
-        const uint32_t b2 = w4a ^ w4b;
-        const uint32_t c8c = w4a & w4b;
-        uint32_t b3, b4;
-        fa(c8a, c8b, c8c, b3, b4);
-        (void)b4;
-        // c = sum - 13 as 4-bit two's complement: (sum + 3) mod 16 (c in [-5, 7]);
-        // voxels outside the tile's output get c = 0
-        const uint32_t r0 = ~b0 & outmask;
-        const uint32_t r1b = ~(b1 ^ b0) & outmask;
-        const uint32_t cy1 = b1 | b0;
-        const uint32_t r2 = (b2 ^ cy1) & outmask;
-        const uint32_t r3 = (b3 ^ (b2 & cy1)) & outmask;
-
-        // ---- bit-planes -> nibbles: Q[k] nibble j = c of voxel 8k + j --------
         uint32_t Q[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const uint32_t sel = (uint32_t)k | ((uint32_t)(4 + k) << 4);
-          uint32_t gq = __byte_perm(__byte_perm(r0, r2, sel), __byte_perm(r1b, r3, sel), 0x5410);
-          uint32_t t = ((gq >> 12) ^ gq) & 0x0000F0F0u;
-          gq ^= t ^ (t << 12);
-          t = ((gq >> 6) ^ gq) & 0x00CC00CCu;
-          gq ^= t ^ (t << 6);
-          t = ((gq >> 3) ^ gq) & 0x0A0A0A0Au;
-          gq ^= t ^ (t << 3);
-          Q[k] = gq;
-        }
+        const uint32_t any = coeff_nibbles(L, outmask, Q);
 
         // ---- per voxel: bin (cell table) + shared-memory reduction ----------
-        if (__any_sync(FULL, (r0 | r1b | r2 | r3) != 0u)) {
+        if (__any_sync(FULL, any != 0u)) {
           if (lut_ok) {
             // groups of 8 voxels, software-pipelined: the table entries of
             // group h+1 are in flight while group h is binned and reduced
@@ -566,6 +578,419 @@ ecc_fast3d_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* 
   }
 }
 
+// ======================================================================
+// Bin-image kernel (the default fast path when the thresholds have a cell
+// table).  Exact reformulation: the histogram only depends on the sublevel
+// sets {x <= tau_j} = {bin(x) <= j}, and a cell's max vertex lies in bin j
+// exactly when the cell belongs to K_j \ K_{j-1}, for ANY total order that
+// refines the bin order.  So each staged plane is first replaced by its bin
+// indices (one table lookup per voxel, the lookup the deposit needs anyway)
+// and the lower-star coefficients are taken in the order (bin, index) --
+// the reference's own tie-break rule applied to the bin image.  Per-voxel
+// coefficients differ from the value order's, the per-bin sums and hence
+// the curve are identical (hard.py:134-143 sums c over bins).
+//
+// The bin image is stored SWAR: word j of a 32-voxel row segment holds the
+// 16-bit bins of voxels j and j + 16, so one 32-bit subtraction
+// (0x8000 | p) - q compares two voxel pairs (bit 15 / 31 = [q <= p]), and a
+// sign-replicating byte permute plus one LOP3 moves four of those results
+// into the bit-sliced word: one instruction per comparison instead of two.
+// Out-of-grid voxels carry the sentinel 0x7FFF, which is never lower.
+// ======================================================================
+constexpr int BROW = 68;                    // words per bin-plane row: 4 x 16 + pad (== 4 mod 32)
+constexpr int BEDGE = 32 * BROW;            // edge words [segment][row]: bin(x - 1) | bin(x + 32) << 16
+constexpr int BPLANE = BEDGE + NW * 32;     // words per bin plane
+constexpr uint32_t BSENT = 0x7FFFu;
+
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+}
+
+struct BRow {
+  uint32_t w[16];   // (bin[j], bin[j + 16])
+  uint32_t e;       // (bin[-1], bin[32])
+};
+__device__ __forceinline__ void load_brow(BRow& R, const uint32_t* buf, int row, int seg) {
+  const uint4* p = reinterpret_cast<const uint4*>(buf + row * BROW + 16 * seg);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint4 t = p[k];
+    R.w[4 * k] = t.x;
+    R.w[4 * k + 1] = t.y;
+    R.w[4 * k + 2] = t.z;
+    R.w[4 * k + 3] = t.w;
+  }
+  R.e = buf[BEDGE + seg * 32 + row];
+}
+// operand word j of row R moved by dx: (bin[j + dx], bin[j + 16 + dx])
+template <int DX>
+__device__ __forceinline__ uint32_t qword(const BRow& R, int j) {
+  if (DX == 0) return R.w[j];
+  if (DX < 0) return j > 0 ? R.w[j - 1] : prmt(R.e, R.w[15], 0x5410u);
+  return j < 15 ? R.w[j + 1] : prmt(R.w[0], R.e, 0x7632u);
+}
+// bit-sliced word of [q <= p] for the 32 voxels, q = row R moved by DX;
+// PP[j] = own word j | 0x80008000
+template <int DX>
+__device__ __forceinline__ uint32_t cmp_word(const uint32_t (&PP)[16], const BRow& R) {
+  uint32_t d[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) d[j] = PP[j] - qword<DX>(R, j);
+  // byte a of prmt(d[k], d[k+8]) = sign of voxel 8a + k, spread over the byte
+  uint32_t acc = prmt(d[0], d[8], 0xFBD9u) & 0x01010101u;
+#pragma unroll
+  for (int k = 1; k < 8; ++k) acc |= prmt(d[k], d[k + 8], 0xFBD9u) & (0x01010101u << k);
+  return acc;
+}
+
+// 4 * bin(x) from the cell table: cell = floor(sat(fma(x, scale, bias)) * cells)
+// read off the low mantissa bits of RZ(g * cells + 2^23) (lut_m is biased by
+// 0x4B000000 entries so that the float's bit pattern indexes it directly)
+__device__ __forceinline__ uint32_t bin4_lut(float x, uint32_t lut_m, float sc, float bi, float fcells) {
+  const float gg = __saturatef(__fmaf_rn(x, sc, bi));
+  const uint32_t addr = lut_m + 8u * __float_as_uint(__fmaf_rz(gg, fcells, 8388608.0f));
+  float t;
+  uint32_t v;
+  asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=f"(t), "=r"(v) : "r"(addr));
+  asm("{\n.reg .pred p;\nsetp.gt.f32 p, %1, %2;\n@p add.u32 %0, %0, 4;\n}\n" : "+r"(v) : "f"(x), "f"(t));
+  return v;
+}
+// bin a 34-voxel row segment (x - 1 .. x + 32) of the staged f32 plane;
+// CHECK: NaN (TMA out-of-bounds fill) -> sentinel for every voxel, else
+// only for the two edge voxels
+template <bool CHECK>
+__device__ __forceinline__ void bin_rowseg(const float* src, uint32_t* dw, uint32_t* de, uint32_t lut_m, float sc,
+                                           float bi, float fcells) {
+  // two halves of 8 words each (voxels j, j + 16) to bound the live registers
+  const float4* s4 = reinterpret_cast<const float4*>(src);
+  uint4* d4 = reinterpret_cast<uint4*>(dw);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    float v[16];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const float4 lo = s4[2 * h + k], hi = s4[4 + 2 * h + k];
+      v[4 * k] = lo.x; v[4 * k + 1] = lo.y; v[4 * k + 2] = lo.z; v[4 * k + 3] = lo.w;
+      v[8 + 4 * k] = hi.x; v[9 + 4 * k] = hi.y; v[10 + 4 * k] = hi.z; v[11 + 4 * k] = hi.w;
+    }
+    uint32_t b[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const uint32_t t = bin4_lut(v[i], lut_m, sc, bi, fcells);
+      b[i] = CHECK ? (v[i] != v[i] ? BSENT : t) : t;   // NaN = TMA out-of-bounds fill
+    }
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+      d4[2 * h + k] = make_uint4(prmt(b[4 * k], b[8 + 4 * k], 0x5410u), prmt(b[4 * k + 1], b[9 + 4 * k], 0x5410u),
+                                 prmt(b[4 * k + 2], b[10 + 4 * k], 0x5410u), prmt(b[4 * k + 3], b[11 + 4 * k], 0x5410u));
+  }
+  const float el = src[-1], er = src[32];
+  const uint32_t bl = bin4_lut(el, lut_m, sc, bi, fcells), br = bin4_lut(er, lut_m, sc, bi, fcells);
+  *de = prmt(el != el ? BSENT : bl, er != er ? BSENT : br, 0x5410u);
+}
+// bin the staged plane into a bin plane: warp -> x segment, lane -> row
+__device__ __forceinline__ void bin_plane(const float* stage, uint32_t* B, bool plane_in, int x0, int y0, int W,
+                                          int H, uint32_t lut_m, float sc, float bi, float fcells) {
+  const int row = threadIdx.x & 31, seg = threadIdx.x >> 5;
+  uint32_t* dw = B + row * BROW + 16 * seg;
+  uint32_t* de = B + BEDGE + seg * 32 + row;
+  const int y = y0 - 1 + row, xs = x0 + 32 * seg;
+  if (!plane_in || y < 0 || y >= H || xs >= W) {
+    const uint32_t s2 = BSENT | (BSENT << 16);
+    uint4* d4 = reinterpret_cast<uint4*>(dw);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) d4[k] = make_uint4(s2, s2, s2, s2);
+    *de = s2;
+    return;
+  }
+  const float* src = stage + row * PITCH + 4 + 32 * seg;
+  if (xs + 32 > W)
+    bin_rowseg<true>(src, dw, de, lut_m, sc, bi, fcells);
+  else
+    bin_rowseg<false>(src, dw, de, lut_m, sc, bi, fcells);
+}
+
+template <int DEP>
+__global__ void __launch_bounds__(NT, 4)
+ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* __restrict__ table_g, int nb,
+                      int cells, int hsize, float lut_scale, float lut_bias, unsigned long long* __restrict__ hist) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* stage = reinterpret_cast<float*>(smem_raw);                            // one f32 plane (TMA)
+  uint32_t* bbuf = reinterpret_cast<uint32_t*>(smem_raw + PLANE_BYTES);          // two bin planes
+  uint64_t* bar = reinterpret_cast<uint64_t*>(bbuf + 2 * BPLANE);
+  LutEntry* s_lut = reinterpret_cast<LutEntry*>(bar + 2);                        // cells + 1
+  int* s_hist = reinterpret_cast<int*>(s_lut + cells + 1);                       // nb + 1 (+ 32 dummies), 16 c
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const float* tab_g = reinterpret_cast<const float*>(table_g);
+  const LutEntry* lut_g = reinterpret_cast<const LutEntry*>(tab_g + ((nb + 2 + 1) & ~1));
+  for (int i = threadIdx.x; i < hsize; i += NT) s_hist[i] = 0;
+  for (int i = threadIdx.x; i <= cells; i += NT) {
+    LutEntry e = lut_g[i];
+    e.b *= 4;   // the bin image holds 4 * bin: the byte offset of the bin's counter
+    s_lut[i] = e;
+  }
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+  }
+  __syncthreads();
+  const uint32_t lut_m = smem_u32(s_lut) - 0x58000000u;   // - 0x4B000000 entries (mod 2^32)
+  const float fcells = (float)cells;
+  char* const hbytes = reinterpret_cast<char*>(s_hist);
+  char* const dummy = hbytes + 4 * (nb + 1 + lane);
+
+  uint32_t phase = 0;
+  int64_t cur_n = -1;
+  const int rm = lane > 0 ? lane - 1 : 0, rp = lane < 31 ? lane + 1 : 31;
+
+  // work partition: see ecc_fast3d_kernel
+  const int64_t Dw = (int64_t)(g.ze - g.zb);
+  const int64_t T = g.items;
+  const int64_t G = gridDim.x, bx = blockIdx.x;
+  int64_t u, u_end, L, zbase;
+  if (g.zchunks > 0) {
+    const int64_t k = g.zchunks;
+    const int64_t K = k * T * Dw / G;
+    if (bx < k * T) {
+      const int64_t sg = bx / T, t = bx % T;
+      zbase = K * sg / k;
+      L = K * (sg + 1) / k - zbase;
+      u = t * L;
+      u_end = u + L;
+    } else {
+      const int64_t r = bx - k * T, R = G - k * T;
+      zbase = K;
+      L = Dw - K;
+      u = T * L * r / R;
+      u_end = T * L * (r + 1) / R;
+    }
+  } else {
+    zbase = 0;
+    L = Dw;
+    u = T * Dw * bx / G;
+    u_end = T * Dw * (bx + 1) / G;
+  }
+  int64_t pending = 0;
+  while (u < u_end) {
+    const int64_t tile = u / L;
+    const int64_t zr = u - tile * L;
+    const int64_t seg = min(L - zr, u_end - u);
+    const int64_t z0 = zbase + zr;
+    u += seg;
+    int64_t rr = tile;
+    const int tx = (int)(rr % g.tiles_x); rr /= g.tiles_x;
+    const int ty = (int)(rr % g.tiles_y); rr /= g.tiles_y;
+    const int64_t n = rr;
+    const int x0 = tx * TXW, y0 = ty * OUTR;
+    const int zs = g.zb + (int)z0;
+    const int ze = zs + (int)seg;          // own planes [zs, ze), halo plane ze
+
+    pending += seg * (TXW * OUTR);
+    if (n != cur_n || pending > (int64_t(1) << 24)) {   // counters hold 16 c: |16 c| <= 112
+      if (cur_n >= 0) {
+        __syncthreads();
+        unsigned long long* h = hist + cur_n * (nb + 1);
+        for (int i = threadIdx.x; i <= nb; i += NT) {
+          const int v = s_hist[i] >> 4;
+          if (v) atomicAdd(h + i, (unsigned long long)(long long)v);
+          s_hist[i] = 0;
+        }
+        __syncthreads();
+      }
+      cur_n = n;
+      pending = seg * (TXW * OUTR);
+    }
+
+    // prologue: bin planes zs - 1 and zs
+#pragma unroll 1
+    for (int p = zs - 1; p <= zs; ++p) {
+      const bool pin = p >= 0 && p < g.D;
+      if (pin) {
+        if (threadIdx.x == 0) {
+          mbar_expect_tx(bar, PLANE_BYTES);
+          tma_load_4d(stage, &tmap, bar, x0 - 4, y0 - 1, p, (int)n);
+        }
+        mbar_wait(bar, phase);
+        phase ^= 1u;
+      }
+      bin_plane(stage, bbuf + (p & 1) * BPLANE, pin, x0, y0, g.W, g.H, lut_m, lut_scale, lut_bias, fcells);
+      __syncthreads();
+    }
+    if (threadIdx.x == 0 && zs + 1 <= ze && zs + 1 < g.D) {
+      mbar_expect_tx(bar, PLANE_BYTES);
+      tma_load_4d(stage, &tmap, bar, x0 - 4, y0 - 1, zs + 1, (int)n);
+    }
+
+    // per-thread validity (rows / columns of this tile)
+    const int y = y0 - 1 + lane;
+    const bool lane_out = lane >= 1 && lane <= 30 && y < g.H;
+    const bool row_up_ok = (y + 1) < g.H;
+    const bool row_dn_ok = (y - 1) >= 0;
+    const int xs = x0 + SEG * warp;
+    const int nvalid = max(0, min(32, g.W - xs));
+    const uint32_t xmask = nvalid >= 32 ? 0xffffffffu : ((1u << nvalid) - 1u);
+    const uint32_t xm_p1 = (nvalid >= 32 ? 0xffffffffu : ((1u << max(nvalid - 1, 0)) - 1u)) | 0x80000000u;
+    const uint32_t outmask = lane_out ? xmask : 0u;
+
+    uint32_t N1[NNEG];
+#pragma unroll
+    for (int k = 0; k < NNEG; ++k) N1[k] = 0;
+
+    for (int s = zs; s <= ze; ++s) {
+      const uint32_t* B0 = bbuf + (s & 1) * BPLANE;         // plane s
+      const uint32_t* B1 = bbuf + ((s - 1) & 1) * BPLANE;   // plane s - 1
+
+      // ---- the 13 negative-offset words of plane s ----
+      uint32_t N0[NNEG];
+      BRow Ro;                    // own row of plane s - 1 (finalised below)
+      uint32_t eA, eB, eP;        // edge words: own row (s), row y-1 (s), row y+1 (s-1)
+      {
+        // rows double-buffered: the next row's loads are in flight while the
+        // current row's words are computed
+        uint32_t PP[16];
+        BRow A, B;
+        load_brow(A, B0, lane, warp);
+        load_brow(B, B0, rm, warp);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) PP[j] = A.w[j] | 0x80008000u;
+        N0[NX] = cmp_word<-1>(PP, A);
+        eA = A.e;
+        load_brow(A, B1, rm, warp);
+        N0[NYM_XM] = cmp_word<-1>(PP, B);
+        N0[NYM_X0] = cmp_word<0>(PP, B);
+        N0[NYM_XP] = cmp_word<1>(PP, B);
+        eB = B.e;
+        load_brow(B, B1, rp, warp);
+        N0[NZ_YM_XM] = cmp_word<-1>(PP, A);
+        N0[NZ_YM_X0] = cmp_word<0>(PP, A);
+        N0[NZ_YM_XP] = cmp_word<1>(PP, A);
+        load_brow(Ro, B1, lane, warp);
+        N0[NZ_YP_XM] = cmp_word<-1>(PP, B);
+        N0[NZ_YP_X0] = cmp_word<0>(PP, B);
+        N0[NZ_YP_XP] = cmp_word<1>(PP, B);
+        eP = B.e;
+        N0[NZ_Y0_XM] = cmp_word<-1>(PP, Ro);
+        N0[NZ_Y0_X0] = cmp_word<0>(PP, Ro);
+        N0[NZ_Y0_XP] = cmp_word<1>(PP, Ro);
+      }
+
+      // plane s - 1's bin plane is no longer read: bin plane s + 1 into it
+      __syncthreads();
+      if (s + 1 <= ze) {
+        const int p = s + 1;
+        const bool pin = p < g.D;
+        if (pin) {
+          mbar_wait(bar, phase);
+          phase ^= 1u;
+        }
+        bin_plane(stage, bbuf + (p & 1) * BPLANE, pin, x0, y0, g.W, g.H, lut_m, lut_scale, lut_bias, fcells);
+        __syncthreads();
+        if (threadIdx.x == 0 && s + 2 <= ze && s + 2 < g.D) {
+          mbar_expect_tx(bar, PLANE_BYTES);
+          tma_load_4d(stage, &tmap, bar, x0 - 4, y0 - 1, s + 2, (int)n);
+        }
+      }
+
+      if (s > zs) {
+        // ---- finalize plane s-1 (registers only) -----------------------------
+        const uint32_t FULL = 0xffffffffu;
+        const uint32_t u_m = __shfl_down_sync(FULL, N1[NYM_XM], 1);
+        const uint32_t u_0 = __shfl_down_sync(FULL, N1[NYM_X0], 1);
+        const uint32_t u_p = __shfl_down_sync(FULL, N1[NYM_XP], 1);
+        const uint32_t d_m = __shfl_up_sync(FULL, N0[NZ_YP_XM], 1);
+        const uint32_t d_0 = __shfl_up_sync(FULL, N0[NZ_YP_X0], 1);
+        const uint32_t d_p = __shfl_up_sync(FULL, N0[NZ_YP_XP], 1);
+        const uint32_t e_m = __shfl_down_sync(FULL, N0[NZ_YM_XM], 1);
+        const uint32_t e_0 = __shfl_down_sync(FULL, N0[NZ_YM_X0], 1);
+        const uint32_t e_p = __shfl_down_sync(FULL, N0[NZ_YM_XP], 1);
+        const uint32_t eU = __shfl_down_sync(FULL, eA, 1);   // row y+1 of plane s
+
+        // segment-edge bits q < p (strict): lo lane vs bin[0], hi lane vs bin[31]
+        const uint32_t PSs = (prmt(Ro.w[0], Ro.w[15], 0x7610u) | 0x80008000u) - 0x00010001u;
+        const uint32_t dR = PSs - Ro.e, dP = PSs - eP, dB = PSs - eB, dA = PSs - eA, dU = PSs - eU;
+        const uint32_t HI = 0x80000000u;
+        const uint32_t E_x = dR & HI;
+        const uint32_t E_yp_xp = dP & HI, E_yp_xm = (dP >> 15) & 1u;
+        const uint32_t E_zp_ym_xp = dB & HI, E_zp_ym_xm = (dB >> 15) & 1u;
+        const uint32_t E_zp_y0_xp = dA & HI, E_zp_y0_xm = (dA >> 15) & 1u;
+        const uint32_t E_zp_yp_xp = dU & HI, E_zp_yp_xm = (dU >> 15) & 1u;
+
+        const uint32_t mz = (s < g.D) ? FULL : 0u;
+        const uint32_t myu = row_up_ok ? FULL : 0u;
+        const uint32_t myd = row_dn_ok ? FULL : 0u;
+
+        uint32_t Lw[3][3][3];
+        Lw[1][1][0] = N1[NX];
+        Lw[1][0][0] = N1[NYM_XM];
+        Lw[1][0][1] = N1[NYM_X0];
+        Lw[1][0][2] = N1[NYM_XP];
+        Lw[0][0][0] = N1[NZ_YM_XM];
+        Lw[0][0][1] = N1[NZ_YM_X0];
+        Lw[0][0][2] = N1[NZ_YM_XP];
+        Lw[0][1][0] = N1[NZ_Y0_XM];
+        Lw[0][1][1] = N1[NZ_Y0_X0];
+        Lw[0][1][2] = N1[NZ_Y0_XP];
+        Lw[0][2][0] = N1[NZ_YP_XM];
+        Lw[0][2][1] = N1[NZ_YP_X0];
+        Lw[0][2][2] = N1[NZ_YP_XP];
+        Lw[1][1][2] = (((~N1[NX]) >> 1) & 0x7fffffffu & xm_p1) | E_x;
+        Lw[1][2][1] = (~u_0) & myu;
+        Lw[1][2][2] = ((((~u_m) >> 1) & 0x7fffffffu & xm_p1) | E_yp_xp) & myu;
+        Lw[1][2][0] = ((~u_p) << 1 | E_yp_xm) & myu;
+        Lw[2][0][1] = (~d_0) & myd & mz;
+        Lw[2][0][2] = ((((~d_m) >> 1) & 0x7fffffffu & xm_p1) | E_zp_ym_xp) & myd & mz;
+        Lw[2][0][0] = ((~d_p) << 1 | E_zp_ym_xm) & myd & mz;
+        Lw[2][1][1] = (~N0[NZ_Y0_X0]) & mz;
+        Lw[2][1][2] = ((((~N0[NZ_Y0_XM]) >> 1) & 0x7fffffffu & xm_p1) | E_zp_y0_xp) & mz;
+        Lw[2][1][0] = ((~N0[NZ_Y0_XP]) << 1 | E_zp_y0_xm) & mz;
+        Lw[2][2][1] = (~e_0) & myu & mz;
+        Lw[2][2][2] = ((((~e_m) >> 1) & 0x7fffffffu & xm_p1) | E_zp_yp_xp) & myu & mz;
+        Lw[2][2][0] = ((~e_p) << 1 | E_zp_yp_xm) & myu & mz;
+
+        uint32_t Q[4];
+        const uint32_t any = coeff_nibbles(Lw, outmask, Q);
+
+        // ---- per voxel: bin from the bin image + shared-memory reduction ----
+        // c moves into the high nibble of a byte, so one sign-replicating
+        // byte permute yields 16 c as int32 (the counters hold 16 c)
+        if (__any_sync(FULL, any != 0u)) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const int m = (i & 7) >> 1;
+            const uint32_t sel = (uint32_t)m | ((uint32_t)(8 | m) << 4) | ((uint32_t)(8 | m) << 8) |
+                                 ((uint32_t)(8 | m) << 12);
+            // even voxels: nibble moved up into the byte's high half; odd: already there
+            const uint32_t bq = (i & 1) ? (Q[i >> 3] & 0xF0F0F0F0u) : ((Q[i >> 3] << 4) & 0xF0F0F0F0u);
+            const int c16 = (int)prmt(bq, 0u, sel);
+            const uint32_t off = i < 16 ? (Ro.w[i] & 0xFFFFu) : (Ro.w[i - 16] >> 16);
+            // lanes with c == 0 add 0 to a private dummy counter: no branch,
+            // no bank traffic on the real counters
+            if (DEP == 0) {
+              if (c16) atomicAdd(reinterpret_cast<int*>(hbytes + off), c16);
+            } else {
+              atomicAdd(reinterpret_cast<int*>(c16 ? hbytes + off : dummy), c16);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < NNEG; ++k) N1[k] = N0[k];
+    }
+  }
+  __syncthreads();
+  if (cur_n >= 0) {
+    unsigned long long* h = hist + cur_n * (nb + 1);
+    for (int i = threadIdx.x; i <= nb; i += NT) {
+      const int v = s_hist[i] >> 4;
+      if (v) atomicAdd(h + i, (unsigned long long)(long long)v);
+    }
+  }
+}
+
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static bool tried = false;
@@ -615,12 +1040,33 @@ int fast3d_launch(const float* x, int64_t D, int64_t H, int64_t W, int64_t batch
   int log2c = 0;
   while ((1 << log2c) < cells) ++log2c;
   const int cell_shift = 23 - log2c;
-  const size_t smem = (size_t)NSTAGE * PLANE_BYTES + 4 * 8 + (size_t)(b->lut_ok ? cells + 1 : 0) * sizeof(LutEntry) +
-                      (size_t)((nb + 1 + 3) & ~3) * 4 + (size_t)(b->lut_ok ? 0 : nb + 2) * 4;
-  cudaError_t e = cudaFuncSetAttribute(ecc_fast3d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  // bin-image kernel whenever the thresholds have a cell table (default);
+  // ECC_B200_F3=value selects the value-order kernel, =branch the bin-image
+  // kernel with a branch around each reduction (A/B checks)
+  const int mode = [] {   // read per launch so tests can switch kernels in-process
+    const char* e = getenv("ECC_B200_F3");
+    if (!e) return 0;
+    if (!strcmp(e, "value")) return 1;
+    if (!strcmp(e, "branch")) return 2;
+    return 0;
+  }();
+  const bool use_bin = b->lut_ok && nb <= 8190 && mode != 1;
+  const int hsize = nb + 33;   // counters of the bin-image kernel: nb + 1 bins + 32 dummies
+  size_t smem;
+  const void* kfn;
+  if (use_bin) {
+    smem = (size_t)PLANE_BYTES + (size_t)2 * BPLANE * 4 + 16 + (size_t)(cells + 1) * sizeof(LutEntry) +
+           (size_t)hsize * 4;
+    kfn = mode == 2 ? (const void*)ecc_fast3d_bin_kernel<0> : (const void*)ecc_fast3d_bin_kernel<1>;
+  } else {
+    smem = (size_t)NSTAGE * PLANE_BYTES + 4 * 8 + (size_t)(b->lut_ok ? cells + 1 : 0) * sizeof(LutEntry) +
+           (size_t)((nb + 1 + 3) & ~3) * 4 + (size_t)(b->lut_ok ? 0 : nb + 2) * 4;
+    kfn = (const void*)ecc_fast3d_kernel;
+  }
+  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(fast3d)");
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ecc_fast3d_kernel, NT, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, NT, smem);
   if (occ < 1) return set_error(ECC_EINVAL, "fast3d kernel does not fit on an SM");
   const int64_t max_ctas = (int64_t)num_sms_fast() * occ;
 
@@ -640,6 +1086,15 @@ int fast3d_launch(const float* x, int64_t D, int64_t H, int64_t W, int64_t batch
   // z-aligned partition when every tile gets at least one CTA (see kernel)
   g.zchunks = (tiles <= grid && grid <= tiles * (ze - zb)) ? (int)(grid / tiles) : 0;
   if (grid < 1) return ECC_OK;
+  if (use_bin) {
+    if (mode == 2)
+      ecc_fast3d_bin_kernel<0><<<(unsigned)grid, NT, smem, stream>>>(map, g, table, nb, cells, hsize, b->lut_scale,
+                                                                       b->lut_bias, hist);
+    else
+      ecc_fast3d_bin_kernel<1><<<(unsigned)grid, NT, smem, stream>>>(map, g, table, nb, cells, hsize, b->lut_scale,
+                                                                       b->lut_bias, hist);
+    return check_launch("ecc_fast3d_bin_kernel");
+  }
   ecc_fast3d_kernel<<<(unsigned)grid, NT, smem, stream>>>(map, g, table, nb, cells, cell_shift, b->lut_scale,
                                                             b->lut_bias, b->lut_ok, hist);
   return check_launch("ecc_fast3d_kernel");

@@ -42,10 +42,34 @@ def _table(taus, dtype_code):
     from paper_2510_20271_b200 import _lib
 
     taus = np.ascontiguousarray(taus, dtype=np.float64)
-    out = np.empty(taus.size + 2, dtype=np.float64 if dtype_code == 2 else np.float32)
+    # the table holds the thresholds with sentinels plus, for float32, the cell table
+    nbytes = int(_lib.lib().ecc_threshold_table_bytes(taus.size, dtype_code))
+    isz = 8 if dtype_code == 2 else 4
+    out = np.empty(nbytes // isz, dtype=np.float64 if dtype_code == 2 else np.float32)
     b = _lib.Binning()
     rc = _lib.lib().ecc_threshold_table(_lib.ptr(taus), taus.size, dtype_code, _lib.ptr(out), ctypes.byref(b))
     return rc, out, b
+
+
+def test_threshold_table_cell_table_exact():
+    """the float32 cell table (bin = b + (x > t) per cell) reproduces searchsorted-left on every float near
+    a threshold and across the range; the bin-image kernel bins every voxel through it."""
+    rng = np.random.default_rng(5)
+    for taus in (np.linspace(0.0, 1.0, 1025)[1:], np.linspace(-3.7, 5.1, 256), np.arange(0.0, 256.0, 1.0)):
+        rc, t, b = _table(taus, 1)
+        assert rc == 0 and b.lut_ok == 1
+        n, cells = taus.size, b.lut_cells
+        t32 = t[1:n + 1]
+        lut = t[(n + 2 + 1) & ~1:].view(np.uint32)[:2 * (cells + 1)].reshape(cells + 1, 2)
+        lt, lb = lut[:, 0].view(np.float32), lut[:, 1].astype(np.int64)
+        probes = np.concatenate([t32, np.nextafter(t32, np.float32(np.inf)), np.nextafter(t32, np.float32(-np.inf)),
+                                 rng.uniform(taus[0] - 1, taus[-1] + 1, 4000).astype(np.float32)]).astype(np.float32)
+        g = np.clip(np.fma(probes, np.float32(b.lut_scale), np.float32(b.lut_bias)) if hasattr(np, 'fma') else
+                    (probes.astype(np.float64) * b.lut_scale + b.lut_bias).astype(np.float32), 0, 1)
+        cell = np.floor(g.astype(np.float64) * cells).astype(np.int64)
+        got = lb[cell] + (probes > lt[cell])
+        want = np.searchsorted(taus, probes.astype(np.float64), side="left")
+        assert np.array_equal(got, want)
 
 
 def test_threshold_table_round_down_exact():
@@ -57,8 +81,9 @@ def test_threshold_table_round_down_exact():
     for taus in hostile:
         rc, t, b = _table(taus, 1)
         assert rc == 0
-        assert t[0] == -np.inf and t[-1] == np.inf
-        t32 = t[1:-1]
+        n = taus.size
+        assert t[0] == -np.inf and t[n + 1] == np.inf
+        t32 = t[1:n + 1]
         assert np.all(t32.astype(np.float64) <= taus)
         nxt = np.nextafter(t32, np.float32(np.inf))
         assert np.all((nxt.astype(np.float64) > taus) | (t32 == np.float32(3.4028235e38)))
