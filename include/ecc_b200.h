@@ -161,6 +161,17 @@ int ecc_soft_backward(const int8_t *coeffs, const float *field_c, const float *f
                       const ecc_soft_params *params_host, const double *upstream, float *d_values, double *d_tau,
                       double *G, void *workspace, void *stream);
 
+/* Finite-difference harness for gradient_check (soft.py:260-359), float64:
+ * 4th-order central differences (soft.py:308-315) with step `step` of
+ * L = sum_j up_j sum_p c_p sigmoid(lam (tau_j - f_p)), f the effective
+ * field (float64, e.g. from ecc_effective_field), coefficients held fixed.
+ * fd_values[n] = dL/dX_p, fd_tau[nbins] = dL/dtau_j, fd_dir[0..ndim) =
+ * dL/du_a (free vector, unprojected), fd_dir[ndim] = dL/dalpha.  All
+ * device pointers except u_host (ndim doubles, host). */
+int ecc_soft_fd(const double *field, const int8_t *coeffs, int ndim, const int64_t *dims, const double *taus,
+                int64_t nbins, const double *upstream, double lam, double alpha, const double *u_host, double step,
+                double *fd_values, double *fd_tau, double *fd_dir, void *stream);
+
 /* Counter-based synthetic float32 grid: out[i] = top-24-bits(splitmix64(
  * seed * K + start + i)) * 2^-24 (identical to the oracle's
  * generator so 2048^3 slabs are reproducible on both sides). */

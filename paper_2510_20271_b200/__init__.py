@@ -5,7 +5,8 @@ Same names and semantics as the reference package's hot-path API
 differentiable curve (soft_ecc / soft_ecc_backward), computed by sm_100a CUDA
 kernels behind a C ABI (include/ecc_b200.h).  Torch-native extensions:
 ``ecc_discrete`` (batched exact curves on device tensors) and the
-``SoftECC`` nn.Module.  Multi-GPU helpers live in ``.distributed``.
+``SoftECC`` nn.Module.  Multi-GPU helpers live in ``.distributed``; grid files and
+the streaming device loader in ``.io``.
 """
 
 from .coefficients import COEFF_RANGE, CoefficientGrid, coefficients_device, compute_coefficients, vertex_order
@@ -34,12 +35,27 @@ from .hard import (
     parse_strategy,
     scan_device,
 )
+from .io import (
+    MAGIC,
+    VERSION_COEFF,
+    VERSION_SCALAR,
+    load_grid_device,
+    load_slab_device,
+    read_coefficients,
+    read_curve,
+    read_grid,
+    save_grid_device,
+    write_coefficients,
+    write_curve,
+    write_grid,
+)
 from .soft import (
     SoftECC,
     SoftECCFunction,
     SoftEccParams,
     SoftGradients,
     effective_field,
+    gradient_check,
     pixel_coordinates,
     reparametrize_direction,
     reparametrize_direction_jvp,
@@ -56,5 +72,7 @@ __all__ = [
     "device_minmax", "ecc_discrete", "effective_field", "flatten_index", "histogram_device", "merge_histograms",
     "parse_strategy", "pixel_coordinates", "reparametrize_direction", "reparametrize_direction_jvp", "scan_device",
     "soft_ecc", "soft_ecc_backward", "thresholds_from_range", "unflatten_index", "uniform_thresholds",
-    "vertex_order",
+    "vertex_order", "gradient_check", "MAGIC", "VERSION_COEFF", "VERSION_SCALAR", "load_grid_device", "load_slab_device",
+    "read_coefficients", "read_curve", "read_grid", "save_grid_device", "write_coefficients", "write_curve",
+    "write_grid",
 ]

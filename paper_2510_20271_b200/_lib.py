@@ -67,6 +67,8 @@ def lib():
                                         vp, vp, vp, vp]
         L.ecc_effective_field.argtypes = [vp, i32, i32, vp, i64, ctypes.c_double, vp, vp, vp]
         L.ecc_counter_grid.argtypes = [ctypes.c_uint64, i64, i64, vp, vp]
+        dbl = ctypes.c_double
+        L.ecc_soft_fd.argtypes = [vp, vp, i32, vp, vp, i64, vp, dbl, dbl, vp, dbl, vp, vp, vp, vp]
         _lib = L
     return _lib
 

@@ -17,7 +17,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libecc_b200.so"
-SOURCES = ["ecc_host.cu", "ecc_discrete.cu", "ecc_fast3d.cu", "ecc_soft.cu"]
+SOURCES = ["ecc_host.cu", "ecc_discrete.cu", "ecc_fast3d.cu", "ecc_soft.cu", "ecc_fdcheck.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

@@ -226,3 +226,59 @@ class TestModule3D:
         dv, dt, _, _, _ = oracle.soft_backward(xi, c, 2000.0, 0.0, [1.0, 0.0], taus0, np.ones(16))
         assert normwise(xt.grad.cpu().numpy(), dv) <= TOL
         assert normwise(m.taus.grad.cpu().numpy(), dt) <= TOL
+
+
+@pytest.mark.gpu
+class TestGradientCheck:
+    """gradient_check (soft.py:260-359) on the device: float64 4th-order finite
+    differences against the fp32 analytic kernels."""
+
+    def _case(self, rng, dims, ndim_u, lam, nb, alpha=0.3):
+        x = rng.random(dims).astype(np.float32).astype(np.float64)
+        u = E.reparametrize_direction([1.0, 2.0, -0.5][:ndim_u])
+        f = oracle.effective_field(x, alpha, u)
+        taus = np.unique(np.linspace(f.min(), f.max(), nb))
+        return x, E.SoftEccParams(lam=lam, alpha=alpha, u=u, taus=E.ThresholdSet(taus))
+
+    def test_fd_harness_matches_oracle_gradients(self, rng):
+        """The FD harness differentiates the reference's loss: its result equals
+        the oracle's float64 analytic gradients to truncation error."""
+        for dims, k, lam, nb in [((24, 20), 2, 50.0, 64), ((7, 8, 9), 3, 10.0, 32)]:
+            x, params = self._case(rng, dims, k, lam, nb)
+            rep = E.gradient_check(E.ScalarGrid(x), params)
+            for key in ("d_values", "d_tau", "d_u", "d_alpha"):
+                assert rep["normwise"][key] <= 1e-4, (dims, key, rep)
+            assert rep["tangency"] <= 1e-8
+            # the harness itself against the oracle (float64 analytic)
+            up = np.random.default_rng(0).uniform(0.5, 1.5, size=len(params.taus))
+            c = oracle.coefficients(oracle.effective_field(x, params.alpha, params.u))
+            dv, dt, du, da, _ = oracle.soft_backward(x, c, params.lam, params.alpha, params.u, params.taus.taus, up)
+            g = E.soft_ecc_backward(E.ScalarGrid(x), E.CoefficientGrid(c), params, up)
+            assert normwise(g.d_tau, dt) <= 1e-4 and normwise(g.d_values, dv) <= 1e-4
+
+    def test_dalpha_against_reference_fd(self, golden):
+        """the harness's d_alpha equals the reference's own FD of _forward_raw in alpha (golden)."""
+        n = int(golden["manifest"][2])
+        checked = 0
+        for k in range(n):
+            x = golden[f"soft{k}_x"]
+            alpha, lam = (float(v) for v in golden[f"soft{k}_params"])
+            if x.size < 16 or alpha == 0.0:
+                continue
+            u = golden[f"soft{k}_u"]
+            params = E.SoftEccParams(lam=lam, alpha=alpha, u=u, taus=E.ThresholdSet(golden[f"soft{k}_taus"]))
+            rep = E.gradient_check(E.ScalarGrid(x), params, upstream=golden[f"soft{k}_upstream"])
+            want = float(golden[f"soft{k}_dalpha_fd"][0])
+            assert abs(rep["fd_alpha"] - want) <= 1e-6 * max(1.0, abs(want)), (k, rep["fd_alpha"], want)
+            assert rep["normwise"]["d_alpha"] <= 1e-4, (k, rep)
+            checked += 1
+        assert checked >= 3
+
+    def test_realistic_size(self, rng):
+        """256 x 256, 256 thresholds, lambda = 50: far beyond the reference's
+        per-pixel loop, every gradient within 1e-4 normwise."""
+        x, params = self._case(rng, (256, 256), 2, 50.0, 256)
+        rep = E.gradient_check(E.ScalarGrid(x), params)
+        for key in ("d_values", "d_tau", "d_u", "d_alpha"):
+            assert rep["normwise"][key] <= 1e-4, (key, rep)
+        assert rep["tangency"] <= 1e-8
