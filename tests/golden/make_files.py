@@ -18,6 +18,8 @@ sys.path.insert(0, "/root/reference/pkg/src")
 
 from ecckit import (  # noqa: E402
     ScalarGrid,
+    SyntheticSpec,
+    generate_grid,
     SoftEccParams,
     compute_coefficients,
     compute_ecc,
@@ -47,6 +49,10 @@ def main():
     ts = uniform_thresholds(f, 16)
     params = SoftEccParams(lam=50.0, alpha=0.3, u=u, taus=ts)
     write_curve(soft_ecc(g2, compute_coefficients(f), params), OUT / "soft_g2d_16.csv")
+    write_grid(generate_grid(SyntheticSpec(kind="gaussian-blobs", dims=(12, 10), seed=4, blobs=3)),
+               OUT / "blobs_12x10_s4_b3.eccg")
+    write_grid(generate_grid(SyntheticSpec(kind="radial-gradient", dims=(5, 6, 7))), OUT / "radial_5x6x7.eccg")
+    write_grid(generate_grid(SyntheticSpec(kind="uniform-random", dims=(4, 5, 6), seed=9)), OUT / "uniform_4x5x6_s9.eccg")
     for p in sorted(OUT.iterdir()):
         print(p.name, p.stat().st_size)
 
