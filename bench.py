@@ -347,7 +347,7 @@ def run_b200(args):
                        "minmax_pass_ms": minmax_ms, "seed": SEED, "curve_xor_checksum": checksum},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
-                         "kernel": "ecc_fast3d_kernel" if W % 4 == 0 else "ecc_sweep_kernel<RawSrc<float>,HistSink<float>>",
+                         "kernel": "ecc_fast3d_bin_kernel" if W % 4 == 0 else "ecc_sweep_kernel<RawSrc<float>,HistSink<float>>",
                          "kernel_ms": kmean, "algorithmic_bytes_per_launch": 4 * vox_rank},
             "cpu_baseline": cpu,
             "e2e": e2e,
