@@ -153,15 +153,22 @@ ecc_soft_kernel(SoftArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
   // ---- compaction of the chunk to c != 0 voxels (order-preserving) -------
+  // Each warp owns CITER x 32 consecutive voxels; all of its coefficient and
+  // field loads are issued up front (one memory latency, not CITER).
   {
-    const int per_warp = (CH + SNW - 1) / SNW;
-    const int w0 = warp * per_warp, w1 = min(w0 + per_warp, nvox);
-    int cnt = 0;
-    for (int base = w0; base < w1; base += 32) {
-      const int i = base + lane;
-      const int cv = i < w1 ? (int)cg[i] : 0;
-      cnt += __popc(__ballot_sync(0xffffffffu, cv != 0));
+    constexpr int CITER = CH / SNW / 32;
+    const int w0 = warp * (CITER * 32), w1 = min(w0 + CITER * 32, nvox);
+    int cvr[CITER];
+    float fvr[CITER];
+#pragma unroll
+    for (int it = 0; it < CITER; ++it) {
+      const int i = w0 + it * 32 + lane;
+      cvr[it] = i < w1 ? (int)cg[i] : 0;
+      fvr[it] = i < w1 ? fg[i] : 0.f;
     }
+    int cnt = 0;
+#pragma unroll
+    for (int it = 0; it < CITER; ++it) cnt += __popc(__ballot_sync(0xffffffffu, cvr[it] != 0));
     if (lane == 0) s_wcount[warp] = cnt;
     __syncthreads();
     int off = 0;
@@ -171,13 +178,14 @@ ecc_soft_kernel(SoftArgs a) {
       for (int w = 0; w < SNW; ++w) tot += s_wcount[w];
       S.count = tot;
     }
-    for (int base = w0; base < w1; base += 32) {
-      const int i = base + lane;
-      const int cv = i < w1 ? (int)cg[i] : 0;
+#pragma unroll
+    for (int it = 0; it < CITER; ++it) {
+      const int i = w0 + it * 32 + lane;
+      const int cv = cvr[it];
       const unsigned m = __ballot_sync(0xffffffffu, cv != 0);
       if (cv != 0) {
         const int k = off + __popc(m & ((1u << lane) - 1u));
-        S.fc[k] = fg[i];
+        S.fc[k] = fvr[it];
         if (!FACT) S.fclo[k] = a.fclo[item * a.n + v0 + i];
         S.pk[k] = i | (cv << 16);
       } else if (BWD && i < w1) {
@@ -235,13 +243,9 @@ ecc_soft_kernel(SoftArgs a) {
   }
   const float koff = FACT ? (float)(ks * (a.m - ml)) : 0.f;   // k f_p - k m_l = k fc + koff
 
-  // warp-uniform trip count: the group reduction shuffles across the warp
-  for (int kb = warp * VW; kb < count; kb += nslots) {
-    const int k = kb + g;
-    const bool valid = k < count;
+  auto voxel_w = [&](int k, bool valid) -> float {
     const float f = valid ? S.fc[k] : 0.f;
-    const int pk = valid ? S.pk[k] : 0;
-    const float cf = (float)(pk >> 16);
+    const float cf = valid ? (float)(S.pk[k] >> 16) : 0.f;
     float w = 0.f;
     if (FACT) {
       const float kf = fminf(fmaxf(__fmaf_rn(a.kscale, f, koff), -B_MAX), B_MAX);
@@ -250,11 +254,52 @@ ecc_soft_kernel(SoftArgs a) {
       const double fd = (double)f + (double)(valid ? S.fclo[k] : 0.f);
       pair_loop_direct<BWD, T>(kt, Lv, l, upv, acc, ks * fd, cf, w);
     }
-    if (BWD) {
+    return w;
+  };
+  const float lamf = (float)a.lam;
+  int kb0 = warp * VW;
+  if (BWD && FACT && Lv == 8) {
+    // deferred group reduction: 8 voxel rounds, then one reduce-scatter over
+    // the 8 lanes of the group (7 shuffles for 8 voxels instead of 24); lane
+    // l ends with the full w of round l and writes that voxel's dX
+    for (; kb0 < count; kb0 += 8 * nslots) {
+      float wv[8];
 #pragma unroll
-      for (int o = 16; o; o >>= 1)
-        if (o < Lv) w += __shfl_xor_sync(0xffffffffu, w, o);   // Lv is warp-uniform
-      if (l == 0 && valid) a.dX[item * a.n + v0 + (pk & 0xffff)] = -cf * ((float)a.lam * w);
+      for (int r = 0; r < 8; ++r) {
+        const int k = kb0 + r * nslots + g;
+        wv[r] = voxel_w(k, k < count);
+      }
+#pragma unroll
+      for (int o = 4, n = 4; o; o >>= 1, n >>= 1) {
+        const bool up = (l & o) != 0;
+#pragma unroll
+        for (int i = 0; i < n; ++i) {
+          const float mine = up ? wv[n + i] : wv[i];
+          const float give = up ? wv[i] : wv[n + i];
+          wv[i] = mine + __shfl_xor_sync(0xffffffffu, give, o);
+        }
+      }
+      const int k = kb0 + l * nslots + g;
+      if (k < count) {
+        const int pk = S.pk[k];
+        a.dX[item * a.n + v0 + (pk & 0xffff)] = -(float)(pk >> 16) * (lamf * wv[0]);
+      }
+    }
+  } else {
+    // warp-uniform trip count: the group reduction shuffles across the warp
+    for (int kb = kb0; kb < count; kb += nslots) {
+      const int k = kb + g;
+      const bool valid = k < count;
+      float w = voxel_w(k, valid);
+      if (BWD) {
+#pragma unroll
+        for (int o = 16; o; o >>= 1)
+          if (o < Lv) w += __shfl_xor_sync(0xffffffffu, w, o);   // Lv is warp-uniform
+        if (l == 0 && valid) {
+          const int pk = S.pk[k];
+          a.dX[item * a.n + v0 + (pk & 0xffff)] = -(float)(pk >> 16) * (lamf * w);
+        }
+      }
     }
   }
 

@@ -3,17 +3,20 @@ import csv, subprocess, sys
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 30
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+extra = sys.argv[3:]          # e.g. --launch-skip 1 --launch-count 1
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass", *extra],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
-hi = next(i for i, r in enumerate(rows) if r and r[0] == "Line No")
-hdr = rows[hi]
-iE = hdr.index("Instructions Executed")
-iS = hdr.index("Warp Stall Sampling (All Samples)")
-st = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
 per, tot, tots = [], 0, 0
-for r in rows[hi + 1:]:
-    if not r or not r[0] or len(r) <= iE:
+hdr = None
+for r in rows:
+    if r and r[0] == "Line No":
+        hdr = r
+        iE = hdr.index("Instructions Executed")
+        iS = hdr.index("Warp Stall Sampling (All Samples)")
+        st = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
+        continue
+    if hdr is None or not r or not r[0] or len(r) <= iE or r[0] in ("File Path", "Function Name", "File Name"):
         continue
     try:
         n, smp = int(r[iE]), int(r[iS])
