@@ -39,7 +39,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not _stale():
         return LIB
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-o", str(LIB), *[str(CSRC / s) for s in SOURCES]]
+    extra = os.environ.get("ECC_B200_NVCC_EXTRA", "").split()   # development A/B switches (-D...)
+    cmd = [nvcc, *NVCC_FLAGS, *extra, "-o", str(LIB), *[str(CSRC / s) for s in SOURCES]]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), flush=True)
