@@ -53,7 +53,9 @@ struct EffSrc {
   double sD, sH, sW;   // 2.0 / (d - 1) in float64 (host-computed like numpy), 0 when d == 1
   // pixel_coordinates (soft.py:79-94): idx * (2/(d-1)) - 1 with two roundings; 0 for d == 1
   __device__ __forceinline__ static double crd(int64_t idx, int64_t d, double s) {
-    return d == 1 ? 0.0 : __dadd_rn(__dmul_rn((double)idx, s), -1.0);
+    // extents are < 2^31 (checked by the launchers), so the int32 -> f64
+    // conversion is exact and avoids the slow 64-bit integer conversion
+    return d == 1 ? 0.0 : __dadd_rn(__dmul_rn((double)(int)idx, s), -1.0);
   }
   __device__ __forceinline__ V at(int64_t lin, int64_t z, int64_t y, int64_t xx) const {
     double v = (double)x[lin];
@@ -483,8 +485,10 @@ static int dims_to3(int ndim, const int64_t* dims, int64_t out[3]) {
   } else {
     return set_error(ECC_EINVAL, "grid must be 2D or 3D");
   }
-  for (int a = 0; a < 3; ++a)
+  for (int a = 0; a < 3; ++a) {
     if (out[a] < 1) return set_error(ECC_EINVAL, "grid extents must be positive");
+    if (out[a] > 2147483647) return set_error(ECC_EINVAL, "grid extent exceeds 2^31 - 1");
+  }
   return ECC_OK;
 }
 
@@ -611,34 +615,47 @@ namespace ecc {
 template <typename T>
 __global__ void __launch_bounds__(256) soft_prep2d_kernel(EffSrc<T> src, double center, int8_t* __restrict__ coeffs,
                                                           float* __restrict__ fc, float* __restrict__ fclo) {
-  __shared__ double tile[10][34];
+  // 32 x 32 outputs per CTA (8 warps x 4 rows); the 34 x 34 effective-field
+  // tile is loaded with all of a thread's global loads in flight at once
+  constexpr int TH = 32, TW = 32, PWD = TW + 2, PHT = TH + 2, NE = PWD * PHT, PER = (NE + 255) / 256;
+  __shared__ double tile[PHT][PWD];
   const int64_t n = blockIdx.z;
-  const int64_t y0 = (int64_t)blockIdx.y * 8, x0 = (int64_t)blockIdx.x * 32;
+  const int64_t y0 = (int64_t)blockIdx.y * TH, x0 = (int64_t)blockIdx.x * TW;
   const int64_t H = src.H, W = src.W;
   const int64_t base = n * H * W;
   const double nanv = __longlong_as_double(0x7ff8000000000000ll);
-  for (int e = threadIdx.x; e < 340; e += 256) {
-    const int ry = e / 34, rx = e - ry * 34;
+  double vals[PER];
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int e = threadIdx.x + 256 * k;
+    const int ry = e / PWD, rx = e - ry * PWD;
     const int64_t yy = y0 - 1 + ry, xx = x0 - 1 + rx;
-    double v = nanv;
-    if (yy >= 0 && yy < H && xx >= 0 && xx < W) v = src.at(base + yy * W + xx, 0, yy, xx);
-    tile[ry][rx] = v;
+    vals[k] = (e < NE && yy >= 0 && yy < H && xx >= 0 && xx < W) ? src.at(base + yy * W + xx, 0, yy, xx) : nanv;
+  }
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int e = threadIdx.x + 256 * k;
+    if (e < NE) tile[e / PWD][e % PWD] = vals[k];
   }
   __syncthreads();
-  const int ty = threadIdx.x >> 5, tx = threadIdx.x & 31;
-  const int64_t y = y0 + ty, x = x0 + tx;
-  if (y < H && x < W) {
-    double v[3][3];
+  const int tx = threadIdx.x & 31, wy = threadIdx.x >> 5;
 #pragma unroll
-    for (int a = 0; a < 3; ++a)
+  for (int q = 0; q < TH / 8; ++q) {
+    const int ty = wy + 8 * q;
+    const int64_t y = y0 + ty, x = x0 + tx;
+    if (y < H && x < W) {
+      double v[3][3];
 #pragma unroll
-      for (int b = 0; b < 3; ++b) v[a][b] = tile[ty + a][tx + b];
-    const int64_t i = base + y * W + x;
-    coeffs[i] = (int8_t)coeff2<double>(v);
-    const double d = v[1][1] - center;
-    const float hi = (float)d;
-    fc[i] = hi;
-    if (fclo) fclo[i] = (float)(d - (double)hi);
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) v[a][b] = tile[ty + a][tx + b];
+      const int64_t i = base + y * W + x;
+      coeffs[i] = (int8_t)coeff2<double>(v);
+      const double d = v[1][1] - center;
+      const float hi = (float)d;
+      fc[i] = hi;
+      if (fclo) fclo[i] = (float)(d - (double)hi);
+    }
   }
 }
 }  // namespace ecc
@@ -655,7 +672,7 @@ extern "C" int ecc_soft_prepare(const void* x, int dtype, int ndim, const int64_
   SoftPrepSink sk{coeffs, field_c, field_lo, p->center, d3[0], d3[1], d3[2]};
   cudaStream_t s = (cudaStream_t)stream;
   if (ndim == 2 && batch <= 65535 && (dtype == ECC_DTYPE_F32 || dtype == ECC_DTYPE_F64)) {
-    dim3 grid((unsigned)((d3[2] + 31) / 32), (unsigned)((d3[1] + 7) / 8), (unsigned)batch);
+    dim3 grid((unsigned)((d3[2] + 31) / 32), (unsigned)((d3[1] + 31) / 32), (unsigned)batch);
     if (grid.y > 65535) goto generic;
     if (dtype == ECC_DTYPE_F32) {
       EffSrc<float> src{(const float*)x, p->alpha, p->u[0], p->u[1], 0.0, 1, d3[1], d3[2], 2,
