@@ -1,4 +1,5 @@
-timeout 600 python -m pytest tests/test_gpu_soft.py tests/test_gpu_discrete.py -m gpu -x -q --timeout 300 2>&1 | tail -1
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_soft16d.csv python tools/prof_soft.py 16 3 > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:soft_prep2d -s 1 -c 1 -o gpurun_out/prof_prep python tools/prof_soft.py 16 2 > /dev/null 2>&1
+timeout 300 python tools/prof_soft3d.py 1024 1 2>&1 | tail -1
+timeout 300 python tools/prof_soft3d.py 512 2 2>&1 | tail -1
+python bench.py > gpurun_out/bench_r01e.json 2> gpurun_out/bench_r01e.err; tail -1 gpurun_out/bench_r01e.json | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['roofline']['frac'], d['soft']['value'], d['soft']['ms_per_step'], d['e2e']['value'])"
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_soft3d.csv python tools/prof_soft3d.py 512 1 > /dev/null 2>&1
 echo done
