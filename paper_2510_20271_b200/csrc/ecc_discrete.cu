@@ -20,22 +20,38 @@ namespace ecc {
 template <typename T>
 struct RawSrc;
 
+// raw(lin) is the bare global load, make(raw, z, y, x) the value it stands
+// for; the sweep issues raw loads one plane ahead and applies make() only
+// when the plane is stored to shared memory, so the loads' latency overlaps
+// the current plane's work.
 template <>
 struct RawSrc<uint8_t> {
   using V = float;
+  using R = float;   // converted at load: nothing left for make()
+  static constexpr bool kTransform = false;
   const uint8_t* __restrict__ x;
+  __device__ __forceinline__ R raw(int64_t lin) const { return (float)x[lin]; }
+  __device__ __forceinline__ V make(R r, int64_t, int64_t, int64_t) const { return r; }
   __device__ __forceinline__ V at(int64_t lin, int64_t, int64_t, int64_t) const { return (float)x[lin]; }
 };
 template <>
 struct RawSrc<float> {
   using V = float;
+  using R = float;
+  static constexpr bool kTransform = false;
   const float* __restrict__ x;
+  __device__ __forceinline__ R raw(int64_t lin) const { return x[lin]; }
+  __device__ __forceinline__ V make(R r, int64_t, int64_t, int64_t) const { return r; }
   __device__ __forceinline__ V at(int64_t lin, int64_t, int64_t, int64_t) const { return x[lin]; }
 };
 template <>
 struct RawSrc<double> {
   using V = double;
+  using R = double;
+  static constexpr bool kTransform = false;
   const double* __restrict__ x;
+  __device__ __forceinline__ R raw(int64_t lin) const { return x[lin]; }
+  __device__ __forceinline__ V make(R r, int64_t, int64_t, int64_t) const { return r; }
   __device__ __forceinline__ V at(int64_t lin, int64_t, int64_t, int64_t) const { return x[lin]; }
 };
 
@@ -57,8 +73,11 @@ struct EffSrc {
     // conversion is exact and avoids the slow 64-bit integer conversion
     return d == 1 ? 0.0 : __dadd_rn(__dmul_rn((double)(int)idx, s), -1.0);
   }
-  __device__ __forceinline__ V at(int64_t lin, int64_t z, int64_t y, int64_t xx) const {
-    double v = (double)x[lin];
+  using R = T;
+  static constexpr bool kTransform = true;
+  __device__ __forceinline__ R raw(int64_t lin) const { return x[lin]; }
+  __device__ __forceinline__ V make(R r, int64_t z, int64_t y, int64_t xx) const {
+    double v = (double)r;
     if (alpha == 0.0) return v;
     double dot;
     if (ndim == 2) {
@@ -69,6 +88,9 @@ struct EffSrc {
       dot = __fma_rn(p2, u2, __fma_rn(p0, u0, __dmul_rn(p1, u1)));
     }
     return __dadd_rn(v, __dmul_rn(alpha, dot));
+  }
+  __device__ __forceinline__ V at(int64_t lin, int64_t z, int64_t y, int64_t xx) const {
+    return make(x[lin], z, y, xx);
   }
 };
 
@@ -223,32 +245,43 @@ ecc_sweep_kernel(Src src, Sink sink, Geom g) {
     const int64_t item_base = n * g.D * g.H * g.W;
     sink.begin_item(n, (ze - zs) * TX * TY);
 
-    // per-thread staging coordinates for cooperative plane loads
-    auto load_plane = [&](int64_t z, V (&buf)[LPT]) {
+    // per-thread staging: raw loads (R) into registers, value transform +
+    // shared-memory store later (see RawSrc)
+    using R = typename Src::R;
+    auto in_plane = [&](int64_t z, int k, int64_t& yy, int64_t& xx) -> bool {
+      const int e = threadIdx.x + k * NT;
+      if (e >= PLANE) return false;
+      const int ry = e / PW, rx = e - ry * PW;
+      yy = y0 - 1 + ry;
+      xx = x0 - 1 + rx;
+      return z >= 0 && z < g.D && yy >= 0 && yy < g.H && xx >= 0 && xx < g.W;
+    };
+    auto load_plane = [&](int64_t z, R (&buf)[LPT]) {
 #pragma unroll
       for (int k = 0; k < LPT; ++k) {
-        int e = threadIdx.x + k * NT;
-        V val = nanv;
-        if (e < PLANE) {
-          int ry = e / PW, rx = e - ry * PW;
-          int64_t yy = y0 - 1 + ry, xx = x0 - 1 + rx;
-          if (z >= 0 && z < g.D && yy >= 0 && yy < g.H && xx >= 0 && xx < g.W)
-            val = src.at(item_base + (z * g.H + yy) * g.W + xx, z, yy, xx);
-        }
-        buf[k] = val;
+        int64_t yy, xx;
+        // sources without a transform load the final value (NaN out of grid)
+        buf[k] = in_plane(z, k, yy, xx) ? src.raw(item_base + (z * g.H + yy) * g.W + xx)
+                                        : (Src::kTransform ? R(0) : R(nanv));
       }
     };
-    auto store_plane = [&](int64_t z, const V (&buf)[LPT]) {
+    auto store_plane = [&](int64_t z, const R (&buf)[LPT]) {
       V* dst = planes + (int)((z + 4) & (NBUF - 1)) * PLANE;
 #pragma unroll
       for (int k = 0; k < LPT; ++k) {
-        int e = threadIdx.x + k * NT;
-        if (e < PLANE) dst[e] = buf[k];
+        const int e = threadIdx.x + k * NT;
+        if (!Src::kTransform) {
+          if (e < PLANE) dst[e] = buf[k];
+        } else {
+          int64_t yy, xx;
+          const bool ok = in_plane(z, k, yy, xx);
+          if (e < PLANE) dst[e] = ok ? src.make(buf[k], z, yy, xx) : nanv;
+        }
       }
     };
 
     {
-      V b0[LPT], b1[LPT], b2[LPT];
+      R b0[LPT], b1[LPT], b2[LPT];
       load_plane(zs - 1, b0);
       load_plane(zs, b1);
       load_plane(zs + 1, b2);
@@ -270,7 +303,7 @@ ecc_sweep_kernel(Src src, Sink sink, Geom g) {
     }
 
     for (int64_t z = zs; z < ze; ++z) {
-      V nxt[LPT];
+      R nxt[LPT];
       const bool more = (z + 2 <= ze);   // plane z+2 is needed by step z+1
       if (more) load_plane(z + 2, nxt);
       // shift window and read plane z+1
