@@ -741,7 +741,7 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
   const uint32_t lut_m = smem_u32(s_lut) - 0x58000000u;   // - 0x4B000000 entries (mod 2^32)
   const float fcells = (float)cells;
   char* const hbytes = reinterpret_cast<char*>(s_hist);
-  char* const dummy = hbytes + 4 * (nb + 1 + lane);
+  const uint32_t dummy_off = 4u * (uint32_t)(nb + 1 + lane);   // < 2^16 for nb <= 8190
 
   uint32_t phase = 0;
   int64_t cur_n = -1;
@@ -958,6 +958,19 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
         // c moves into the high nibble of a byte, so one sign-replicating
         // byte permute yields 16 c as int32 (the counters hold 16 c)
         if (__any_sync(FULL, any != 0u)) {
+          // counter offsets per voxel: the voxel's own 16-bit lane (4 bin) when
+          // c != 0, else this lane's private dummy counter (adding 0 there costs
+          // no bank traffic on the real counters).  Selected once per word:
+          // bits j, j+16 of the nonzero mask -> byte masks -> one LOP3.
+          uint32_t Wm[16];
+          if (DEP == 1) {
+            const uint32_t d2 = dummy_off | (dummy_off << 16);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const uint32_t keep = prmt(any << (15 - j), 0u, 0xBB99u);
+              Wm[j] = (Ro.w[j] & keep) | (d2 & ~keep);
+            }
+          }
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
             const int m = (i & 7) >> 1;
@@ -966,13 +979,12 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
             // even voxels: nibble moved up into the byte's high half; odd: already there
             const uint32_t bq = (i & 1) ? (Q[i >> 3] & 0xF0F0F0F0u) : ((Q[i >> 3] << 4) & 0xF0F0F0F0u);
             const int c16 = (int)prmt(bq, 0u, sel);
-            const uint32_t off = i < 16 ? (Ro.w[i] & 0xFFFFu) : (Ro.w[i - 16] >> 16);
-            // lanes with c == 0 add 0 to a private dummy counter: no branch,
-            // no bank traffic on the real counters
             if (DEP == 0) {
+              const uint32_t off = i < 16 ? (Ro.w[i] & 0xFFFFu) : (Ro.w[i - 16] >> 16);
               if (c16) atomicAdd(reinterpret_cast<int*>(hbytes + off), c16);
             } else {
-              atomicAdd(reinterpret_cast<int*>(c16 ? hbytes + off : dummy), c16);
+              const uint32_t off = i < 16 ? (Wm[i] & 0xFFFFu) : (Wm[i - 16] >> 16);
+              atomicAdd(reinterpret_cast<int*>(hbytes + off), c16);
             }
           }
         }
