@@ -358,10 +358,11 @@ ecc_soft_kernel(SoftArgs a) {
   };
   const float lamf = (float)a.lam;
   int kb0 = warp * VW;
-  if (BWD && FACT && Lv == 8) {
-    // deferred group reduction: 8 voxel rounds, then one reduce-scatter over
-    // the 8 lanes of the group (7 shuffles for 8 voxels instead of 24); lane
-    // l ends with the full w of round l and writes that voxel's dX
+  if (BWD && FACT && Lv >= 8) {
+    // deferred group reduction: 8 voxel rounds, then (Lv > 8) a butterfly
+    // over the lane offsets >= 8 and one reduce-scatter over 8 lanes (7
+    // shuffles for 8 voxels instead of 3 per voxel); lane l < 8 ends with the
+    // full w of round l and writes that voxel's dX
     for (; kb0 < count; kb0 += 8 * nslots) {
       float wv[8];
 #pragma unroll
@@ -369,6 +370,12 @@ ecc_soft_kernel(SoftArgs a) {
         const int k = kb0 + r * nslots + g;
         wv[r] = voxel_w(k, k < count);
       }
+#pragma unroll
+      for (int o = 16; o >= 8; o >>= 1)
+        if (o < Lv) {
+#pragma unroll
+          for (int r = 0; r < 8; ++r) wv[r] += __shfl_xor_sync(0xffffffffu, wv[r], o);
+        }
 #pragma unroll
       for (int o = 4, n = 4; o; o >>= 1, n >>= 1) {
         const bool up = (l & o) != 0;
@@ -379,8 +386,8 @@ ecc_soft_kernel(SoftArgs a) {
           wv[i] = mine + __shfl_xor_sync(0xffffffffu, give, o);
         }
       }
-      const int k = kb0 + l * nslots + g;
-      if (k < count) {
+      const int k = kb0 + (l & 7) * nslots + g;
+      if (l < 8 && k < count) {
         const int pk = S.pk[k];
         a.dX[item * a.n + v0 + (pk & 0xffff)] = -(float)(pk >> 16) * (lamf * wv[0]);
       }
@@ -583,10 +590,12 @@ static int soft_launch(const int8_t* coeffs, const float* fc, const float* fclo,
   a.dX = dX;
   cudaStream_t s = (cudaStream_t)stream;
   const size_t smem = soft_smem();
-  // 32 thresholds per lane (fewer w shuffles per pair); ECC_SOFT_BWD_T=16
-  // selects the half-register backward variant (measured equal on B200)
-  const char* tenv = getenv("ECC_SOFT_BWD_T");
-  const bool t16 = BWD && nbins <= 16 * 32 && (tenv && tenv[0] == '1');
+  // 16 thresholds per lane (~80 registers, 3 CTAs/SM): on 16 x 1024^2,
+  // B = 256 the forward takes 522 vs 559 us and the backward 837 vs 868 us
+  // compared with 32 per lane; ECC_SOFT_FWD_T / ECC_SOFT_BWD_T = 32 override
+  const char* tenv = getenv(BWD ? "ECC_SOFT_BWD_T" : "ECC_SOFT_FWD_T");
+  const int tsel = tenv ? atoi(tenv) : 16;
+  const bool t16 = nbins <= 16 * 32 && tsel == 16;
   auto kfn = p->factorized ? (t16 ? ecc_soft_kernel<BWD, true, 16> : ecc_soft_kernel<BWD, true, 32>)
                            : (t16 ? ecc_soft_kernel<BWD, false, 16> : ecc_soft_kernel<BWD, false, 32>);
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
