@@ -343,10 +343,13 @@ ecc_soft_kernel(SoftArgs a) {
     if (FACT) {
       const float kf = fminf(fmaxf(__fmaf_rn(a.kscale, f, koff), -B_MAX), B_MAX);
       // forward: packed FFMA2 pairs with 3/8 of the reciprocals as Newton
-      // iterations (559 vs 616 us on 16 x 1024^2); backward: scalar FFMA, all
-      // reciprocals on MUFU (the packed / emulated variants measured 877-924
-      // vs 867 us -- the backward is latency-bound, not issue-bound)
-      if (BWD)
+      // iterations; backward: packed FFMA2 with every reciprocal on MUFU
+      // (emulating 1-2 of 8 there measured slower: the backward is
+      // latency-bound).  The scalar loop stays as the A/B reference.
+#ifndef ECC_BWD_PACKED
+#define ECC_BWD_PACKED 1   // packed FFMA2 backward (801 vs 838 us at 16 thresholds per lane)
+#endif
+      if (BWD && !ECC_BWD_PACKED)
         pair_loop_fact<BWD, T, 1024>(at, upv, acc, ex2_approx(kf), cf, w);
       else
         pair_loop_fact2<BWD, T>(at2, up2, acc2, ex2_approx(kf), cf, w);
@@ -413,7 +416,7 @@ ecc_soft_kernel(SoftArgs a) {
   // ---- fixed-order reduction of acc over the CTA's voxel slots ------------
   __syncthreads();   // chunk arrays no longer needed (red aliases them)
   const int rowlen = Lv * T;
-  if (FACT && !BWD) {
+  if (FACT && (!BWD || ECC_BWD_PACKED)) {
 #pragma unroll
     for (int i = 0; i < T / 2; ++i) f2_unpack(acc2[i], acc[2 * i], acc[2 * i + 1]);
   }
