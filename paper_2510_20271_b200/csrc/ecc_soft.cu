@@ -77,10 +77,13 @@ __device__ __forceinline__ float rcp_fma(float x) {
 // smem layout of a chunk after compaction
 struct ChunkSmem {
   float fc[CH];     // centred field f_p - m of the non-zero voxels
-  float fclo[CH];   // its float32 remainder (direct mode: f - tau in float64)
   int pk[CH];       // voxel index within the chunk | (c << 16)
   int count;
+  int pad[3];
 };
+// after ChunkSmem: factorised mode  atab[MAXB_PASS] (float)
+//                  direct mode      fclo[CH] (float remainders), kt[MAXB_PASS] (double)
+constexpr size_t CHUNK_BYTES = sizeof(ChunkSmem);
 
 // log2 bound of the per-lane factor a_j; b_p is clamped to 2^+-(126 - A_MAX)
 // so a_j b_p stays inside [2^-126, 2^126] (no overflow, no inf*0)
@@ -222,10 +225,14 @@ __device__ __forceinline__ void pair_loop_direct(const double* __restrict__ kt, 
 }
 
 template <bool BWD, bool FACT, int T>
-__global__ void __launch_bounds__(SNT, (T == 16 ? 3 : 2))
+__global__ void __launch_bounds__(SNT, (T == 8 ? 4 : (T == 16 ? 3 : 2)))
 ecc_soft_kernel(SoftArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ChunkSmem& S = *reinterpret_cast<ChunkSmem*>(smem_raw);
+  unsigned char* tail = smem_raw + CHUNK_BYTES;
+  float* s_fclo = reinterpret_cast<float*>(tail);                                   // direct mode
+  double* kt = reinterpret_cast<double*>(tail + sizeof(float) * CH);                 // direct mode
+  float* atab = reinterpret_cast<float*>(tail);                                      // factorised
   float* red = reinterpret_cast<float*>(smem_raw);   // reused after the main loop
   __shared__ int s_wcount[SNW];
   __shared__ double s_g[SNW][4];
@@ -272,7 +279,7 @@ ecc_soft_kernel(SoftArgs a) {
       if (cv != 0) {
         const int k = off + __popc(m & ((1u << lane) - 1u));
         S.fc[k] = fvr[it];
-        if (!FACT) S.fclo[k] = a.fclo[item * a.n + v0 + i];
+        if (!FACT) s_fclo[k] = a.fclo[item * a.n + v0 + i];
         S.pk[k] = i | (cv << 16);
       } else if (BWD && i < w1) {
         a.dX[item * a.n + v0 + i] = 0.f;
@@ -297,9 +304,6 @@ ecc_soft_kernel(SoftArgs a) {
   // m_l (factorised: a_j = 2^{-k (tau_j - m_l)}, b_{p,l} = 2^{k (f_p - m_l)}).
   // The per-threshold factors are computed once per CTA into shared memory.
   const double ks = a.lam * LOG2E;
-  unsigned char* tail = smem_raw + ((sizeof(ChunkSmem) + 15) & ~size_t(15));
-  double* kt = reinterpret_cast<double*>(tail);                               // direct mode
-  float* atab = reinterpret_cast<float*>(tail + sizeof(double) * MAXB_PASS);  // factorised
   if (FACT) {
     for (int j = threadIdx.x; j < Lv * T; j += SNT) {
       float av = 0.f;
@@ -354,7 +358,7 @@ ecc_soft_kernel(SoftArgs a) {
       else
         pair_loop_fact2<BWD, T>(at2, up2, acc2, ex2_approx(kf), cf, w);
     } else {
-      const double fd = (double)f + (double)(valid ? S.fclo[k] : 0.f);
+      const double fd = (double)f + (double)(valid ? s_fclo[k] : 0.f);
       pair_loop_direct<BWD, T>(kt, Lv, l, upv, acc, ks * fd, cf, w);
     }
     return w;
@@ -527,9 +531,10 @@ __global__ void ecc_soft_reduce_g(const double* __restrict__ gpart, int64_t chun
   if (threadIdx.x < ndim) G[item * ndim + threadIdx.x] = sm[0][threadIdx.x];
 }
 
-static size_t soft_smem() {
-  size_t chunk = ((sizeof(ChunkSmem) + 15) & ~size_t(15)) + (sizeof(double) + sizeof(float)) * MAXB_PASS;
-  size_t red = sizeof(float) * (size_t)SNT * TT;   // nslots*rowlen = 8*VW*Lv*TT = 256*TT
+static size_t soft_smem(bool fact, int T) {
+  const size_t chunk = CHUNK_BYTES + (fact ? sizeof(float) * MAXB_PASS
+                                           : sizeof(float) * CH + sizeof(double) * MAXB_PASS);
+  const size_t red = sizeof(float) * (size_t)SNT * T;   // nslots * rowlen = 8 * VW * Lv * T = 256 T
   return chunk > red ? chunk : red;
 }
 
@@ -592,15 +597,18 @@ static int soft_launch(const int8_t* coeffs, const float* fc, const float* fclo,
   a.gpart = a.part + (size_t)(batch * chunks) * (size_t)nbins;
   a.dX = dX;
   cudaStream_t s = (cudaStream_t)stream;
-  const size_t smem = soft_smem();
   // 16 thresholds per lane (~80 registers, 3 CTAs/SM): on 16 x 1024^2,
   // B = 256 the forward takes 522 vs 559 us and the backward 837 vs 868 us
   // compared with 32 per lane; ECC_SOFT_FWD_T / ECC_SOFT_BWD_T = 32 override
   const char* tenv = getenv(BWD ? "ECC_SOFT_BWD_T" : "ECC_SOFT_FWD_T");
   const int tsel = tenv ? atoi(tenv) : 16;
-  const bool t16 = nbins <= 16 * 32 && tsel == 16;
-  auto kfn = p->factorized ? (t16 ? ecc_soft_kernel<BWD, true, 16> : ecc_soft_kernel<BWD, true, 32>)
-                           : (t16 ? ecc_soft_kernel<BWD, false, 16> : ecc_soft_kernel<BWD, false, 32>);
+  const int T = (tsel == 8 && nbins <= 8 * 32) ? 8 : (tsel <= 16 && nbins <= 16 * 32) ? 16 : 32;
+  const bool fact = p->factorized != 0;
+  auto kfn = fact ? (T == 8 ? ecc_soft_kernel<BWD, true, 8> : T == 16 ? ecc_soft_kernel<BWD, true, 16>
+                                                                        : ecc_soft_kernel<BWD, true, 32>)
+                  : (T == 8 ? ecc_soft_kernel<BWD, false, 8> : T == 16 ? ecc_soft_kernel<BWD, false, 16>
+                                                                         : ecc_soft_kernel<BWD, false, 32>);
+  const size_t smem = soft_smem(fact, T);
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(soft)");
   const int64_t grid = batch * chunks;
