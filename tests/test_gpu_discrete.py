@@ -345,3 +345,28 @@ class TestFastPath2D:
         ts = E.ThresholdSet(np.arange(0.0, 256.0, 5.0))
         got = E.ecc_discrete(torch.from_numpy(x).cuda(), ts).cpu().numpy()
         assert np.array_equal(got, oracle.curve(x.astype(np.float64), ts.taus))
+
+
+class TestBinKernelLimits:
+    """The bin-image kernel takes nb <= 8190 (16-bit lanes hold 4 * bin); larger
+    threshold sets fall back to the value-order kernel.  Both sides of the
+    limit, and non-power-of-two cell tables, stay bit-exact."""
+
+    @pytest.mark.parametrize("nb", [1000, 4097, 8190, 8191, 12000])
+    def test_many_bins(self, rng, nb):
+        x = rng.random((20, 45, 132)).astype(np.float32)
+        t = torch.from_numpy(x).cuda()
+        ts = E.thresholds_from_range(float(x.min()), float(x.max()), nb)
+        fast, gen = TestFastPath._both(t, ts)
+        want = np.append(*oracle.histogram(x, ts.taus))
+        assert np.array_equal(fast[0], want) and np.array_equal(gen[0], want)
+
+    def test_hot_bin_and_ties(self, rng):
+        """few distinct values: every voxel lands in a handful of bins (atomic
+        hot spots, most neighbour pairs tie)."""
+        x = rng.integers(0, 3, (33, 61, 128)).astype(np.float32)
+        t = torch.from_numpy(x).cuda()
+        ts = E.ThresholdSet(np.linspace(-0.5, 2.5, 7))
+        fast, gen = TestFastPath._both(t, ts)
+        want = np.append(*oracle.histogram(x, ts.taus))
+        assert np.array_equal(fast[0], want) and np.array_equal(gen[0], want)
