@@ -583,15 +583,17 @@ ecc_fast3d_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* 
 // table).  Exact reformulation: the histogram only depends on the sublevel
 // sets {x <= tau_j} = {bin(x) <= j}, and a cell's max vertex lies in bin j
 // exactly when the cell belongs to K_j \ K_{j-1}, for ANY total order that
-// refines the bin order.  So each staged plane is first replaced by its bin
-// indices (one table lookup per voxel, the lookup the deposit needs anyway)
-// and the lower-star coefficients are taken in the order (bin, index) --
-// the reference's own tie-break rule applied to the bin image.  Per-voxel
-// coefficients differ from the value order's, the per-bin sums and hence
-// the curve are identical (hard.py:134-143 sums c over bins).
+// refines the bin order.  So each staged plane is first replaced by its
+// cell-table rank v = 2 cell + (x > t_cell) (one 4-byte table lookup per
+// voxel), a non-decreasing function of x whose bin is b(cell) + v % 2, and
+// the lower-star coefficients are taken in the order (rank, index) -- the
+// reference's own tie-break rule applied to the rank image.  Per-voxel
+// coefficients differ from the value order's; the per-bin sums and hence
+// the curve are identical (hard.py:134-143 sums c over bins).  The CTA
+// counts 16 c per rank and folds ranks into bins when it flushes.
 //
-// The bin image is stored SWAR: word j of a 32-voxel row segment holds the
-// 16-bit bins of voxels j and j + 16, so one 32-bit subtraction
+// The rank image is stored SWAR: word j of a 32-voxel row segment holds the
+// 16-bit ranks of voxels j and j + 16, so one 32-bit subtraction
 // (0x8000 | p) - q compares two voxel pairs (bit 15 / 31 = [q <= p]), and a
 // sign-replicating byte permute plus one LOP3 moves four of those results
 // into the bit-sliced word: one instruction per comparison instead of two.
@@ -645,16 +647,22 @@ __device__ __forceinline__ uint32_t cmp_word(const uint32_t (&PP)[16], const BRo
   return acc;
 }
 
-// 4 * bin(x) from the cell table: cell = floor(sat(fma(x, scale, bias)) * cells)
-// read off the low mantissa bits of RZ(g * cells + 2^23) (lut_m is biased by
-// 0x4B000000 entries so that the float's bit pattern indexes it directly)
+// Rank of x in the cell table: v = 2 cell + (x > t_cell), cell = floor(sat(
+// fma(x, scale, bias)) * cells).  v is a non-decreasing function of x whose
+// bin is b(cell) + v % 2, so it refines the bin order as the lower-star
+// argument requires, while the shared table holds only the 4-byte
+// thresholds (one bank per lookup instead of two); the cells' bins b(cell)
+// are only needed when the rank counters are folded into the histogram.
 __device__ __forceinline__ uint32_t bin4_lut(float x, uint32_t lut_m, float sc, float bi, float fcells) {
+  // key = bits(RZ(g * cells + 2^23)) = 0x4B000000 + cell; lut_m is the float
+  // table of the cells' thresholds biased by -0x4B000000 entries, and the
+  // returned rank v = 2 cell + (x > t_cell) = 2 key - 0x96000000 + (x > t)
   const float gg = __saturatef(__fmaf_rn(x, sc, bi));
-  const uint32_t addr = lut_m + 8u * __float_as_uint(__fmaf_rz(gg, fcells, 8388608.0f));
+  const uint32_t key = __float_as_uint(__fmaf_rz(gg, fcells, 8388608.0f));
   float t;
-  uint32_t v;
-  asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=f"(t), "=r"(v) : "r"(addr));
-  asm("{\n.reg .pred p;\nsetp.gt.f32 p, %1, %2;\n@p add.u32 %0, %0, 4;\n}\n" : "+r"(v) : "f"(x), "f"(t));
+  asm volatile("ld.shared.b32 %0, [%1];" : "=f"(t) : "r"(lut_m + 4u * key));
+  uint32_t v = 2u * key + 0x6A000000u;
+  asm("{\n.reg .pred p;\nsetp.gt.f32 p, %1, %2;\n@p add.u32 %0, %0, 1;\n}\n" : "+r"(v) : "f"(x), "f"(t));
   return v;
 }
 // bin a 34-voxel row segment (x - 1 .. x + 32) of the staged f32 plane;
@@ -721,18 +729,14 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
   uint32_t* bbuf = reinterpret_cast<uint32_t*>(smem_raw + PLANE_BYTES);          // two bin planes
   uint64_t* bar = reinterpret_cast<uint64_t*>(bbuf + 2 * BPLANE);
   int* s_rounds = reinterpret_cast<int*>(bar + 1);                               // WS: binning arrivals
-  LutEntry* s_lut = reinterpret_cast<LutEntry*>(bar + 2);                        // cells + 1
-  int* s_hist = reinterpret_cast<int*>(s_lut + cells + 1);                       // nb + 1 (+ 32 dummies), 16 c
+  float* s_t = reinterpret_cast<float*>(bar + 2);                                // cells + 1 thresholds
+  int* s_hist = reinterpret_cast<int*>(s_t + ((cells + 1 + 3) & ~3));            // 2 (cells + 1) ranks + 32 dummies, 16 c
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const float* tab_g = reinterpret_cast<const float*>(table_g);
   const LutEntry* lut_g = reinterpret_cast<const LutEntry*>(tab_g + ((nb + 2 + 1) & ~1));
   for (int i = threadIdx.x; i < hsize; i += NT) s_hist[i] = 0;
-  for (int i = threadIdx.x; i <= cells; i += NT) {
-    LutEntry e = lut_g[i];
-    e.b *= 4;   // the bin image holds 4 * bin: the byte offset of the bin's counter
-    s_lut[i] = e;
-  }
+  for (int i = threadIdx.x; i <= cells; i += NT) s_t[i] = lut_g[i].t;
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
     *s_rounds = 0;
@@ -740,10 +744,32 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
   }
   __syncthreads();
-  const uint32_t lut_m = smem_u32(s_lut) - 0x58000000u;   // - 0x4B000000 entries (mod 2^32)
+  const uint32_t lut_m = smem_u32(s_t) - 0x2C000000u;   // - 0x4B000000 entries of 4 bytes (mod 2^32)
   const float fcells = (float)cells;
-  char* const hbytes = reinterpret_cast<char*>(s_hist);
-  const uint32_t dummy_off = 4u * (uint32_t)(nb + 1 + lane);   // < 2^16 for nb <= 8190
+  const int nranks = 2 * (cells + 1);
+  const uint32_t dummy_off = (uint32_t)(nranks + lane);   // dummy counter index (< 2^15)
+  // fold the rank counters (16 c per voxel) into the global bins: rank v is
+  // bin b(v / 2) + v % 2; runs of ranks with the same bin are summed first
+  auto flush = [&](int64_t item) {
+    unsigned long long* h = hist + item * (nb + 1);
+    const int per = (nranks + NT - 1) / NT;
+    const int v0 = threadIdx.x * per, v1 = min(v0 + per, nranks);
+    long long acc = 0;
+    int cur = -1;
+    for (int v = v0; v < v1; ++v) {
+      const int c = s_hist[v];
+      s_hist[v] = 0;
+      if (!c) continue;
+      const int bin = lut_g[v >> 1].b + (v & 1);
+      if (bin != cur) {
+        if (cur >= 0 && acc) atomicAdd(h + cur, (unsigned long long)(acc >> 4));
+        cur = bin;
+        acc = 0;
+      }
+      acc += c;
+    }
+    if (cur >= 0 && acc) atomicAdd(h + cur, (unsigned long long)(acc >> 4));
+  };
 
   uint32_t phase = 0;
   int64_t cur_n = -1;
@@ -795,12 +821,7 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
     if (n != cur_n || pending > (int64_t(1) << 24)) {   // counters hold 16 c: |16 c| <= 112
       if (cur_n >= 0) {
         __syncthreads();
-        unsigned long long* h = hist + cur_n * (nb + 1);
-        for (int i = threadIdx.x; i <= nb; i += NT) {
-          const int v = s_hist[i] >> 4;
-          if (v) atomicAdd(h + i, (unsigned long long)(long long)v);
-          s_hist[i] = 0;
-        }
+        flush(cur_n);
         __syncthreads();
       }
       cur_n = n;
@@ -985,7 +1006,7 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
         // c moves into the high nibble of a byte, so one sign-replicating
         // byte permute yields 16 c as int32 (the counters hold 16 c)
         if (__any_sync(FULL, any != 0u)) {
-          // counter offsets per voxel: the voxel's own 16-bit lane (4 bin) when
+          // counter index per voxel: the voxel's own 16-bit lane (its rank) when
           // c != 0, else this lane's private dummy counter (adding 0 there costs
           // no bank traffic on the real counters).  Selected once per word:
           // bits j, j+16 of the nonzero mask -> byte masks -> one LOP3.
@@ -1007,11 +1028,11 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
             const uint32_t bq = (i & 1) ? (Q[i >> 3] & 0xF0F0F0F0u) : ((Q[i >> 3] << 4) & 0xF0F0F0F0u);
             const int c16 = (int)prmt(bq, 0u, sel);
             if (DEP == 0) {
-              const uint32_t off = i < 16 ? (Ro.w[i] & 0xFFFFu) : (Ro.w[i - 16] >> 16);
-              if (c16) atomicAdd(reinterpret_cast<int*>(hbytes + off), c16);
+              const uint32_t idx = i < 16 ? (Ro.w[i] & 0xFFFFu) : (Ro.w[i - 16] >> 16);
+              if (c16) atomicAdd(s_hist + idx, c16);
             } else {
-              const uint32_t off = i < 16 ? (Wm[i] & 0xFFFFu) : (Wm[i - 16] >> 16);
-              atomicAdd(reinterpret_cast<int*>(hbytes + off), c16);
+              const uint32_t idx = i < 16 ? (Wm[i] & 0xFFFFu) : (Wm[i - 16] >> 16);
+              atomicAdd(s_hist + idx, c16);
             }
           }
         }
@@ -1021,13 +1042,7 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
     }
   }
   __syncthreads();
-  if (cur_n >= 0) {
-    unsigned long long* h = hist + cur_n * (nb + 1);
-    for (int i = threadIdx.x; i <= nb; i += NT) {
-      const int v = s_hist[i] >> 4;
-      if (v) atomicAdd(h + i, (unsigned long long)(long long)v);
-    }
-  }
+  if (cur_n >= 0) flush(cur_n);
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -1091,12 +1106,12 @@ int fast3d_launch(const float* x, int64_t D, int64_t H, int64_t W, int64_t batch
     if (!strcmp(e, "ws")) return 3;
     return 0;
   }();
-  const bool use_bin = b->lut_ok && nb <= 8190 && mode != 1;
-  const int hsize = nb + 33;   // counters of the bin-image kernel: nb + 1 bins + 32 dummies
+  const bool use_bin = b->lut_ok && cells <= 16382 && mode != 1;
+  const int hsize = 2 * (cells + 1) + 32;   // rank counters of the bin-image kernel + 32 dummies
   size_t smem;
   const void* kfn;
   if (use_bin) {
-    smem = (size_t)PLANE_BYTES + (size_t)2 * BPLANE * 4 + 16 + (size_t)(cells + 1) * sizeof(LutEntry) +
+    smem = (size_t)PLANE_BYTES + (size_t)2 * BPLANE * 4 + 16 + (size_t)((cells + 1 + 3) & ~3) * 4 +
            (size_t)hsize * 4;
     kfn = mode == 2 ? (const void*)ecc_fast3d_bin_kernel<0, false>
                     : mode == 3 ? (const void*)ecc_fast3d_bin_kernel<1, true> : (const void*)ecc_fast3d_bin_kernel<1, false>;
