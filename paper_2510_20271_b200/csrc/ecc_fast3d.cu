@@ -1095,15 +1095,16 @@ int fast3d_launch(const float* x, int64_t D, int64_t H, int64_t W, int64_t batch
   while ((1 << log2c) < cells) ++log2c;
   const int cell_shift = 23 - log2c;
   // bin-image kernel whenever the thresholds have a cell table (default);
-  // ECC_B200_F3=value selects the value-order kernel, =branch the bin-image
-  // kernel with a branch around each reduction, =ws its warp-independent
-  // variant (no CTA barriers in the z loop; +1.5 % at 1024^3, -6 % at 512^3)
+  // default: the rank-image kernel with warp-independent pipelines (no CTA
+  // barriers in the z loop; +2-3 % over the CTA-barrier pipeline).
+  // ECC_B200_F3=value selects the value-order kernel, =branch a branch
+  // around each reduction, =cta the CTA-barrier pipeline (A/B checks)
   const int mode = [] {   // read per launch so tests can switch kernels in-process
     const char* e = getenv("ECC_B200_F3");
     if (!e) return 0;
     if (!strcmp(e, "value")) return 1;
     if (!strcmp(e, "branch")) return 2;
-    if (!strcmp(e, "ws")) return 3;
+    if (!strcmp(e, "cta")) return 3;
     return 0;
   }();
   const bool use_bin = b->lut_ok && cells <= 16382 && mode != 1;
@@ -1113,8 +1114,8 @@ int fast3d_launch(const float* x, int64_t D, int64_t H, int64_t W, int64_t batch
   if (use_bin) {
     smem = (size_t)PLANE_BYTES + (size_t)2 * BPLANE * 4 + 16 + (size_t)((cells + 1 + 3) & ~3) * 4 +
            (size_t)hsize * 4;
-    kfn = mode == 2 ? (const void*)ecc_fast3d_bin_kernel<0, false>
-                    : mode == 3 ? (const void*)ecc_fast3d_bin_kernel<1, true> : (const void*)ecc_fast3d_bin_kernel<1, false>;
+    kfn = mode == 2 ? (const void*)ecc_fast3d_bin_kernel<0, true>
+                    : mode == 3 ? (const void*)ecc_fast3d_bin_kernel<1, false> : (const void*)ecc_fast3d_bin_kernel<1, true>;
   } else {
     smem = (size_t)NSTAGE * PLANE_BYTES + 4 * 8 + (size_t)(b->lut_ok ? cells + 1 : 0) * sizeof(LutEntry) +
            (size_t)((nb + 1 + 3) & ~3) * 4 + (size_t)(b->lut_ok ? 0 : nb + 2) * 4;
@@ -1145,14 +1146,14 @@ int fast3d_launch(const float* x, int64_t D, int64_t H, int64_t W, int64_t batch
   if (grid < 1) return ECC_OK;
   if (use_bin) {
     if (mode == 2)
-      ecc_fast3d_bin_kernel<0, false><<<(unsigned)grid, NT, smem, stream>>>(map, g, table, nb, cells, hsize,
-                                                                              b->lut_scale, b->lut_bias, hist);
-    else if (mode == 3)
-      ecc_fast3d_bin_kernel<1, true><<<(unsigned)grid, NT, smem, stream>>>(map, g, table, nb, cells, hsize,
+      ecc_fast3d_bin_kernel<0, true><<<(unsigned)grid, NT, smem, stream>>>(map, g, table, nb, cells, hsize,
                                                                              b->lut_scale, b->lut_bias, hist);
-    else
+    else if (mode == 3)
       ecc_fast3d_bin_kernel<1, false><<<(unsigned)grid, NT, smem, stream>>>(map, g, table, nb, cells, hsize,
                                                                               b->lut_scale, b->lut_bias, hist);
+    else
+      ecc_fast3d_bin_kernel<1, true><<<(unsigned)grid, NT, smem, stream>>>(map, g, table, nb, cells, hsize,
+                                                                             b->lut_scale, b->lut_bias, hist);
     return check_launch("ecc_fast3d_bin_kernel");
   }
   ecc_fast3d_kernel<<<(unsigned)grid, NT, smem, stream>>>(map, g, table, nb, cells, cell_shift, b->lut_scale,

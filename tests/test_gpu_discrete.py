@@ -223,7 +223,7 @@ class TestFastPath:
               (17, 90, 260), (64, 31, 4), (1, 1, 64), (40, 1, 40), (65, 47, 68)]
 
     KERNELS = {"bin": {}, "value": {"ECC_B200_F3": "value"}, "branch": {"ECC_B200_F3": "branch"},
-               "ws": {"ECC_B200_F3": "ws"}, "generic": {"ECC_B200_GENERIC": "1"}}
+               "cta": {"ECC_B200_F3": "cta"}, "generic": {"ECC_B200_GENERIC": "1"}}
 
     @classmethod
     def _all(cls, t, ts, **kw):
@@ -245,7 +245,7 @@ class TestFastPath:
     @classmethod
     def _both(cls, t, ts, **kw):
         out = cls._all(t, ts, **kw)
-        for name in ("value", "branch", "ws"):
+        for name in ("value", "branch", "cta"):
             assert np.array_equal(out[name], out["bin"]), name
         return out["bin"], out["generic"]
 
