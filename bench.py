@@ -323,6 +323,11 @@ def run_b200(args):
                "api": api + " (pinned host -> HBM copy inside the timed region)"}
         del host
 
+    # --- north-star volume (1024^3 f32, 1024 bins; N = 1 only) ---------------
+    ns = None
+    if world == 1 and not args.no_ns:
+        ns = bench_ns(args, dev)
+
     # --- soft ECC C3 (forward + backward) -------------------------------------
     soft = None
     if not args.no_soft:
@@ -353,11 +358,51 @@ def run_b200(args):
             "e2e": e2e,
             "gpu_launches": 2 * args.steps,
             "clocks": clocks.summary(),
+            "north_star": ns,
             "soft": soft,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def bench_ns(args, dev):
+    """The north-star case on one GPU: 1024^3 float32, 1024 uniform thresholds,
+    device-resident input (4 GiB > L2), CUDA-event timing over K steps.  The
+    curve is checked against the size-independent invariants (sum c = 1)."""
+    import torch
+
+    import paper_2510_20271_b200 as E
+    from paper_2510_20271_b200 import _lib
+
+    L = _lib.lib()
+    n = 1024
+    x = torch.empty((n, n, n), dtype=torch.float32, device=dev)
+    _lib.check(L.ecc_counter_grid(SEED + 1, 0, x.numel(), _lib.ptr(x), _lib.stream_ptr(x)))
+    lo, hi, _ = E.device_minmax(x)
+    taus = E.thresholds_from_range(lo, hi, NB)
+    curve, hist = E.ecc_discrete(x, taus, return_hist=True)
+    assert int(hist.sum()) == 1 and int(curve[-1]) == 1, "ECC invariant violated at 1024^3"
+    for _ in range(3):
+        E.histogram_device(x, taus)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    steps = max(3, min(args.steps, 10))
+    e0.record()
+    for _ in range(steps):
+        E.histogram_device(x, taus)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    peak, peak_kind = _peaks()
+    gbs = 4.0 * x.numel() / (ms * 1e-3) / 1e9
+    out = {"workload": "NS: 3D 1024^3 float32, discrete ECC, 1024 uniform thresholds (device-resident)",
+           "value": x.numel() / (ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": ms, "steps": steps,
+           "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
+                        "peak_source": peak_kind}}
+    del x
+    torch.cuda.empty_cache()
+    return out
 
 
 def bench_soft(args, dev, world, rank):
@@ -436,6 +481,7 @@ def main():
     ap.add_argument("--no-soft", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-ns", action="store_true", help="skip the 1024^3 north-star measurement")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
