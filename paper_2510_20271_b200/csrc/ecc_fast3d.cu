@@ -665,10 +665,38 @@ __device__ __forceinline__ uint32_t bin4_lut(float x, uint32_t lut_m, float sc, 
   asm("{\n.reg .pred p;\nsetp.gt.f32 p, %1, %2;\n@p add.u32 %0, %0, 1;\n}\n" : "+r"(v) : "f"(x), "f"(t));
   return v;
 }
+// Edge-table rank (host flag lut_edge, ecc_host.cu build_edge): sub-cells are
+// sixteenths of the boundary-aligned cells; key + 1 = 0x4B000000 + sub + 1, so
+// idx = (key + 1) >> 4 is the cell for interior sub-cells and the nearest
+// boundary for the first/last sixteenth, where the boundary threshold decides
+// between ranks idx and idx + 1.  Interior voxels skip the table (t = -inf
+// makes the compare true: rank = cell + 1).  Only ~1/8 of the lanes load,
+// which is what takes the random table lookups off the shared-memory pipe.
+__device__ __forceinline__ uint32_t rank_edge(float x, uint32_t tE_m, float sc, float bi, float fcells16) {
+  const float gg = __saturatef(__fmaf_rn(x, sc, bi));
+  const uint32_t k1 = __float_as_uint(__fmaf_rz(gg, fcells16, 8388608.0f)) + 1u;
+  const uint32_t idx = k1 >> 4;   // low 16 bits: boundary / cell index
+  float t = __int_as_float(0xff800000);
+  asm volatile(
+      "{\n.reg .pred pe;\n.reg .b32 s;\n"
+      "and.b32 s, %2, 14;\n"
+      "setp.eq.u32 pe, s, 0;\n"
+      "@pe ld.shared.f32 %0, [%1];\n}\n"
+      : "+f"(t)
+      : "r"(tE_m + 4u * idx), "r"(k1));
+  uint32_t v = idx;
+  asm("{\n.reg .pred p;\nsetp.gt.f32 p, %1, %2;\n@p add.u32 %0, %0, 1;\n}\n" : "+r"(v) : "f"(x), "f"(t));
+  return v;
+}
+template <bool EDGE>
+__device__ __forceinline__ uint32_t rank_of(float x, uint32_t m, float sc, float bi, float fc) {
+  return EDGE ? rank_edge(x, m, sc, bi, fc) : bin4_lut(x, m, sc, bi, fc);
+}
+
 // bin a 34-voxel row segment (x - 1 .. x + 32) of the staged f32 plane;
 // CHECK: NaN (TMA out-of-bounds fill) -> sentinel for every voxel, else
 // only for the two edge voxels
-template <bool CHECK>
+template <bool CHECK, bool EDGE>
 __device__ __forceinline__ void bin_rowseg(const float* src, uint32_t* dw, uint32_t* de, uint32_t lut_m, float sc,
                                            float bi, float fcells) {
   // two halves of 8 words each (voxels j, j + 16) to bound the live registers
@@ -686,7 +714,7 @@ __device__ __forceinline__ void bin_rowseg(const float* src, uint32_t* dw, uint3
     uint32_t b[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-      const uint32_t t = bin4_lut(v[i], lut_m, sc, bi, fcells);
+      const uint32_t t = rank_of<EDGE>(v[i], lut_m, sc, bi, fcells);
       b[i] = CHECK ? (v[i] != v[i] ? BSENT : t) : t;   // NaN = TMA out-of-bounds fill
     }
 #pragma unroll
@@ -695,10 +723,11 @@ __device__ __forceinline__ void bin_rowseg(const float* src, uint32_t* dw, uint3
                                  prmt(b[4 * k + 2], b[10 + 4 * k], 0x5410u), prmt(b[4 * k + 3], b[11 + 4 * k], 0x5410u));
   }
   const float el = src[-1], er = src[32];
-  const uint32_t bl = bin4_lut(el, lut_m, sc, bi, fcells), br = bin4_lut(er, lut_m, sc, bi, fcells);
+  const uint32_t bl = rank_of<EDGE>(el, lut_m, sc, bi, fcells), br = rank_of<EDGE>(er, lut_m, sc, bi, fcells);
   *de = prmt(el != el ? BSENT : bl, er != er ? BSENT : br, 0x5410u);
 }
 // bin the staged plane into a bin plane: warp -> x segment, lane -> row
+template <bool EDGE>
 __device__ __forceinline__ void bin_plane(const float* stage, uint32_t* B, bool plane_in, int x0, int y0, int W,
                                           int H, uint32_t lut_m, float sc, float bi, float fcells) {
   const int row = threadIdx.x & 31, seg = threadIdx.x >> 5;
@@ -715,12 +744,12 @@ __device__ __forceinline__ void bin_plane(const float* stage, uint32_t* B, bool 
   }
   const float* src = stage + row * PITCH + 4 + 32 * seg;
   if (xs + 32 > W)
-    bin_rowseg<true>(src, dw, de, lut_m, sc, bi, fcells);
+    bin_rowseg<true, EDGE>(src, dw, de, lut_m, sc, bi, fcells);
   else
-    bin_rowseg<false>(src, dw, de, lut_m, sc, bi, fcells);
+    bin_rowseg<false, EDGE>(src, dw, de, lut_m, sc, bi, fcells);
 }
 
-template <int DEP, bool WS>
+template <int DEP, bool WS, bool EDGE>
 __global__ void __launch_bounds__(NT, 4)
 ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* __restrict__ table_g, int nb,
                       int cells, int hsize, float lut_scale, float lut_bias, unsigned long long* __restrict__ hist) {
@@ -735,8 +764,11 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const float* tab_g = reinterpret_cast<const float*>(table_g);
   const LutEntry* lut_g = reinterpret_cast<const LutEntry*>(tab_g + ((nb + 2 + 1) & ~1));
+  // edge mode: boundary thresholds and the rank -> bin map follow the cell table
+  const float* tE_g = reinterpret_cast<const float*>(lut_g + cells + 1);
+  const int* rbin_g = reinterpret_cast<const int*>(tE_g + cells + 1);
   for (int i = threadIdx.x; i < hsize; i += NT) s_hist[i] = 0;
-  for (int i = threadIdx.x; i <= cells; i += NT) s_t[i] = lut_g[i].t;
+  for (int i = threadIdx.x; i <= cells; i += NT) s_t[i] = EDGE ? tE_g[i] : lut_g[i].t;
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
     *s_rounds = 0;
@@ -744,9 +776,11 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
   }
   __syncthreads();
-  const uint32_t lut_m = smem_u32(s_t) - 0x2C000000u;   // - 0x4B000000 entries of 4 bytes (mod 2^32)
-  const float fcells = (float)cells;
-  const int nranks = 2 * (cells + 1);
+  // table base biased so that the float bits index it directly (mod 2^32):
+  // 2-rank mode by key = 0x4B000000 + cell, edge mode by (key16 + 1) >> 4
+  const uint32_t lut_m = smem_u32(s_t) - (EDGE ? 0x12C00000u : 0x2C000000u);
+  const float fcells = EDGE ? (float)(16 * cells) : (float)cells;
+  const int nranks = EDGE ? cells + 2 : 2 * (cells + 1);
   const uint32_t dummy_off = (uint32_t)(nranks + lane);   // dummy counter index (< 2^15)
   // fold the rank counters (16 c per voxel) into the global bins: rank v is
   // bin b(v / 2) + v % 2; runs of ranks with the same bin are summed first
@@ -760,7 +794,7 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
       const int c = s_hist[v];
       s_hist[v] = 0;
       if (!c) continue;
-      const int bin = lut_g[v >> 1].b + (v & 1);
+      const int bin = EDGE ? rbin_g[v] : lut_g[v >> 1].b + (v & 1);
       if (bin != cur) {
         if (cur >= 0 && acc) atomicAdd(h + cur, (unsigned long long)(acc >> 4));
         cur = bin;
@@ -861,7 +895,7 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
         mbar_wait(bar, phase);
         phase ^= 1u;
       }
-      bin_plane(stage, bbuf + (p & 1) * BPLANE, pin, x0, y0, g.W, g.H, lut_m, lut_scale, lut_bias, fcells);
+      bin_plane<EDGE>(stage, bbuf + (p & 1) * BPLANE, pin, x0, y0, g.W, g.H, lut_m, lut_scale, lut_bias, fcells);
       if (WS) {
         if (pin) round_done(p);
         else __syncwarp();
@@ -933,7 +967,7 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
           mbar_wait(bar, phase);
           phase ^= 1u;
         }
-        bin_plane(stage, bbuf + (p & 1) * BPLANE, pin, x0, y0, g.W, g.H, lut_m, lut_scale, lut_bias, fcells);
+        bin_plane<EDGE>(stage, bbuf + (p & 1) * BPLANE, pin, x0, y0, g.W, g.H, lut_m, lut_scale, lut_bias, fcells);
         if (WS) {
           if (pin) round_done(p);
           else __syncwarp();
@@ -1105,17 +1139,23 @@ int fast3d_launch(const float* x, int64_t D, int64_t H, int64_t W, int64_t batch
     if (!strcmp(e, "value")) return 1;
     if (!strcmp(e, "branch")) return 2;
     if (!strcmp(e, "cta")) return 3;
+    if (!strcmp(e, "rank2")) return 4;
     return 0;
   }();
   const bool use_bin = b->lut_ok && cells <= 16382 && mode != 1;
-  const int hsize = 2 * (cells + 1) + 32;   // rank counters of the bin-image kernel + 32 dummies
+  const bool edge = b->lut_edge && mode != 4;
+  const int hsize = (edge ? cells + 2 : 2 * (cells + 1)) + 32;   // rank counters + 32 dummies
   size_t smem;
   const void* kfn;
   if (use_bin) {
     smem = (size_t)PLANE_BYTES + (size_t)2 * BPLANE * 4 + 16 + (size_t)((cells + 1 + 3) & ~3) * 4 +
            (size_t)hsize * 4;
-    kfn = mode == 2 ? (const void*)ecc_fast3d_bin_kernel<0, true>
-                    : mode == 3 ? (const void*)ecc_fast3d_bin_kernel<1, false> : (const void*)ecc_fast3d_bin_kernel<1, true>;
+    kfn = edge ? (mode == 2 ? (const void*)ecc_fast3d_bin_kernel<0, true, true>
+                            : mode == 3 ? (const void*)ecc_fast3d_bin_kernel<1, false, true>
+                                        : (const void*)ecc_fast3d_bin_kernel<1, true, true>)
+               : (mode == 2 ? (const void*)ecc_fast3d_bin_kernel<0, true, false>
+                            : mode == 3 ? (const void*)ecc_fast3d_bin_kernel<1, false, false>
+                                        : (const void*)ecc_fast3d_bin_kernel<1, true, false>);
   } else {
     smem = (size_t)NSTAGE * PLANE_BYTES + 4 * 8 + (size_t)(b->lut_ok ? cells + 1 : 0) * sizeof(LutEntry) +
            (size_t)((nb + 1 + 3) & ~3) * 4 + (size_t)(b->lut_ok ? 0 : nb + 2) * 4;
@@ -1145,15 +1185,9 @@ int fast3d_launch(const float* x, int64_t D, int64_t H, int64_t W, int64_t batch
   g.zchunks = (tiles <= grid && grid <= tiles * (ze - zb)) ? (int)(grid / tiles) : 0;
   if (grid < 1) return ECC_OK;
   if (use_bin) {
-    if (mode == 2)
-      ecc_fast3d_bin_kernel<0, true><<<(unsigned)grid, NT, smem, stream>>>(map, g, table, nb, cells, hsize,
-                                                                             b->lut_scale, b->lut_bias, hist);
-    else if (mode == 3)
-      ecc_fast3d_bin_kernel<1, false><<<(unsigned)grid, NT, smem, stream>>>(map, g, table, nb, cells, hsize,
-                                                                              b->lut_scale, b->lut_bias, hist);
-    else
-      ecc_fast3d_bin_kernel<1, true><<<(unsigned)grid, NT, smem, stream>>>(map, g, table, nb, cells, hsize,
-                                                                             b->lut_scale, b->lut_bias, hist);
+    using KFn = void (*)(const CUtensorMap, Geom, const void*, int, int, int, float, float, unsigned long long*);
+    KFn k = reinterpret_cast<KFn>(const_cast<void*>(kfn));
+    k<<<(unsigned)grid, NT, smem, stream>>>(map, g, table, nb, cells, hsize, b->lut_scale, b->lut_bias, hist);
     return check_launch("ecc_fast3d_bin_kernel");
   }
   ecc_fast3d_kernel<<<(unsigned)grid, NT, smem, stream>>>(map, g, table, nb, cells, cell_shift, b->lut_scale,

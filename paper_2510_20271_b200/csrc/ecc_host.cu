@@ -4,6 +4,7 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <algorithm>
 #include <cmath>
 #include <limits>
 #include <vector>
@@ -124,9 +125,16 @@ static int64_t bin32(float x, const float* t32, int64_t nb) {
 }
 
 // Build the cell table for thresholds t32 (non-decreasing); returns cells or 0.
-static int build_lut(const float* t32, int64_t nb, int cells, float* scale_out, float* bias_out, LutEntryH* lut) {
+// The cell grid maps [lo, hi] onto [0, 1]; by default lo/hi are the first and
+// last thresholds.  aligned != 0 maps [t_0 - w, t_last] (w the mean spacing)
+// instead, so that uniform thresholds fall on cell boundaries (cells == nb),
+// which is what the edge tables below need.
+static int build_lut(const float* t32, int64_t nb, int cells, float* scale_out, float* bias_out, LutEntryH* lut,
+                     int aligned = 0) {
   if (nb < 2) return 0;
-  const float lo = t32[0], hi = t32[nb - 1];
+  float lo = t32[0];
+  const float hi = t32[nb - 1];
+  if (aligned) lo = (float)((double)t32[0] - ((double)hi - (double)t32[0]) / (double)(nb - 1));
   if (!std::isfinite(lo) || !std::isfinite(hi) || !(hi > lo)) return 0;
   volatile float span = hi - lo;
   if (!std::isfinite((float)span)) return 0;
@@ -161,6 +169,72 @@ static int build_lut(const float* t32, int64_t nb, int cells, float* scale_out, 
   *scale_out = scale;
   *bias_out = bias;
   return cells;
+}
+
+// Edge tables for the float32 rank kernel (ecc_fast3d.cu).  Sub-cells are
+// sixteenths of cells, sub(x) = floor(sat(fma(x, scale, bias)) * 16 cells),
+// computed by the device exactly as here.  When every threshold lies in the
+// first or last sub-cell of a cell, a voxel needs its threshold only when it
+// falls in such an edge sub-cell: rank(x) = idx + (x > tE[idx]) with
+// idx = (sub(x) + 1) / 16 for edge sub-cells, and rank = cell + 1 otherwise.
+// tE[b] is the threshold at boundary b (between cells b-1 and b), or the
+// largest float below sub-cell 16 b when the boundary has none.  Every rank's
+// floats are verified to share one bin (rbin[rank]).  Returns 1 on success.
+static int build_edge(const float* t32, int64_t nb, int cells, float scale, float bias, float* tE,
+                      int32_t* rbin) {
+  const int nsub = cells * 16;
+  if (cells + 2 >= 0x7FFF) return 0;   // ranks live in 16-bit lanes below the sentinel
+  const uint32_t kmin = fkey(-std::numeric_limits<float>::max());
+  const uint32_t kmax = fkey(std::numeric_limits<float>::max());
+  std::vector<uint32_t> first((size_t)nsub + 2);   // first key with sub >= s
+  for (int s = 0; s <= nsub + 1; ++s) {
+    uint32_t a = kmin, b = kmax + 1;
+    while (a < b) {
+      const uint32_t mid = a + (b - a) / 2;
+      if (cell_of(keyf(mid), scale, bias, nsub) >= s) b = mid; else a = mid + 1;
+    }
+    first[s] = a;
+  }
+  std::vector<char> has((size_t)cells + 1, 0);
+  for (int64_t j = 0; j < nb; ++j) {
+    const float t = t32[j];
+    const int sidx = cell_of(t, scale, bias, nsub);
+    if ((sidx & 15) != 0 && (sidx & 15) != 15) return 0;   // threshold inside a cell
+    const int bnd = (sidx + 1) >> 4;
+    if (bnd > cells) return 0;
+    if (has[bnd] && tE[bnd] != t) return 0;               // two thresholds at one boundary
+    has[bnd] = 1;
+    tE[bnd] = t;
+  }
+  for (int bnd = 0; bnd <= cells; ++bnd)
+    if (!has[bnd]) {
+      const uint32_t f = first[(size_t)16 * bnd];
+      tE[bnd] = f > kmin ? keyf(f - 1) : -std::numeric_limits<float>::infinity();
+    }
+  std::vector<int64_t> rb((size_t)cells + 2, -1);
+  auto assign = [&](int r, uint32_t klo, uint32_t khi) -> bool {
+    if (klo > khi) return true;
+    const int64_t b0 = bin32(keyf(klo), t32, nb), b1 = bin32(keyf(khi), t32, nb);
+    if (b0 != b1) return false;
+    if (rb[r] >= 0 && rb[r] != b0) return false;
+    rb[r] = b0;
+    return true;
+  };
+  for (int sidx = 0; sidx <= nsub; ++sidx) {
+    if (first[sidx] >= first[sidx + 1]) continue;   // empty sub-cell
+    const uint32_t klo = first[sidx], khi = first[sidx + 1] - 1;
+    const int sub = sidx & 15;
+    if (sub != 0 && sub != 15) {
+      if (!assign((sidx >> 4) + 1, klo, khi)) return 0;
+    } else {
+      const int idx = (sidx + 1) >> 4;
+      const uint32_t kt = fkey(tE[idx]);
+      if (!assign(idx, klo, std::min(khi, kt))) return 0;
+      if (kt < khi && !assign(idx + 1, std::max(klo, kt + 1), khi)) return 0;
+    }
+  }
+  for (int r = 0; r <= cells + 1; ++r) rbin[r] = (int32_t)(rb[r] >= 0 ? rb[r] : 0);
+  return 1;
 }
 
 __global__ void counter_grid_kernel(uint64_t seed, int64_t start, int64_t count, float* out) {
@@ -200,6 +274,8 @@ extern "C" int ecc_threshold_table(const double* taus, int64_t nb, int dtype, vo
     if (!(taus[j] > taus[j - 1])) return set_error(ECC_EINVAL, "thresholds must be strictly increasing");
   b->nbins = nb;
   b->lut_ok = 0;
+  b->lut_edge = 0;
+  b->lut_pad = 0;
   b->lut_cells = 0;
   b->lut_scale = 0.0f;
   b->lut_bias = 0.0f;
@@ -212,6 +288,21 @@ extern "C" int ecc_threshold_table(const double* taus, int64_t nb, int dtype, vo
     LutEntryH* lut = reinterpret_cast<LutEntryH*>(t + ((nb + 2 + 1) & ~int64_t(1)));
     int64_t cells = 1;
     while (cells < nb) cells <<= 1;
+    if (cells == nb && nb >= 2) {
+      // power-of-two threshold count: try the boundary-aligned grid first
+      float sc = 0.f, bi = 0.f;
+      if (build_lut(t + 1, nb, (int)cells, &sc, &bi, lut, 1)) {
+        float* tE = reinterpret_cast<float*>(lut + cells + 1);
+        int32_t* rbin = reinterpret_cast<int32_t*>(tE + cells + 1);
+        if (build_edge(t + 1, nb, (int)cells, sc, bi, tE, rbin)) {
+          b->lut_ok = 1;
+          b->lut_edge = 1;
+          b->lut_cells = (int32_t)cells;
+          b->lut_scale = sc;
+          b->lut_bias = bi;
+        }
+      }
+    }
     for (; cells <= 4 * nb && cells <= (1 << 16) && !b->lut_ok; cells <<= 1) {
       float sc = 0.f, bi = 0.f;
       if (build_lut(t + 1, nb, (int)cells, &sc, &bi, lut)) {
@@ -219,6 +310,9 @@ extern "C" int ecc_threshold_table(const double* taus, int64_t nb, int dtype, vo
         b->lut_cells = (int32_t)cells;
         b->lut_scale = sc;
         b->lut_bias = bi;
+        float* tE = reinterpret_cast<float*>(lut + cells + 1);
+        int32_t* rbin = reinterpret_cast<int32_t*>(tE + cells + 1);
+        b->lut_edge = build_edge(t + 1, nb, (int)cells, sc, bi, tE, rbin);
       }
     }
   } else if (dtype == ECC_DTYPE_F64) {
@@ -250,5 +344,7 @@ extern "C" size_t ecc_threshold_table_bytes(int64_t nb, int dtype) {
   while (cells < nb) cells <<= 1;
   cells *= 4;
   if (cells > (1 << 16)) cells = 1 << 16;
-  return sizeof(float) * (size_t)((nb + 2 + 1) & ~int64_t(1)) + sizeof(LutEntryH) * (size_t)(cells + 1);
+  // thresholds with sentinels, cell table, edge thresholds, rank -> bin
+  return sizeof(float) * (size_t)((nb + 2 + 1) & ~int64_t(1)) + sizeof(LutEntryH) * (size_t)(cells + 1) +
+         sizeof(float) * (size_t)(cells + 1) + sizeof(int32_t) * (size_t)(cells + 2);
 }

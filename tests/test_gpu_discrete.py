@@ -223,7 +223,8 @@ class TestFastPath:
               (17, 90, 260), (64, 31, 4), (1, 1, 64), (40, 1, 40), (65, 47, 68)]
 
     KERNELS = {"bin": {}, "value": {"ECC_B200_F3": "value"}, "branch": {"ECC_B200_F3": "branch"},
-               "cta": {"ECC_B200_F3": "cta"}, "generic": {"ECC_B200_GENERIC": "1"}}
+               "cta": {"ECC_B200_F3": "cta"}, "rank2": {"ECC_B200_F3": "rank2"},
+               "generic": {"ECC_B200_GENERIC": "1"}}
 
     @classmethod
     def _all(cls, t, ts, **kw):
@@ -245,7 +246,7 @@ class TestFastPath:
     @classmethod
     def _both(cls, t, ts, **kw):
         out = cls._all(t, ts, **kw)
-        for name in ("value", "branch", "cta"):
+        for name in ("value", "branch", "cta", "rank2"):
             assert np.array_equal(out[name], out["bin"]), name
         return out["bin"], out["generic"]
 
