@@ -118,3 +118,34 @@ def test_key_roundtrip(L):
         b = struct.unpack("<Q", struct.pack("<d", v))[0]
         key = (~b & 0xFFFFFFFFFFFFFFFF) if b >> 63 else (b | (1 << 63))
         assert L.ecc_key_to_double(key) == v
+
+
+def test_threshold_table_edge_ranks_exact():
+    """Edge tables (power-of-two bin counts, boundary-aligned cells): emulating the
+    device's rank (ecc_fast3d.cu rank_edge) and folding it through rbin reproduces
+    searchsorted-left for probes at and around every threshold and across the range."""
+    import paper_2510_20271_b200 as E
+
+    rng = np.random.default_rng(11)
+    for lo, hi, nb in ((0.0, 1.0, 1024), (-3.7, 5.1, 256), (2.3e-8, 0.99999994, 2048), (0.0, 255.0, 512)):
+        taus = E.thresholds_from_range(lo, hi, nb).taus
+        rc, t, b = _table(taus, 1)
+        assert rc == 0 and b.lut_ok == 1 and b.lut_edge == 1, (lo, hi, nb)
+        n, cells = taus.size, b.lut_cells
+        off = (n + 2 + 1) & ~1
+        lut_words = 2 * (cells + 1)
+        tE = t[off + lut_words: off + lut_words + cells + 1]
+        rbin = t[off + lut_words + cells + 1: off + lut_words + cells + 1 + cells + 2].view(np.int32)
+        t32 = t[1:n + 1]
+        probes = np.concatenate([t32, np.nextafter(t32, np.float32(np.inf)), np.nextafter(t32, np.float32(-np.inf)),
+                                 rng.uniform(lo - 1, hi + 1, 20000).astype(np.float32)]).astype(np.float32)
+        g = np.clip((probes.astype(np.float64) * np.float32(b.lut_scale) + np.float32(b.lut_bias))
+                    .astype(np.float32), 0, 1)
+        k1 = np.floor(g.astype(np.float64) * 16 * cells).astype(np.int64) + 1
+        idx = k1 >> 4
+        edge = (k1 & 14) == 0
+        tt = np.where(edge, tE[np.minimum(idx, cells)], -np.inf)
+        rank = idx + (probes > tt)
+        got = rbin[rank]
+        want = np.searchsorted(taus, probes.astype(np.float64), side="left")
+        assert np.array_equal(got, want), (lo, hi, nb)
