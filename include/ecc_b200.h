@@ -56,10 +56,10 @@ typedef struct {
   float lut_bias;
   int32_t lut_cells;
   int32_t lut_ok;
-  /* 1: every threshold lies in the first or last sixteenth of its cell, and
+  /* 1: every threshold lies in the first or last 1/256 of its cell, and
    * the table also holds the boundary thresholds tE[cells + 1] and the
    * rank -> bin map rbin[cells + 2] after the cell table; the rank kernel then
-   * looks a threshold up only for voxels in those edge sixteenths. */
+   * looks a threshold up only for voxels in those edge sub-cells. */
   int32_t lut_edge;
   int32_t lut_pad;
 } ecc_binning;

@@ -666,26 +666,27 @@ __device__ __forceinline__ uint32_t bin4_lut(float x, uint32_t lut_m, float sc, 
   return v;
 }
 // Edge-table rank (host flag lut_edge, ecc_host.cu build_edge): sub-cells are
-// sixteenths of the boundary-aligned cells; key + 1 = 0x4B000000 + sub + 1, so
-// idx = (key + 1) >> 4 is the cell for interior sub-cells and the nearest
-// boundary for the first/last sixteenth, where the boundary threshold decides
-// between ranks idx and idx + 1.  Interior voxels skip the table (t = -inf
-// makes the compare true: rank = cell + 1).  Only ~1/8 of the lanes load,
-// which is what takes the random table lookups off the shared-memory pipe.
-__device__ __forceinline__ uint32_t rank_edge(float x, uint32_t tE_m, float sc, float bi, float fcells16) {
+// 1/256 of the boundary-aligned cells; k1 = key + 1 = 0x4B000000 + sub + 1, so
+// bits 8..23 of k1 are the cell for interior sub-cells and the nearest
+// boundary for the first/last sub-cell of a cell, where the boundary
+// threshold decides between that index and the next.  The rank is returned
+// in bits 8..23 (the SWAR packing takes bytes 1-2).  Interior voxels skip the
+// table (t = -inf makes the compare true: rank = cell + 1); for edge voxels
+// (k1 & 0xFE) == 0, so k1 >> 6 is already 4 * index.  Only ~1 % of the voxels
+// read a threshold, which takes the random lookups off the shared-memory pipe.
+__device__ __forceinline__ uint32_t rank_edge(float x, uint32_t tE_m, float sc, float bi, float fcells256) {
   const float gg = __saturatef(__fmaf_rn(x, sc, bi));
-  const uint32_t k1 = __float_as_uint(__fmaf_rz(gg, fcells16, 8388608.0f)) + 1u;
-  const uint32_t idx = k1 >> 4;   // low 16 bits: boundary / cell index
+  const uint32_t k1 = __float_as_uint(__fmaf_rz(gg, fcells256, 8388608.0f)) + 1u;
   float t = __int_as_float(0xff800000);
   asm volatile(
       "{\n.reg .pred pe;\n.reg .b32 s;\n"
-      "and.b32 s, %2, 14;\n"
+      "and.b32 s, %2, 254;\n"
       "setp.eq.u32 pe, s, 0;\n"
       "@pe ld.shared.f32 %0, [%1];\n}\n"
       : "+f"(t)
-      : "r"(tE_m + 4u * idx), "r"(k1));
-  uint32_t v = idx;
-  asm("{\n.reg .pred p;\nsetp.gt.f32 p, %1, %2;\n@p add.u32 %0, %0, 1;\n}\n" : "+r"(v) : "f"(x), "f"(t));
+      : "r"(tE_m + (k1 >> 6)), "r"(k1));
+  uint32_t v = k1;
+  asm("{\n.reg .pred p;\nsetp.gt.f32 p, %1, %2;\n@p add.u32 %0, %0, 256;\n}\n" : "+r"(v) : "f"(x), "f"(t));
   return v;
 }
 template <bool EDGE>
@@ -699,7 +700,10 @@ __device__ __forceinline__ uint32_t rank_of(float x, uint32_t m, float sc, float
 template <bool CHECK, bool EDGE>
 __device__ __forceinline__ void bin_rowseg(const float* src, uint32_t* dw, uint32_t* de, uint32_t lut_m, float sc,
                                            float bi, float fcells) {
-  // two halves of 8 words each (voxels j, j + 16) to bound the live registers
+  // two halves of 8 words each (voxels j, j + 16) to bound the live registers;
+  // the rank sits in bits 0..15 (2-rank mode) or 8..23 (edge mode)
+  constexpr uint32_t PK = EDGE ? 0x6521u : 0x5410u;
+  constexpr uint32_t SENT = EDGE ? (BSENT << 8) : BSENT;
   const float4* s4 = reinterpret_cast<const float4*>(src);
   uint4* d4 = reinterpret_cast<uint4*>(dw);
 #pragma unroll
@@ -715,16 +719,16 @@ __device__ __forceinline__ void bin_rowseg(const float* src, uint32_t* dw, uint3
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       const uint32_t t = rank_of<EDGE>(v[i], lut_m, sc, bi, fcells);
-      b[i] = CHECK ? (v[i] != v[i] ? BSENT : t) : t;   // NaN = TMA out-of-bounds fill
+      b[i] = CHECK ? (v[i] != v[i] ? SENT : t) : t;   // NaN = TMA out-of-bounds fill
     }
 #pragma unroll
     for (int k = 0; k < 2; ++k)
-      d4[2 * h + k] = make_uint4(prmt(b[4 * k], b[8 + 4 * k], 0x5410u), prmt(b[4 * k + 1], b[9 + 4 * k], 0x5410u),
-                                 prmt(b[4 * k + 2], b[10 + 4 * k], 0x5410u), prmt(b[4 * k + 3], b[11 + 4 * k], 0x5410u));
+      d4[2 * h + k] = make_uint4(prmt(b[4 * k], b[8 + 4 * k], PK), prmt(b[4 * k + 1], b[9 + 4 * k], PK),
+                                 prmt(b[4 * k + 2], b[10 + 4 * k], PK), prmt(b[4 * k + 3], b[11 + 4 * k], PK));
   }
   const float el = src[-1], er = src[32];
   const uint32_t bl = rank_of<EDGE>(el, lut_m, sc, bi, fcells), br = rank_of<EDGE>(er, lut_m, sc, bi, fcells);
-  *de = prmt(el != el ? BSENT : bl, er != er ? BSENT : br, 0x5410u);
+  *de = prmt(el != el ? SENT : bl, er != er ? SENT : br, PK);
 }
 // bin the staged plane into a bin plane: warp -> x segment, lane -> row
 template <bool EDGE>
@@ -777,9 +781,9 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
   }
   __syncthreads();
   // table base biased so that the float bits index it directly (mod 2^32):
-  // 2-rank mode by key = 0x4B000000 + cell, edge mode by (key16 + 1) >> 4
-  const uint32_t lut_m = smem_u32(s_t) - (EDGE ? 0x12C00000u : 0x2C000000u);
-  const float fcells = EDGE ? (float)(16 * cells) : (float)cells;
+  // 2-rank mode by key = 0x4B000000 + cell, edge mode by (key256 + 1) >> 6
+  const uint32_t lut_m = smem_u32(s_t) - (EDGE ? 0x012C0000u : 0x2C000000u);
+  const float fcells = EDGE ? (float)(256 * cells) : (float)cells;
   const int nranks = EDGE ? cells + 2 : 2 * (cells + 1);
   const uint32_t dummy_off = (uint32_t)(nranks + lane);   // dummy counter index (< 2^15)
   // fold the rank counters (16 c per voxel) into the global bins: rank v is

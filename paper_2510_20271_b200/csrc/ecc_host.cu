@@ -129,6 +129,8 @@ static int64_t bin32(float x, const float* t32, int64_t nb) {
 // last thresholds.  aligned != 0 maps [t_0 - w, t_last] (w the mean spacing)
 // instead, so that uniform thresholds fall on cell boundaries (cells == nb),
 // which is what the edge tables below need.
+constexpr int EDGE_SUB = 256;   // edge sub-cells per cell (ecc_fast3d.cu rank_edge)
+
 static int build_lut(const float* t32, int64_t nb, int cells, float* scale_out, float* bias_out, LutEntryH* lut,
                      int aligned = 0) {
   if (nb < 2) return 0;
@@ -172,35 +174,45 @@ static int build_lut(const float* t32, int64_t nb, int cells, float* scale_out, 
 }
 
 // Edge tables for the float32 rank kernel (ecc_fast3d.cu).  Sub-cells are
-// sixteenths of cells, sub(x) = floor(sat(fma(x, scale, bias)) * 16 cells),
+// 1/256 of a cell, sub(x) = floor(sat(fma(x, scale, bias)) * 256 cells),
 // computed by the device exactly as here.  When every threshold lies in the
 // first or last sub-cell of a cell, a voxel needs its threshold only when it
 // falls in such an edge sub-cell: rank(x) = idx + (x > tE[idx]) with
-// idx = (sub(x) + 1) / 16 for edge sub-cells, and rank = cell + 1 otherwise.
+// idx = (sub(x) + 1) / 256 for edge sub-cells, and rank = cell + 1 otherwise.
 // tE[b] is the threshold at boundary b (between cells b-1 and b), or the
-// largest float below sub-cell 16 b when the boundary has none.  Every rank's
-// floats are verified to share one bin (rbin[rank]).  Returns 1 on success.
+// largest float below sub-cell 256 b when the boundary has none.  rank() is
+// non-decreasing in x, so each rank's floats form one key interval, found by
+// binary search; every interval is verified to lie in one bin (rbin[rank]).
+// Returns 1 on success.
+static int edge_rank(float x, float scale, float bias, int cells, const float* tE) {
+  const int sidx = cell_of(x, scale, bias, cells * EDGE_SUB);
+  const int k1 = sidx + 1;
+  const int idx = k1 / EDGE_SUB;
+  if ((k1 % EDGE_SUB) <= 1) return idx + (x > tE[idx] ? 1 : 0);
+  return idx + 1;
+}
+
 static int build_edge(const float* t32, int64_t nb, int cells, float scale, float bias, float* tE,
                       int32_t* rbin) {
-  const int nsub = cells * 16;
-  if (cells + 2 >= 0x7FFF) return 0;   // ranks live in 16-bit lanes below the sentinel
+  const int nsub = cells * EDGE_SUB;
+  if (cells + 2 >= 0x7FFF || nsub >= (1 << 23)) return 0;
   const uint32_t kmin = fkey(-std::numeric_limits<float>::max());
   const uint32_t kmax = fkey(std::numeric_limits<float>::max());
-  std::vector<uint32_t> first((size_t)nsub + 2);   // first key with sub >= s
-  for (int s = 0; s <= nsub + 1; ++s) {
+  auto first_key = [&](auto pred) {   // first finite key with pred(x) true (pred monotone)
     uint32_t a = kmin, b = kmax + 1;
     while (a < b) {
       const uint32_t mid = a + (b - a) / 2;
-      if (cell_of(keyf(mid), scale, bias, nsub) >= s) b = mid; else a = mid + 1;
+      if (pred(keyf(mid))) b = mid; else a = mid + 1;
     }
-    first[s] = a;
-  }
+    return a;
+  };
   std::vector<char> has((size_t)cells + 1, 0);
   for (int64_t j = 0; j < nb; ++j) {
     const float t = t32[j];
     const int sidx = cell_of(t, scale, bias, nsub);
-    if ((sidx & 15) != 0 && (sidx & 15) != 15) return 0;   // threshold inside a cell
-    const int bnd = (sidx + 1) >> 4;
+    const int sub = sidx % EDGE_SUB;
+    if (sub != 0 && sub != EDGE_SUB - 1) return 0;        // threshold inside a cell
+    const int bnd = (sidx + 1) / EDGE_SUB;
     if (bnd > cells) return 0;
     if (has[bnd] && tE[bnd] != t) return 0;               // two thresholds at one boundary
     has[bnd] = 1;
@@ -208,32 +220,21 @@ static int build_edge(const float* t32, int64_t nb, int cells, float scale, floa
   }
   for (int bnd = 0; bnd <= cells; ++bnd)
     if (!has[bnd]) {
-      const uint32_t f = first[(size_t)16 * bnd];
+      const uint32_t f = first_key([&](float x) { return cell_of(x, scale, bias, nsub) >= EDGE_SUB * bnd; });
       tE[bnd] = f > kmin ? keyf(f - 1) : -std::numeric_limits<float>::infinity();
     }
-  std::vector<int64_t> rb((size_t)cells + 2, -1);
-  auto assign = [&](int r, uint32_t klo, uint32_t khi) -> bool {
-    if (klo > khi) return true;
-    const int64_t b0 = bin32(keyf(klo), t32, nb), b1 = bin32(keyf(khi), t32, nb);
-    if (b0 != b1) return false;
-    if (rb[r] >= 0 && rb[r] != b0) return false;
-    rb[r] = b0;
-    return true;
-  };
-  for (int sidx = 0; sidx <= nsub; ++sidx) {
-    if (first[sidx] >= first[sidx + 1]) continue;   // empty sub-cell
-    const uint32_t klo = first[sidx], khi = first[sidx + 1] - 1;
-    const int sub = sidx & 15;
-    if (sub != 0 && sub != 15) {
-      if (!assign((sidx >> 4) + 1, klo, khi)) return 0;
-    } else {
-      const int idx = (sidx + 1) >> 4;
-      const uint32_t kt = fkey(tE[idx]);
-      if (!assign(idx, klo, std::min(khi, kt))) return 0;
-      if (kt < khi && !assign(idx + 1, std::max(klo, kt + 1), khi)) return 0;
-    }
+  // rank r holds keys [lo_r, lo_{r+1}); each nonempty interval must sit in one bin
+  std::vector<uint32_t> lo((size_t)cells + 4);
+  for (int r = 0; r <= cells + 3; ++r)
+    lo[r] = first_key([&](float x) { return edge_rank(x, scale, bias, cells, tE) >= r; });
+  for (int r = 0; r <= cells + 1; ++r) {
+    rbin[r] = 0;
+    if (lo[r] >= lo[r + 1]) continue;
+    const int64_t b0 = bin32(keyf(lo[r]), t32, nb), b1 = bin32(keyf(lo[r + 1] - 1), t32, nb);
+    if (b0 != b1) return 0;
+    rbin[r] = (int32_t)b0;
   }
-  for (int r = 0; r <= cells + 1; ++r) rbin[r] = (int32_t)(rb[r] >= 0 ? rb[r] : 0);
+  if (lo[cells + 2] <= kmax) return 0;   // no float may rank above cells + 1
   return 1;
 }
 

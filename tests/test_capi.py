@@ -141,9 +141,9 @@ def test_threshold_table_edge_ranks_exact():
                                  rng.uniform(lo - 1, hi + 1, 20000).astype(np.float32)]).astype(np.float32)
         g = np.clip((probes.astype(np.float64) * np.float32(b.lut_scale) + np.float32(b.lut_bias))
                     .astype(np.float32), 0, 1)
-        k1 = np.floor(g.astype(np.float64) * 16 * cells).astype(np.int64) + 1
-        idx = k1 >> 4
-        edge = (k1 & 14) == 0
+        k1 = np.floor(g.astype(np.float64) * 256 * cells).astype(np.int64) + 1
+        idx = k1 >> 8
+        edge = (k1 & 254) == 0
         tt = np.where(edge, tE[np.minimum(idx, cells)], -np.inf)
         rank = idx + (probes > tt)
         got = rbin[rank]

@@ -1,2 +1,3 @@
-python tools/prof_discrete.py 512 2 >/dev/null 2>&1 && ncu --set full --clock-control none --import-source on -k regex:fast3d -s 1 -c 1 -o gpurun_out/prof_edge python tools/prof_discrete.py 512 2 > /dev/null 2>&1
+timeout 900 python -m pytest tests/test_gpu_discrete.py tests/test_cli.py tests/test_io.py -m gpu -x -q --timeout 600 2>&1 | tail -2
+for M in default rank2; do echo "== $M"; ECC_B200_F3=$M timeout 100 python tools/quick_bench.py 2>&1 | grep hist; done
 echo done
