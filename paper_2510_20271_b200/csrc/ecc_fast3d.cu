@@ -676,7 +676,8 @@ __device__ __forceinline__ uint32_t bin4_lut(float x, uint32_t lut_m, float sc, 
 // read a threshold, which takes the random lookups off the shared-memory pipe.
 __device__ __forceinline__ uint32_t rank_edge(float x, uint32_t tE_m, float sc, float bi, float fcells256) {
   const float gg = __saturatef(__fmaf_rn(x, sc, bi));
-  const uint32_t k1 = __float_as_uint(__fmaf_rz(gg, fcells256, 8388608.0f)) + 1u;
+  // RZ(g C + 2^23 + 1) = 2^23 + 1 + floor(g C): the +1 rides in the magic constant
+  const uint32_t k1 = __float_as_uint(__fmaf_rz(gg, fcells256, 8388609.0f));
   float t = __int_as_float(0xff800000);
   asm volatile(
       "{\n.reg .pred pe;\n.reg .b32 s;\n"
