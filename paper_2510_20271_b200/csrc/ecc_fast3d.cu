@@ -53,6 +53,7 @@ constexpr uint32_t PLANE_BYTES = PLANE * 4;
 struct Geom {
   int W, H, D;
   int tiles_x, tiles_y, zchunks, zc;
+  int one;             // 1 at run time: multipliers built from it keep shifts/adds on the FMA pipe
   int zb, ze;          // deposit planes [zb, ze)
   int64_t items;
 };
@@ -134,6 +135,42 @@ __device__ __forceinline__ void words3(const Row& A, const float (&pc)[32], uint
   }
 }
 
+// The ALU pipe (LOP3, PRMT, SHF, IADD3) issues at half rate on sm_100 (16
+// lanes/clk/SMSP, tools/microbench/pipes.cu) and is the bottleneck of the rank
+// kernel; these helpers put shifts and adds on the FMA pipe (IMAD / IMAD.HI).
+// ptxas turns a multiply by a KNOWN power of two back into a shift, so the
+// left-shift multipliers are derived from Geom::one (a run-time 1).
+#ifndef ECC_F3_FMA_TR
+#define ECC_F3_FMA_TR 0
+#endif
+#ifndef ECC_F3_FMA_PP
+#define ECC_F3_FMA_PP 1
+#endif
+#ifndef ECC_F3_FMA_DEP
+#define ECC_F3_FMA_DEP 1
+#endif
+template <int S>
+__device__ __forceinline__ uint32_t shr_fma(uint32_t x) {   // x >> S, IMAD.HI
+  uint32_t r;
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(x), "n"(1u << (32 - S)));
+  return r;
+}
+__device__ __forceinline__ uint32_t mul_fma(uint32_t x, uint32_t m) {   // x * m, IMAD (m run-time)
+  uint32_t r;
+  asm("mul.lo.u32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(m));
+  return r;
+}
+__device__ __forceinline__ uint32_t mad_fma(uint32_t x, uint32_t m, uint32_t c) {   // x * m + c, IMAD
+  uint32_t r;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(x), "r"(m), "r"(c));
+  return r;
+}
+__device__ __forceinline__ uint32_t madhi_fma(uint32_t x, uint32_t m, uint32_t c) {   // (x * m) >> 32 + c
+  uint32_t r;
+  asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(x), "r"(m), "r"(c));
+  return r;
+}
+
 // full adder on bit-planes
 __device__ __forceinline__ void fa(uint32_t a, uint32_t b, uint32_t c, uint32_t& s, uint32_t& co) {
   s = a ^ b ^ c;
@@ -182,7 +219,8 @@ __device__ __forceinline__ uint32_t word1(QF q, const float (&pc)[32]) {
 // squares, cubes, signed count by a carry-save adder tree, then nibbles
 // Q[k] (nibble j = c of voxel 8k + j, 4-bit two's complement); returns the
 // OR of the bit-planes (0 when every c is 0)
-__device__ __forceinline__ uint32_t coeff_nibbles(const uint32_t (&L)[3][3][3], uint32_t outmask, uint32_t (&Q)[4]) {
+__device__ __forceinline__ uint32_t coeff_nibbles(const uint32_t (&L)[3][3][3], uint32_t outmask, uint32_t (&Q)[4],
+                                                  uint32_t one = 0u) {
   // squares (coefficients.py:119-126) and cubes (128-136) on words
   uint32_t Sxy[2][2], Szx[2][2], Szy[2][2];
 #pragma unroll
@@ -252,12 +290,21 @@ __device__ __forceinline__ uint32_t coeff_nibbles(const uint32_t (&L)[3][3][3], 
   for (int k = 0; k < 4; ++k) {
     const uint32_t sel = (uint32_t)k | ((uint32_t)(4 + k) << 4);
     uint32_t gq = __byte_perm(__byte_perm(r0, r2, sel), __byte_perm(r1b, r3, sel), 0x5410);
-    uint32_t t = ((gq >> 12) ^ gq) & 0x0000F0F0u;
-    gq ^= t ^ (t << 12);
-    t = ((gq >> 6) ^ gq) & 0x00CC00CCu;
-    gq ^= t ^ (t << 6);
-    t = ((gq >> 3) ^ gq) & 0x0A0A0A0Au;
-    gq ^= t ^ (t << 3);
+    if (ECC_F3_FMA_TR && one) {   // delta swaps with the shifts on the FMA pipe
+      uint32_t t = (shr_fma<12>(gq) ^ gq) & 0x0000F0F0u;
+      gq ^= t ^ mul_fma(t, one << 12);
+      t = (shr_fma<6>(gq) ^ gq) & 0x00CC00CCu;
+      gq ^= t ^ mul_fma(t, one << 6);
+      t = (shr_fma<3>(gq) ^ gq) & 0x0A0A0A0Au;
+      gq ^= t ^ mul_fma(t, one << 3);
+    } else {
+      uint32_t t = ((gq >> 12) ^ gq) & 0x0000F0F0u;
+      gq ^= t ^ (t << 12);
+      t = ((gq >> 6) ^ gq) & 0x00CC00CCu;
+      gq ^= t ^ (t << 6);
+      t = ((gq >> 3) ^ gq) & 0x0A0A0A0Au;
+      gq ^= t ^ (t << 3);
+    }
     Q[k] = gq;
   }
 
@@ -787,6 +834,8 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
   const float fcells = EDGE ? (float)(256 * cells) : (float)cells;
   const int nranks = EDGE ? cells + 2 : 2 * (cells + 1);
   const uint32_t dummy_off = (uint32_t)(nranks + lane);   // dummy counter index (< 2^15)
+  const uint32_t one = (uint32_t)g.one;
+  const uint32_t hbase = smem_u32(s_hist);
   // fold the rank counters (16 c per voxel) into the global bins: rank v is
   // bin b(v / 2) + v % 2; runs of ranks with the same bin are summed first
   auto flush = [&](int64_t item) {
@@ -941,7 +990,8 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
         load_brow(A, B0, lane, warp);
         load_brow(B, B0, rm, warp);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) PP[j] = A.w[j] | 0x80008000u;
+        for (int j = 0; j < 16; ++j)   // | == + (bits 15, 31 clear)
+          PP[j] = ECC_F3_FMA_PP ? mad_fma(A.w[j], one, 0x80008000u) : (A.w[j] | 0x80008000u);
         N0[NX] = cmp_word<-1>(PP, A);
         eA = A.e;
         load_brow(A, B1, rm, warp);
@@ -1039,7 +1089,7 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
         Lw[2][2][0] = ((~e_p) << 1 | E_zp_yp_xm) & myu & mz;
 
         uint32_t Q[4];
-        const uint32_t any = coeff_nibbles(Lw, outmask, Q);
+        const uint32_t any = coeff_nibbles(Lw, outmask, Q, one);
 
         // ---- per voxel: bin from the bin image + shared-memory reduction ----
         // c moves into the high nibble of a byte, so one sign-replicating
@@ -1070,8 +1120,14 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
               const uint32_t idx = i < 16 ? (Ro.w[i] & 0xFFFFu) : (Ro.w[i - 16] >> 16);
               if (c16) atomicAdd(s_hist + idx, c16);
             } else {
-              const uint32_t idx = i < 16 ? (Wm[i] & 0xFFFFu) : (Wm[i - 16] >> 16);
-              atomicAdd(s_hist + idx, c16);
+              if (ECC_F3_FMA_DEP) {   // counter address on the FMA pipe: 4 * lane + base
+                const uint32_t addr = i < 16 ? madhi_fma(mul_fma(Wm[i], one << 16), 1u << 18, hbase)
+                                             : mad_fma(shr_fma<16>(Wm[i - 16]), one << 2, hbase);
+                asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(addr), "r"(c16) : "memory");
+              } else {
+                const uint32_t idx = i < 16 ? (Wm[i] & 0xFFFFu) : (Wm[i - 16] >> 16);
+                atomicAdd(s_hist + idx, c16);
+              }
             }
           }
         }
@@ -1183,6 +1239,7 @@ int fast3d_launch(const float* x, int64_t D, int64_t H, int64_t W, int64_t batch
   g.tiles_y = (int)((H + OUTR - 1) / OUTR);
   const int64_t tiles = (int64_t)g.tiles_x * g.tiles_y * batch;
   g.zc = 0;
+  g.one = 1;
   g.items = tiles;   // the kernel splits tiles x planes evenly over the grid
   const int64_t total = tiles * (ze - zb);
   const int64_t grid = total < max_ctas ? total : max_ctas;

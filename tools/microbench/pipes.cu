@@ -63,6 +63,51 @@ __global__ void k_mix(float* o, float a, float b, int n) {
   if (s == 1.2345f) o[0] = s;
 }
 
+
+__global__ void k_lop3(float* o, float a, float b, int n) {
+  unsigned c[8];
+  unsigned m = __float_as_uint(a), q = __float_as_uint(b);
+  for (int i = 0; i < 8; ++i) c[i] = threadIdx.x * 7 + i;
+  for (int it = 0; it < n; ++it)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(c[i]) : "r"(m), "r"(q));
+  unsigned s = 0; for (int i = 0; i < 8; ++i) s += c[i];
+  if (s == 12345u) o[0] = 1.f;
+}
+__global__ void k_prmt(float* o, float a, float b, int n) {
+  unsigned c[8];
+  unsigned m = __float_as_uint(a);
+  for (int i = 0; i < 8; ++i) c[i] = threadIdx.x * 7 + i;
+  for (int it = 0; it < n; ++it)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) asm volatile("prmt.b32 %0, %0, %1, 0x1234;" : "+r"(c[i]) : "r"(m));
+  unsigned s = 0; for (int i = 0; i < 8; ++i) s += c[i];
+  if (s == 12345u) o[0] = 1.f;
+}
+__global__ void k_iadd(float* o, float a, float b, int n) {
+  unsigned c[8];
+  unsigned m = __float_as_uint(a);
+  for (int i = 0; i < 8; ++i) c[i] = threadIdx.x * 7 + i;
+  for (int it = 0; it < n; ++it)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) asm volatile("sub.u32 %0, %1, %0;" : "+r"(c[i]) : "r"(m));
+  unsigned s = 0; for (int i = 0; i < 8; ++i) s += c[i];
+  if (s == 12345u) o[0] = 1.f;
+}
+__global__ void k_mix_alu_fma(float* o, float a, float b, int n) {
+  unsigned c[8];
+  unsigned m = __float_as_uint(a), q = __float_as_uint(b);
+  for (int i = 0; i < 8; ++i) c[i] = threadIdx.x * 7 + i;
+  for (int it = 0; it < n; ++it)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(c[i]) : "r"(m), "r"(q));
+      asm volatile("sub.u32 %0, %1, %0;" : "+r"(c[i + 4]) : "r"(m));
+    }
+  unsigned s = 0; for (int i = 0; i < 8; ++i) s += c[i];
+  if (s == 12345u) o[0] = 1.f;
+}
+
 template <typename K>
 int run(const char* name, K kern, double ops_per_iter_thread) {
   float* o; CK(cudaMalloc(&o, 4));
@@ -87,5 +132,9 @@ int main() {
   run("rcp", k_rcp, 8);
   run("rcp+fadd", k_rcp, 8);
   run("mix", k_mix, 8);         // pairs (8 rcp + 32 lane-fma)
+  run("lop3", k_lop3, 8);
+  run("prmt", k_prmt, 8);
+  run("sub.u32", k_iadd, 8);
+  run("lop3+sub", k_mix_alu_fma, 4);   // per-iteration ops: 4 lop3 + 4 sub -> counted as 4
   return 0;
 }
