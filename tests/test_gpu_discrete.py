@@ -371,3 +371,29 @@ class TestBinKernelLimits:
         fast, gen = TestFastPath._both(t, ts)
         want = np.append(*oracle.histogram(x, ts.taus))
         assert np.array_equal(fast[0], want) and np.array_equal(gen[0], want)
+
+
+class TestEdgeRanking:
+    """Edge-table ranking (power-of-two bin counts): voxels sitting exactly on
+    thresholds, one ulp either side, at the range ends and outside the range."""
+
+    @pytest.mark.parametrize("nb", [256, 1024, 2048])
+    def test_values_on_and_around_thresholds(self, rng, nb):
+        ts = E.thresholds_from_range(-1.25, 3.5, nb)
+        t32 = ts.taus.astype(np.float32)
+        pool = np.concatenate([t32, np.nextafter(t32, np.float32(np.inf)), np.nextafter(t32, np.float32(-np.inf)),
+                               np.float32([-1e30, -5.0, -1.25, 3.5, 7.0, 1e30, 0.0, -0.0, 1e-40])])
+        x = rng.choice(pool, size=(19, 37, 132)).astype(np.float32)
+        t = torch.from_numpy(x).cuda()
+        _, b = ts.device_table(_lib_dtype_f32(), t.device)
+        assert b.lut_edge == 1
+        out = TestFastPath._all(t, ts)
+        want = np.append(*oracle.histogram(x, ts.taus))
+        for name, h in out.items():
+            assert np.array_equal(h[0], want), name
+
+
+def _lib_dtype_f32():
+    from paper_2510_20271_b200 import _lib
+
+    return _lib.DTYPE_F32
