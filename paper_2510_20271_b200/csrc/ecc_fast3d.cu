@@ -687,11 +687,19 @@ __device__ __forceinline__ uint32_t cmp_word(const uint32_t (&PP)[16], const BRo
   uint32_t d[16];
 #pragma unroll
   for (int j = 0; j < 16; ++j) d[j] = PP[j] - qword<DX>(R, j);
-  // byte a of prmt(d[k], d[k+8]) = sign of voxel 8a + k, spread over the byte
-  uint32_t acc = prmt(d[0], d[8], 0xFBD9u) & 0x01010101u;
+  // byte a of m[k] = prmt(d[k], d[k+8]) = sign of voxel 8a + k, spread over
+  // the byte; a three-level select tree (7 LOP3, depth 3) puts bit k of every
+  // byte from m[k]: select(0x55) pairs, select(0x33) quads, select(0x0F) octets
+  uint32_t m[8];
 #pragma unroll
-  for (int k = 1; k < 8; ++k) acc |= prmt(d[k], d[k + 8], 0xFBD9u) & (0x01010101u << k);
-  return acc;
+  for (int k = 0; k < 8; ++k) m[k] = prmt(d[k], d[k + 8], 0xFBD9u);
+  const uint32_t m01 = (m[0] & 0x55555555u) | (m[1] & 0xAAAAAAAAu);
+  const uint32_t m23 = (m[2] & 0x55555555u) | (m[3] & 0xAAAAAAAAu);
+  const uint32_t m45 = (m[4] & 0x55555555u) | (m[5] & 0xAAAAAAAAu);
+  const uint32_t m67 = (m[6] & 0x55555555u) | (m[7] & 0xAAAAAAAAu);
+  const uint32_t m03 = (m01 & 0x33333333u) | (m23 & 0xCCCCCCCCu);
+  const uint32_t m47 = (m45 & 0x33333333u) | (m67 & 0xCCCCCCCCu);
+  return (m03 & 0x0F0F0F0Fu) | (m47 & 0xF0F0F0F0u);
 }
 
 // Rank of x in the cell table: v = 2 cell + (x > t_cell), cell = floor(sat(
