@@ -645,12 +645,15 @@ namespace ecc {
 // 2D soft prepare: one CTA per 32x8 pixel tile; the float64 effective field of
 // the tile and its one-pixel halo is built once in shared memory (NaN outside
 // the grid), then each thread writes its pixel's coefficient and centred field.
+#ifndef PREP_TH
+#define PREP_TH 32   // output rows per CTA of the 2D soft prepare
+#endif
 template <typename T>
 __global__ void __launch_bounds__(256) soft_prep2d_kernel(EffSrc<T> src, double center, int8_t* __restrict__ coeffs,
                                                           float* __restrict__ fc, float* __restrict__ fclo) {
   // 32 x 32 outputs per CTA (8 warps x 4 rows); the 34 x 34 effective-field
   // tile is loaded with all of a thread's global loads in flight at once
-  constexpr int TH = 32, TW = 32, PWD = TW + 2, PHT = TH + 2, NE = PWD * PHT, PER = (NE + 255) / 256;
+  constexpr int TH = PREP_TH, TW = 32, PWD = TW + 2, PHT = TH + 2, NE = PWD * PHT, PER = (NE + 255) / 256;
   __shared__ double tile[PHT][PWD];
   const int64_t n = blockIdx.z;
   const int64_t y0 = (int64_t)blockIdx.y * TH, x0 = (int64_t)blockIdx.x * TW;
@@ -705,7 +708,7 @@ extern "C" int ecc_soft_prepare(const void* x, int dtype, int ndim, const int64_
   SoftPrepSink sk{coeffs, field_c, field_lo, p->center, d3[0], d3[1], d3[2]};
   cudaStream_t s = (cudaStream_t)stream;
   if (ndim == 2 && batch <= 65535 && (dtype == ECC_DTYPE_F32 || dtype == ECC_DTYPE_F64)) {
-    dim3 grid((unsigned)((d3[2] + 31) / 32), (unsigned)((d3[1] + 31) / 32), (unsigned)batch);
+    dim3 grid((unsigned)((d3[2] + 31) / 32), (unsigned)((d3[1] + PREP_TH - 1) / PREP_TH), (unsigned)batch);
     if (grid.y > 65535) goto generic;
     if (dtype == ECC_DTYPE_F32) {
       EffSrc<float> src{(const float*)x, p->alpha, p->u[0], p->u[1], 0.0, 1, d3[1], d3[2], 2,

@@ -1,4 +1,4 @@
-for V in "-DECC_F3_FMA_PP=0" "-DECC_F3_FMA_PP=1" "-DECC_F3_FMA_TR=1" "-DECC_F3_FMA_DEP=1"; do
-  ECC_B200_NVCC_EXTRA="$V" python -c "from paper_2510_20271_b200.build import build; build(force=True)" > /dev/null 2>&1
-  echo "== $V"; timeout 100 python tools/quick_bench.py 2>&1 | grep hist
+for V in 16 32 64; do
+  ECC_B200_NVCC_EXTRA="-DPREP_TH=$V" python -c "from paper_2510_20271_b200.build import build; build(force=True)" > /dev/null 2>&1
+  ncu --metrics gpu__time_duration.sum --clock-control none -k regex:soft_prep2d -c 3 python tools/prof_soft.py 16 2 2>&1 | grep duration | head -3 | sed "s/^/TH=$V /"
 done
