@@ -280,7 +280,10 @@ ecc_soft_kernel(SoftArgs a) {
         const int k = off + __popc(m & ((1u << lane) - 1u));
         S.fc[k] = fvr[it];
         if (!FACT) s_fclo[k] = a.fclo[item * a.n + v0 + i];
-        S.pk[k] = i | (cv << 16);
+        // upper half: the float32 bits of c (small integers have a zero low
+        // half), so the pair loop reads c with one AND instead of an I2F on
+        // the XU pipe that the reciprocals saturate; lower half: the voxel
+        S.pk[k] = i | (int)(__float_as_uint((float)cv) & 0xFFFF0000u);
       } else if (BWD && i < w1) {
         a.dX[item * a.n + v0 + i] = 0.f;
       }
@@ -342,7 +345,7 @@ ecc_soft_kernel(SoftArgs a) {
 
   auto voxel_w = [&](int k, bool valid) -> float {
     const float f = valid ? S.fc[k] : 0.f;
-    const float cf = valid ? (float)(S.pk[k] >> 16) : 0.f;
+    const float cf = valid ? __uint_as_float((uint32_t)S.pk[k] & 0xFFFF0000u) : 0.f;
     float w = 0.f;
     if (FACT) {
       const float kf = fminf(fmaxf(__fmaf_rn(a.kscale, f, koff), -B_MAX), B_MAX);
@@ -396,7 +399,7 @@ ecc_soft_kernel(SoftArgs a) {
       const int k = kb0 + (l & 7) * nslots + g;
       if (l < 8 && k < count) {
         const int pk = S.pk[k];
-        a.dX[item * a.n + v0 + (pk & 0xffff)] = -(float)(pk >> 16) * (lamf * wv[0]);
+        a.dX[item * a.n + v0 + (pk & 0xffff)] = -__uint_as_float((uint32_t)pk & 0xFFFF0000u) * (lamf * wv[0]);
       }
     }
   } else {
@@ -411,7 +414,7 @@ ecc_soft_kernel(SoftArgs a) {
           if (o < Lv) w += __shfl_xor_sync(0xffffffffu, w, o);   // Lv is warp-uniform
         if (l == 0 && valid) {
           const int pk = S.pk[k];
-          a.dX[item * a.n + v0 + (pk & 0xffff)] = -(float)(pk >> 16) * (lamf * w);
+          a.dX[item * a.n + v0 + (pk & 0xffff)] = -__uint_as_float((uint32_t)pk & 0xFFFF0000u) * (lamf * w);
         }
       }
     }
