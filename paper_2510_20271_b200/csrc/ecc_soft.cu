@@ -58,6 +58,26 @@ __device__ __forceinline__ float ex2_approx(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// 2^x on the FMA pipe for |x| <= 126 (the per-voxel factor b_p): x = n + f
+// with n = rint(x) from the 1.5 * 2^23 magic add, 2^f by its degree-6 Taylor
+// polynomial on [-1/2, 1/2] (relative error ~1.2e-7, like ex2.approx), and n
+// added to the exponent field.  Frees the XU pipe, which the reciprocals
+// saturate in the backward pass.
+__device__ __forceinline__ float ex2_fma(float x) {
+  const float r = __fadd_rn(x, 12582912.0f);
+  const float f = __fsub_rn(x, __fsub_rn(r, 12582912.0f));
+  float p = 1.5403530e-4f;
+  p = __fmaf_rn(p, f, 1.3333558e-3f);
+  p = __fmaf_rn(p, f, 9.6181291e-3f);
+  p = __fmaf_rn(p, f, 5.5504109e-2f);
+  p = __fmaf_rn(p, f, 2.4022651e-1f);
+  p = __fmaf_rn(p, f, 6.9314718e-1f);
+  p = __fmaf_rn(p, f, 1.0f);
+  return __int_as_float(__float_as_int(p) + ((__float_as_int(r) - 0x4B400000) << 23));
+}
+#ifndef ECC_SOFT_EX2_FMA
+#define ECC_SOFT_EX2_FMA 0   // 0: MUFU.EX2 (default); 1: FMA-pipe 2^x in the backward, 2: in both (measured slower: 830 / 577 vs 808 / 527 us)
+#endif
 __device__ __forceinline__ float rcp_approx(float x) {
   float y;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -357,9 +377,11 @@ ecc_soft_kernel(SoftArgs a) {
 #define ECC_BWD_PACKED 1   // packed FFMA2 backward (801 vs 838 us at 16 thresholds per lane)
 #endif
       if (BWD && !ECC_BWD_PACKED)
-        pair_loop_fact<BWD, T, 1024>(at, upv, acc, ex2_approx(kf), cf, w);
+        pair_loop_fact<BWD, T, 1024>(at, upv, acc, ECC_SOFT_EX2_FMA >= 1 ? ex2_fma(kf) : ex2_approx(kf), cf, w);
       else
-        pair_loop_fact2<BWD, T>(at2, up2, acc2, ex2_approx(kf), cf, w);
+        pair_loop_fact2<BWD, T>(at2, up2, acc2,
+                                (BWD ? ECC_SOFT_EX2_FMA >= 1 : ECC_SOFT_EX2_FMA >= 2) ? ex2_fma(kf) : ex2_approx(kf),
+                                cf, w);
     } else {
       const double fd = (double)f + (double)(valid ? s_fclo[k] : 0.f);
       pair_loop_direct<BWD, T>(kt, Lv, l, upv, acc, ks * fd, cf, w);
