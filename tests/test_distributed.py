@@ -129,3 +129,53 @@ def test_slab_bounds_cover():
             assert spans[0][0] == 0 and spans[-1][1] == depth
             assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))
             assert max(b - a for a, b in spans) - min(b - a for a, b in spans) <= 1
+
+
+def _file_worker(rank, world, port, path, nbins, result_q):
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from oracle import oracle
+    from paper_2510_20271_b200 import distributed as D
+    from paper_2510_20271_b200.grid import thresholds_from_range
+    from paper_2510_20271_b200.io import load_slab_device, read_grid
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        # each rank reads its own planes plus the two neighbour planes from the
+        # file: no halo exchange (exchange=False)
+        padded, (z0, z1) = load_slab_device(path, rank, world, "cpu")
+        lo, hi = D.global_range(padded[1:-1].to(torch.float64))
+        taus = thresholds_from_range(lo, hi, nbins)
+        hist = D.slab_histogram(padded, taus, exchange=False, hist_fn=_oracle_hist)
+        if rank == 0:
+            full = read_grid(path).values.astype(np.float32)
+            bins, ovf = oracle.histogram(full, taus.taus)
+            result_q.put(bool(np.array_equal(hist.numpy(), np.append(bins, ovf))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_file_backed_slabs(tmp_path, world):
+    """io.load_slab_device + slab_histogram(exchange=False) over gloo equals the
+    whole volume's histogram (the file-backed C5 path)."""
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from oracle import oracle
+    from paper_2510_20271_b200.io import write_grid
+
+    dims = (13, 10, 12)
+    path = tmp_path / "v.eccg"
+    write_grid(oracle.counter_grid(5, dims).reshape(dims), path)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_file_worker, args=(r, world, port, str(path), 48, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    assert q.get(timeout=5) is True
