@@ -284,17 +284,15 @@ def run_b200(args):
     e2e = None
     if not args.no_e2e:
         # every step: this rank's slab pinned host -> HBM, the public API call,
-        # curve HBM -> host (N = 1: ecc_discrete; N > 1: distributed.slab_curve,
+        # curve HBM -> host (N = 1: ecc_discrete_host; N > 1: distributed.slab_curve,
         # which adds the halo exchange and the histogram all-reduce)
         host = torch.empty((P, H, W), dtype=torch.float32, pin_memory=True)
         host.copy_(own.cpu())
         if world == 1:
-            xdev = torch.empty((P, H, W), dtype=torch.float32, device=dev)
-
             def e2e_step():
-                xdev.copy_(host, non_blocking=True)
-                return E.ecc_discrete(xdev, taus).cpu()
-            api = "paper_2510_20271_b200.ecc_discrete"
+                return E.ecc_discrete_host(host, taus, chunk_planes=256).cpu()
+            api = ("paper_2510_20271_b200.ecc_discrete_host (256-plane chunks: the host->device copy of one "
+                   "chunk overlaps the kernel of the previous one)")
         else:
             buf = D.alloc_padded_slab(P, (H, W), torch.float32, dev)
 

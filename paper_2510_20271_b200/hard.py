@@ -159,6 +159,76 @@ def ecc_discrete(x: torch.Tensor, taus, ndim: int | None = None, return_hist: bo
     return (curve, hist) if return_hist else curve
 
 
+class _StreamState:
+    """Device buffers of ecc_discrete_host, cached per (shape, chunk, device)."""
+
+    cache: dict = {}
+
+
+def ecc_discrete_host(x_host: torch.Tensor, taus, chunk_planes: int = 64, device=None, return_hist: bool = False):
+    """Exact ECC of a 3D volume held in HOST memory, streamed to the GPU.
+
+    The volume (float32 / uint8 / float64, [D, H, W], row-major) is cut into
+    z-chunks; the host-to-device copy of chunk k + 1 (plus its one-plane
+    halos) runs on a copy stream while the fused kernel deposits chunk k
+    (ecc_histogram_range) on the compute stream, so the end-to-end time is
+    the larger of the PCIe transfer and the compute instead of their sum, and
+    the volume need not fit in device memory.  Pass pinned memory
+    (``tensor.pin_memory()``) for asynchronous copies.  The result equals
+    ecc_discrete(x_host.cuda(), taus) bit for bit (histograms are exactly
+    additive over planes, hard.py:99-118; the tie-break is translation
+    invariant, coefficients.py:141-152).
+    """
+    if isinstance(x_host, np.ndarray):
+        x_host = torch.from_numpy(np.ascontiguousarray(x_host))
+    if x_host.is_cuda or x_host.ndim != 3:
+        raise ValueError("ecc_discrete_host takes a 3-D host tensor")
+    if chunk_planes < 1:
+        raise ValueError(f"chunk_planes must be >= 1, got {chunk_planes}")
+    x_host = x_host.contiguous()
+    ts = taus if isinstance(taus, ThresholdSet) else ThresholdSet(taus)
+    dev = torch.device(device) if device is not None else _lib.device()
+    D, H, W = (int(d) for d in x_host.shape)
+    code = _lib.dtype_code(x_host)
+    nb = len(ts)
+    table, binning = ts.device_table(code, dev)
+    cp = min(chunk_planes, D)
+    key = (x_host.dtype, cp, H, W, nb, str(dev))
+    st = _StreamState.cache.get(key)
+    if st is None:
+        st = {"bufs": [torch.empty((cp + 2, H, W), dtype=x_host.dtype, device=dev) for _ in range(2)],
+              "part": [torch.empty(nb + 1, dtype=torch.int64, device=dev) for _ in range(2)],
+              "copy": torch.cuda.Stream(dev)}
+        _StreamState.cache = {key: st}   # one cached configuration
+    main = torch.cuda.current_stream(dev)
+    cs = st["copy"]
+    total = torch.zeros(nb + 1, dtype=torch.int64, device=dev)
+    freed = [None, None]
+    cs.wait_stream(main)
+    for c, z0 in enumerate(range(0, D, cp)):
+        z1 = min(z0 + cp, D)
+        lo, hi = max(z0 - 1, 0), min(z1 + 1, D)
+        buf, part = st["bufs"][c % 2], st["part"][c % 2]
+        with torch.cuda.stream(cs):
+            if freed[c % 2] is not None:
+                cs.wait_event(freed[c % 2])       # the kernel that last read this buffer is done
+            buf[:hi - lo].copy_(x_host[lo:hi], non_blocking=True)
+            copied = torch.cuda.Event()
+            copied.record(cs)
+        main.wait_event(copied)
+        view = buf[:hi - lo]
+        d = _lib.dims_arg(view.shape)
+        _lib.check(_lib.lib().ecc_histogram_range(_lib.ptr(view), code, 3, _lib.ptr(d), 1, z0 - lo, z1 - lo,
+                                                  _lib.ptr(table), _lib.ctypes.byref(binning), _lib.ptr(part),
+                                                  _lib.ctypes.c_void_p(main.cuda_stream)))
+        total += part
+        ev = torch.cuda.Event()
+        ev.record(main)
+        freed[c % 2] = ev
+    curve = scan_device(total.reshape(1, -1), nb)[0]
+    return (curve, total) if return_hist else curve
+
+
 def _check_strategy(strategy, workers):
     if workers < 1:
         raise ValueError(f"workers must be >= 1, got {workers}")

@@ -397,3 +397,23 @@ def _lib_dtype_f32():
     from paper_2510_20271_b200 import _lib
 
     return _lib.DTYPE_F32
+
+
+class TestHostStreaming:
+    """ecc_discrete_host: z-chunks copied on a side stream while the previous
+    chunk is deposited; bit-exact with the device-resident call."""
+
+    @pytest.mark.parametrize("chunk", [1, 7, 64, 1000])
+    def test_chunks_equal_device_call(self, rng, chunk):
+        x = rng.random((37, 45, 132)).astype(np.float32)
+        ts = E.thresholds_from_range(float(x.min()), float(x.max()), 256)
+        want_c, want_h = E.ecc_discrete(torch.from_numpy(x).cuda(), ts, return_hist=True)
+        for host in (torch.from_numpy(x), torch.from_numpy(x).pin_memory()):
+            c, h = E.ecc_discrete_host(host, ts, chunk_planes=chunk, return_hist=True)
+            assert torch.equal(c, want_c) and torch.equal(h, want_h)
+
+    def test_uint8_and_generic_shapes(self, rng):
+        x = rng.integers(0, 256, (20, 31, 50), dtype=np.uint8)   # W % 4 != 0: generic kernel
+        ts = E.ThresholdSet(np.arange(0.0, 256.0, 9.0))
+        c = E.ecc_discrete_host(x, ts, chunk_planes=6)
+        assert np.array_equal(c.cpu().numpy(), oracle.curve(x.astype(np.float64), ts.taus))
