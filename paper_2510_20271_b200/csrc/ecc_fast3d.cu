@@ -809,8 +809,11 @@ __device__ __forceinline__ void bin_plane(const float* stage, uint32_t* B, bool 
     bin_rowseg<false, EDGE>(src, dw, de, lut_m, sc, bi, fcells);
 }
 
+#ifndef ECC_F3_MINB
+#define ECC_F3_MINB 4   // resident CTAs per SM the register budget is sized for
+#endif
 template <int DEP, bool WS, bool EDGE>
-__global__ void __launch_bounds__(NT, 4)
+__global__ void __launch_bounds__(NT, ECC_F3_MINB)
 ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* __restrict__ table_g, int nb,
                       int cells, int hsize, float lut_scale, float lut_bias, unsigned long long* __restrict__ hist) {
   extern __shared__ __align__(128) unsigned char smem_raw[];

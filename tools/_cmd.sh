@@ -1,2 +1,4 @@
-timeout 600 python -m pytest tests/test_gpu_discrete.py -m gpu -x -q --timeout 300 -k "HostStreaming" 2>&1 | tail -2
-python bench.py --no-soft --no-ns --no-cpu 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['e2e'])"
+for V in 3 4; do
+  ECC_B200_NVCC_EXTRA="-DECC_F3_MINB=$V" python -c "from paper_2510_20271_b200.build import build; build(force=True)" > /dev/null 2>&1
+  echo "== minb $V"; timeout 100 python tools/quick_bench.py 2>&1 | grep hist
+done
