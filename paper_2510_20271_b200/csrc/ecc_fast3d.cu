@@ -740,7 +740,7 @@ __device__ __forceinline__ uint32_t rank_edge(float x, uint32_t tE_m, float sc, 
       "setp.eq.u32 pe, s, 0;\n"
       "@pe ld.shared.f32 %0, [%1];\n}\n"
       : "+f"(t)
-      : "r"(tE_m + (k1 >> 6)), "r"(k1));
+      : "r"(madhi_fma(k1, 1u << 26, tE_m)), "r"(k1));   // tE_m + (k1 >> 6) as IMAD.HI (FMA pipe)
   uint32_t v = k1;
   asm("{\n.reg .pred p;\nsetp.gt.f32 p, %1, %2;\n@p add.u32 %0, %0, 256;\n}\n" : "+r"(v) : "f"(x), "f"(t));
   return v;
