@@ -553,6 +553,9 @@ extern "C" int ecc_histogram_range(const void* x, int dtype, int ndim, const int
   auto* h = reinterpret_cast<unsigned long long*>(hist);
   switch (dtype) {
     case ECC_DTYPE_U8: {
+      if (fast3d_u8_eligible(x, d3[0], d3[1], d3[2], batch, nb) && !getenv("ECC_B200_GENERIC"))
+        return fast3d_u8_launch((const uint8_t*)x, d3[0], d3[1], d3[2], batch, plane_begin, plane_end, table,
+                                binning, h, s);
       HistSink<float> sk{(const float*)table, h, bp};
       return launch_sweep(RawSrc<uint8_t>{(const uint8_t*)x}, sk, d3, batch, HistSink<float>::smem_bytes(nb), s,
                           plane_begin, plane_end);

@@ -786,6 +786,56 @@ __device__ __forceinline__ void bin_rowseg(const float* src, uint32_t* dw, uint3
   const uint32_t bl = rank_of<EDGE>(el, lut_m, sc, bi, fcells), br = rank_of<EDGE>(er, lut_m, sc, bi, fcells);
   *de = prmt(el != el ? SENT : bl, er != er ? SENT : br, PK);
 }
+// uint8 grids: the value itself is the rank (every level set is one value,
+// so it lies inside a bin and ties keep the reference's index order: the
+// per-voxel coefficients even equal the reference's).  The staged plane is
+// 176 bytes per row (x0 - 16 .. x0 + 159: 16-byte aligned segments, pitch
+// == 12 words mod 32 for conflict-free LDS.128); TMA fills out-of-bounds
+// bytes with 0, so validity comes from the coordinates.
+constexpr int U8_PITCH = 176;
+constexpr uint32_t U8_PLANE_BYTES = U8_PITCH * 32;
+template <bool CHECK>
+__device__ __forceinline__ void rank_rowseg_u8(const unsigned char* src, uint32_t* dw, uint32_t* de, int xs, int W) {
+  const uint4 a = *reinterpret_cast<const uint4*>(src), b = *reinterpret_cast<const uint4*>(src + 16);
+  const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, bw[4] = {b.x, b.y, b.z, b.w};
+  uint32_t w[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const uint32_t r = (uint32_t)(j & 3);
+    w[j] = prmt(aw[j >> 2], bw[j >> 2], r | ((4u + r) << 8)) & 0x00FF00FFu;   // (byte j, byte j + 16)
+    if (CHECK) {
+      if (xs + j >= W) w[j] = (w[j] & 0xFFFF0000u) | BSENT;
+      if (xs + 16 + j >= W) w[j] = (w[j] & 0x0000FFFFu) | (BSENT << 16);
+    }
+  }
+  uint4* d4 = reinterpret_cast<uint4*>(dw);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) d4[k] = make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
+  const uint32_t l = xs >= 1 ? (uint32_t)src[-1] : BSENT;
+  const uint32_t rr = xs + 32 < W ? (uint32_t)src[32] : BSENT;
+  *de = l | (rr << 16);
+}
+__device__ __forceinline__ void rank_plane_u8(const unsigned char* stage, uint32_t* B, bool plane_in, int x0, int y0,
+                                              int W, int H) {
+  const int row = threadIdx.x & 31, seg = threadIdx.x >> 5;
+  uint32_t* dw = B + row * BROW + 16 * seg;
+  uint32_t* de = B + BEDGE + seg * 32 + row;
+  const int y = y0 - 1 + row, xs = x0 + 32 * seg;
+  if (!plane_in || y < 0 || y >= H || xs >= W) {
+    const uint32_t s2 = BSENT | (BSENT << 16);
+    uint4* d4 = reinterpret_cast<uint4*>(dw);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) d4[k] = make_uint4(s2, s2, s2, s2);
+    *de = s2;
+    return;
+  }
+  const unsigned char* src = stage + row * U8_PITCH + 16 + 32 * seg;
+  if (xs + 32 > W)
+    rank_rowseg_u8<true>(src, dw, de, xs, W);
+  else
+    rank_rowseg_u8<false>(src, dw, de, xs, W);
+}
+
 // bin the staged plane into a bin plane: warp -> x segment, lane -> row
 template <bool EDGE>
 __device__ __forceinline__ void bin_plane(const float* stage, uint32_t* B, bool plane_in, int x0, int y0, int W,
@@ -812,13 +862,14 @@ __device__ __forceinline__ void bin_plane(const float* stage, uint32_t* B, bool 
 #ifndef ECC_F3_MINB
 #define ECC_F3_MINB 4   // resident CTAs per SM the register budget is sized for
 #endif
-template <int DEP, bool WS, bool EDGE>
+template <int DEP, bool WS, bool EDGE, bool U8 = false>
 __global__ void __launch_bounds__(NT, ECC_F3_MINB)
 ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* __restrict__ table_g, int nb,
                       int cells, int hsize, float lut_scale, float lut_bias, unsigned long long* __restrict__ hist) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  float* stage = reinterpret_cast<float*>(smem_raw);                            // one f32 plane (TMA)
-  uint32_t* bbuf = reinterpret_cast<uint32_t*>(smem_raw + PLANE_BYTES);          // two bin planes
+  constexpr uint32_t STAGE_BYTES = U8 ? U8_PLANE_BYTES : PLANE_BYTES;
+  float* stage = reinterpret_cast<float*>(smem_raw);                            // one staged plane (TMA)
+  uint32_t* bbuf = reinterpret_cast<uint32_t*>(smem_raw + STAGE_BYTES);          // two rank planes
   uint64_t* bar = reinterpret_cast<uint64_t*>(bbuf + 2 * BPLANE);
   int* s_rounds = reinterpret_cast<int*>(bar + 1);                               // WS: binning arrivals
   float* s_t = reinterpret_cast<float*>(bar + 2);                                // cells + 1 thresholds
@@ -831,7 +882,8 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
   const float* tE_g = reinterpret_cast<const float*>(lut_g + cells + 1);
   const int* rbin_g = reinterpret_cast<const int*>(tE_g + cells + 1);
   for (int i = threadIdx.x; i < hsize; i += NT) s_hist[i] = 0;
-  for (int i = threadIdx.x; i <= cells; i += NT) s_t[i] = EDGE ? tE_g[i] : lut_g[i].t;
+  if (!U8)
+    for (int i = threadIdx.x; i <= cells; i += NT) s_t[i] = EDGE ? tE_g[i] : lut_g[i].t;
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
     *s_rounds = 0;
@@ -843,7 +895,7 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
   // 2-rank mode by key = 0x4B000000 + cell, edge mode by (key256 + 1) >> 6
   const uint32_t lut_m = smem_u32(s_t) - (EDGE ? 0x012C0000u : 0x2C000000u);
   const float fcells = EDGE ? (float)(256 * cells) : (float)cells;
-  const int nranks = EDGE ? cells + 2 : 2 * (cells + 1);
+  const int nranks = U8 ? 256 : EDGE ? cells + 2 : 2 * (cells + 1);
   const uint32_t dummy_off = (uint32_t)(nranks + lane);   // dummy counter index (< 2^15)
   const uint32_t one = (uint32_t)g.one;
   const uint32_t hbase = smem_u32(s_hist);
@@ -859,7 +911,17 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
       const int c = s_hist[v];
       s_hist[v] = 0;
       if (!c) continue;
-      const int bin = EDGE ? rbin_g[v] : lut_g[v >> 1].b + (v & 1);
+      int bin;
+      if (U8) {   // searchsorted-left of the value over the float32 thresholds
+        int lo = 0, hi = nb;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (tab_g[mid + 1] < (float)v) lo = mid + 1; else hi = mid;
+        }
+        bin = lo;
+      } else {
+        bin = EDGE ? rbin_g[v] : lut_g[v >> 1].b + (v & 1);
+      }
       if (bin != cur) {
         if (cur >= 0 && acc) atomicAdd(h + cur, (unsigned long long)(acc >> 4));
         cur = bin;
@@ -932,8 +994,8 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
     // shared f32 stage: after every warp has binned plane q (4 arrivals on
     // s_rounds) the last one to arrive issues the TMA of plane q + 1.
     auto issue = [&](int p) {
-      mbar_expect_tx(bar, PLANE_BYTES);
-      tma_load_4d(stage, &tmap, bar, x0 - 4, y0 - 1, p, (int)n);
+      mbar_expect_tx(bar, STAGE_BYTES);
+      tma_load_4d(stage, &tmap, bar, x0 - (U8 ? 16 : 4), y0 - 1, p, (int)n);
     };
     auto round_done = [&](int p) {
       __syncwarp();
@@ -960,7 +1022,10 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
         mbar_wait(bar, phase);
         phase ^= 1u;
       }
-      bin_plane<EDGE>(stage, bbuf + (p & 1) * BPLANE, pin, x0, y0, g.W, g.H, lut_m, lut_scale, lut_bias, fcells);
+      if (U8)
+        rank_plane_u8(reinterpret_cast<const unsigned char*>(stage), bbuf + (p & 1) * BPLANE, pin, x0, y0, g.W, g.H);
+      else
+        bin_plane<EDGE>(stage, bbuf + (p & 1) * BPLANE, pin, x0, y0, g.W, g.H, lut_m, lut_scale, lut_bias, fcells);
       if (WS) {
         if (pin) round_done(p);
         else __syncwarp();
@@ -1033,7 +1098,11 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
           mbar_wait(bar, phase);
           phase ^= 1u;
         }
-        bin_plane<EDGE>(stage, bbuf + (p & 1) * BPLANE, pin, x0, y0, g.W, g.H, lut_m, lut_scale, lut_bias, fcells);
+        if (U8)
+          rank_plane_u8(reinterpret_cast<const unsigned char*>(stage), bbuf + (p & 1) * BPLANE, pin, x0, y0, g.W,
+                        g.H);
+        else
+          bin_plane<EDGE>(stage, bbuf + (p & 1) * BPLANE, pin, x0, y0, g.W, g.H, lut_m, lut_scale, lut_bias, fcells);
         if (WS) {
           if (pin) round_done(p);
           else __syncwarp();
@@ -1266,6 +1335,63 @@ int fast3d_launch(const float* x, int64_t D, int64_t H, int64_t W, int64_t batch
   ecc_fast3d_kernel<<<(unsigned)grid, NT, smem, stream>>>(map, g, table, nb, cells, cell_shift, b->lut_scale,
                                                             b->lut_bias, b->lut_ok, hist);
   return check_launch("ecc_fast3d_kernel");
+}
+
+// uint8 grids: the rank kernel with the value as rank (no threshold table in
+// the sweep; ranks are folded into bins when the CTA flushes).
+bool fast3d_u8_eligible(const void* x, int64_t D, int64_t H, int64_t W, int64_t batch, int64_t nb) {
+  if (((uintptr_t)x & 15u) != 0) return false;
+  if (W % 16 != 0) return false;   // TMA strides are multiples of 16 bytes
+  if (W > (1 << 30) || H > (1 << 30) || D > (1 << 30) || batch > (1 << 30)) return false;
+  if (nb > ECC_MAX_BINS) return false;
+  return fast::encode_fn() != nullptr;
+}
+
+int fast3d_u8_launch(const uint8_t* x, int64_t D, int64_t H, int64_t W, int64_t batch, int64_t zb, int64_t ze,
+                     const void* table, const ecc_binning* b, unsigned long long* hist, cudaStream_t stream) {
+  using namespace fast;
+  CUtensorMap map;
+  const cuuint64_t gdim[4] = {(cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)D, (cuuint64_t)batch};
+  const cuuint64_t gstride[3] = {(cuuint64_t)W, (cuuint64_t)(W * H), (cuuint64_t)(W * H * D)};
+  const cuuint32_t box[4] = {U8_PITCH, 32, 1, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<uint8_t*>(x), gdim, gstride, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(ECC_ECUDA, "cuTensorMapEncodeTiled(u8) failed");
+  const int nb = (int)b->nbins;
+  const char* env = getenv("ECC_B200_F3");
+  const bool cta = env && !strcmp(env, "cta");
+  const int hsize = 256 + 32;
+  const size_t smem = (size_t)U8_PLANE_BYTES + (size_t)2 * BPLANE * 4 + 16 + 4 * 4 + (size_t)hsize * 4;
+  const void* kfn = cta ? (const void*)ecc_fast3d_bin_kernel<1, false, false, true>
+                        : (const void*)ecc_fast3d_bin_kernel<1, true, false, true>;
+  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(fast3d u8)");
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, NT, smem);
+  if (occ < 1) return set_error(ECC_EINVAL, "fast3d u8 kernel does not fit on an SM");
+  const int64_t max_ctas = (int64_t)num_sms_fast() * occ;
+  Geom g;
+  g.W = (int)W;
+  g.H = (int)H;
+  g.D = (int)D;
+  g.zb = (int)zb;
+  g.ze = (int)ze;
+  g.tiles_x = (int)((W + TXW - 1) / TXW);
+  g.tiles_y = (int)((H + OUTR - 1) / OUTR);
+  const int64_t tiles = (int64_t)g.tiles_x * g.tiles_y * batch;
+  g.zc = 0;
+  g.one = 1;
+  g.items = tiles;
+  const int64_t total = tiles * (ze - zb);
+  const int64_t grid = total < max_ctas ? total : max_ctas;
+  g.zchunks = (tiles <= grid && grid <= tiles * (ze - zb)) ? (int)(grid / tiles) : 0;
+  if (grid < 1) return ECC_OK;
+  using KFn = void (*)(const CUtensorMap, Geom, const void*, int, int, int, float, float, unsigned long long*);
+  KFn k = reinterpret_cast<KFn>(const_cast<void*>(kfn));
+  k<<<(unsigned)grid, NT, smem, stream>>>(map, g, table, nb, 0, hsize, 0.f, 0.f, hist);
+  return check_launch("ecc_fast3d_bin_kernel<u8>");
 }
 
 }  // namespace ecc

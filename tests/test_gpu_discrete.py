@@ -417,3 +417,25 @@ class TestHostStreaming:
         ts = E.ThresholdSet(np.arange(0.0, 256.0, 9.0))
         c = E.ecc_discrete_host(x, ts, chunk_planes=6)
         assert np.array_equal(c.cpu().numpy(), oracle.curve(x.astype(np.float64), ts.taus))
+
+
+class TestFastPathU8:
+    """uint8 volumes (W % 16 == 0) take the rank kernel with the value as rank."""
+
+    @pytest.mark.parametrize("dims", [(1, 4, 16), (9, 33, 48), (17, 61, 128), (5, 90, 144), (40, 31, 256)])
+    def test_u8_volumes(self, rng, dims):
+        x = rng.integers(0, 256, dims, dtype=np.uint8)
+        t = torch.from_numpy(x).cuda()
+        for taus in (np.arange(0.0, 256.0, 1.0), np.arange(2.5, 250.0, 7.25), np.array([-3.0, 0.0, 127.5, 255.0, 300.0])):
+            ts = E.ThresholdSet(taus)
+            out = TestFastPath._all(t, ts)
+            want = np.append(*oracle.histogram(x.astype(np.float64), taus))
+            for name, h in out.items():
+                assert np.array_equal(h[0], want), (dims, name)
+
+    def test_u8_batched_and_ties(self, rng):
+        xs = rng.integers(0, 3, (3, 12, 40, 64), dtype=np.uint8)
+        ts = E.ThresholdSet(np.array([0.0, 1.0, 2.0]))
+        h = E.histogram_device(torch.from_numpy(xs).cuda(), ts, ndim=3).cpu().numpy()
+        for i in range(3):
+            assert np.array_equal(h[i], np.append(*oracle.histogram(xs[i].astype(np.float64), ts.taus)))
