@@ -1220,6 +1220,201 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
   if (cur_n >= 0) flush(cur_n);
 }
 
+// ======================================================================
+// 2D rank kernel (2-D grids / D == 1): one rank plane per 128 x 30 tile, no
+// z pipeline.  The tiles of a CTA form the pipeline instead: the TMA of tile
+// t + 1 is issued (by the last warp to finish ranking tile t) while tile t is
+// compared and deposited.  Only the four in-plane negative words (x - 1 and
+// the three y - 1 neighbours) are formed; the coefficient is the 2-D one,
+// c = 1 - E + S (coefficients.py:109-126), from the same word logic with the
+// z words zero (folded at compile time).
+// ======================================================================
+template <bool EDGE, bool U8>
+__global__ void __launch_bounds__(NT, ECC_F3_MINB)
+ecc_fast2d_rank_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* __restrict__ table_g, int nb,
+                       int cells, int hsize, float lut_scale, float lut_bias, unsigned long long* __restrict__ hist) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  constexpr uint32_t STAGE_BYTES = U8 ? U8_PLANE_BYTES : PLANE_BYTES;
+  float* stage = reinterpret_cast<float*>(smem_raw);
+  uint32_t* bbuf = reinterpret_cast<uint32_t*>(smem_raw + STAGE_BYTES);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(bbuf + 2 * BPLANE);
+  int* s_rounds = reinterpret_cast<int*>(bar + 1);
+  float* s_t = reinterpret_cast<float*>(bar + 2);
+  int* s_hist = reinterpret_cast<int*>(s_t + ((cells + 1 + 3) & ~3));
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const float* tab_g = reinterpret_cast<const float*>(table_g);
+  const LutEntry* lut_g = reinterpret_cast<const LutEntry*>(tab_g + ((nb + 2 + 1) & ~1));
+  const float* tE_g = reinterpret_cast<const float*>(lut_g + cells + 1);
+  const int* rbin_g = reinterpret_cast<const int*>(tE_g + cells + 1);
+  for (int i = threadIdx.x; i < hsize; i += NT) s_hist[i] = 0;
+  if (!U8)
+    for (int i = threadIdx.x; i <= cells; i += NT) s_t[i] = EDGE ? tE_g[i] : lut_g[i].t;
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    *s_rounds = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+  }
+  __syncthreads();
+  const uint32_t lut_m = smem_u32(s_t) - (EDGE ? 0x012C0000u : 0x2C000000u);
+  const float fcells = EDGE ? (float)(256 * cells) : (float)cells;
+  const int nranks = U8 ? 256 : EDGE ? cells + 2 : 2 * (cells + 1);
+  const uint32_t dummy_off = (uint32_t)(nranks + lane);
+  const uint32_t one = (uint32_t)g.one;
+  const uint32_t hbase = smem_u32(s_hist);
+  auto flush = [&](int64_t item) {
+    unsigned long long* h = hist + item * (nb + 1);
+    const int per = (nranks + NT - 1) / NT;
+    const int v0 = threadIdx.x * per, v1 = min(v0 + per, nranks);
+    long long acc = 0;
+    int cur = -1;
+    for (int v = v0; v < v1; ++v) {
+      const int c = s_hist[v];
+      s_hist[v] = 0;
+      if (!c) continue;
+      int bin;
+      if (U8) {
+        int lo = 0, hi = nb;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (tab_g[mid + 1] < (float)v) lo = mid + 1; else hi = mid;
+        }
+        bin = lo;
+      } else {
+        bin = EDGE ? rbin_g[v] : lut_g[v >> 1].b + (v & 1);
+      }
+      if (bin != cur) {
+        if (cur >= 0 && acc) atomicAdd(h + cur, (unsigned long long)(acc >> 4));
+        cur = bin;
+        acc = 0;
+      }
+      acc += c;
+    }
+    if (cur >= 0 && acc) atomicAdd(h + cur, (unsigned long long)(acc >> 4));
+  };
+
+  // contiguous, image-major tile range per CTA
+  const int64_t T = g.items;
+  const int64_t t_begin = T * (int64_t)blockIdx.x / gridDim.x, t_end = T * ((int64_t)blockIdx.x + 1) / gridDim.x;
+  auto origin = [&](int64_t t, int& x0, int& y0, int64_t& n) {
+    int64_t r = t;
+    x0 = (int)(r % g.tiles_x) * TXW;
+    r /= g.tiles_x;
+    y0 = (int)(r % g.tiles_y) * OUTR;
+    n = r / g.tiles_y;
+  };
+  auto issue = [&](int64_t t) {
+    int x0, y0;
+    int64_t n;
+    origin(t, x0, y0, n);
+    mbar_expect_tx(bar, STAGE_BYTES);
+    tma_load_4d(stage, &tmap, bar, x0 - (U8 ? 16 : 4), y0 - 1, 0, (int)n);
+  };
+  if (threadIdx.x == 0 && t_begin < t_end) issue(t_begin);
+  uint32_t phase = 0;
+  int64_t cur_n = -1;
+  const int rm = lane > 0 ? lane - 1 : 0;
+  const uint32_t FULL = 0xffffffffu;
+  for (int64_t t = t_begin, it = 0; t < t_end; ++t, ++it) {
+    int x0, y0;
+    int64_t n;
+    origin(t, x0, y0, n);
+    if (n != cur_n) {   // uniform across the CTA: every warp walks the same tiles
+      __syncthreads();
+      if (cur_n >= 0) flush(cur_n);
+      __syncthreads();
+      cur_n = n;
+    }
+    uint32_t* B = bbuf + (it & 1) * BPLANE;
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    if (U8)
+      rank_plane_u8(reinterpret_cast<const unsigned char*>(stage), B, true, x0, y0, g.W, g.H);
+    else
+      bin_plane<EDGE>(stage, B, true, x0, y0, g.W, g.H, lut_m, lut_scale, lut_bias, fcells);
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      const int old = atomicAdd(s_rounds, 1);
+      if ((old & 3) == 3 && t + 1 < t_end) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(t + 1);
+      }
+    }
+
+    // per-thread validity (rows / columns of this tile)
+    const int y = y0 - 1 + lane;
+    const bool lane_out = lane >= 1 && lane <= 30 && y < g.H;
+    const uint32_t myu = (y + 1) < g.H ? FULL : 0u;
+    const int xs = x0 + SEG * warp;
+    const int nvalid = max(0, min(32, g.W - xs));
+    const uint32_t xmask = nvalid >= 32 ? 0xffffffffu : ((1u << nvalid) - 1u);
+    const uint32_t xm_p1 = (nvalid >= 32 ? 0xffffffffu : ((1u << max(nvalid - 1, 0)) - 1u)) | 0x80000000u;
+    const uint32_t outmask = lane_out ? xmask : 0u;
+
+    // the four in-plane negative words
+    BRow A, Bm;
+    load_brow(A, B, lane, warp);
+    load_brow(Bm, B, rm, warp);
+    uint32_t PP[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) PP[j] = mad_fma(A.w[j], one, 0x80008000u);
+    const uint32_t nx = cmp_word<-1>(PP, A);
+    const uint32_t nym_m = cmp_word<-1>(PP, Bm), nym_0 = cmp_word<0>(PP, Bm), nym_p = cmp_word<1>(PP, Bm);
+    // row y + 1: its (0, -1, dx) words and its edge word
+    const uint32_t u_m = __shfl_down_sync(FULL, nym_m, 1);
+    const uint32_t u_0 = __shfl_down_sync(FULL, nym_0, 1);
+    const uint32_t u_p = __shfl_down_sync(FULL, nym_p, 1);
+    const uint32_t eU = __shfl_down_sync(FULL, A.e, 1);
+    const uint32_t PSs = (prmt(A.w[0], A.w[15], 0x7610u) | 0x80008000u) - 0x00010001u;
+    const uint32_t dR = PSs - A.e, dU = PSs - eU;
+    const uint32_t E_x = dR & 0x80000000u;
+    const uint32_t E_yp_xp = dU & 0x80000000u, E_yp_xm = (dU >> 15) & 1u;
+
+    uint32_t Lw[3][3][3];
+#pragma unroll
+    for (int a = 0; a < 3; a += 2)
+#pragma unroll
+      for (int b = 0; b < 3; ++b)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) Lw[a][b][c] = 0u;   // no z neighbours
+    Lw[1][1][1] = 0u;
+    Lw[1][1][0] = nx;
+    Lw[1][0][0] = nym_m;
+    Lw[1][0][1] = nym_0;
+    Lw[1][0][2] = nym_p;
+    Lw[1][1][2] = (((~nx) >> 1) & 0x7fffffffu & xm_p1) | E_x;
+    Lw[1][2][1] = (~u_0) & myu;
+    Lw[1][2][2] = ((((~u_m) >> 1) & 0x7fffffffu & xm_p1) | E_yp_xp) & myu;
+    Lw[1][2][0] = ((~u_p) << 1 | E_yp_xm) & myu;
+    uint32_t Q[4];
+    const uint32_t any = coeff_nibbles(Lw, outmask, Q, one);
+    if (__any_sync(FULL, any != 0u)) {
+      const uint32_t d2 = dummy_off | (dummy_off << 16);
+      uint32_t Wm[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const uint32_t keep = prmt(any << (15 - j), 0u, 0xBB99u);
+        Wm[j] = (A.w[j] & keep) | (d2 & ~keep);
+      }
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int m = (i & 7) >> 1;
+        const uint32_t sel = (uint32_t)m | ((uint32_t)(8 | m) << 4) | ((uint32_t)(8 | m) << 8) |
+                             ((uint32_t)(8 | m) << 12);
+        const uint32_t bq = (i & 1) ? (Q[i >> 3] & 0xF0F0F0F0u) : ((Q[i >> 3] << 4) & 0xF0F0F0F0u);
+        const int c16 = (int)prmt(bq, 0u, sel);
+        const uint32_t addr = i < 16 ? madhi_fma(mul_fma(Wm[i], one << 16), 1u << 18, hbase)
+                                     : mad_fma(shr_fma<16>(Wm[i - 16]), one << 2, hbase);
+        asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(addr), "r"(c16) : "memory");
+      }
+    }
+  }
+  __syncthreads();
+  if (cur_n >= 0) flush(cur_n);
+}
+
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static bool tried = false;
@@ -1252,6 +1447,37 @@ bool fast3d_eligible(const void* x, int64_t D, int64_t H, int64_t W, int64_t bat
   return fast::encode_fn() != nullptr;
 }
 
+// 2-D tile pipeline (ecc_fast2d_rank_kernel): contiguous tile ranges per CTA
+static int launch_2d(const CUtensorMap& map, const void* kfn, size_t smem, int64_t W, int64_t H, int64_t batch,
+                     const void* table, int nb, int cells, int hsize, float scale, float bias,
+                     unsigned long long* hist, cudaStream_t stream) {
+  using namespace fast;
+  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(fast2d)");
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, NT, smem);
+  if (occ < 1) return set_error(ECC_EINVAL, "fast2d kernel does not fit on an SM");
+  Geom g;
+  g.W = (int)W;
+  g.H = (int)H;
+  g.D = 1;
+  g.zb = 0;
+  g.ze = 1;
+  g.tiles_x = (int)((W + TXW - 1) / TXW);
+  g.tiles_y = (int)((H + OUTR - 1) / OUTR);
+  g.zc = 0;
+  g.zchunks = 0;
+  g.one = 1;
+  g.items = (int64_t)g.tiles_x * g.tiles_y * batch;
+  const int64_t max_ctas = (int64_t)num_sms_fast() * occ;
+  const int64_t grid = g.items < max_ctas ? g.items : max_ctas;
+  if (grid < 1) return ECC_OK;
+  using KFn = void (*)(const CUtensorMap, Geom, const void*, int, int, int, float, float, unsigned long long*);
+  KFn k = reinterpret_cast<KFn>(const_cast<void*>(kfn));
+  k<<<(unsigned)grid, NT, smem, stream>>>(map, g, table, nb, cells, hsize, scale, bias, hist);
+  return check_launch("ecc_fast2d_rank_kernel");
+}
+
 int fast3d_launch(const float* x, int64_t D, int64_t H, int64_t W, int64_t batch, int64_t zb, int64_t ze,
                   const void* table, const ecc_binning* b, unsigned long long* hist, cudaStream_t stream) {
   using namespace fast;
@@ -1273,7 +1499,8 @@ int fast3d_launch(const float* x, int64_t D, int64_t H, int64_t W, int64_t batch
   // default: the rank-image kernel with warp-independent pipelines (no CTA
   // barriers in the z loop; +2-3 % over the CTA-barrier pipeline).
   // ECC_B200_F3=value selects the value-order kernel, =branch a branch
-  // around each reduction, =cta the CTA-barrier pipeline (A/B checks)
+  // around each reduction, =cta the CTA-barrier pipeline, =no2d the 3-D kernel
+  // for single planes (A/B checks)
   const int mode = [] {   // read per launch so tests can switch kernels in-process
     const char* e = getenv("ECC_B200_F3");
     if (!e) return 0;
@@ -1281,6 +1508,7 @@ int fast3d_launch(const float* x, int64_t D, int64_t H, int64_t W, int64_t batch
     if (!strcmp(e, "branch")) return 2;
     if (!strcmp(e, "cta")) return 3;
     if (!strcmp(e, "rank2")) return 4;
+    if (!strcmp(e, "no2d")) return 5;
     return 0;
   }();
   const bool use_bin = b->lut_ok && cells <= 16382 && mode != 1;
@@ -1302,6 +1530,10 @@ int fast3d_launch(const float* x, int64_t D, int64_t H, int64_t W, int64_t batch
            (size_t)((nb + 1 + 3) & ~3) * 4 + (size_t)(b->lut_ok ? 0 : nb + 2) * 4;
     kfn = (const void*)ecc_fast3d_kernel;
   }
+  if (use_bin && D == 1 && mode != 3 && mode != 5)   // single planes: the 2-D tile pipeline
+    return launch_2d(map, edge ? (const void*)ecc_fast2d_rank_kernel<true, false>
+                               : (const void*)ecc_fast2d_rank_kernel<false, false>,
+                     smem, W, H, batch, table, nb, cells, hsize, b->lut_scale, b->lut_bias, hist, stream);
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(fast3d)");
   int occ = 0;
@@ -1366,6 +1598,9 @@ int fast3d_u8_launch(const uint8_t* x, int64_t D, int64_t H, int64_t W, int64_t 
   const size_t smem = (size_t)U8_PLANE_BYTES + (size_t)2 * BPLANE * 4 + 16 + 4 * 4 + (size_t)hsize * 4;
   const void* kfn = cta ? (const void*)ecc_fast3d_bin_kernel<1, false, false, true>
                         : (const void*)ecc_fast3d_bin_kernel<1, true, false, true>;
+  if (D == 1 && !cta && !(env && !strcmp(env, "no2d")))
+    return launch_2d(map, (const void*)ecc_fast2d_rank_kernel<false, true>, smem, W, H, batch, table, nb, 0, hsize,
+                     0.f, 0.f, hist, stream);
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(fast3d u8)");
   int occ = 0;

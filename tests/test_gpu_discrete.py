@@ -223,7 +223,7 @@ class TestFastPath:
               (17, 90, 260), (64, 31, 4), (1, 1, 64), (40, 1, 40), (65, 47, 68)]
 
     KERNELS = {"bin": {}, "value": {"ECC_B200_F3": "value"}, "branch": {"ECC_B200_F3": "branch"},
-               "cta": {"ECC_B200_F3": "cta"}, "rank2": {"ECC_B200_F3": "rank2"},
+               "cta": {"ECC_B200_F3": "cta"}, "rank2": {"ECC_B200_F3": "rank2"}, "no2d": {"ECC_B200_F3": "no2d"},
                "generic": {"ECC_B200_GENERIC": "1"}}
 
     @classmethod
@@ -246,7 +246,7 @@ class TestFastPath:
     @classmethod
     def _both(cls, t, ts, **kw):
         out = cls._all(t, ts, **kw)
-        for name in ("value", "branch", "cta", "rank2"):
+        for name in ("value", "branch", "cta", "rank2", "no2d"):
             assert np.array_equal(out[name], out["bin"]), name
         return out["bin"], out["generic"]
 
@@ -439,3 +439,29 @@ class TestFastPathU8:
         h = E.histogram_device(torch.from_numpy(xs).cuda(), ts, ndim=3).cpu().numpy()
         for i in range(3):
             assert np.array_equal(h[i], np.append(*oracle.histogram(xs[i].astype(np.float64), ts.taus)))
+
+
+class TestFastPath2DTiles:
+    """2-D grids and D == 1 volumes take the 2-D tile pipeline (float32 and uint8)."""
+
+    @pytest.mark.parametrize("hw", [(4, 16), (30, 128), (31, 132), (61, 260), (200, 48), (1, 64)])
+    def test_2d_batches(self, rng, hw):
+        xs = rng.random((5,) + hw).astype(np.float32)
+        t = torch.from_numpy(xs).cuda()
+        for nb in (7, 256, 1024):
+            ts = E.thresholds_from_range(float(xs.min()), float(xs.max()), nb)
+            out = TestFastPath._all(t, ts, ndim=2)
+            for i in range(5):
+                want = np.append(*oracle.histogram(xs[i], ts.taus))
+                for name, h in out.items():
+                    assert np.array_equal(h[i], want), (hw, nb, name, i)
+
+    def test_2d_u8(self, rng):
+        xs = rng.integers(0, 256, (4, 70, 128), dtype=np.uint8)
+        t = torch.from_numpy(xs).cuda()
+        ts = E.ThresholdSet(np.arange(0.0, 256.0, 3.0))
+        out = TestFastPath._all(t, ts, ndim=2)
+        for i in range(4):
+            want = np.append(*oracle.histogram(xs[i].astype(np.float64), ts.taus))
+            for name, h in out.items():
+                assert np.array_equal(h[i], want), (name, i)
