@@ -181,9 +181,12 @@ def run_b200(args):
     from paper_2510_20271_b200 import distributed as D
 
     world, rank, local = _dist_env()
+    # ECC_BENCH_FORCE_DIST=1 runs the multi-GPU code path (NCCL, halo exchange,
+    # all-reduces) even with one rank: a one-GPU check of the N > 1 plumbing
+    dist_on = world > 1 or os.environ.get("ECC_BENCH_FORCE_DIST") == "1"
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    if dist_on:
         dist.init_process_group("nccl", device_id=dev)
     L = _lib.lib()
     stream = torch.cuda.current_stream(dev)
@@ -199,7 +202,7 @@ def run_b200(args):
     torch.cuda.synchronize()
     for _ in range(2):  # second call timed (first pays lazy init)
         t0 = time.perf_counter()
-        if world > 1:
+        if dist_on:
             lo, hi = D.global_range(own)
         else:
             lo, hi, _ = E.device_minmax(own)
@@ -209,14 +212,14 @@ def run_b200(args):
     table, binning = taus.device_table(_lib.DTYPE_F32, dev)
     hist = torch.empty(NB + 1, dtype=torch.int64, device=dev)
     curve = torch.empty(NB, dtype=torch.int64, device=dev)
-    view, z0, z1 = (own, 0, P) if world == 1 else D.slab_view(padded)
+    view, z0, z1 = (own, 0, P) if not dist_on else D.slab_view(padded)
     dims = _lib.dims_arg(view.shape)
     kstart = torch.cuda.Event(enable_timing=True)
     kend = torch.cuda.Event(enable_timing=True)
     kernel_ms = []
 
     def step(record=False):
-        if world > 1:
+        if dist_on:
             D.exchange_halos(padded)
         if record:
             kstart.record(stream)
@@ -225,7 +228,7 @@ def run_b200(args):
                                          _lib.ctypes.c_void_p(stream.cuda_stream)))
         if record:
             kend.record(stream)
-        if world > 1:
+        if dist_on:
             dist.all_reduce(hist)
         _lib.check(L.ecc_scan(_lib.ptr(hist), 1, NB, _lib.ptr(curve), _lib.ctypes.c_void_p(stream.cuda_stream)))
 
@@ -238,7 +241,7 @@ def run_b200(args):
     checksum = int(np.bitwise_xor.reduce(c.view(np.uint64)))
 
     def barrier():
-        if world > 1:
+        if dist_on:
             dist.barrier(device_ids=[local])
         torch.cuda.synchronize()
 
@@ -259,7 +262,7 @@ def run_b200(args):
         step(record=True)
         kend.synchronize()
         kernel_ms.append(kstart.elapsed_time(kend))
-    if world > 1:
+    if dist_on:
         t = torch.tensor([total_ms, statistics.mean(kernel_ms)], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms, kmean = float(t[0]), float(t[1])
@@ -288,7 +291,7 @@ def run_b200(args):
         # which adds the halo exchange and the histogram all-reduce)
         host = torch.empty((P, H, W), dtype=torch.float32, pin_memory=True)
         host.copy_(own.cpu())
-        if world == 1:
+        if not dist_on:
             def e2e_step():
                 return E.ecc_discrete_host(host, taus, chunk_planes=256).cpu()
             api = ("paper_2510_20271_b200.ecc_discrete_host (256-plane chunks: the host->device copy of one "
@@ -312,7 +315,7 @@ def run_b200(args):
             e2e_step()
         barrier()
         e_ms = (time.perf_counter() - t0) * 1e3 / reps
-        if world > 1:
+        if dist_on:
             t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t[0])
@@ -329,7 +332,7 @@ def run_b200(args):
     # --- soft ECC C3 (forward + backward) -------------------------------------
     soft = None
     if not args.no_soft:
-        soft = bench_soft(args, dev, world, rank)
+        soft = bench_soft(args, dev, world, rank, dist_on)
 
     # --- CPU baseline (rank 0, N = 1) ----------------------------------------
     cpu = None
@@ -343,7 +346,7 @@ def run_b200(args):
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": "C2: 3D 512^3 float32 volume, discrete ECC, 1024 uniform thresholds"
-                       + (" (z-slab per GPU, halo exchange + NCCL histogram all-reduce)" if world > 1 else ""),
+                       + (" (z-slab per GPU, halo exchange + NCCL histogram all-reduce)" if dist_on else ""),
                        "volume": [P * world, H, W], "bins": NB, "parallelism": f"zslab{world}",
                        "l2": "input larger than L2 (512 MiB per GPU), no flush",
                        "thresholds": "given (uniform over the device min/max, computed once)",
@@ -360,7 +363,7 @@ def run_b200(args):
             "soft": soft,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist_on:
         dist.destroy_process_group()
 
 
@@ -403,7 +406,7 @@ def bench_ns(args, dev):
     return out
 
 
-def bench_soft(args, dev, world, rank):
+def bench_soft(args, dev, world, rank, dist_on=False):
     import torch
 
     import paper_2510_20271_b200 as E
@@ -423,7 +426,7 @@ def bench_soft(args, dev, world, rank):
         m.zero_grad(set_to_none=True)
         chi = m(x)
         chi.backward(up)
-        if world > 1:
+        if dist_on:
             from paper_2510_20271_b200 import distributed as D
 
             D.allreduce_soft_grads(m)
@@ -439,7 +442,7 @@ def bench_soft(args, dev, world, rank):
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
-    if world > 1:
+    if dist_on:
         import torch.distributed as dist
 
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
