@@ -8,12 +8,14 @@ current CUDA stream.
 from __future__ import annotations
 
 import ctypes
+import os
 from pathlib import Path
 
 import numpy as np
 import torch
 
-_LIB_PATH = Path(__file__).resolve().parent / "libecc_b200.so"
+# ECC_B200_LIB: an alternative in-tree build (kernel A/B experiments under tools/)
+_LIB_PATH = Path(os.environ.get("ECC_B200_LIB") or Path(__file__).resolve().parent / "libecc_b200.so")
 _lib = None
 
 ECC_OK = 0

@@ -682,17 +682,34 @@ __device__ __forceinline__ uint32_t qword(const BRow& R, int j) {
 }
 // bit-sliced word of [q <= p] for the 32 voxels, q = row R moved by DX;
 // PP[j] = own word j | 0x80008000
+#ifndef ECC_F3_PACK
+#define ECC_F3_PACK 0   // 1: sign bytes merged on the FMA pipe (IMAD Horner chain + 255^-1);
+                        // measured slower (1024^3: 560 vs 583 Gvoxel/s): the kernel is
+                        // issue-bound, and the chain adds one instruction per word
+#endif
 template <int DX>
-__device__ __forceinline__ uint32_t cmp_word(const uint32_t (&PP)[16], const BRow& R) {
+__device__ __forceinline__ uint32_t cmp_word(const uint32_t (&PP)[16], const BRow& R, uint32_t two) {
   uint32_t d[16];
 #pragma unroll
   for (int j = 0; j < 16; ++j) d[j] = PP[j] - qword<DX>(R, j);
   // byte a of m[k] = prmt(d[k], d[k+8]) = sign of voxel 8a + k, spread over
-  // the byte; a three-level select tree (7 LOP3, depth 3) puts bit k of every
-  // byte from m[k]: select(0x55) pairs, select(0x33) quads, select(0x0F) octets
+  // the byte (0x00 or 0xFF)
   uint32_t m[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) m[k] = prmt(d[k], d[k + 8], 0xFBD9u);
+  if (ECC_F3_PACK) {
+    // sum_k m[k] 2^k = 255 V (mod 2^32), V = the wanted word (byte a, bit k =
+    // voxel 8a + k; the byte sums stay below 256 so nothing carries), and 255
+    // is odd: V = (sum_k m[k] 2^k) * 255^-1 mod 2^32.  Eight IMADs (FMA pipe,
+    // full rate; `two` is a run-time 2 so ptxas keeps them as IMADs) instead
+    // of seven half-rate LOP3s.
+    uint32_t acc = m[7];
+#pragma unroll
+    for (int k = 6; k >= 0; --k) acc = mad_fma(acc, two, m[k]);
+    return acc * 0xFEFEFEFFu;
+  }
+  // a three-level select tree (7 LOP3, depth 3) puts bit k of every byte
+  // from m[k]: select(0x55) pairs, select(0x33) quads, select(0x0F) octets
   const uint32_t m01 = (m[0] & 0x55555555u) | (m[1] & 0xAAAAAAAAu);
   const uint32_t m23 = (m[2] & 0x55555555u) | (m[3] & 0xAAAAAAAAu);
   const uint32_t m45 = (m[4] & 0x55555555u) | (m[5] & 0xAAAAAAAAu);
@@ -898,6 +915,7 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
   const int nranks = U8 ? 256 : EDGE ? cells + 2 : 2 * (cells + 1);
   const uint32_t dummy_off = (uint32_t)(nranks + lane);   // dummy counter index (< 2^15)
   const uint32_t one = (uint32_t)g.one;
+  const uint32_t two = one << 1;
   const uint32_t hbase = smem_u32(s_hist);
   // fold the rank counters (16 c per voxel) into the global bins: rank v is
   // bin b(v / 2) + v % 2; runs of ranks with the same bin are summed first
@@ -1068,25 +1086,25 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
 #pragma unroll
         for (int j = 0; j < 16; ++j)   // | == + (bits 15, 31 clear)
           PP[j] = ECC_F3_FMA_PP ? mad_fma(A.w[j], one, 0x80008000u) : (A.w[j] | 0x80008000u);
-        N0[NX] = cmp_word<-1>(PP, A);
+        N0[NX] = cmp_word<-1>(PP, A, two);
         eA = A.e;
         load_brow(A, B1, rm, warp);
-        N0[NYM_XM] = cmp_word<-1>(PP, B);
-        N0[NYM_X0] = cmp_word<0>(PP, B);
-        N0[NYM_XP] = cmp_word<1>(PP, B);
+        N0[NYM_XM] = cmp_word<-1>(PP, B, two);
+        N0[NYM_X0] = cmp_word<0>(PP, B, two);
+        N0[NYM_XP] = cmp_word<1>(PP, B, two);
         eB = B.e;
         load_brow(B, B1, rp, warp);
-        N0[NZ_YM_XM] = cmp_word<-1>(PP, A);
-        N0[NZ_YM_X0] = cmp_word<0>(PP, A);
-        N0[NZ_YM_XP] = cmp_word<1>(PP, A);
+        N0[NZ_YM_XM] = cmp_word<-1>(PP, A, two);
+        N0[NZ_YM_X0] = cmp_word<0>(PP, A, two);
+        N0[NZ_YM_XP] = cmp_word<1>(PP, A, two);
         load_brow(Ro, B1, lane, warp);
-        N0[NZ_YP_XM] = cmp_word<-1>(PP, B);
-        N0[NZ_YP_X0] = cmp_word<0>(PP, B);
-        N0[NZ_YP_XP] = cmp_word<1>(PP, B);
+        N0[NZ_YP_XM] = cmp_word<-1>(PP, B, two);
+        N0[NZ_YP_X0] = cmp_word<0>(PP, B, two);
+        N0[NZ_YP_XP] = cmp_word<1>(PP, B, two);
         eP = B.e;
-        N0[NZ_Y0_XM] = cmp_word<-1>(PP, Ro);
-        N0[NZ_Y0_X0] = cmp_word<0>(PP, Ro);
-        N0[NZ_Y0_XP] = cmp_word<1>(PP, Ro);
+        N0[NZ_Y0_XM] = cmp_word<-1>(PP, Ro, two);
+        N0[NZ_Y0_X0] = cmp_word<0>(PP, Ro, two);
+        N0[NZ_Y0_XP] = cmp_word<1>(PP, Ro, two);
       }
 
       // plane s - 1's bin plane is no longer read: bin plane s + 1 into it
@@ -1262,6 +1280,7 @@ ecc_fast2d_rank_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const v
   const int nranks = U8 ? 256 : EDGE ? cells + 2 : 2 * (cells + 1);
   const uint32_t dummy_off = (uint32_t)(nranks + lane);
   const uint32_t one = (uint32_t)g.one;
+  const uint32_t two = one << 1;
   const uint32_t hbase = smem_u32(s_hist);
   auto flush = [&](int64_t item) {
     unsigned long long* h = hist + item * (nb + 1);
@@ -1360,8 +1379,8 @@ ecc_fast2d_rank_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const v
     uint32_t PP[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) PP[j] = mad_fma(A.w[j], one, 0x80008000u);
-    const uint32_t nx = cmp_word<-1>(PP, A);
-    const uint32_t nym_m = cmp_word<-1>(PP, Bm), nym_0 = cmp_word<0>(PP, Bm), nym_p = cmp_word<1>(PP, Bm);
+    const uint32_t nx = cmp_word<-1>(PP, A, two);
+    const uint32_t nym_m = cmp_word<-1>(PP, Bm, two), nym_0 = cmp_word<0>(PP, Bm, two), nym_p = cmp_word<1>(PP, Bm, two);
     // row y + 1: its (0, -1, dx) words and its edge word
     const uint32_t u_m = __shfl_down_sync(FULL, nym_m, 1);
     const uint32_t u_0 = __shfl_down_sync(FULL, nym_0, 1);
