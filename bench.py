@@ -334,6 +334,10 @@ def run_b200(args):
     if not args.no_soft:
         soft = bench_soft(args, dev, world, rank, dist_on)
 
+    # --- C5 per-GPU slab and C4 (one 1024^3 soft item per GPU) -----------------
+    c5 = None if args.no_c5 else bench_c5_slab(args, dev, world, rank, dist_on)
+    c4 = None if args.no_soft or args.no_c4 else bench_c4(args, dev, world, rank, dist_on)
+
     # --- CPU baseline (rank 0, N = 1) ----------------------------------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -361,6 +365,8 @@ def run_b200(args):
             "clocks": clocks.summary(),
             "north_star": ns,
             "soft": soft,
+            "c4": c4,
+            "c5_slab": c5,
         }
         print(json.dumps(line), flush=True)
     if dist_on:
@@ -402,6 +408,130 @@ def bench_ns(args, dev):
            "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
                         "peak_source": peak_kind}}
     del x
+    torch.cuda.empty_cache()
+    return out
+
+
+def bench_c5_slab(args, dev, world, rank, dist_on=False):
+    """One GPU's share of C5 (3D 2048^3 float32, z-slabs over 8 GPUs): a
+    256 x 2048 x 2048 slab (4 GiB) of the counter-generated C5 volume (the
+    planes rank r would own in an 8-way split, r = this rank mod 8) plus its
+    two halo planes, swept by the fused kernel over its own planes
+    (ecc_histogram_range, the per-rank kernel of distributed.slab_histogram).
+    Thresholds: 1024 uniform over [0, 1) edges of the generator's range.
+    The halo exchange and the 8 KiB histogram all-reduce are timed by the
+    multi-GPU C2 line; here the slab kernel alone, CUDA events."""
+    import torch
+
+    import paper_2510_20271_b200 as E
+    from paper_2510_20271_b200 import _lib
+    from paper_2510_20271_b200 import distributed as D
+
+    L = _lib.lib()
+    P, H, W = 256, 2048, 2048
+    part = rank % 8
+    padded = D.alloc_padded_slab(P, (H, W), torch.float32, dev)
+    z0 = part * P
+    lo_plane = max(z0 - 1, 0)
+    hi_plane = min(z0 + P + 1, 8 * P)
+    first = 1 - (z0 - lo_plane)
+    view = padded[first:first + (hi_plane - lo_plane)]
+    _lib.check(L.ecc_counter_grid(SEED + 2, lo_plane * H * W, view.numel(), _lib.ptr(view), _lib.stream_ptr(view)))
+    taus = E.thresholds_from_range(0.0, 1.0 - 2.0 ** -24, NB)
+    table, binning = taus.device_table(_lib.DTYPE_F32, dev)
+    hist = torch.zeros(NB + 1, dtype=torch.int64, device=dev)
+    zlo, zhi = z0 - lo_plane, z0 - lo_plane + P
+    dims = _lib.dims_arg(view.shape)
+    stream = torch.cuda.current_stream(dev)
+
+    def run():
+        _lib.check(L.ecc_histogram_range(_lib.ptr(view), _lib.DTYPE_F32, 3, _lib.ptr(dims), 1, zlo, zhi,
+                                         _lib.ptr(table), _lib.ctypes.byref(binning), _lib.ptr(hist),
+                                         _lib.ctypes.c_void_p(stream.cuda_stream)))
+
+    run()
+    torch.cuda.synchronize()
+    for _ in range(2):
+        run()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    steps = max(3, min(args.steps, 10))
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(steps):
+        run()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    if dist_on:
+        import torch.distributed as dist
+
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t[0])
+    peak, peak_kind = _peaks()
+    vox = P * H * W
+    gbs = 4.0 * vox / (ms * 1e-3) / 1e9
+    out = {"workload": "C5 per-GPU slab: planes [%d, %d) of the 2048^3 float32 counter volume (+ halos), "
+                       "1024 thresholds, fused slab kernel (ecc_histogram_range)" % (z0, z0 + P),
+           "value": vox * world / (ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": ms, "steps": steps,
+           "n_gpus": world, "scaling": "weak",
+           "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
+                        "peak_source": peak_kind}}
+    del padded, view
+    torch.cuda.empty_cache()
+    return out
+
+
+def bench_c4(args, dev, world, rank, dist_on=False):
+    """C4: 3D 1024^3 float32 soft ECC, forward + backward, learnable tau / v /
+    alpha, batch-sharded (one item per GPU), B = 256, lambda = 50, alpha =
+    0.3, u = normalize(1, 2, -0.5); the shared parameters'
+    gradients are all-reduced under torchrun (distributed.allreduce_soft_grads)."""
+    import torch
+
+    import paper_2510_20271_b200 as E
+
+    n, B, lam, alpha = 1024, 256, 50.0, 0.3
+    g = torch.Generator(device=dev)
+    g.manual_seed(SEED + 100 + rank)
+    x = torch.rand((1, n, n, n), device=dev, generator=g, dtype=torch.float32)
+    v = np.array([1.0, 2.0, -0.5])
+    u = v / np.linalg.norm(v)
+    span = alpha * np.abs(u).sum()
+    m = E.SoftECC(np.linspace(-span, 1.0 + span, B + 1)[1:], v, alpha=alpha, lam=lam).to(dev)
+    up = torch.ones((1, B), dtype=torch.float64, device=dev)
+
+    def step():
+        m.zero_grad(set_to_none=True)
+        m(x).backward(up)
+        if dist_on:
+            from paper_2510_20271_b200 import distributed as D
+
+            D.allreduce_soft_grads(m)
+
+    step()
+    torch.cuda.synchronize()
+    steps = 2
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    if dist_on:
+        import torch.distributed as dist
+
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t[0])
+    assert bool(torch.isfinite(m.taus.grad).all()), "non-finite d_tau at C4"
+    vox = n ** 3 * world
+    out = {"workload": "C4: 3D 1024^3 float32 soft ECC fwd+bwd, learnable tau/u/alpha, one item per GPU",
+           "value": vox / (ms * 1e-3), "unit": "voxel/s", "ms_per_step": ms, "steps": steps,
+           "n_gpus": world, "bins": B, "lambda": lam, "alpha": alpha, "parallelism": f"batch{world}",
+           "algorithmic_pairs_per_s": 2 * vox * B / (ms * 1e-3)}
+    del x, m
     torch.cuda.empty_cache()
     return out
 
@@ -486,6 +616,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-ns", action="store_true", help="skip the 1024^3 north-star measurement")
+    ap.add_argument("--no-c4", action="store_true", help="skip the 1024^3 soft (C4) measurement")
+    ap.add_argument("--no-c5", action="store_true", help="skip the C5 per-GPU slab measurement")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
