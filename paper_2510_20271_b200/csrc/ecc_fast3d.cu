@@ -684,8 +684,8 @@ __device__ __forceinline__ uint32_t qword(const BRow& R, int j) {
 // PP[j] = own word j | 0x80008000
 #ifndef ECC_F3_PACK
 #define ECC_F3_PACK 0   // 1: sign bytes merged on the FMA pipe (IMAD Horner chain + 255^-1);
-                        // measured slower (1024^3: 560 vs 583 Gvoxel/s): the kernel is
-                        // issue-bound, and the chain adds one instruction per word
+                        // measured slower (1024^3: 561 vs 582 Gvoxel/s, Horner chain or
+                        // balanced tree): IMAD does not relieve the ALU pipe here
 #endif
 template <int DX>
 __device__ __forceinline__ uint32_t cmp_word(const uint32_t (&PP)[16], const BRow& R, uint32_t two) {
@@ -703,10 +703,12 @@ __device__ __forceinline__ uint32_t cmp_word(const uint32_t (&PP)[16], const BRo
     // is odd: V = (sum_k m[k] 2^k) * 255^-1 mod 2^32.  Eight IMADs (FMA pipe,
     // full rate; `two` is a run-time 2 so ptxas keeps them as IMADs) instead
     // of seven half-rate LOP3s.
-    uint32_t acc = m[7];
-#pragma unroll
-    for (int k = 6; k >= 0; --k) acc = mad_fma(acc, two, m[k]);
-    return acc * 0xFEFEFEFFu;
+    // balanced tree (depth 4) of IMADs with run-time multipliers 2, 4, 16
+    const uint32_t four = two << 1, sixteen = two << 3;
+    const uint32_t a01 = mad_fma(m[1], two, m[0]), a23 = mad_fma(m[3], two, m[2]);
+    const uint32_t a45 = mad_fma(m[5], two, m[4]), a67 = mad_fma(m[7], two, m[6]);
+    const uint32_t a03 = mad_fma(a23, four, a01), a47 = mad_fma(a67, four, a45);
+    return mad_fma(a47, sixteen, a03) * 0xFEFEFEFFu;
   }
   // a three-level select tree (7 LOP3, depth 3) puts bit k of every byte
   // from m[k]: select(0x55) pairs, select(0x33) quads, select(0x0F) octets
