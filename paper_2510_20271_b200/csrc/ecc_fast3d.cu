@@ -879,7 +879,8 @@ __device__ __forceinline__ void bin_plane(const float* stage, uint32_t* B, bool 
 }
 
 #ifndef ECC_F3_MINB
-#define ECC_F3_MINB 4   // resident CTAs per SM the register budget is sized for
+#define ECC_F3_MINB 5   // resident CTAs per SM the register budget is sized for (96 registers;
+                          // 5 x 44.7 KB shared fits too): 1024^3 591 vs 583 Gvoxel/s at 4
 #endif
 template <int DEP, bool WS, bool EDGE, bool U8 = false>
 __global__ void __launch_bounds__(NT, ECC_F3_MINB)

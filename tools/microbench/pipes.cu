@@ -108,6 +108,72 @@ __global__ void k_mix_alu_fma(float* o, float a, float b, int n) {
   if (s == 12345u) o[0] = 1.f;
 }
 
+__global__ void k_imad(float* o, float a, float b, int n) {
+  unsigned c[8];
+  unsigned m = __float_as_uint(a), q = __float_as_uint(b);
+  for (int i = 0; i < 8; ++i) c[i] = threadIdx.x * 7 + i;
+  for (int it = 0; it < n; ++it)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(c[i]) : "r"(m), "r"(q));
+  unsigned s = 0; for (int i = 0; i < 8; ++i) s += c[i];
+  if (s == 12345u) o[0] = 1.f;
+}
+__global__ void k_imadhi(float* o, float a, float b, int n) {
+  unsigned c[8];
+  unsigned m = __float_as_uint(a), q = __float_as_uint(b);
+  for (int i = 0; i < 8; ++i) c[i] = threadIdx.x * 7 + i;
+  for (int it = 0; it < n; ++it)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) asm volatile("mad.hi.u32 %0, %0, %1, %2;" : "+r"(c[i]) : "r"(m), "r"(q));
+  unsigned s = 0; for (int i = 0; i < 8; ++i) s += c[i];
+  if (s == 12345u) o[0] = 1.f;
+}
+// 4 lop3 + 4 imad per iteration (8 ops)
+__global__ void k_lop3_imad(float* o, float a, float b, int n) {
+  unsigned c[8];
+  unsigned m = __float_as_uint(a), q = __float_as_uint(b);
+  for (int i = 0; i < 8; ++i) c[i] = threadIdx.x * 7 + i;
+  for (int it = 0; it < n; ++it)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(c[i]) : "r"(m), "r"(q));
+      asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(c[i + 4]) : "r"(m), "r"(q));
+    }
+  unsigned s = 0; for (int i = 0; i < 8; ++i) s += c[i];
+  if (s == 12345u) o[0] = 1.f;
+}
+// 4 lop3 + 4 ffma per iteration (8 ops)
+__global__ void k_lop3_ffma(float* o, float a, float b, int n) {
+  unsigned c[4];
+  float f[4];
+  unsigned m = __float_as_uint(a), q = __float_as_uint(b);
+  for (int i = 0; i < 4; ++i) { c[i] = threadIdx.x * 7 + i; f[i] = threadIdx.x * 1e-3f + i; }
+  for (int it = 0; it < n; ++it)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(c[i]) : "r"(m), "r"(q));
+      asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+f"(f[i]) : "f"(a), "f"(b));
+    }
+  unsigned s = 0; for (int i = 0; i < 4; ++i) s += c[i] + __float_as_uint(f[i]);
+  if (s == 12345u) o[0] = 1.f;
+}
+// 2 lop3 + 1 prmt + 1 imad (the compare mix)
+__global__ void k_cmpmix(float* o, float a, float b, int n) {
+  unsigned c[8];
+  unsigned m = __float_as_uint(a), q = __float_as_uint(b);
+  for (int i = 0; i < 8; ++i) c[i] = threadIdx.x * 7 + i;
+  for (int it = 0; it < n; ++it)
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(c[i]) : "r"(m), "r"(q));
+      asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(c[i + 2]) : "r"(m), "r"(q));
+      asm volatile("prmt.b32 %0, %0, %1, 0x1234;" : "+r"(c[i + 4]) : "r"(m));
+      asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(c[i + 6]) : "r"(m), "r"(q));
+    }
+  unsigned s = 0; for (int i = 0; i < 8; ++i) s += c[i];
+  if (s == 12345u) o[0] = 1.f;
+}
+
 template <typename K>
 int run(const char* name, K kern, double ops_per_iter_thread) {
   float* o; CK(cudaMalloc(&o, 4));
@@ -135,6 +201,11 @@ int main() {
   run("lop3", k_lop3, 8);
   run("prmt", k_prmt, 8);
   run("sub.u32", k_iadd, 8);
-  run("lop3+sub", k_mix_alu_fma, 4);   // per-iteration ops: 4 lop3 + 4 sub -> counted as 4
+  run("lop3+sub", k_mix_alu_fma, 8);   // 4 lop3 + 4 sub per iteration
+  run("imad", k_imad, 8);
+  run("imad.hi", k_imadhi, 8);
+  run("lop3+imad", k_lop3_imad, 8);
+  run("lop3+ffma", k_lop3_ffma, 8);
+  run("cmpmix", k_cmpmix, 8);          // 4 lop3 + 2 prmt + 2 imad
   return 0;
 }
