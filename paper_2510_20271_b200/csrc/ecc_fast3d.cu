@@ -29,6 +29,8 @@
 // out-of-bounds fill) into a 3-stage shared-memory ring guarded by
 // mbarriers; one thread issues, all threads wait on the stage's parity.
 #include <cuda.h>
+#include <atomic>
+#include <algorithm>
 #include <cudaTypedefs.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -56,6 +58,8 @@ struct Geom {
   int one;             // 1 at run time: multipliers built from it keep shifts/adds on the FMA pipe
   int zb, ze;          // deposit planes [zb, ze)
   int64_t items;
+  unsigned int* wq = nullptr;   // dynamic work queue (rank kernel): next unit, zeroed before the launch
+  int zunit = 0;                // planes per dynamic unit (0: static partition)
 };
 
 struct LutEntry {
@@ -985,12 +989,35 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
     u_end = T * Dw * (bx + 1) / G;
   }
   int64_t pending = 0;
+  // dynamic mode (g.zunit > 0): units of zunit planes of one tile, z-chunk
+  // major (CTAs working at the same time sit on neighbouring tiles at the same
+  // depth), handed out by one global counter.  The warp scheduler favours the
+  // oldest CTAs of an SM, so equal static shares finish staggered (measured:
+  // 0.53 ... 1.0 of the kernel time) and the SM runs its tail with one or two
+  // CTAs; with a queue the faster CTAs take more units and all finish together.
+  const int64_t nzc = g.zunit > 0 ? (Dw + g.zunit - 1) / g.zunit : 0;
+  const int64_t nunits = nzc * T;
+  unsigned int* s_unit = reinterpret_cast<unsigned int*>(s_rounds + 1);
+  if (g.zunit > 0) { u = 0; u_end = 1; }
   while (u < u_end) {
-    const int64_t tile = u / L;
-    const int64_t zr = u - tile * L;
-    const int64_t seg = min(L - zr, u_end - u);
-    const int64_t z0 = zbase + zr;
-    u += seg;
+    int64_t tile, seg, z0;
+    if (g.zunit > 0) {
+      __syncthreads();   // everyone is done with the previous unit's s_unit
+      if (threadIdx.x == 0) *s_unit = atomicAdd(g.wq, 1u);
+      __syncthreads();
+      const int64_t un = *s_unit;
+      if (un >= nunits) break;
+      const int64_t zc = un / T;
+      tile = un - zc * T;
+      z0 = zc * g.zunit;
+      seg = min((int64_t)g.zunit, Dw - z0);
+    } else {
+      tile = u / L;
+      const int64_t zr = u - tile * L;
+      seg = min(L - zr, u_end - u);
+      z0 = zbase + zr;
+      u += seg;
+    }
     int64_t rr = tile;
     const int tx = (int)(rr % g.tiles_x); rr /= g.tiles_x;
     const int ty = (int)(rr % g.tiles_y); rr /= g.tiles_y;
@@ -1470,6 +1497,46 @@ bool fast3d_eligible(const void* x, int64_t D, int64_t H, int64_t W, int64_t bat
 }
 
 // 2-D tile pipeline (ecc_fast2d_rank_kernel): contiguous tile ranges per CTA
+#ifndef ECC_F3_DYN
+#define ECC_F3_DYN 48   // largest dynamic work unit in planes (0: static partition only)
+#endif
+// Work-queue counters of the rank kernel: a ring of slots so launches on
+// different streams never share one; each launch zeroes its slot on its own
+// stream first.
+__device__ unsigned int g_f3_wq[64];
+static unsigned int* work_slot(cudaStream_t stream) {
+  static unsigned int* base = nullptr;
+  static std::atomic<unsigned> seq{0};
+  if (!base) {
+    void* p = nullptr;
+    cudaError_t e = cudaGetSymbolAddress(&p, g_f3_wq);
+    if (e != cudaSuccess) { set_cuda_error(e, "cudaGetSymbolAddress(work queue)"); return nullptr; }
+    base = static_cast<unsigned int*>(p);
+  }
+  unsigned int* slot = base + (seq.fetch_add(1) % 64);
+  cudaError_t e = cudaMemsetAsync(slot, 0, sizeof(unsigned int), stream);
+  if (e != cudaSuccess) { set_cuda_error(e, "cudaMemsetAsync(work queue)"); return nullptr; }
+  return slot;
+}
+
+// Dynamic schedule of the rank kernel: units of P/4 planes (P = planes per
+// CTA), 24..48 -- large enough that the per-unit restart (halo plane,
+// pipeline fill) stays small, and enough of them to even out the CTAs'
+// speeds.  Below P = 96 the static partition measured as fast or faster
+// (512^3 f32: P = 50).  Returns nonzero on a CUDA error.
+static int set_dynamic(fast::Geom& g, int64_t total, int64_t grid, int64_t depth, cudaStream_t stream) {
+  g.wq = nullptr;
+  g.zunit = 0;
+  if (!ECC_F3_DYN) return 0;
+  const int64_t P = total / grid;
+  int z = P >= 96 ? (int)std::min<int64_t>(ECC_F3_DYN, std::max<int64_t>(24, (P / 4) & ~7)) : 0;
+  if (const char* zu = getenv("ECC_B200_F3_ZUNIT")) z = atoi(zu);   // A/B experiments
+  if (z <= 0 || z >= depth) return 0;
+  if (!(g.wq = work_slot(stream))) return 1;
+  g.zunit = z;
+  return 0;
+}
+
 static int launch_2d(const CUtensorMap& map, const void* kfn, size_t smem, int64_t W, int64_t H, int64_t batch,
                      const void* table, int nb, int cells, int hsize, float scale, float bias,
                      unsigned long long* hist, cudaStream_t stream) {
@@ -1575,12 +1642,15 @@ int fast3d_launch(const float* x, int64_t D, int64_t H, int64_t W, int64_t batch
   g.zc = 0;
   g.one = 1;
   g.items = tiles;   // the kernel splits tiles x planes evenly over the grid
+  g.wq = nullptr;
+  g.zunit = 0;
   const int64_t total = tiles * (ze - zb);
   const int64_t grid = total < max_ctas ? total : max_ctas;
   // z-aligned partition when every tile gets at least one CTA (see kernel)
   g.zchunks = (tiles <= grid && grid <= tiles * (ze - zb)) ? (int)(grid / tiles) : 0;
   if (grid < 1) return ECC_OK;
   if (use_bin) {
+    if (mode != 3 && mode != 2 && set_dynamic(g, total, grid, ze - zb, stream)) return ECC_ECUDA;
     using KFn = void (*)(const CUtensorMap, Geom, const void*, int, int, int, float, float, unsigned long long*);
     KFn k = reinterpret_cast<KFn>(const_cast<void*>(kfn));
     k<<<(unsigned)grid, NT, smem, stream>>>(map, g, table, nb, cells, hsize, b->lut_scale, b->lut_bias, hist);
@@ -1645,6 +1715,7 @@ int fast3d_u8_launch(const uint8_t* x, int64_t D, int64_t H, int64_t W, int64_t 
   const int64_t grid = total < max_ctas ? total : max_ctas;
   g.zchunks = (tiles <= grid && grid <= tiles * (ze - zb)) ? (int)(grid / tiles) : 0;
   if (grid < 1) return ECC_OK;
+  if (set_dynamic(g, total, grid, ze - zb, stream)) return ECC_ECUDA;
   using KFn = void (*)(const CUtensorMap, Geom, const void*, int, int, int, float, float, unsigned long long*);
   KFn k = reinterpret_cast<KFn>(const_cast<void*>(kfn));
   k<<<(unsigned)grid, NT, smem, stream>>>(map, g, table, nb, 0, hsize, 0.f, 0.f, hist);

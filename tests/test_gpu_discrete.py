@@ -224,6 +224,7 @@ class TestFastPath:
 
     KERNELS = {"bin": {}, "value": {"ECC_B200_F3": "value"}, "branch": {"ECC_B200_F3": "branch"},
                "cta": {"ECC_B200_F3": "cta"}, "rank2": {"ECC_B200_F3": "rank2"}, "no2d": {"ECC_B200_F3": "no2d"},
+               "dyn4": {"ECC_B200_F3_ZUNIT": "4"}, "dyn7": {"ECC_B200_F3_ZUNIT": "7"},
                "generic": {"ECC_B200_GENERIC": "1"}}
 
     @classmethod
@@ -246,7 +247,7 @@ class TestFastPath:
     @classmethod
     def _both(cls, t, ts, **kw):
         out = cls._all(t, ts, **kw)
-        for name in ("value", "branch", "cta", "rank2", "no2d"):
+        for name in ("value", "branch", "cta", "rank2", "no2d", "dyn4", "dyn7"):
             assert np.array_equal(out[name], out["bin"]), name
         return out["bin"], out["generic"]
 
@@ -288,11 +289,19 @@ class TestFastPath:
             assert np.array_equal(fast[0], want) and np.array_equal(gen[0], want)
 
     def test_batched(self, rng):
+        import os
+
         xs = rng.random((3, 10, 37, 44)).astype(np.float32)
         ts = E.ThresholdSet(np.linspace(0.01, 0.99, 129))
-        h = E.histogram_device(torch.from_numpy(xs).cuda(), ts, ndim=3).cpu().numpy()
-        for i in range(3):
-            assert np.array_equal(h[i], np.append(*oracle.histogram(xs[i], ts.taus)))
+        for zunit in (None, "3"):   # static partition, dynamic work queue (units span items)
+            if zunit:
+                os.environ["ECC_B200_F3_ZUNIT"] = zunit
+            try:
+                h = E.histogram_device(torch.from_numpy(xs).cuda(), ts, ndim=3).cpu().numpy()
+            finally:
+                os.environ.pop("ECC_B200_F3_ZUNIT", None)
+            for i in range(3):
+                assert np.array_equal(h[i], np.append(*oracle.histogram(xs[i], ts.taus))), (zunit, i)
 
     def test_plane_range_slabs(self, rng):
         """ecc_histogram_range: slabs with halos sum to the whole volume (C5 path)."""
