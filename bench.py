@@ -214,19 +214,21 @@ def run_b200(args):
     curve = torch.empty(NB, dtype=torch.int64, device=dev)
     view, z0, z1 = (own, 0, P) if not dist_on else D.slab_view(padded)
     dims = _lib.dims_arg(view.shape)
-    kstart = torch.cuda.Event(enable_timing=True)
-    kend = torch.cuda.Event(enable_timing=True)
+    # kernel-only timing: one event pair per step around the histogram kernel,
+    # steps back to back (no host sync in between), read after the last one
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     kernel_ms = []
 
-    def step(record=False):
+    def step(record=None):
         if dist_on:
             D.exchange_halos(padded)
-        if record:
+        if record is not None:
+            kstart, kend = kev[record]
             kstart.record(stream)
         _lib.check(L.ecc_histogram_range(_lib.ptr(view), _lib.DTYPE_F32, 3, _lib.ptr(dims), 1, z0, z1,
                                          _lib.ptr(table), _lib.ctypes.byref(binning), _lib.ptr(hist),
                                          _lib.ctypes.c_void_p(stream.cuda_stream)))
-        if record:
+        if record is not None:
             kend.record(stream)
         if dist_on:
             dist.all_reduce(hist)
@@ -258,10 +260,10 @@ def run_b200(args):
         barrier()
     total_ms = ev0.elapsed_time(ev1)
     # kernel-only timing of the dominant kernel (same stream, separate pass)
-    for _ in range(args.steps):
-        step(record=True)
-        kend.synchronize()
-        kernel_ms.append(kstart.elapsed_time(kend))
+    for i in range(args.steps):
+        step(record=i)
+    torch.cuda.synchronize()
+    kernel_ms = [a.elapsed_time(b) for a, b in kev]
     if dist_on:
         t = torch.tensor([total_ms, statistics.mean(kernel_ms)], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -403,10 +405,19 @@ def bench_ns(args, dev):
     ms = e0.elapsed_time(e1) / steps
     peak, peak_kind = _peaks()
     gbs = 4.0 * x.numel() / (ms * 1e-3) / 1e9
+    traffic = None
+    tfile = ROOT / "profiles" / "ncu_traffic.json"
+    if tfile.exists():
+        try:
+            t = json.loads(tfile.read_text()).get("north_star", {})
+            traffic = t["dram_read_bytes"] + t["dram_write_bytes"]
+        except (ValueError, OSError, KeyError):
+            traffic = None
     out = {"workload": "NS: 3D 1024^3 float32, discrete ECC, 1024 uniform thresholds (device-resident)",
            "value": x.numel() / (ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": ms, "steps": steps,
            "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
-                        "peak_source": peak_kind}}
+                        "peak_source": peak_kind, "traffic": traffic,
+                        "algorithmic_bytes_per_launch": 4 * x.numel()}}
     del x
     torch.cuda.empty_cache()
     return out
