@@ -208,6 +208,16 @@ def run_b200(args):
             lo, hi, _ = E.device_minmax(own)
         torch.cuda.synchronize()
         minmax_ms = (time.perf_counter() - t0) * 1e3
+    # device time of the min/max pass alone (K4; CUDA events, no host sync inside)
+    mm_out = torch.empty(3, dtype=torch.int64, device=dev)
+    m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    m0.record(stream)
+    for _ in range(5):
+        _lib.check(L.ecc_minmax(_lib.ptr(own), _lib.DTYPE_F32, own.numel(), _lib.ptr(mm_out),
+                                _lib.ctypes.c_void_p(stream.cuda_stream)))
+    m1.record(stream)
+    torch.cuda.synchronize()
+    minmax_kernel_ms = m0.elapsed_time(m1) / 5
     taus = E.thresholds_from_range(lo, hi, NB)
     table, binning = taus.device_table(_lib.DTYPE_F32, dev)
     hist = torch.empty(NB + 1, dtype=torch.int64, device=dev)
@@ -356,7 +366,8 @@ def run_b200(args):
                        "volume": [P * world, H, W], "bins": NB, "parallelism": f"zslab{world}",
                        "l2": "input larger than L2 (512 MiB per GPU), no flush",
                        "thresholds": "given (uniform over the device min/max, computed once)",
-                       "minmax_pass_ms": minmax_ms, "seed": SEED, "curve_xor_checksum": checksum},
+                       "minmax_pass_ms": minmax_ms, "minmax_kernel_ms": minmax_kernel_ms,
+                       "minmax_kernel_gbs": 4.0 * own.numel() / (minmax_kernel_ms * 1e-3) / 1e9, "seed": SEED, "curve_xor_checksum": checksum},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
                          "kernel": "ecc_fast3d_bin_kernel" if W % 4 == 0 else "ecc_sweep_kernel<RawSrc<float>,HistSink<float>>",
