@@ -40,12 +40,10 @@ def alloc_padded_slab(planes: int, plane_shape, dtype, device) -> torch.Tensor:
     return torch.empty((planes + 2, *plane_shape), dtype=dtype, device=device)
 
 
-def exchange_halos(padded: torch.Tensor, group=None) -> None:
-    """Fill padded[0] / padded[-1] from the z-neighbour ranks.
-
-    padded[1:-1] holds this rank's own planes; the end ranks' outer halo
-    planes are left untouched (they are excluded by `slab_view`).
-    """
+def start_halo_exchange(padded: torch.Tensor, group=None) -> list:
+    """Post the sends/receives that fill padded[0] / padded[-1] from the
+    z-neighbour ranks; returns the requests (wait on them before reading the
+    halo planes).  The own planes padded[1:-1] are only read meanwhile."""
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     ops = []
@@ -55,9 +53,17 @@ def exchange_halos(padded: torch.Tensor, group=None) -> None:
     if rank < world - 1:
         ops.append(dist.P2POp(dist.isend, padded[-2].contiguous(), _peer(group, rank + 1), group))
         ops.append(dist.P2POp(dist.irecv, padded[-1], _peer(group, rank + 1), group))
-    if ops:
-        for req in dist.batch_isend_irecv(ops):
-            req.wait()
+    return dist.batch_isend_irecv(ops) if ops else []
+
+
+def exchange_halos(padded: torch.Tensor, group=None) -> None:
+    """Fill padded[0] / padded[-1] from the z-neighbour ranks.
+
+    padded[1:-1] holds this rank's own planes; the end ranks' outer halo
+    planes are left untouched (they are excluded by `slab_view`).
+    """
+    for req in start_halo_exchange(padded, group):
+        req.wait()
 
 
 def _peer(group, group_rank: int) -> int:
@@ -88,19 +94,34 @@ def _cuda_slab_hist(view: torch.Tensor, z0: int, z1: int, taus) -> torch.Tensor:
 
 
 def slab_histogram(padded: torch.Tensor, taus, group=None, exchange: bool = True,
-                   hist_fn: Callable | None = None) -> torch.Tensor:
+                   hist_fn: Callable | None = None, overlap: bool = True) -> torch.Tensor:
     """Global (B+1) int64 histogram of a z-slab-partitioned 3D volume.
 
     padded: [planes + 2, H, W] (own planes at 1..planes; halos filled here
     when `exchange`).  hist_fn(view, plane_begin, plane_end, taus) -> (B+1)
     int64 histogram of planes [plane_begin, plane_end) of the contiguous
     view; defaults to the CUDA kernel (ecc_histogram_range).
+
+    overlap (with exchange, >= 3 own planes, >1 rank): the interior planes
+    [1, planes - 1) need only this rank's own data, so they are swept while
+    the halo planes are in flight; the two boundary planes follow once the
+    halos have arrived.  Histograms are additive over plane ranges, so the
+    sum equals the single sweep bit for bit.
     """
-    if exchange:
-        exchange_halos(padded, group)
-    view, z0, z1 = slab_view(padded, group)
     fn = hist_fn or _cuda_slab_hist
-    hist = fn(view, z0, z1, taus)
+    planes = padded.shape[0] - 2
+    if exchange and overlap and planes >= 3 and dist.get_world_size(group) > 1:
+        reqs = start_halo_exchange(padded, group)
+        hist = fn(padded[1:-1], 1, planes - 1, taus)
+        for req in reqs:
+            req.wait()
+        view, z0, z1 = slab_view(padded, group)
+        hist = hist + fn(view, z0, z0 + 1, taus) + fn(view, z1 - 1, z1, taus)
+    else:
+        if exchange:
+            exchange_halos(padded, group)
+        view, z0, z1 = slab_view(padded, group)
+        hist = fn(view, z0, z1, taus)
     dist.all_reduce(hist, op=dist.ReduceOp.SUM, group=group)
     return hist
 
