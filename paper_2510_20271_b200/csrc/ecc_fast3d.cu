@@ -1505,16 +1505,26 @@ bool fast3d_eligible(const void* x, int64_t D, int64_t H, int64_t W, int64_t bat
 // stream first.
 __device__ unsigned int g_f3_wq[64];
 static unsigned int* work_slot(cudaStream_t stream) {
-  static unsigned int* base = nullptr;
+  // the symbol has one instance per device: cache its address per device
+  constexpr int MAXDEV = 64;
+  static std::atomic<unsigned int*> base[MAXDEV];
   static std::atomic<unsigned> seq{0};
-  if (!base) {
-    void* p = nullptr;
-    cudaError_t e = cudaGetSymbolAddress(&p, g_f3_wq);
-    if (e != cudaSuccess) { set_cuda_error(e, "cudaGetSymbolAddress(work queue)"); return nullptr; }
-    base = static_cast<unsigned int*>(p);
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess || dev < 0 || dev >= MAXDEV) {
+    set_cuda_error(e != cudaSuccess ? e : cudaErrorInvalidDevice, "cudaGetDevice(work queue)");
+    return nullptr;
   }
-  unsigned int* slot = base + (seq.fetch_add(1) % 64);
-  cudaError_t e = cudaMemsetAsync(slot, 0, sizeof(unsigned int), stream);
+  unsigned int* b = base[dev].load();
+  if (!b) {
+    void* p = nullptr;
+    e = cudaGetSymbolAddress(&p, g_f3_wq);
+    if (e != cudaSuccess) { set_cuda_error(e, "cudaGetSymbolAddress(work queue)"); return nullptr; }
+    b = static_cast<unsigned int*>(p);
+    base[dev].store(b);
+  }
+  unsigned int* slot = b + (seq.fetch_add(1) % 64);
+  e = cudaMemsetAsync(slot, 0, sizeof(unsigned int), stream);
   if (e != cudaSuccess) { set_cuda_error(e, "cudaMemsetAsync(work queue)"); return nullptr; }
   return slot;
 }
