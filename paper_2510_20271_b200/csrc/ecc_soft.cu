@@ -182,27 +182,35 @@ __device__ __forceinline__ constexpr bool emu_slot(int i) {
          (BWD ? ECC_EMU_BWD : ECC_EMU_FWD) > 0;
 }
 
+// The a-pairs arrive NEGATED (nat = -a_j): den = 1 + a b is formed as
+// nden = fma(-a, b, -1) = -den, so no operand ever needs a sign flip (an
+// f32x2 FMA has no negate modifier; a 64-bit XOR costs two LOP3 per pair of
+// lanes).  Forward: r = rcp(-nden) (MUFU takes the negation for free),
+// Newton steps r (2 + nden r).  Backward: rn = rcp(nden) = -sigma and
+// fma(rn, rn, rn) = sigma^2 - sigma = -sigma (1 - sigma), so the backward
+// accumulates negated w and d_tau partials; w is negated on return and acc
+// by the caller.  Every rounding is the sign mirror of the positive form,
+// so the results are bit-identical to it.
 template <bool BWD, int T>
-__device__ __forceinline__ void pair_loop_fact2(const f2_t (&at)[T / 2], const f2_t (&up)[T / 2], f2_t (&acc)[T / 2],
+__device__ __forceinline__ void pair_loop_fact2(const f2_t (&nat)[T / 2], const f2_t (&up)[T / 2], f2_t (&acc)[T / 2],
                                                 float b, float cf, float& w) {
-  const f2_t b2 = f2_pack(b, b), one2 = f2_pack(1.f, 1.f), two2 = f2_pack(2.f, 2.f), cf2 = f2_pack(cf, cf);
-  f2_t r[T / 2];
+  const f2_t b2 = f2_pack(b, b), mone2 = f2_pack(-1.f, -1.f), two2 = f2_pack(2.f, 2.f), cf2 = f2_pack(cf, cf);
+  f2_t r[T / 2];   // forward: sigma; backward: -sigma
 #pragma unroll
   for (int i = 0; i < T / 2; ++i) {
-    const f2_t den = fma2(at[i], b2, one2);
+    const f2_t nden = fma2(nat[i], b2, mone2);
+    float dx, dy;
+    f2_unpack(nden, dx, dy);
     if (emu_slot<BWD>(i)) {
-      // seed 0x7EF311C3 - bits(x) (< 12.5 % error), three Newton steps r (2 - x r)
-      float dx, dy;
-      f2_unpack(den, dx, dy);
-      f2_t q = f2_pack(__int_as_float(0x7EF311C3 - __float_as_int(dx)),
-                       __int_as_float(0x7EF311C3 - __float_as_int(dy)));
+      // seed 0x7EF311C3 - bits(den) = 0xFEF311C3 - bits(-den) (< 12.5 % error),
+      // three Newton steps r (2 - den r)
+      f2_t q = f2_pack(__int_as_float((int)(0xFEF311C3u - (uint32_t)__float_as_int(dx))),
+                       __int_as_float((int)(0xFEF311C3u - (uint32_t)__float_as_int(dy))));
 #pragma unroll
-      for (int k = 0; k < 3; ++k) q = mul2(q, fnma2(den, q, two2));
-      r[i] = q;
+      for (int k = 0; k < 3; ++k) q = mul2(q, fma2(nden, q, two2));
+      r[i] = BWD ? mul2(q, mone2) : q;
     } else {
-      float dx, dy;
-      f2_unpack(den, dx, dy);
-      r[i] = f2_pack(rcp_approx(dx), rcp_approx(dy));
+      r[i] = BWD ? f2_pack(rcp_approx(dx), rcp_approx(dy)) : f2_pack(rcp_approx(-dx), rcp_approx(-dy));
     }
   }
   if (!BWD) {
@@ -212,14 +220,14 @@ __device__ __forceinline__ void pair_loop_fact2(const f2_t (&at)[T / 2], const f
     f2_t w0 = 0ull, w1 = 0ull;
 #pragma unroll
     for (int i = 0; i < T / 2; ++i) {
-      const f2_t s1 = fnma2(r[i], r[i], r[i]);   // r - r^2 = sigma (1 - sigma)
-      if (i & 1) w1 = fma2(up[i], s1, w1); else w0 = fma2(up[i], s1, w0);
-      acc[i] = fma2(cf2, s1, acc[i]);
+      const f2_t ns1 = fma2(r[i], r[i], r[i]);   // sigma^2 - sigma = -sigma (1 - sigma)
+      if (i & 1) w1 = fma2(up[i], ns1, w1); else w0 = fma2(up[i], ns1, w0);
+      acc[i] = fma2(cf2, ns1, acc[i]);
     }
     float a0, a1, c0, c1;
     f2_unpack(w0, a0, a1);
     f2_unpack(w1, c0, c1);
-    w = (a0 + c0) + (a1 + c1);
+    w = -((a0 + c0) + (a1 + c1));
   }
 }
 
@@ -357,7 +365,7 @@ ecc_soft_kernel(SoftArgs a) {
   }
 #pragma unroll
   for (int i = 0; i < T / 2; ++i) {
-    at2[i] = f2_pack(at[2 * i], at[2 * i + 1]);
+    at2[i] = f2_pack(-at[2 * i], -at[2 * i + 1]);   // negated: see pair_loop_fact2
     up2[i] = f2_pack(upv[2 * i], upv[2 * i + 1]);
     acc2[i] = 0ull;
   }
@@ -448,6 +456,10 @@ ecc_soft_kernel(SoftArgs a) {
   if (FACT && (!BWD || ECC_BWD_PACKED)) {
 #pragma unroll
     for (int i = 0; i < T / 2; ++i) f2_unpack(acc2[i], acc[2 * i], acc[2 * i + 1]);
+    if (BWD) {   // the packed backward accumulates -d_tau (see pair_loop_fact2)
+#pragma unroll
+      for (int t = 0; t < T; ++t) acc[t] = -acc[t];
+    }
   }
 #pragma unroll
   for (int t = 0; t < T; ++t) red[slot * rowlen + l * T + t] = acc[t];
