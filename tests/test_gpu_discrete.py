@@ -312,17 +312,27 @@ class TestFastPath:
         ts = E.ThresholdSet(np.linspace(0.0, 1.0, 65)[1:])
         t = torch.from_numpy(x).cuda()
         table, binning = ts.device_table(_lib.DTYPE_F32, t.device)
-        total = np.zeros(65, np.int64)
-        for z0, z1 in [(0, 7), (7, 8), (8, 16), (16, 23)]:
-            lo, hi = max(0, z0 - 1), min(D, z1 + 1)
-            view = t[lo:hi]
-            hist = torch.empty(65, dtype=torch.int64, device="cuda")
-            d = _lib.dims_arg(view.shape)
-            _lib.check(_lib.lib().ecc_histogram_range(_lib.ptr(view), _lib.DTYPE_F32, 3, _lib.ptr(d), 1, z0 - lo,
-                                                      z1 - lo, _lib.ptr(table), _lib.ctypes.byref(binning),
-                                                      _lib.ptr(hist), _lib.stream_ptr(view)))
-            total += hist.cpu().numpy()
-        assert np.array_equal(total, np.append(*oracle.histogram(x, ts.taus)))
+        want = np.append(*oracle.histogram(x, ts.taus))
+        import os
+
+        for zunit in (None, "2", "3"):   # static partition and the dynamic work queue
+            if zunit:
+                os.environ["ECC_B200_F3_ZUNIT"] = zunit
+            try:
+                total = np.zeros(65, np.int64)
+                for z0, z1 in [(0, 7), (7, 8), (8, 16), (16, 23)]:
+                    lo, hi = max(0, z0 - 1), min(D, z1 + 1)
+                    view = t[lo:hi]
+                    hist = torch.empty(65, dtype=torch.int64, device="cuda")
+                    d = _lib.dims_arg(view.shape)
+                    _lib.check(_lib.lib().ecc_histogram_range(_lib.ptr(view), _lib.DTYPE_F32, 3, _lib.ptr(d), 1,
+                                                              z0 - lo, z1 - lo, _lib.ptr(table),
+                                                              _lib.ctypes.byref(binning), _lib.ptr(hist),
+                                                              _lib.stream_ptr(view)))
+                    total += hist.cpu().numpy()
+            finally:
+                os.environ.pop("ECC_B200_F3_ZUNIT", None)
+            assert np.array_equal(total, want), zunit
 
     def test_large_volume_invariants(self):
         """256^3 counter grid: bit-exact vs oracle, sum c = 1, tail = 1."""
