@@ -108,6 +108,12 @@ constexpr size_t CHUNK_BYTES = sizeof(ChunkSmem);
 // log2 bound of the per-lane factor a_j; b_p is clamped to 2^+-(126 - A_MAX)
 // so a_j b_p stays inside [2^-126, 2^126] (no overflow, no inf*0)
 constexpr float A_MAX = 40.f;
+#ifndef ECC_SOFT_PAIR
+#define ECC_SOFT_PAIR 1   // paired reciprocals (pair_loop_prod) when the margin allows: bit 0 forward,
+                          // bit 1 backward (measured: forward 816 vs 875 us, backward 1.43 vs 1.36 ms
+                          // on 16 x 1024^2 -- the backward is latency-bound and the pairing lengthens
+                          // its dependency chain, so it keeps one reciprocal per pair)
+#endif
 constexpr float B_MAX = 126.f - A_MAX;
 
 template <bool BWD, int T, int EMU_EVERY>
@@ -221,6 +227,51 @@ __device__ __forceinline__ void pair_loop_fact2(const f2_t (&nat)[T / 2], const 
 #pragma unroll
     for (int i = 0; i < T / 2; ++i) {
       const f2_t ns1 = fma2(r[i], r[i], r[i]);   // sigma^2 - sigma = -sigma (1 - sigma)
+      if (i & 1) w1 = fma2(up[i], ns1, w1); else w0 = fma2(up[i], ns1, w0);
+      acc[i] = fma2(cf2, ns1, acc[i]);
+    }
+    float a0, a1, c0, c1;
+    f2_unpack(w0, a0, a1);
+    f2_unpack(w1, c0, c1);
+    w = -((a0 + c0) + (a1 + c1));
+  }
+}
+
+// Paired reciprocals (factorised mode, the default when the thresholds allow
+// it): slot i (thresholds 2i, 2i+1) is paired lane-wise with slot T/2-1-i
+// (T-2-2i, T-1-2i), whose factors a_j are near the reciprocals of slot i's
+// (the block is centred), and one reciprocal R = 1 / (d d') of the product of
+// the two denominators serves both: sigma = d' R, sigma' = d R.  One MUFU per
+// two (voxel, threshold) pairs instead of one per pair, for two FMULs.  The
+// product stays finite because b_p is clamped to 2^(+-bc), bc = (126 -
+// max log2(a a')) / 2 - 1 (computed per lane block in the kernel), and the
+// clamp changes sigma by at most 2^(A - bc) <= 2^-24 (A = max |log2 a|); the
+// kernel falls back to pair_loop_fact2 when that margin is not met.
+// Negated factors as in pair_loop_fact2 (nd = -d): forward sigma = nd' *
+// rcp(-P), backward -sigma = nd' * rcp(P).
+template <bool BWD, int T>
+__device__ __forceinline__ void pair_loop_prod(const f2_t (&nat)[T / 2], const f2_t (&up)[T / 2], f2_t (&acc)[T / 2],
+                                               float b, float cf, float& w) {
+  const f2_t b2 = f2_pack(b, b), mone2 = f2_pack(-1.f, -1.f), cf2 = f2_pack(cf, cf);
+  f2_t r[T / 2];   // forward: sigma; backward: -sigma
+#pragma unroll
+  for (int i = 0; i < T / 4; ++i) {
+    const int ip = T / 2 - 1 - i;
+    const f2_t nd = fma2(nat[i], b2, mone2), ndp = fma2(nat[ip], b2, mone2);
+    float px, py;
+    f2_unpack(mul2(nd, ndp), px, py);   // d d' > 0
+    const f2_t R = BWD ? f2_pack(rcp_approx(px), rcp_approx(py)) : f2_pack(rcp_approx(-px), rcp_approx(-py));
+    r[i] = mul2(ndp, R);
+    r[ip] = mul2(nd, R);
+  }
+  if (!BWD) {
+#pragma unroll
+    for (int i = 0; i < T / 2; ++i) acc[i] = fma2(cf2, r[i], acc[i]);
+  } else {
+    f2_t w0 = 0ull, w1 = 0ull;
+#pragma unroll
+    for (int i = 0; i < T / 2; ++i) {
+      const f2_t ns1 = fma2(r[i], r[i], r[i]);   // -sigma (1 - sigma)
       if (i & 1) w1 = fma2(up[i], ns1, w1); else w0 = fma2(up[i], ns1, w0);
       acc[i] = fma2(cf2, ns1, acc[i]);
     }
@@ -352,6 +403,23 @@ ecc_soft_kernel(SoftArgs a) {
     }
   }
   __syncthreads();
+  // paired-reciprocal mode (factorised): this lane block's b clamp and margin
+  float bc = B_MAX;
+  bool prod = false;
+  if (FACT && (ECC_SOFT_PAIR & (BWD ? 2 : 1))) {
+    float amax = 0.f, dmax = 0.f;
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      const int tp = (T - 2 - 2 * (t >> 1)) + (t & 1);   // lane-wise partner (slot T/2-1-i)
+      const float x0 = atab[l * T + t], x1 = atab[l * T + tp];
+      const float l0 = x0 > 0.f ? __log2f(x0) : 0.f, l1 = x1 > 0.f ? __log2f(x1) : 0.f;
+      amax = fmaxf(amax, fabsf(l0));
+      dmax = fmaxf(dmax, l0 + l1);
+    }
+    bc = fminf(B_MAX, 0.5f * (126.f - dmax) - 1.f);
+    prod = __syncthreads_and(bc - amax >= 24.f);
+    if (!prod) bc = B_MAX;
+  }
   float at[T], upv[T], acc[T];          // direct mode
   f2_t at2[T / 2], up2[T / 2], acc2[T / 2];  // factorised mode (packed pairs)
   const int j0 = l * T;
@@ -376,7 +444,7 @@ ecc_soft_kernel(SoftArgs a) {
     const float cf = valid ? __uint_as_float((uint32_t)S.pk[k] & 0xFFFF0000u) : 0.f;
     float w = 0.f;
     if (FACT) {
-      const float kf = fminf(fmaxf(__fmaf_rn(a.kscale, f, koff), -B_MAX), B_MAX);
+      const float kf = fminf(fmaxf(__fmaf_rn(a.kscale, f, koff), -bc), bc);
       // forward: packed FFMA2 pairs with 3/8 of the reciprocals as Newton
       // iterations; backward: packed FFMA2 with every reciprocal on MUFU
       // (emulating 1-2 of 8 there measured slower: the backward is
@@ -386,6 +454,8 @@ ecc_soft_kernel(SoftArgs a) {
 #endif
       if (BWD && !ECC_BWD_PACKED)
         pair_loop_fact<BWD, T, 1024>(at, upv, acc, ECC_SOFT_EX2_FMA >= 1 ? ex2_fma(kf) : ex2_approx(kf), cf, w);
+      else if (prod)
+        pair_loop_prod<BWD, T>(at2, up2, acc2, ex2_approx(kf), cf, w);
       else
         pair_loop_fact2<BWD, T>(at2, up2, acc2,
                                 (BWD ? ECC_SOFT_EX2_FMA >= 1 : ECC_SOFT_EX2_FMA >= 2) ? ex2_fma(kf) : ex2_approx(kf),
