@@ -179,7 +179,8 @@ __device__ __forceinline__ f2_t fnma2(f2_t a, f2_t b, f2_t c) {
 #define ECC_EMU_FWD 3   // emulated slots per 8 (forward)
 #endif
 #ifndef ECC_EMU_BWD
-#define ECC_EMU_BWD 0   // emulated slots per 8 (backward)
+#define ECC_EMU_BWD 1   // emulated slots per 8 (backward): 1 measured 10.73 vs 10.83 ms on C3 (3 runs each);
+                        // 2 was slower (before the sign-flip-free FMAs: 11.41 vs 11.10)
 #endif
 template <bool BWD>
 __device__ __forceinline__ constexpr bool emu_slot(int i) {
@@ -445,10 +446,11 @@ ecc_soft_kernel(SoftArgs a) {
     float w = 0.f;
     if (FACT) {
       const float kf = fminf(fmaxf(__fmaf_rn(a.kscale, f, koff), -bc), bc);
-      // forward: packed FFMA2 pairs with 3/8 of the reciprocals as Newton
-      // iterations; backward: packed FFMA2 with every reciprocal on MUFU
-      // (emulating 1-2 of 8 there measured slower: the backward is
-      // latency-bound).  The scalar loop stays as the A/B reference.
+      // forward: paired reciprocals (pair_loop_prod) when the margin allows,
+      // else packed FFMA2 pairs with 3/8 of the reciprocals as Newton
+      // iterations; backward: packed FFMA2 with 1/8 of the reciprocals as
+      // Newton iterations (ECC_EMU_BWD).  The scalar loop stays as the A/B
+      // reference.
 #ifndef ECC_BWD_PACKED
 #define ECC_BWD_PACKED 1   // packed FFMA2 backward (801 vs 838 us at 16 thresholds per lane)
 #endif
