@@ -638,6 +638,10 @@ def bench_soft(args, dev, world, rank, dist_on=False):
             "roofline": {"bound": "sfu", "unit": "MUFU ops/s", "achieved": mufu_ops / (ms * 1e-3),
                          "peak": mufu_peak, "frac": mufu_ops / (ms * 1e-3) / mufu_peak,
                          "nonzero_fraction": nz, "algorithmic_pairs_per_s": pairs / (ms * 1e-3),
+                         # one MUFU per (voxel, threshold) pair per pass bounds fwd+bwd at
+                         # mufu_peak / (2 B) voxels/s; skipping c = 0 voxels and pairing reciprocals beat it
+                         "survey_sfu_bound_voxel_s": mufu_peak / (2 * B),
+                         "vs_survey_sfu_bound": (vox / (ms * 1e-3)) / (mufu_peak / (2 * B)),
                          "mufu_per_executed_pair": {"forward": 0.5, "backward": 7.0 / 8.0},
                          "note": "achieved counts the MUFU operations the kernels issue (c = 0 voxels are "
                                  "skipped; the forward pairs its reciprocals, one per two pairs; 1/8 of the "
