@@ -101,7 +101,7 @@ class TestCommandsGPU:
         assert cli.main(["bench", "--sizes", "40x36,20x24x28", "--bins", "64", "--repeats", "2",
                          "--report", str(rep), "--csv", str(tmp_path / "b.csv")]) == 0
         rows = json.loads(rep.read_text())["rows"]
-        assert len(rows) == 6 and len({r["checksum"] for r in rows if r["dims"] == [40, 36]}) == 1
+        assert len(rows) == 2 * len(cli.VARIANTS) and len({r["checksum"] for r in rows if r["dims"] == [40, 36]}) == 1
 
 
 def test_generators_match_reference_files(tmp_path):
