@@ -710,7 +710,8 @@ extern "C" int ecc_soft_prepare(const void* x, int dtype, int ndim, const int64_
   if (batch < 1) return set_error(ECC_EINVAL, "batch must be >= 1");
   SoftPrepSink sk{coeffs, field_c, field_lo, p->center, d3[0], d3[1], d3[2]};
   cudaStream_t s = (cudaStream_t)stream;
-  if (ndim == 2 && batch <= 65535 && (dtype == ECC_DTYPE_F32 || dtype == ECC_DTYPE_F64)) {
+  if (ndim == 2 && batch <= 65535 && (dtype == ECC_DTYPE_F32 || dtype == ECC_DTYPE_F64) &&
+      !getenv("ECC_B200_GENERIC")) {
     dim3 grid((unsigned)((d3[2] + 31) / 32), (unsigned)((d3[1] + PREP_TH - 1) / PREP_TH), (unsigned)batch);
     if (grid.y > 65535) goto generic;
     if (dtype == ECC_DTYPE_F32) {

@@ -282,3 +282,30 @@ class TestGradientCheck:
         for key in ("d_values", "d_tau", "d_u", "d_alpha"):
             assert rep["normwise"][key] <= 1e-4, (key, rep)
         assert rep["tangency"] <= 1e-8
+
+
+class TestPrepare2D:
+    """The 2-D soft prepare kernel (soft_prep2d_kernel) against the generic
+    sweep: the same coefficients and centred field, bit for bit."""
+
+    @pytest.mark.parametrize("hw,batch", [((8, 8), 1), ((37, 23), 2), ((70, 33), 3), ((1, 40), 2), ((65, 1), 1),
+                                          ((100, 130), 2)])
+    def test_matches_generic_sweep(self, rng, hw, batch):
+        import os
+
+        for dtype, lam, hw_, alpha in ((np.float32, 50.0, 0.01, 0.3), (np.float64, 500.0, 1.0, 0.3),
+                                       (np.float32, 50.0, 0.01, 0.0)):
+            x = rng.random((batch,) + hw).astype(dtype)
+            x[..., ::3, :] = np.round(x[..., ::3, :] * 4) / 4       # ties in the effective field
+            u = E.reparametrize_direction([1.0, 2.0])
+            p = E.soft._params(lam, alpha, u, -0.5, 1.5, 2, hw_)
+            t = torch.from_numpy(x).cuda()
+            c1, (f1, l1) = E.soft.soft_prepare_device(t, hw, batch, p)
+            os.environ["ECC_B200_GENERIC"] = "1"
+            try:
+                c2, (f2, l2) = E.soft.soft_prepare_device(t, hw, batch, p)
+            finally:
+                del os.environ["ECC_B200_GENERIC"]
+            assert torch.equal(c1, c2) and torch.equal(f1, f2), (hw, dtype, alpha)
+            if l1 is not None:
+                assert torch.equal(l1, l2)
