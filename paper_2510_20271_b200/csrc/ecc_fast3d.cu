@@ -652,7 +652,15 @@ ecc_fast3d_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* 
 // ======================================================================
 constexpr int BROW = 68;                    // words per bin-plane row: 4 x 16 + pad (== 4 mod 32)
 constexpr int BEDGE = 32 * BROW;            // edge words [segment][row]: bin(x - 1) | bin(x + 32) << 16
-constexpr int BPLANE = BEDGE + NW * 32;     // words per bin plane
+// Sentinel row: what lane 0 reads as row y - 1 and lane 31 as row y + 1.
+// Those lanes are halo rows except in the first / last tile of a column,
+// where they are output rows whose missing neighbour lies outside the grid
+// (rank_tile_rows).  Its data sits at == 28 mod 32 (the bank group no other
+// lane of lanes 0-7 touches in a y - 1 load), its edge words in row pads at
+// banks 31 (free in a y - 1 load) and 0 (free in a y + 1 load).
+constexpr int BSROW = BEDGE + NW * 32 + 28;
+constexpr int BSE_DN = 7 * BROW + 67, BSE_UP = 0 * BROW + 64;
+constexpr int BPLANE = BSROW + NW * 16;     // words per bin plane
 constexpr uint32_t BSENT = 0x7FFFu;
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
@@ -676,6 +684,58 @@ __device__ __forceinline__ void load_brow(BRow& R, const uint32_t* buf, int row,
     R.w[4 * k + 3] = t.w;
   }
   R.e = buf[BEDGE + seg * 32 + row];
+}
+struct BOff {
+  int d, e;   // word offsets of a row segment's data and edge word in a bin plane
+};
+__device__ __forceinline__ BOff brow_dn(int lane, int seg) {   // row y - 1
+  return lane > 0 ? BOff{(lane - 1) * BROW + 16 * seg, BEDGE + seg * 32 + lane - 1} : BOff{BSROW + 16 * seg, BSE_DN};
+}
+__device__ __forceinline__ BOff brow_up(int lane, int seg) {   // row y + 1
+  return lane < 31 ? BOff{(lane + 1) * BROW + 16 * seg, BEDGE + seg * 32 + lane + 1} : BOff{BSROW + 16 * seg, BSE_UP};
+}
+__device__ __forceinline__ void load_brow(BRow& R, const uint32_t* buf, BOff o) {
+  const uint4* p = reinterpret_cast<const uint4*>(buf + o.d);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint4 t = p[k];
+    R.w[4 * k] = t.x;
+    R.w[4 * k + 1] = t.y;
+    R.w[4 * k + 2] = t.z;
+    R.w[4 * k + 3] = t.w;
+  }
+  R.e = buf[o.e];
+}
+__device__ __forceinline__ void init_sentinels(uint32_t* bbuf) {   // both bin planes; never overwritten
+  const uint32_t s2 = BSENT | (BSENT << 16);
+  if (threadIdx.x < 2 * NW * 16) bbuf[(threadIdx.x / (NW * 16)) * BPLANE + BSROW + threadIdx.x % (NW * 16)] = s2;
+  if (threadIdx.x < 2) {
+    bbuf[threadIdx.x * BPLANE + BSE_DN] = s2;
+    bbuf[threadIdx.x * BPLANE + BSE_UP] = s2;
+  }
+}
+// y tiling of the rank kernels: 32 lanes = 32 staged rows from o; rows
+// [f, e) are deposited.  Interior tiles deposit lanes 1-30; the first tile
+// of a column also deposits lane 0 (row 0) and the last, aligned to the
+// bottom of the grid, lane 31 (row H - 1), so H = 30 k + 2 takes k + 1
+// tiles instead of k + 2 (512: 17 instead of 18).
+__host__ __device__ __forceinline__ int rank_tiles_y(int H) {
+  return H <= 32 ? 1 : 2 + (H - 62 > 0 ? (H - 62 + OUTR - 1) / OUTR : 0);
+}
+__device__ __forceinline__ void rank_tile_rows(int ty, int T, int H, int& o, int& f, int& e) {
+  if (ty == 0) {
+    o = 0;
+    f = 0;
+    e = T == 1 ? H : OUTR + 1;
+  } else if (ty == T - 1) {
+    o = H - 32;
+    f = OUTR * ty + 1;
+    e = H;
+  } else {
+    o = OUTR * ty;
+    f = o + 1;
+    e = o + OUTR + 1;
+  }
 }
 // operand word j of row R moved by dx: (bin[j + dx], bin[j + 16 + dx])
 template <int DX>
@@ -908,6 +968,7 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
   for (int i = threadIdx.x; i < hsize; i += NT) s_hist[i] = 0;
   if (!U8)
     for (int i = threadIdx.x; i <= cells; i += NT) s_t[i] = EDGE ? tE_g[i] : lut_g[i].t;
+  init_sentinels(bbuf);
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
     *s_rounds = 0;
@@ -959,7 +1020,7 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
 
   uint32_t phase = 0;
   int64_t cur_n = -1;
-  const int rm = lane > 0 ? lane - 1 : 0, rp = lane < 31 ? lane + 1 : 31;
+  const BOff rm = brow_dn(lane, warp), rp = brow_up(lane, warp);
 
   // work partition: see ecc_fast3d_kernel
   const int64_t Dw = (int64_t)(g.ze - g.zb);
@@ -1022,11 +1083,13 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
     const int tx = (int)(rr % g.tiles_x); rr /= g.tiles_x;
     const int ty = (int)(rr % g.tiles_y); rr /= g.tiles_y;
     const int64_t n = rr;
-    const int x0 = tx * TXW, y0 = ty * OUTR;
+    int yo, yf, ye;
+    rank_tile_rows(ty, g.tiles_y, g.H, yo, yf, ye);
+    const int x0 = tx * TXW, y0 = yo + 1;   // staged rows y0 - 1 ... y0 + 30
     const int zs = g.zb + (int)z0;
     const int ze = zs + (int)seg;          // own planes [zs, ze), halo plane ze
 
-    pending += seg * (TXW * OUTR);
+    pending += seg * (TXW * 32);
     if (n != cur_n || pending > (int64_t(1) << 24)) {   // counters hold 16 c: |16 c| <= 112
       if (cur_n >= 0) {
         __syncthreads();
@@ -1034,7 +1097,7 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
         __syncthreads();
       }
       cur_n = n;
-      pending = seg * (TXW * OUTR);
+      pending = seg * (TXW * 32);
     }
 
     // WS (warp-independent) mode: each warp bins and reads only its own
@@ -1085,7 +1148,7 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
 
     // per-thread validity (rows / columns of this tile)
     const int y = y0 - 1 + lane;
-    const bool lane_out = lane >= 1 && lane <= 30 && y < g.H;
+    const bool lane_out = y >= yf && y < ye;
     const bool row_up_ok = (y + 1) < g.H;
     const bool row_dn_ok = (y - 1) >= 0;
     const int xs = x0 + SEG * warp;
@@ -1112,18 +1175,18 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
         uint32_t PP[16];
         BRow A, B;
         load_brow(A, B0, lane, warp);
-        load_brow(B, B0, rm, warp);
+        load_brow(B, B0, rm);
 #pragma unroll
         for (int j = 0; j < 16; ++j)   // | == + (bits 15, 31 clear)
           PP[j] = ECC_F3_FMA_PP ? mad_fma(A.w[j], one, 0x80008000u) : (A.w[j] | 0x80008000u);
         N0[NX] = cmp_word<-1>(PP, A, two);
         eA = A.e;
-        load_brow(A, B1, rm, warp);
+        load_brow(A, B1, rm);
         N0[NYM_XM] = cmp_word<-1>(PP, B, two);
         N0[NYM_X0] = cmp_word<0>(PP, B, two);
         N0[NYM_XP] = cmp_word<1>(PP, B, two);
         eB = B.e;
-        load_brow(B, B1, rp, warp);
+        load_brow(B, B1, rp);
         N0[NZ_YM_XM] = cmp_word<-1>(PP, A, two);
         N0[NZ_YM_X0] = cmp_word<0>(PP, A, two);
         N0[NZ_YM_XP] = cmp_word<1>(PP, A, two);
@@ -1298,6 +1361,7 @@ ecc_fast2d_rank_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const v
   for (int i = threadIdx.x; i < hsize; i += NT) s_hist[i] = 0;
   if (!U8)
     for (int i = threadIdx.x; i <= cells; i += NT) s_t[i] = EDGE ? tE_g[i] : lut_g[i].t;
+  init_sentinels(bbuf);
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
     *s_rounds = 0;
@@ -1346,29 +1410,31 @@ ecc_fast2d_rank_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const v
   // contiguous, image-major tile range per CTA
   const int64_t T = g.items;
   const int64_t t_begin = T * (int64_t)blockIdx.x / gridDim.x, t_end = T * ((int64_t)blockIdx.x + 1) / gridDim.x;
-  auto origin = [&](int64_t t, int& x0, int& y0, int64_t& n) {
+  auto origin = [&](int64_t t, int& x0, int& y0, int64_t& n, int& yf, int& ye) {
     int64_t r = t;
     x0 = (int)(r % g.tiles_x) * TXW;
     r /= g.tiles_x;
-    y0 = (int)(r % g.tiles_y) * OUTR;
+    int yo;
+    rank_tile_rows((int)(r % g.tiles_y), g.tiles_y, g.H, yo, yf, ye);
+    y0 = yo + 1;
     n = r / g.tiles_y;
   };
   auto issue = [&](int64_t t) {
-    int x0, y0;
+    int x0, y0, yf, ye;
     int64_t n;
-    origin(t, x0, y0, n);
+    origin(t, x0, y0, n, yf, ye);
     mbar_expect_tx(bar, STAGE_BYTES);
     tma_load_4d(stage, &tmap, bar, x0 - (U8 ? 16 : 4), y0 - 1, 0, (int)n);
   };
   if (threadIdx.x == 0 && t_begin < t_end) issue(t_begin);
   uint32_t phase = 0;
   int64_t cur_n = -1;
-  const int rm = lane > 0 ? lane - 1 : 0;
+  const BOff rm = brow_dn(lane, warp);
   const uint32_t FULL = 0xffffffffu;
   for (int64_t t = t_begin, it = 0; t < t_end; ++t, ++it) {
-    int x0, y0;
+    int x0, y0, yf, ye;
     int64_t n;
-    origin(t, x0, y0, n);
+    origin(t, x0, y0, n, yf, ye);
     if (n != cur_n) {   // uniform across the CTA: every warp walks the same tiles
       __syncthreads();
       if (cur_n >= 0) flush(cur_n);
@@ -1394,7 +1460,7 @@ ecc_fast2d_rank_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const v
 
     // per-thread validity (rows / columns of this tile)
     const int y = y0 - 1 + lane;
-    const bool lane_out = lane >= 1 && lane <= 30 && y < g.H;
+    const bool lane_out = y >= yf && y < ye;
     const uint32_t myu = (y + 1) < g.H ? FULL : 0u;
     const int xs = x0 + SEG * warp;
     const int nvalid = max(0, min(32, g.W - xs));
@@ -1405,7 +1471,7 @@ ecc_fast2d_rank_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const v
     // the four in-plane negative words
     BRow A, Bm;
     load_brow(A, B, lane, warp);
-    load_brow(Bm, B, rm, warp);
+    load_brow(Bm, B, rm);
     uint32_t PP[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) PP[j] = mad_fma(A.w[j], one, 0x80008000u);
@@ -1563,7 +1629,7 @@ static int launch_2d(const CUtensorMap& map, const void* kfn, size_t smem, int64
   g.zb = 0;
   g.ze = 1;
   g.tiles_x = (int)((W + TXW - 1) / TXW);
-  g.tiles_y = (int)((H + OUTR - 1) / OUTR);
+  g.tiles_y = rank_tiles_y((int)H);
   g.zc = 0;
   g.zchunks = 0;
   g.one = 1;
@@ -1647,7 +1713,7 @@ int fast3d_launch(const float* x, int64_t D, int64_t H, int64_t W, int64_t batch
   g.zb = (int)zb;
   g.ze = (int)ze;
   g.tiles_x = (int)((W + TXW - 1) / TXW);
-  g.tiles_y = (int)((H + OUTR - 1) / OUTR);
+  g.tiles_y = use_bin ? rank_tiles_y((int)H) : (int)((H + OUTR - 1) / OUTR);
   const int64_t tiles = (int64_t)g.tiles_x * g.tiles_y * batch;
   g.zc = 0;
   g.one = 1;
@@ -1716,7 +1782,7 @@ int fast3d_u8_launch(const uint8_t* x, int64_t D, int64_t H, int64_t W, int64_t 
   g.zb = (int)zb;
   g.ze = (int)ze;
   g.tiles_x = (int)((W + TXW - 1) / TXW);
-  g.tiles_y = (int)((H + OUTR - 1) / OUTR);
+  g.tiles_y = rank_tiles_y((int)H);
   const int64_t tiles = (int64_t)g.tiles_x * g.tiles_y * batch;
   g.zc = 0;
   g.one = 1;

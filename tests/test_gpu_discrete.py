@@ -484,3 +484,40 @@ class TestFastPath2DTiles:
             want = np.append(*oracle.histogram(xs[i].astype(np.float64), ts.taus))
             for name, h in out.items():
                 assert np.array_equal(h[i], want), (name, i)
+
+
+class TestRankTileRows:
+    """The rank kernels' y tiling: the first tile of a column deposits lane 0
+    (row 0) and the last, bottom-aligned tile deposits lane 31 (row H - 1),
+    whose missing neighbours are read from the sentinel row.  Heights on
+    both sides of every tiling change (1, 2 or 3 tiles, 30 k + 1, 30 k + 2,
+    512), plateau-heavy values so that tie-breaking across the tile
+    boundaries matters, f32 (3-D and 2-D kernels) and uint8."""
+
+    HEIGHTS = [2, 31, 32, 33, 34, 61, 62, 63, 64, 91, 92, 93, 94, 122, 152, 512]
+
+    @pytest.mark.parametrize("h", HEIGHTS)
+    def test_heights(self, rng, h):
+        for dt in (np.float32, np.uint8):
+            x = rng.integers(0, 5, (3, h, 144)).astype(dt)
+            t = torch.from_numpy(x).cuda()
+            ts = E.ThresholdSet(np.array([0.0, 1.0, 2.5, 3.0]))
+            want = np.append(*oracle.histogram(x.astype(np.float64), ts.taus))
+            out = TestFastPath._all(t, ts)
+            for name, hh in out.items():
+                assert np.array_equal(hh[0], want), (h, dt, name)
+            # the same planes as a batch of 2-D images (the 2-D tile kernel)
+            h2 = E.histogram_device(t, ts, ndim=2).cpu().numpy()
+            for i in range(3):
+                assert np.array_equal(h2[i], np.append(*oracle.histogram(x[i].astype(np.float64), ts.taus))), (h, dt, i)
+
+    def test_uniform_thresholds_512_rows(self, rng):
+        """The bench's edge-ranking table (1024 uniform thresholds) on a
+        512-row volume: 17 tiles per column instead of 18."""
+        x = rng.random((6, 512, 128)).astype(np.float32)
+        x[:, ::7, :] = np.round(x[:, ::7, :] * 16) / 16
+        t = torch.from_numpy(x).cuda()
+        ts = E.thresholds_from_range(float(x.min()), float(x.max()), 1024)
+        fast, gen = TestFastPath._both(t, ts)
+        assert np.array_equal(fast, gen)
+        assert np.array_equal(fast[0], np.append(*oracle.histogram(x, ts.taus)))
