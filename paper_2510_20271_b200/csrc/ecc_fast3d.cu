@@ -688,11 +688,16 @@ __device__ __forceinline__ void load_brow(BRow& R, const uint32_t* buf, int row,
 struct BOff {
   int d, e;   // word offsets of a row segment's data and edge word in a bin plane
 };
-__device__ __forceinline__ BOff brow_dn(int lane, int seg) {   // row y - 1
-  return lane > 0 ? BOff{(lane - 1) * BROW + 16 * seg, BEDGE + seg * 32 + lane - 1} : BOff{BSROW + 16 * seg, BSE_DN};
+// row y - 1 / y + 1 of this lane; the outer lanes read the sentinel row only
+// in the tiles where they are output rows (sent), else their own row (the
+// same address as their neighbour lane's: a broadcast, no bank conflict)
+__device__ __forceinline__ BOff brow_dn(int lane, int seg, bool sent) {
+  const int r = lane > 0 ? lane - 1 : 0;
+  return lane == 0 && sent ? BOff{BSROW + 16 * seg, BSE_DN} : BOff{r * BROW + 16 * seg, BEDGE + seg * 32 + r};
 }
-__device__ __forceinline__ BOff brow_up(int lane, int seg) {   // row y + 1
-  return lane < 31 ? BOff{(lane + 1) * BROW + 16 * seg, BEDGE + seg * 32 + lane + 1} : BOff{BSROW + 16 * seg, BSE_UP};
+__device__ __forceinline__ BOff brow_up(int lane, int seg, bool sent) {
+  const int r = lane < 31 ? lane + 1 : 31;
+  return lane == 31 && sent ? BOff{BSROW + 16 * seg, BSE_UP} : BOff{r * BROW + 16 * seg, BEDGE + seg * 32 + r};
 }
 __device__ __forceinline__ void load_brow(BRow& R, const uint32_t* buf, BOff o) {
   const uint4* p = reinterpret_cast<const uint4*>(buf + o.d);
@@ -716,26 +721,17 @@ __device__ __forceinline__ void init_sentinels(uint32_t* bbuf) {   // both bin p
 }
 // y tiling of the rank kernels: 32 lanes = 32 staged rows from o; rows
 // [f, e) are deposited.  Interior tiles deposit lanes 1-30; the first tile
-// of a column also deposits lane 0 (row 0) and the last, aligned to the
-// bottom of the grid, lane 31 (row H - 1), so H = 30 k + 2 takes k + 1
-// tiles instead of k + 2 (512: 17 instead of 18).
+// of a column starts at row 0 and also deposits lane 0, and the last also
+// deposits lane 31 when that is row H - 1, so H = 30 k + 2 takes k + 1
+// tiles instead of k + 2 (512: 17 instead of 18).  Rows past H - 1 are
+// sentinels (not ranked), as before.
 __host__ __device__ __forceinline__ int rank_tiles_y(int H) {
-  return H <= 32 ? 1 : 2 + (H - 62 > 0 ? (H - 62 + OUTR - 1) / OUTR : 0);
+  return H <= 32 ? 1 : 1 + (H - 32 + OUTR - 1) / OUTR;
 }
 __device__ __forceinline__ void rank_tile_rows(int ty, int T, int H, int& o, int& f, int& e) {
-  if (ty == 0) {
-    o = 0;
-    f = 0;
-    e = T == 1 ? H : OUTR + 1;
-  } else if (ty == T - 1) {
-    o = H - 32;
-    f = OUTR * ty + 1;
-    e = H;
-  } else {
-    o = OUTR * ty;
-    f = o + 1;
-    e = o + OUTR + 1;
-  }
+  o = OUTR * ty;
+  f = ty == 0 ? 0 : o + 1;
+  e = ty == T - 1 ? H : o + OUTR + 1;
 }
 // operand word j of row R moved by dx: (bin[j + dx], bin[j + 16 + dx])
 template <int DX>
@@ -1020,7 +1016,7 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
 
   uint32_t phase = 0;
   int64_t cur_n = -1;
-  const BOff rm = brow_dn(lane, warp), rp = brow_up(lane, warp);
+  BOff rm, rp;   // per tile (brow_dn / brow_up)
 
   // work partition: see ecc_fast3d_kernel
   const int64_t Dw = (int64_t)(g.ze - g.zb);
@@ -1086,6 +1082,8 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
     int yo, yf, ye;
     rank_tile_rows(ty, g.tiles_y, g.H, yo, yf, ye);
     const int x0 = tx * TXW, y0 = yo + 1;   // staged rows y0 - 1 ... y0 + 30
+    rm = brow_dn(lane, warp, yo == 0);
+    rp = brow_up(lane, warp, yo + 31 == g.H - 1);
     const int zs = g.zb + (int)z0;
     const int ze = zs + (int)seg;          // own planes [zs, ze), halo plane ze
 
@@ -1429,7 +1427,6 @@ ecc_fast2d_rank_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const v
   if (threadIdx.x == 0 && t_begin < t_end) issue(t_begin);
   uint32_t phase = 0;
   int64_t cur_n = -1;
-  const BOff rm = brow_dn(lane, warp);
   const uint32_t FULL = 0xffffffffu;
   for (int64_t t = t_begin, it = 0; t < t_end; ++t, ++it) {
     int x0, y0, yf, ye;
@@ -1442,6 +1439,7 @@ ecc_fast2d_rank_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const v
       cur_n = n;
     }
     uint32_t* B = bbuf + (it & 1) * BPLANE;
+    const BOff rm = brow_dn(lane, warp, y0 == 1);
     mbar_wait(bar, phase);
     phase ^= 1u;
     if (U8)
