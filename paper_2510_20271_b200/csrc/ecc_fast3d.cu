@@ -77,10 +77,13 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
+#ifndef ECC_F3_WAIT_SLEEP
+#define ECC_F3_WAIT_SLEEP 0   // ns of __nanosleep between failed polls (0: spin on try_wait)
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
-  uint32_t done;
-  do {
+  for (;;) {
+    uint32_t done;
     asm volatile(
         "{\n"
         ".reg .pred p;\n"
@@ -90,7 +93,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "=r"(done)
         : "r"(a), "r"(parity)
         : "memory");
-  } while (!done);
+    if (done) break;
+    if (ECC_F3_WAIT_SLEEP) __nanosleep(ECC_F3_WAIT_SLEEP);
+  }
 }
 __device__ __forceinline__ void tma_load_4d(float* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
                                             int c3) {
