@@ -320,9 +320,10 @@ def run_b200(args):
         host.copy_(own.cpu())
         if not dist_on:
             def e2e_step():
-                return E.ecc_discrete_host(host, taus, chunk_planes=256).cpu()
-            api = ("paper_2510_20271_b200.ecc_discrete_host (256-plane chunks: the host->device copy of one "
-                   "chunk overlaps the kernel of the previous one)")
+                return E.ecc_discrete_host(host, taus, chunk_planes=64).cpu()
+            api = ("paper_2510_20271_b200.ecc_discrete_host (resident layout, 64-plane chunks: every plane "
+                   "crosses PCIe once; the planes already on the device are deposited while the next chunk "
+                   "is copied)")
         else:
             buf = D.alloc_padded_slab(P, (H, W), torch.float32, dev)
 

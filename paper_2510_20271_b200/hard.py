@@ -165,19 +165,32 @@ class _StreamState:
     cache: dict = {}
 
 
-def ecc_discrete_host(x_host: torch.Tensor, taus, chunk_planes: int = 64, device=None, return_hist: bool = False):
+RESIDENT_MAX_BYTES = 8 << 30   # ecc_discrete_host(resident=None): volumes up to this size stay in HBM
+
+
+def ecc_discrete_host(x_host: torch.Tensor, taus, chunk_planes: int = 64, device=None, return_hist: bool = False,
+                      resident=None):
     """Exact ECC of a 3D volume held in HOST memory, streamed to the GPU.
 
     The volume (float32 / uint8 / float64, [D, H, W], row-major) is cut into
-    z-chunks; the host-to-device copy of chunk k + 1 (plus its one-plane
-    halos) runs on a copy stream while the fused kernel deposits chunk k
-    (ecc_histogram_range) on the compute stream, so the end-to-end time is
-    the larger of the PCIe transfer and the compute instead of their sum, and
-    the volume need not fit in device memory.  Pass pinned memory
-    (``tensor.pin_memory()``) for asynchronous copies.  The result equals
-    ecc_discrete(x_host.cuda(), taus) bit for bit (histograms are exactly
-    additive over planes, hard.py:99-118; the tie-break is translation
-    invariant, coefficients.py:141-152).
+    z-chunks of ``chunk_planes`` planes whose host-to-device copies run on a
+    copy stream while the fused kernel (ecc_histogram_range) deposits the
+    planes already on the device, so the end-to-end time is the larger of
+    the PCIe transfer and the compute instead of their sum.  Two layouts:
+
+    * resident (default for volumes up to RESIDENT_MAX_BYTES): the chunks
+      land in one device copy of the volume, every plane crosses PCIe once,
+      and after chunk k arrives the kernel deposits every plane whose z + 1
+      neighbour is on the device; only the last chunk's deposit follows the
+      last copy, so small chunks leave a short tail.
+    * ring (``resident=False``, or larger volumes): two (chunk + 2)-plane
+      device buffers, each chunk copied with its one-plane halos, so the
+      volume need not fit in device memory.
+
+    Pass pinned memory (``tensor.pin_memory()``) for asynchronous copies.
+    The result equals ecc_discrete(x_host.cuda(), taus) bit for bit
+    (histograms are exactly additive over planes, hard.py:99-118; the
+    tie-break is translation invariant, coefficients.py:141-152).
     """
     if isinstance(x_host, np.ndarray):
         x_host = torch.from_numpy(np.ascontiguousarray(x_host))
@@ -193,6 +206,10 @@ def ecc_discrete_host(x_host: torch.Tensor, taus, chunk_planes: int = 64, device
     nb = len(ts)
     table, binning = ts.device_table(code, dev)
     cp = min(chunk_planes, D)
+    if resident is None:
+        resident = x_host.numel() * x_host.element_size() <= RESIDENT_MAX_BYTES
+    if resident:
+        return _ecc_discrete_host_resident(x_host, ts, cp, dev, code, table, binning, return_hist)
     key = (x_host.dtype, cp, H, W, nb, str(dev))
     st = _StreamState.cache.get(key)
     if st is None:
@@ -225,6 +242,42 @@ def ecc_discrete_host(x_host: torch.Tensor, taus, chunk_planes: int = 64, device
         ev = torch.cuda.Event()
         ev.record(main)
         freed[c % 2] = ev
+    curve = scan_device(total.reshape(1, -1), nb)[0]
+    return (curve, total) if return_hist else curve
+
+
+def _ecc_discrete_host_resident(x_host, ts, cp, dev, code, table, binning, return_hist):
+    D, H, W = (int(d) for d in x_host.shape)
+    nb = len(ts)
+    nchunks = (D + cp - 1) // cp
+    key = ("resident", x_host.dtype, D, H, W, nb, nchunks, str(dev))
+    st = _StreamState.cache.get(key)
+    if st is None:
+        st = {"vol": torch.empty((D, H, W), dtype=x_host.dtype, device=dev),
+              "parts": torch.empty((nchunks, nb + 1), dtype=torch.int64, device=dev),
+              "copy": torch.cuda.Stream(dev)}
+        _StreamState.cache = {key: st}   # one cached configuration
+    vol, parts, cs = st["vol"], st["parts"], st["copy"]
+    main = torch.cuda.current_stream(dev)
+    d = _lib.dims_arg(vol.shape)
+    cs.wait_stream(main)   # the previous call's kernels are done with vol and parts
+    a = 0                  # planes [0, a) deposited
+    for k in range(nchunks):
+        z0, z1 = k * cp, min((k + 1) * cp, D)
+        with torch.cuda.stream(cs):
+            vol[z0:z1].copy_(x_host[z0:z1], non_blocking=True)
+            copied = torch.cuda.Event()
+            copied.record(cs)
+        main.wait_event(copied)
+        b = D if z1 == D else z1 - 1   # plane p is deposited once plane p + 1 is on the device
+        if b > a:
+            _lib.check(_lib.lib().ecc_histogram_range(_lib.ptr(vol), code, 3, _lib.ptr(d), 1, a, b,
+                                                      _lib.ptr(table), _lib.ctypes.byref(binning),
+                                                      _lib.ptr(parts[k]), _lib.ctypes.c_void_p(main.cuda_stream)))
+        else:
+            parts[k].zero_()
+        a = max(a, b)
+    total = parts.sum(0)
     curve = scan_device(total.reshape(1, -1), nb)[0]
     return (curve, total) if return_hist else curve
 

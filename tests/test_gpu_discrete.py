@@ -422,20 +422,30 @@ class TestHostStreaming:
     """ecc_discrete_host: z-chunks copied on a side stream while the previous
     chunk is deposited; bit-exact with the device-resident call."""
 
-    @pytest.mark.parametrize("chunk", [1, 7, 64, 1000])
-    def test_chunks_equal_device_call(self, rng, chunk):
+    @pytest.mark.parametrize("resident", [None, False])
+    @pytest.mark.parametrize("chunk", [1, 2, 7, 36, 64, 1000])
+    def test_chunks_equal_device_call(self, rng, chunk, resident):
         x = rng.random((37, 45, 132)).astype(np.float32)
         ts = E.thresholds_from_range(float(x.min()), float(x.max()), 256)
         want_c, want_h = E.ecc_discrete(torch.from_numpy(x).cuda(), ts, return_hist=True)
         for host in (torch.from_numpy(x), torch.from_numpy(x).pin_memory()):
-            c, h = E.ecc_discrete_host(host, ts, chunk_planes=chunk, return_hist=True)
-            assert torch.equal(c, want_c) and torch.equal(h, want_h)
+            for _ in range(2):   # the second call reuses the cached device buffers
+                c, h = E.ecc_discrete_host(host, ts, chunk_planes=chunk, return_hist=True, resident=resident)
+                assert torch.equal(c, want_c) and torch.equal(h, want_h)
 
-    def test_uint8_and_generic_shapes(self, rng):
+    @pytest.mark.parametrize("resident", [None, False])
+    def test_uint8_and_generic_shapes(self, rng, resident):
         x = rng.integers(0, 256, (20, 31, 50), dtype=np.uint8)   # W % 4 != 0: generic kernel
         ts = E.ThresholdSet(np.arange(0.0, 256.0, 9.0))
-        c = E.ecc_discrete_host(x, ts, chunk_planes=6)
+        c = E.ecc_discrete_host(x, ts, chunk_planes=6, resident=resident)
         assert np.array_equal(c.cpu().numpy(), oracle.curve(x.astype(np.float64), ts.taus))
+
+    def test_single_plane_and_consecutive_volumes(self, rng):
+        ts = E.ThresholdSet(np.linspace(0.0, 1.0, 33))
+        for dims in ((1, 40, 64), (3, 40, 64), (3, 40, 64)):
+            x = torch.from_numpy(rng.random(dims).astype(np.float32)).pin_memory()
+            want = E.ecc_discrete(x.cuda(), ts)
+            assert torch.equal(E.ecc_discrete_host(x, ts, chunk_planes=2), want)
 
 
 class TestFastPathU8:

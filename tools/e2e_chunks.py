@@ -24,5 +24,9 @@ def timeit(fn, reps=8):
     torch.cuda.synchronize()
     return (time.perf_counter() - t0) * 1e3 / reps
 print(f"whole copy + kernel: {timeit(whole):.2f} ms")
-for cp in (32, 64, 128, 256, 512):
-    print(f"host streaming chunk {cp}: {timeit(lambda: E.ecc_discrete_host(host, ts, chunk_planes=cp).cpu()):.2f} ms")
+ref = whole()
+for res in (False, True):
+    for cp in (16, 32, 64, 128, 256):
+        assert torch.equal(E.ecc_discrete_host(host, ts, chunk_planes=cp, resident=res).cpu(), ref)
+        ms = timeit(lambda: E.ecc_discrete_host(host, ts, chunk_planes=cp, resident=res).cpu())
+        print(f"host streaming resident={res} chunk {cp}: {ms:.3f} ms")
