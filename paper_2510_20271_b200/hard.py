@@ -206,10 +206,17 @@ def ecc_discrete_host(x_host: torch.Tensor, taus, chunk_planes: int = 64, device
     nb = len(ts)
     table, binning = ts.device_table(code, dev)
     cp = min(chunk_planes, D)
-    if resident is None:
+    auto = resident is None
+    if auto:
         resident = x_host.numel() * x_host.element_size() <= RESIDENT_MAX_BYTES
     if resident:
-        return _ecc_discrete_host_resident(x_host, ts, cp, dev, code, table, binning, return_hist)
+        try:
+            return _ecc_discrete_host_resident(x_host, ts, cp, dev, code, table, binning, return_hist)
+        except torch.cuda.OutOfMemoryError:
+            if not auto:
+                raise
+            _StreamState.cache = {}   # no room for the whole volume: stream through the ring
+            torch.cuda.empty_cache()
     key = (x_host.dtype, cp, H, W, nb, str(dev))
     st = _StreamState.cache.get(key)
     if st is None:
