@@ -289,7 +289,9 @@ extern "C" int ecc_threshold_table(const double* taus, int64_t nb, int dtype, vo
     LutEntryH* lut = reinterpret_cast<LutEntryH*>(t + ((nb + 2 + 1) & ~int64_t(1)));
     int64_t cells = 1;
     while (cells < nb) cells <<= 1;
-    if (cells == nb && nb >= 2) {
+    // every cell count tried here must stay within ecc_threshold_table_bytes'
+    // cap (1 << 16 cells), which sized the caller's buffer
+    if (cells == nb && nb >= 2 && cells <= (1 << 16)) {
       // power-of-two threshold count: try the boundary-aligned grid first
       float sc = 0.f, bi = 0.f;
       if (build_lut(t + 1, nb, (int)cells, &sc, &bi, lut, 1)) {

@@ -149,3 +149,22 @@ def test_threshold_table_edge_ranks_exact():
         got = rbin[rank]
         want = np.searchsorted(taus, probes.astype(np.float64), side="left")
         assert np.array_equal(got, want), (lo, hi, nb)
+
+
+@pytest.mark.parametrize("nb", [1 << 16, 1 << 17, 1 << 18, 1 << 20])
+def test_threshold_table_large_power_of_two_stays_in_buffer(nb):
+    """Regression (advisor round 1): a power-of-two threshold count above the
+    cell cap used to build a cell table past the size ecc_threshold_table_bytes
+    reports.  The table must fit the reported size: a guard region after it
+    stays untouched."""
+    from paper_2510_20271_b200 import _lib
+
+    taus = np.linspace(0.0, 1.0, nb + 1)[1:]
+    nbytes = int(_lib.lib().ecc_threshold_table_bytes(nb, 1))
+    guard = 1 << 16
+    buf = np.full(nbytes // 4 + guard, np.float32(1.2345), dtype=np.float32)
+    b = _lib.Binning()
+    rc = _lib.lib().ecc_threshold_table(_lib.ptr(taus), nb, 1, _lib.ptr(buf), ctypes.byref(b))
+    assert rc == 0
+    assert np.all(buf[nbytes // 4:] == np.float32(1.2345)), "threshold table wrote past its reported size"
+    assert b.lut_cells <= (1 << 16)
