@@ -56,12 +56,13 @@ typedef struct {
   float lut_bias;
   int32_t lut_cells;
   int32_t lut_ok;
-  /* 1: every threshold lies in the first or last 1/256 of its cell, and
-   * the table also holds the boundary thresholds tE[cells + 1] and the
-   * rank -> bin map rbin[cells + 2] after the cell table; the rank kernel then
-   * looks a threshold up only for voxels in those edge sub-cells. */
+  /* 1: every threshold lies in the first or last 1/lut_edge_sub of its
+   * cell (lut_edge_sub = 1024, else 256), and the table also holds the
+   * boundary thresholds tE[cells + 1] and the rank -> bin map
+   * rbin[cells + 2] after the cell table; the rank kernel then looks a
+   * threshold up only for voxels in those edge sub-cells. */
   int32_t lut_edge;
-  int32_t lut_pad;
+  int32_t lut_edge_sub;
 } ecc_binning;
 
 /* Version string and thread-local description of the last failure. */

@@ -34,7 +34,7 @@ class Binning(ctypes.Structure):
     _fields_ = [("t0", ctypes.c_double), ("inv_w", ctypes.c_double), ("nbins", ctypes.c_int64),
                 ("mode", ctypes.c_int32), ("max_correction", ctypes.c_int32), ("lut_scale", ctypes.c_float),
                 ("lut_bias", ctypes.c_float), ("lut_cells", ctypes.c_int32), ("lut_ok", ctypes.c_int32),
-                ("lut_edge", ctypes.c_int32), ("lut_pad", ctypes.c_int32)]
+                ("lut_edge", ctypes.c_int32), ("lut_edge_sub", ctypes.c_int32)]
 
 
 class SoftParams(ctypes.Structure):

@@ -60,6 +60,8 @@ struct Geom {
   int64_t items;
   unsigned int* wq = nullptr;   // dynamic work queue (rank kernel): next unit, zeroed before the launch
   int zunit = 0;                // planes per dynamic unit (0: static partition)
+  float r4_magic = 0.f;         // edge4 rank (R4): M = 2^23 + 1024 + z
+  uint32_t r4_emask = 0;        //                  edge test mask 0x3FF & ~(2z - 1)
 };
 
 struct LutEntry {
@@ -834,6 +836,308 @@ __device__ __forceinline__ uint32_t rank_of(float x, uint32_t m, float sc, float
   return EDGE ? rank_edge(x, m, sc, bi, fc) : bin4_lut(x, m, sc, bi, fc);
 }
 
+
+// ---- edge4 ranking (EK = 2): the edge-table rank with a fix-up pass ------
+// With S = lut_edge_sub sub-cells per cell verified by the host (1024 or 256,
+// ecc_host.cu build_edge) and z = 1024 / S, the device computes
+//   k = RZ(g * 1024 cells + M),  M = 2^23 + 1024 + z,  g = sat(fma(x, scale, bias)),
+// i.e. m = sub + 1024 + z in the mantissa with sub = floor(g * 1024 cells).
+// The field f = bits 8..23 of k & ~3 = 4 (b + 1), b = floor((sub + z) / 1024):
+// the nearest cell boundary for the first / last z of a cell's 1024
+// sub-cells (exactly the host's first / last 1/S), the cell otherwise.  Those
+// edge voxels -- (k & 0x3FF & ~(2z - 1)) == 0 -- compare against the boundary
+// threshold: rank = b + 1 - [x <= tE[b]], i.e. f -= 4.  That is the host's
+// edge_rank for every float32 (K2 "edge4" has the derivation), kept
+// pre-multiplied by 4 so the 16-bit field is the byte offset of the voxel's
+// counter.  Interior voxels cost one FFMA.SAT, half an FFMA2 (two voxels per
+// fma.rz.f32x2), half a PRMT + LOP3 and the edge test; edge voxels (1/512 of
+// uniform data at S = 1024) are flagged in a mask and fixed in shared memory
+// after the row is stored.
+#ifndef ECC_R4_ROT
+#define ECC_R4_ROT 1
+#endif
+#ifndef ECC_R4_IDP
+#define ECC_R4_IDP 1   // deposit operands by IDP.4A / IDP.2A (FMA pipe) instead of PRMT (ALU)
+#endif
+__device__ __forceinline__ int dp4a_s8(uint32_t a, uint32_t b, int c) {   // sum of signed byte products + c
+  int r;
+  asm("dp4a.s32.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
+}
+__device__ __forceinline__ uint32_t dp2a_lo(uint32_t a, uint32_t b, uint32_t c) {   // a.h0 b.b0 + a.h1 b.b1 + c
+  uint32_t r;
+  asm("dp2a.lo.u32.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
+}
+struct R4 {
+  float sc, bi, fc, magic;   // scale, bias, 1024 cells, M
+  uint32_t emask;            // 0x3FF & ~(2z - 1)
+  uint32_t tE_s;             // shared-memory byte address of tE (TEG = false)
+  const float* tE_g;         // global tE (TEG = true; L1-cached, read only by edge voxels)
+  uint32_t one;              // a run-time 1 (keeps multiplies by it on the FMA pipe)
+};
+__device__ __forceinline__ uint64_t f2pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void fma2_rz(float a0, float a1, uint64_t b2, uint64_t c2, uint32_t& r0, uint32_t& r1) {
+  uint64_t r;
+  asm("fma.rz.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2pack(a0, a1)), "l"(b2), "l"(c2));
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(r0), "=r"(r1) : "l"(r));
+}
+template <bool TEG>
+__device__ __forceinline__ float r4_boundary(const R4& r, uint32_t f) {   // tE[f / 4 - 1]
+  if (TEG) return __ldg(r.tE_g + (f >> 2) - 1);
+  float t;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(t) : "r"(r.tE_s + f - 4u));
+  return t;
+}
+// full edge4 field of one value (the segment-edge voxels and the fix-up)
+template <bool TEG>
+__device__ __forceinline__ uint32_t rank4_field(float x, const R4& r) {
+  const float gg = __saturatef(__fmaf_rn(x, r.sc, r.bi));
+  const uint32_t k = __float_as_uint(__fmaf_rz(gg, r.fc, r.magic));
+  uint32_t f = (k >> 8) & 0xFFFCu;
+  if ((k & r.emask) == 0u && !(x > r4_boundary<TEG>(r, f))) f -= 4u;
+  return f;
+}
+// Rank a 34-voxel row segment (x - 1 .. x + 32) into 16 SWAR words + the
+// edge word.  ROT: lanes with (lane >> 2) odd take the two float4 chunks of a
+// pair in the other order, which makes the LDS.128 of a 40-float staged row
+// pitch (per-warp TMA boxes) free of bank conflicts; the words go to the
+// matching (dynamic) offsets.
+template <bool CHECK, bool TEG, bool ROT>
+__device__ __forceinline__ void rank4_rowseg(const float* src, uint32_t* dw, uint32_t* de, const R4& r) {
+  const float4* s4 = reinterpret_cast<const float4*>(src);
+  const uint64_t fc2 = f2pack(r.fc, r.fc), mg2 = f2pack(r.magic, r.magic);
+  const int q = ROT ? (int)((threadIdx.x >> 2) & 1u) : 0;
+  uint32_t emask = 0;   // bit i: voxel i lies in an edge sub-cell
+#pragma unroll
+  for (int gi = 0; gi < 4; ++gi) {
+    const int g = (ROT && ECC_R4_ROT) ? (gi ^ q) : gi;   // chunk pair: voxels 4g..4g+3 and 16+4g..16+4g+3
+    const float4 lo = s4[g], hi = s4[4 + g];
+    const float a[4] = {lo.x, lo.y, lo.z, lo.w}, b[4] = {hi.x, hi.y, hi.z, hi.w};
+    uint32_t w[4];
+    uint32_t em = 0;   // bits m (voxel 4g + m) and 16 + m (voxel 16 + 4g + m)
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      uint32_t ka, kb;
+      fma2_rz(__saturatef(__fmaf_rn(a[m], r.sc, r.bi)), __saturatef(__fmaf_rn(b[m], r.sc, r.bi)), fc2, mg2, ka, kb);
+      w[m] = prmt(ka, kb, 0x6521u) & 0xFFFCFFFCu;
+      bool ea = (ka & r.emask) == 0u, eb = (kb & r.emask) == 0u;
+      if (CHECK) {   // NaN = TMA out-of-bounds fill: sentinel, never fixed up
+        const bool na = a[m] != a[m], nbn = b[m] != b[m];
+        if (na) w[m] = (w[m] & 0xFFFF0000u) | BSENT;
+        if (nbn) w[m] = (w[m] & 0x0000FFFFu) | (BSENT << 16);
+        ea = ea && !na;
+        eb = eb && !nbn;
+      }
+      if (ea) em |= 1u << m;
+      if (eb) em |= 1u << (16 + m);
+    }
+    reinterpret_cast<uint4*>(dw)[g] = make_uint4(w[0], w[1], w[2], w[3]);
+    emask |= ROT ? (em << (4 * g)) : (em << (4 * gi));
+  }
+  const float el = src[-1], er = src[32];
+  const uint32_t bl = el != el ? BSENT : rank4_field<TEG>(el, r);
+  const uint32_t br = er != er ? BSENT : rank4_field<TEG>(er, r);
+  *de = bl | (br << 16);
+  // fix-up: the edge voxels compare against their boundary threshold (this
+  // thread wrote the words above, so it may update them in place)
+  while (emask) {
+    const int i = __ffs(emask) - 1;
+    emask &= emask - 1u;
+    const float x = src[i];
+    const float gg = __saturatef(__fmaf_rn(x, r.sc, r.bi));
+    const uint32_t f = (__float_as_uint(__fmaf_rz(gg, r.fc, r.magic)) >> 8) & 0xFFFCu;
+    if (!(x > r4_boundary<TEG>(r, f))) dw[i & 15] -= 4u << ((i >> 4) << 4);
+  }
+}
+
+// Per-warp staged planes of the rank4 kernel: a 40 x 32 float TMA box per
+// warp (columns xs - 4 .. xs + 35, rows y0 - 1 .. y0 + 30), rank plane layout
+// as bin_plane's.
+constexpr int WPITCH = 40;
+constexpr int WSTAGE = WPITCH * 32;
+constexpr uint32_t WSTAGE_BYTES = WSTAGE * 4;
+__device__ __forceinline__ void rank4_plane_w(const float* stage, uint32_t* B, bool plane_in, int xs, int y0, int W,
+                                              int H, const R4& r4) {
+  const int row = threadIdx.x & 31, seg = threadIdx.x >> 5;
+  uint32_t* dw = B + row * BROW + 16 * seg;
+  uint32_t* de = B + BEDGE + seg * 32 + row;
+  const int y = y0 - 1 + row;
+  if (!plane_in || y < 0 || y >= H || xs >= W) {
+    const uint32_t s2 = BSENT | (BSENT << 16);
+    uint4* d4 = reinterpret_cast<uint4*>(dw);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) d4[k] = make_uint4(s2, s2, s2, s2);
+    *de = s2;
+    return;
+  }
+  const float* src = stage + row * WPITCH + 4;
+  if (xs + 32 > W)
+    rank4_rowseg<true, true, true>(src, dw, de, r4);
+  else
+    rank4_rowseg<false, true, true>(src, dw, de, r4);
+}
+
+// Deferred-fix variant for the per-warp kernel.  The row is ranked without
+// threshold lookups; a lane with exactly one edge voxel (the common case:
+// ~6 % of rows at 1024 sub-cells) loads that voxel's boundary threshold now
+// and applies the fix after the finalize step, so the global-memory latency
+// hides behind independent work; rows with two or more edge voxels (rare)
+// are fixed at once while the staged plane is still valid.
+struct R4Fix {       // *(u32 *)addr -= dec unless x > t
+  uint32_t addr;     // shared-memory byte address of the rank word (0: none)
+  uint32_t dec;
+  float x, t;
+};
+struct R4Row {       // what rank4_rowseg_d leaves for the fix-up decision
+  uint32_t emask;    // interior edge voxels
+  uint32_t fl, fr;   // x-edge fields, not yet fixed
+  bool el_e, er_e;   // x-edge voxels in edge sub-cells
+};
+template <bool CHECK>
+__device__ __forceinline__ R4Row rank4_rowseg_d(const float* src, uint32_t* dw, uint32_t* de, const R4& r) {
+  const float4* s4 = reinterpret_cast<const float4*>(src);
+  const uint64_t fc2 = f2pack(r.fc, r.fc), mg2 = f2pack(r.magic, r.magic);
+  const int q = ECC_R4_ROT ? (int)((threadIdx.x >> 2) & 1u) : 0;
+  const uint32_t e2 = r.emask | (r.emask << 16);
+  R4Row o;
+  o.emask = 0;
+  uint32_t X[8];   // interior flags as 0x00 / 0xFF bytes (edge-mask gather, see below)
+#pragma unroll
+  for (int gi = 0; gi < 4; ++gi) {
+    const int g = gi ^ q;   // chunk pair: voxels 4g..4g+3 and 16+4g..16+4g+3 (rotated: no LDS.128 bank conflicts)
+    const float4 lo = s4[g], hi = s4[4 + g];
+    const float a[4] = {lo.x, lo.y, lo.z, lo.w}, b[4] = {hi.x, hi.y, hi.z, hi.w};
+    uint32_t w[4], eg[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      uint32_t ka, kb;
+      fma2_rz(__saturatef(__fmaf_rn(a[m], r.sc, r.bi)), __saturatef(__fmaf_rn(b[m], r.sc, r.bi)), fc2, mg2, ka, kb);
+      w[m] = prmt(ka, kb, 0x6521u) & 0xFFFCFFFCu;
+      // edge test of the pair as 16-bit lanes: ((k & emask) | 0x8000) - 1 keeps
+      // bit 15 (31) set exactly for interior voxels
+      eg[m] = mad_fma((prmt(ka, kb, 0x5410u) & e2) | 0x80008000u, r.one, 0xFFFEFFFFu);
+      if (CHECK) {   // NaN = TMA out-of-bounds fill: sentinel, never an edge voxel
+        const bool na = a[m] != a[m], nbn = b[m] != b[m];
+        if (na) {
+          w[m] = (w[m] & 0xFFFF0000u) | BSENT;
+          eg[m] |= 0x00008000u;
+        }
+        if (nbn) {
+          w[m] = (w[m] & 0x0000FFFFu) | (BSENT << 16);
+          eg[m] |= 0x80000000u;
+        }
+      }
+    }
+    reinterpret_cast<uint4*>(dw)[g] = make_uint4(w[0], w[1], w[2], w[3]);
+    // X[2 gi + h] bytes = interior flags of voxels 4g + 2h, 4g + 2h + 1,
+    // 16 + 4g + 2h, 16 + 4g + 2h + 1
+    X[2 * gi] = prmt(eg[0], eg[1], 0xFBD9u);
+    X[2 * gi + 1] = prmt(eg[2], eg[3], 0xFBD9u);
+  }
+  // select tree (as cmp_word): bit 8 a + k of the result = byte a of X[k];
+  // inverted, it is the edge mask in the order voxel(8 a + k) (r4_voxel)
+  {
+    const uint32_t m01 = (X[0] & 0x55555555u) | (X[1] & 0xAAAAAAAAu);
+    const uint32_t m23 = (X[2] & 0x55555555u) | (X[3] & 0xAAAAAAAAu);
+    const uint32_t m45 = (X[4] & 0x55555555u) | (X[5] & 0xAAAAAAAAu);
+    const uint32_t m67 = (X[6] & 0x55555555u) | (X[7] & 0xAAAAAAAAu);
+    const uint32_t m03 = (m01 & 0x33333333u) | (m23 & 0xCCCCCCCCu);
+    const uint32_t m47 = (m45 & 0x33333333u) | (m67 & 0xCCCCCCCCu);
+    o.emask = ~((m03 & 0x0F0F0F0Fu) | (m47 & 0xF0F0F0F0u));
+  }
+  const float el = src[-1], er = src[32];
+  const uint32_t kl = __float_as_uint(__fmaf_rz(__saturatef(__fmaf_rn(el, r.sc, r.bi)), r.fc, r.magic));
+  const uint32_t kr = __float_as_uint(__fmaf_rz(__saturatef(__fmaf_rn(er, r.sc, r.bi)), r.fc, r.magic));
+  const bool nl = el != el, nr = er != er;
+  o.fl = nl ? BSENT : (kl >> 8) & 0xFFFCu;
+  o.fr = nr ? BSENT : (kr >> 8) & 0xFFFCu;
+  o.el_e = !nl && (kl & r.emask) == 0u;
+  o.er_e = !nr && (kr & r.emask) == 0u;
+  *de = o.fl | (o.fr << 16);
+  return o;
+}
+// voxel index of bit j of rank4_rowseg_d's edge mask: bit 8 a + k is byte a of
+// X[k], k = 2 gi + h, chunk g = gi ^ q; bytes 0..3 = voxels 4g + 2h, + 1, 16 + 4g + 2h, + 1
+__device__ __forceinline__ int r4_voxel(int j) {
+  const int a = j >> 3, k = j & 7;
+  const int g = (k >> 1) ^ (ECC_R4_ROT ? (int)((threadIdx.x >> 2) & 1u) : 0);
+  return ((a >> 1) << 4) + 4 * g + 2 * (k & 1) + (a & 1);
+}
+__device__ __forceinline__ void r4_apply(const R4Fix& fx) {
+  if (fx.addr != 0u && !(fx.x > fx.t)) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(fx.addr) : "memory");
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(fx.addr), "r"(v - fx.dec) : "memory");
+  }
+}
+// rank4_plane_w with deferred fixes
+__device__ __forceinline__ R4Fix rank4_plane_wd(const float* stage, uint32_t* B, bool plane_in, int xs, int y0,
+                                                int W, int H, const R4& r4) {
+  const int row = threadIdx.x & 31, seg = threadIdx.x >> 5;
+  uint32_t* dw = B + row * BROW + 16 * seg;
+  uint32_t* de = B + BEDGE + seg * 32 + row;
+  const int y = y0 - 1 + row;
+  const float* src = stage + row * WPITCH + 4;
+  R4Row o{0u, 0u, 0u, false, false};
+  if (!plane_in || y < 0 || y >= H || xs >= W) {
+    const uint32_t s2 = BSENT | (BSENT << 16);
+    uint4* d4 = reinterpret_cast<uint4*>(dw);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) d4[k] = make_uint4(s2, s2, s2, s2);
+    *de = s2;
+  } else if (xs + 32 > W) {
+    o = rank4_rowseg_d<true>(src, dw, de, r4);
+  } else {
+    o = rank4_rowseg_d<false>(src, dw, de, r4);
+  }
+  const int cnt = __popc(o.emask) + (int)o.el_e + (int)o.er_e;
+  R4Fix fx{0u, 0u, 0.f, 0.f};
+  if (cnt >= 2) {   // rare: every edge voxel of this row now
+    uint32_t em = o.emask;
+    while (em) {
+      const int i = r4_voxel(__ffs(em) - 1);
+      em &= em - 1u;
+      const float x = src[i];
+      const uint32_t f =
+          (__float_as_uint(__fmaf_rz(__saturatef(__fmaf_rn(x, r4.sc, r4.bi)), r4.fc, r4.magic)) >> 8) & 0xFFFCu;
+      if (!(x > __ldg(r4.tE_g + (f >> 2) - 1))) dw[i & 15] -= 4u << ((i >> 4) << 4);
+    }
+    uint32_t e = *de;
+    if (o.el_e && !(src[-1] > __ldg(r4.tE_g + (o.fl >> 2) - 1))) e -= 4u;
+    if (o.er_e && !(src[32] > __ldg(r4.tE_g + (o.fr >> 2) - 1))) e -= 4u << 16;
+    *de = e;
+  } else if (cnt == 1) {
+    // the row's single edge voxel: threshold load issued now, fix applied later (r4_apply)
+    float x;
+    uint32_t f;
+    if (o.emask) {
+      const int i = r4_voxel(__ffs(o.emask) - 1);
+      x = src[i];
+      f = (__float_as_uint(__fmaf_rz(__saturatef(__fmaf_rn(x, r4.sc, r4.bi)), r4.fc, r4.magic)) >> 8) & 0xFFFCu;
+      fx.addr = smem_u32(dw + (i & 15));
+      fx.dec = 4u << ((i >> 4) << 4);
+    } else if (o.el_e) {
+      x = src[-1];
+      f = o.fl;
+      fx.addr = smem_u32(de);
+      fx.dec = 4u;
+    } else {
+      x = src[32];
+      f = o.fr;
+      fx.addr = smem_u32(de);
+      fx.dec = 4u << 16;
+    }
+    fx.x = x;
+    fx.t = __ldg(r4.tE_g + (f >> 2) - 1);
+  }
+  return fx;
+}
+
 // bin a 34-voxel row segment (x - 1 .. x + 32) of the staged f32 plane;
 // CHECK: NaN (TMA out-of-bounds fill) -> sentinel for every voxel, else
 // only for the two edge voxels
@@ -921,9 +1225,10 @@ __device__ __forceinline__ void rank_plane_u8(const unsigned char* stage, uint32
 }
 
 // bin the staged plane into a bin plane: warp -> x segment, lane -> row
-template <bool EDGE>
+template <int EK>
 __device__ __forceinline__ void bin_plane(const float* stage, uint32_t* B, bool plane_in, int x0, int y0, int W,
-                                          int H, uint32_t lut_m, float sc, float bi, float fcells) {
+                                          int H, uint32_t lut_m, float sc, float bi, float fcells, const R4& r4) {
+  constexpr bool EDGE = EK != 0;
   const int row = threadIdx.x & 31, seg = threadIdx.x >> 5;
   uint32_t* dw = B + row * BROW + 16 * seg;
   uint32_t* de = B + BEDGE + seg * 32 + row;
@@ -937,20 +1242,27 @@ __device__ __forceinline__ void bin_plane(const float* stage, uint32_t* B, bool 
     return;
   }
   const float* src = stage + row * PITCH + 4 + 32 * seg;
-  if (xs + 32 > W)
+  if (EK == 2) {   // 2-D kernel: tE in shared memory, shared 140-float stage rows
+    if (xs + 32 > W)
+      rank4_rowseg<true, false, false>(src, dw, de, r4);
+    else
+      rank4_rowseg<false, false, false>(src, dw, de, r4);
+  } else if (xs + 32 > W) {
     bin_rowseg<true, EDGE>(src, dw, de, lut_m, sc, bi, fcells);
-  else
+  } else {
     bin_rowseg<false, EDGE>(src, dw, de, lut_m, sc, bi, fcells);
+  }
 }
 
 #ifndef ECC_F3_MINB
 #define ECC_F3_MINB 5   // resident CTAs per SM the register budget is sized for (96 registers;
                           // 5 x 44.7 KB shared fits too): 1024^3 591 vs 583 Gvoxel/s at 4
 #endif
-template <int DEP, bool WS, bool EDGE, bool U8 = false>
+template <int DEP, bool WS, int EK, bool U8 = false>
 __global__ void __launch_bounds__(NT, ECC_F3_MINB)
 ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* __restrict__ table_g, int nb,
                       int cells, int hsize, float lut_scale, float lut_bias, unsigned long long* __restrict__ hist) {
+  constexpr bool EDGE = EK != 0;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr uint32_t STAGE_BYTES = U8 ? U8_PLANE_BYTES : PLANE_BYTES;
   float* stage = reinterpret_cast<float*>(smem_raw);                            // one staged plane (TMA)
@@ -979,8 +1291,12 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
   __syncthreads();
   // table base biased so that the float bits index it directly (mod 2^32):
   // 2-rank mode by key = 0x4B000000 + cell, edge mode by (key256 + 1) >> 6
-  const uint32_t lut_m = smem_u32(s_t) - (EDGE ? 0x012C0000u : 0x2C000000u);
-  const float fcells = EDGE ? (float)(256 * cells) : (float)cells;
+  // table base: edge4 adds the field to the plain address; the older ranks
+  // index a biased base with the float bits (2-rank: key = 0x4B000000 + cell,
+  // edge: (key256 + 1) >> 6)
+  const uint32_t lut_m = smem_u32(s_t) - (EK == 2 ? 0u : EDGE ? 0x012C0000u : 0x2C000000u);
+  const float fcells = EK == 2 ? (float)(1024 * cells) : EDGE ? (float)(256 * cells) : (float)cells;
+  const R4 r4{lut_scale, lut_bias, fcells, g.r4_magic, g.r4_emask, smem_u32(s_t), nullptr, (uint32_t)g.one};
   const int nranks = U8 ? 256 : EDGE ? cells + 2 : 2 * (cells + 1);
   const uint32_t dummy_off = (uint32_t)(nranks + lane);   // dummy counter index (< 2^15)
   const uint32_t one = (uint32_t)g.one;
@@ -1139,7 +1455,7 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
       if (U8)
         rank_plane_u8(reinterpret_cast<const unsigned char*>(stage), bbuf + (p & 1) * BPLANE, pin, x0, y0, g.W, g.H);
       else
-        bin_plane<EDGE>(stage, bbuf + (p & 1) * BPLANE, pin, x0, y0, g.W, g.H, lut_m, lut_scale, lut_bias, fcells);
+        bin_plane<EK>(stage, bbuf + (p & 1) * BPLANE, pin, x0, y0, g.W, g.H, lut_m, lut_scale, lut_bias, fcells, r4);
       if (WS) {
         if (pin) round_done(p);
         else __syncwarp();
@@ -1216,7 +1532,7 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
           rank_plane_u8(reinterpret_cast<const unsigned char*>(stage), bbuf + (p & 1) * BPLANE, pin, x0, y0, g.W,
                         g.H);
         else
-          bin_plane<EDGE>(stage, bbuf + (p & 1) * BPLANE, pin, x0, y0, g.W, g.H, lut_m, lut_scale, lut_bias, fcells);
+          bin_plane<EK>(stage, bbuf + (p & 1) * BPLANE, pin, x0, y0, g.W, g.H, lut_m, lut_scale, lut_bias, fcells, r4);
         if (WS) {
           if (pin) round_done(p);
           else __syncwarp();
@@ -1295,7 +1611,8 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
           // bits j, j+16 of the nonzero mask -> byte masks -> one LOP3.
           uint32_t Wm[16];
           if (DEP == 1) {
-            const uint32_t d2 = dummy_off | (dummy_off << 16);
+            const uint32_t dof = EK == 2 ? 4u * dummy_off : dummy_off;   // edge4 ranks are byte offsets
+            const uint32_t d2 = dof | (dof << 16);
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
               const uint32_t keep = prmt(any << (15 - j), 0u, 0xBB99u);
@@ -1310,9 +1627,16 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
             // even voxels: nibble moved up into the byte's high half; odd: already there
             const uint32_t bq = (i & 1) ? (Q[i >> 3] & 0xF0F0F0F0u) : ((Q[i >> 3] << 4) & 0xF0F0F0F0u);
             const int c16 = (int)prmt(bq, 0u, sel);
-            if (DEP == 0) {
+            if (DEP == 2) {   // edge4: the field is the byte offset, every voxel deposits
+              const uint32_t addr = hbase + (i < 16 ? prmt(Ro.w[i], 0u, 0x4410u) : prmt(Ro.w[i - 16], 0u, 0x4432u));
+              asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(addr), "r"(c16) : "memory");
+            } else if (DEP == 0) {
               const uint32_t idx = i < 16 ? (Ro.w[i] & 0xFFFFu) : (Ro.w[i - 16] >> 16);
               if (c16) atomicAdd(s_hist + idx, c16);
+            } else if (EK == 2) {   // byte offsets
+              const uint32_t addr = i < 16 ? madhi_fma(mul_fma(Wm[i], one << 16), 1u << 16, hbase)
+                                           : mad_fma(shr_fma<16>(Wm[i - 16]), one, hbase);
+              asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(addr), "r"(c16) : "memory");
             } else {
               if (ECC_F3_FMA_DEP) {   // counter address on the FMA pipe: 4 * lane + base
                 const uint32_t addr = i < 16 ? madhi_fma(mul_fma(Wm[i], one << 16), 1u << 18, hbase)
@@ -1334,6 +1658,391 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
   if (cur_n >= 0) flush(cur_n);
 }
 
+template <int DEP>
+__global__ void __launch_bounds__(NT, ECC_F3_MINB)
+ecc_rank4_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* __restrict__ table_g, int nb,
+                 int cells, int hsize, float lut_scale, float lut_bias, unsigned long long* __restrict__ hist) {
+  constexpr int EK = 2;
+  constexpr bool EDGE = true, WS = true, U8 = false;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* stage_all = reinterpret_cast<float*>(smem_raw);                         // NW per-warp staged planes (TMA)
+  uint32_t* bbuf = reinterpret_cast<uint32_t*>(smem_raw + NW * WSTAGE_BYTES);     // two rank planes
+  uint64_t* bars = reinterpret_cast<uint64_t*>(bbuf + 2 * BPLANE);               // one mbarrier per warp
+  unsigned int* s_unit = reinterpret_cast<unsigned int*>(bars + NW);            // dynamic schedule: the CTA's unit
+  int* s_hist = reinterpret_cast<int*>(bars + NW + 1);                          // cells + 2 ranks (+ 32 dummies), 16 c
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const float* tab_g = reinterpret_cast<const float*>(table_g);
+  const LutEntry* lut_g = reinterpret_cast<const LutEntry*>(tab_g + ((nb + 2 + 1) & ~1));
+  // edge mode: boundary thresholds and the rank -> bin map follow the cell table
+  const float* tE_g = reinterpret_cast<const float*>(lut_g + cells + 1);
+  const int* rbin_g = reinterpret_cast<const int*>(tE_g + cells + 1);
+  for (int i = threadIdx.x; i < hsize; i += NT) s_hist[i] = 0;
+  init_sentinels(bbuf);
+  if (threadIdx.x == 0) {
+    for (int w = 0; w < NW; ++w) mbar_init(&bars[w], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+  }
+  __syncthreads();
+  float* stage = stage_all + warp * WSTAGE;   // this warp's staged plane: rows y0 - 1 .., columns xs - 4 .. xs + 35
+  uint64_t* bar = &bars[warp];
+  // table base biased so that the float bits index it directly (mod 2^32):
+  // 2-rank mode by key = 0x4B000000 + cell, edge mode by (key256 + 1) >> 6
+  // table base: edge4 adds the field to the plain address; the older ranks
+  // index a biased base with the float bits (2-rank: key = 0x4B000000 + cell,
+  // edge: (key256 + 1) >> 6)
+  // edge4 ranks, boundary thresholds read from global memory (L1) by the rare edge voxels
+  const R4 r4{lut_scale, lut_bias, (float)(1024 * cells), g.r4_magic, g.r4_emask, 0u, tE_g, (uint32_t)g.one};
+  const int nranks = U8 ? 256 : EDGE ? cells + 2 : 2 * (cells + 1);
+  const uint32_t dummy_off = (uint32_t)(nranks + lane);   // dummy counter index (< 2^15)
+  const uint32_t one = (uint32_t)g.one;
+  const uint32_t two = one << 1;
+  const uint32_t hbase = smem_u32(s_hist);
+  // fold the rank counters (16 c per voxel) into the global bins: rank v is
+  // bin b(v / 2) + v % 2; runs of ranks with the same bin are summed first
+  auto flush = [&](int64_t item) {
+    unsigned long long* h = hist + item * (nb + 1);
+    const int per = (nranks + NT - 1) / NT;
+    const int v0 = threadIdx.x * per, v1 = min(v0 + per, nranks);
+    long long acc = 0;
+    int cur = -1;
+    for (int v = v0; v < v1; ++v) {
+      const int c = s_hist[v];
+      s_hist[v] = 0;
+      if (!c) continue;
+      int bin;
+      if (U8) {   // searchsorted-left of the value over the float32 thresholds
+        int lo = 0, hi = nb;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (tab_g[mid + 1] < (float)v) lo = mid + 1; else hi = mid;
+        }
+        bin = lo;
+      } else {
+        bin = EDGE ? rbin_g[v] : lut_g[v >> 1].b + (v & 1);
+      }
+      if (bin != cur) {
+        if (cur >= 0 && acc) atomicAdd(h + cur, (unsigned long long)(acc >> 4));
+        cur = bin;
+        acc = 0;
+      }
+      acc += c;
+    }
+    if (cur >= 0 && acc) atomicAdd(h + cur, (unsigned long long)(acc >> 4));
+  };
+
+  uint32_t phase = 0;
+  int64_t cur_n = -1;
+  BOff rm, rp;   // per tile (brow_dn / brow_up)
+
+  // work partition: see ecc_fast3d_kernel
+  const int64_t Dw = (int64_t)(g.ze - g.zb);
+  const int64_t T = g.items;
+  const int64_t G = gridDim.x, bx = blockIdx.x;
+  int64_t u, u_end, L, zbase;
+  if (g.zchunks > 0) {
+    const int64_t k = g.zchunks;
+    const int64_t K = k * T * Dw / G;
+    if (bx < k * T) {
+      const int64_t sg = bx / T, t = bx % T;
+      zbase = K * sg / k;
+      L = K * (sg + 1) / k - zbase;
+      u = t * L;
+      u_end = u + L;
+    } else {
+      const int64_t r = bx - k * T, R = G - k * T;
+      zbase = K;
+      L = Dw - K;
+      u = T * L * r / R;
+      u_end = T * L * (r + 1) / R;
+    }
+  } else {
+    zbase = 0;
+    L = Dw;
+    u = T * Dw * bx / G;
+    u_end = T * Dw * (bx + 1) / G;
+  }
+  int64_t pending = 0;
+  // dynamic mode (g.zunit > 0): units of zunit planes of one tile, z-chunk
+  // major (CTAs working at the same time sit on neighbouring tiles at the same
+  // depth), handed out by one global counter.  The warp scheduler favours the
+  // oldest CTAs of an SM, so equal static shares finish staggered (measured:
+  // 0.53 ... 1.0 of the kernel time) and the SM runs its tail with one or two
+  // CTAs; with a queue the faster CTAs take more units and all finish together.
+  const int64_t nzc = g.zunit > 0 ? (Dw + g.zunit - 1) / g.zunit : 0;
+  const int64_t nunits = nzc * T;
+  if (g.zunit > 0) { u = 0; u_end = 1; }
+  while (u < u_end) {
+    int64_t tile, seg, z0;
+    if (g.zunit > 0) {
+      __syncthreads();   // everyone is done with the previous unit's s_unit
+      if (threadIdx.x == 0) *s_unit = atomicAdd(g.wq, 1u);
+      __syncthreads();
+      const int64_t un = *s_unit;
+      if (un >= nunits) break;
+      const int64_t zc = un / T;
+      tile = un - zc * T;
+      z0 = zc * g.zunit;
+      seg = min((int64_t)g.zunit, Dw - z0);
+    } else {
+      tile = u / L;
+      const int64_t zr = u - tile * L;
+      seg = min(L - zr, u_end - u);
+      z0 = zbase + zr;
+      u += seg;
+    }
+    int64_t rr = tile;
+    const int tx = (int)(rr % g.tiles_x); rr /= g.tiles_x;
+    const int ty = (int)(rr % g.tiles_y); rr /= g.tiles_y;
+    const int64_t n = rr;
+    int yo, yf, ye;
+    rank_tile_rows(ty, g.tiles_y, g.H, yo, yf, ye);
+    const int x0 = tx * TXW, y0 = yo + 1;   // staged rows y0 - 1 ... y0 + 30
+    rm = brow_dn(lane, warp, yo == 0);
+    rp = brow_up(lane, warp, yo + 31 == g.H - 1);
+    const int zs = g.zb + (int)z0;
+    const int ze = zs + (int)seg;          // own planes [zs, ze), halo plane ze
+
+    pending += seg * (TXW * 32);
+    if (n != cur_n || pending > (int64_t(1) << 24)) {   // counters hold 16 c: |16 c| <= 112
+      if (cur_n >= 0) {
+        __syncthreads();
+        flush(cur_n);
+        __syncthreads();
+      }
+      cur_n = n;
+      pending = seg * (TXW * 32);
+    }
+
+    // Every warp stages, ranks and reads only its own 32-column segment: its
+    // own TMA box (40 x 32 floats, columns xs - 4 .. xs + 35) and mbarrier, so
+    // the next plane's load is issued as soon as this warp has ranked the
+    // current one -- no warp waits for another (round 1 staged one 140-column
+    // plane per CTA, issued when the last of the four warps had ranked it).
+    const int xs_w = x0 + SEG * warp;
+    auto issue = [&](int p) {   // after __syncwarp: the warp's reads of the stage are done
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(bar, WSTAGE_BYTES);
+        tma_load_4d(stage, &tmap, bar, xs_w - 4, y0 - 1, p, (int)n);
+      }
+    };
+    auto rank = [&](int p, bool pin) {
+      const R4Fix fx = rank4_plane_wd(stage, bbuf + (p & 1) * BPLANE, pin, xs_w, y0, g.W, g.H, r4);
+      __syncwarp();
+      return fx;
+    };
+    // prologue: rank planes zs - 1 and zs
+    __syncwarp();   // the previous segment is done with this warp's stage and rank-plane segment
+    {
+      const int p = zs - 1;
+      const bool pin = p >= 0;
+      if (pin) {
+        issue(p);
+        mbar_wait(bar, phase);
+        phase ^= 1u;
+      }
+      r4_apply(rank(p, pin));
+    }
+    issue(zs);
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    r4_apply(rank(zs, true));
+    __syncwarp();
+    if (zs + 1 <= ze && zs + 1 < g.D) issue(zs + 1);
+
+    // per-thread validity (rows / columns of this tile)
+    const int y = y0 - 1 + lane;
+    const bool lane_out = y >= yf && y < ye;
+    const bool row_up_ok = (y + 1) < g.H;
+    const bool row_dn_ok = (y - 1) >= 0;
+    const int xs = x0 + SEG * warp;
+    const int nvalid = max(0, min(32, g.W - xs));
+    const uint32_t xmask = nvalid >= 32 ? 0xffffffffu : ((1u << nvalid) - 1u);
+    const uint32_t xm_p1 = (nvalid >= 32 ? 0xffffffffu : ((1u << max(nvalid - 1, 0)) - 1u)) | 0x80000000u;
+    const uint32_t outmask = lane_out ? xmask : 0u;
+
+    uint32_t N1[NNEG];
+#pragma unroll
+    for (int k = 0; k < NNEG; ++k) N1[k] = 0;
+
+    for (int s = zs; s <= ze; ++s) {
+      const uint32_t* B0 = bbuf + (s & 1) * BPLANE;         // plane s
+      const uint32_t* B1 = bbuf + ((s - 1) & 1) * BPLANE;   // plane s - 1
+
+      // ---- the 13 negative-offset words of plane s ----
+      uint32_t N0[NNEG];
+      BRow Ro;                    // own row of plane s - 1 (finalised below)
+      uint32_t eA, eB, eP;        // edge words: own row (s), row y-1 (s), row y+1 (s-1)
+      {
+        // rows double-buffered: the next row's loads are in flight while the
+        // current row's words are computed
+        uint32_t PP[16];
+        BRow A, B;
+        load_brow(A, B0, lane, warp);
+        load_brow(B, B0, rm);
+#pragma unroll
+        for (int j = 0; j < 16; ++j)   // | == + (bits 15, 31 clear)
+          PP[j] = ECC_F3_FMA_PP ? mad_fma(A.w[j], one, 0x80008000u) : (A.w[j] | 0x80008000u);
+        N0[NX] = cmp_word<-1>(PP, A, two);
+        eA = A.e;
+        load_brow(A, B1, rm);
+        N0[NYM_XM] = cmp_word<-1>(PP, B, two);
+        N0[NYM_X0] = cmp_word<0>(PP, B, two);
+        N0[NYM_XP] = cmp_word<1>(PP, B, two);
+        eB = B.e;
+        load_brow(B, B1, rp);
+        N0[NZ_YM_XM] = cmp_word<-1>(PP, A, two);
+        N0[NZ_YM_X0] = cmp_word<0>(PP, A, two);
+        N0[NZ_YM_XP] = cmp_word<1>(PP, A, two);
+        load_brow(Ro, B1, lane, warp);
+        N0[NZ_YP_XM] = cmp_word<-1>(PP, B, two);
+        N0[NZ_YP_X0] = cmp_word<0>(PP, B, two);
+        N0[NZ_YP_XP] = cmp_word<1>(PP, B, two);
+        eP = B.e;
+        N0[NZ_Y0_XM] = cmp_word<-1>(PP, Ro, two);
+        N0[NZ_Y0_X0] = cmp_word<0>(PP, Ro, two);
+        N0[NZ_Y0_XP] = cmp_word<1>(PP, Ro, two);
+      }
+
+      // plane s - 1's bin plane is no longer read: bin plane s + 1 into it
+      __syncwarp();
+      R4Fix fix{0u, 0u, 0.f, 0.f};
+      if (s + 1 <= ze) {
+        const int p = s + 1;
+        const bool pin = p < g.D;
+        if (pin) {
+          mbar_wait(bar, phase);
+          phase ^= 1u;
+        }
+        fix = rank(p, pin);
+        if (pin && p + 1 <= ze && p + 1 < g.D) issue(p + 1);
+      }
+
+      if (s > zs) {
+        // ---- finalize plane s-1 (registers only) -----------------------------
+        const uint32_t FULL = 0xffffffffu;
+        const uint32_t u_m = __shfl_down_sync(FULL, N1[NYM_XM], 1);
+        const uint32_t u_0 = __shfl_down_sync(FULL, N1[NYM_X0], 1);
+        const uint32_t u_p = __shfl_down_sync(FULL, N1[NYM_XP], 1);
+        const uint32_t d_m = __shfl_up_sync(FULL, N0[NZ_YP_XM], 1);
+        const uint32_t d_0 = __shfl_up_sync(FULL, N0[NZ_YP_X0], 1);
+        const uint32_t d_p = __shfl_up_sync(FULL, N0[NZ_YP_XP], 1);
+        const uint32_t e_m = __shfl_down_sync(FULL, N0[NZ_YM_XM], 1);
+        const uint32_t e_0 = __shfl_down_sync(FULL, N0[NZ_YM_X0], 1);
+        const uint32_t e_p = __shfl_down_sync(FULL, N0[NZ_YM_XP], 1);
+        const uint32_t eU = __shfl_down_sync(FULL, eA, 1);   // row y+1 of plane s
+
+        // segment-edge bits q < p (strict): lo lane vs bin[0], hi lane vs bin[31]
+        const uint32_t PSs = (prmt(Ro.w[0], Ro.w[15], 0x7610u) | 0x80008000u) - 0x00010001u;
+        const uint32_t dR = PSs - Ro.e, dP = PSs - eP, dB = PSs - eB, dA = PSs - eA, dU = PSs - eU;
+        const uint32_t HI = 0x80000000u;
+        const uint32_t E_x = dR & HI;
+        const uint32_t E_yp_xp = dP & HI, E_yp_xm = (dP >> 15) & 1u;
+        const uint32_t E_zp_ym_xp = dB & HI, E_zp_ym_xm = (dB >> 15) & 1u;
+        const uint32_t E_zp_y0_xp = dA & HI, E_zp_y0_xm = (dA >> 15) & 1u;
+        const uint32_t E_zp_yp_xp = dU & HI, E_zp_yp_xm = (dU >> 15) & 1u;
+
+        const uint32_t mz = (s < g.D) ? FULL : 0u;
+        const uint32_t myu = row_up_ok ? FULL : 0u;
+        const uint32_t myd = row_dn_ok ? FULL : 0u;
+
+        uint32_t Lw[3][3][3];
+        Lw[1][1][0] = N1[NX];
+        Lw[1][0][0] = N1[NYM_XM];
+        Lw[1][0][1] = N1[NYM_X0];
+        Lw[1][0][2] = N1[NYM_XP];
+        Lw[0][0][0] = N1[NZ_YM_XM];
+        Lw[0][0][1] = N1[NZ_YM_X0];
+        Lw[0][0][2] = N1[NZ_YM_XP];
+        Lw[0][1][0] = N1[NZ_Y0_XM];
+        Lw[0][1][1] = N1[NZ_Y0_X0];
+        Lw[0][1][2] = N1[NZ_Y0_XP];
+        Lw[0][2][0] = N1[NZ_YP_XM];
+        Lw[0][2][1] = N1[NZ_YP_X0];
+        Lw[0][2][2] = N1[NZ_YP_XP];
+        Lw[1][1][2] = (((~N1[NX]) >> 1) & 0x7fffffffu & xm_p1) | E_x;
+        Lw[1][2][1] = (~u_0) & myu;
+        Lw[1][2][2] = ((((~u_m) >> 1) & 0x7fffffffu & xm_p1) | E_yp_xp) & myu;
+        Lw[1][2][0] = ((~u_p) << 1 | E_yp_xm) & myu;
+        Lw[2][0][1] = (~d_0) & myd & mz;
+        Lw[2][0][2] = ((((~d_m) >> 1) & 0x7fffffffu & xm_p1) | E_zp_ym_xp) & myd & mz;
+        Lw[2][0][0] = ((~d_p) << 1 | E_zp_ym_xm) & myd & mz;
+        Lw[2][1][1] = (~N0[NZ_Y0_X0]) & mz;
+        Lw[2][1][2] = ((((~N0[NZ_Y0_XM]) >> 1) & 0x7fffffffu & xm_p1) | E_zp_y0_xp) & mz;
+        Lw[2][1][0] = ((~N0[NZ_Y0_XP]) << 1 | E_zp_y0_xm) & mz;
+        Lw[2][2][1] = (~e_0) & myu & mz;
+        Lw[2][2][2] = ((((~e_m) >> 1) & 0x7fffffffu & xm_p1) | E_zp_yp_xp) & myu & mz;
+        Lw[2][2][0] = ((~e_p) << 1 | E_zp_yp_xm) & myu & mz;
+
+        uint32_t Q[4];
+        const uint32_t any = coeff_nibbles(Lw, outmask, Q, one);
+
+        // ---- per voxel: bin from the bin image + shared-memory reduction ----
+        // c moves into the high nibble of a byte, so one sign-replicating
+        // byte permute yields 16 c as int32 (the counters hold 16 c)
+        if (__any_sync(FULL, any != 0u) && (DEP != 2 || (y >= 0 && y < g.H))) {
+          // counter index per voxel: the voxel's own 16-bit lane (its rank) when
+          // c != 0, else this lane's private dummy counter (adding 0 there costs
+          // no bank traffic on the real counters).  Selected once per word:
+          // bits j, j+16 of the nonzero mask -> byte masks -> one LOP3.
+          uint32_t Wm[16];
+          if (DEP == 1) {
+            const uint32_t dof = EK == 2 ? 4u * dummy_off : dummy_off;   // edge4 ranks are byte offsets
+            const uint32_t d2 = dof | (dof << 16);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const uint32_t keep = prmt(any << (15 - j), 0u, 0xBB99u);
+              Wm[j] = (Ro.w[j] & keep) | (d2 & ~keep);
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const int m = (i & 7) >> 1;
+            const uint32_t sel = (uint32_t)m | ((uint32_t)(8 | m) << 4) | ((uint32_t)(8 | m) << 8) |
+                                 ((uint32_t)(8 | m) << 12);
+            // even voxels: nibble moved up into the byte's high half; odd: already there
+            const uint32_t bq = (i & 1) ? (Q[i >> 3] & 0xF0F0F0F0u) : ((Q[i >> 3] << 4) & 0xF0F0F0F0u);
+            // 16 c and the counter address come from byte / half-word dot
+            // products (IDP.4A / IDP.2A run on the FMA pipe; the PRMTs they
+            // replace were ALU work, the kernel's busiest pipe)
+            const int c16 = ECC_R4_IDP ? dp4a_s8(bq, 1u << (8 * m), 0) : (int)prmt(bq, 0u, sel);
+            if (DEP == 2) {   // edge4: the field is the byte offset, every voxel deposits
+              const uint32_t addr = ECC_R4_IDP ? dp2a_lo(i < 16 ? Ro.w[i] : Ro.w[i - 16], i < 16 ? 1u : 0x100u, hbase)
+                                               : hbase + (i < 16 ? prmt(Ro.w[i], 0u, 0x4410u)
+                                                                 : prmt(Ro.w[i - 16], 0u, 0x4432u));
+              asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(addr), "r"(c16) : "memory");
+            } else if (DEP == 0) {
+              const uint32_t idx = i < 16 ? (Ro.w[i] & 0xFFFFu) : (Ro.w[i - 16] >> 16);
+              if (c16) atomicAdd(s_hist + idx, c16);
+            } else if (EK == 2) {   // byte offsets
+              const uint32_t addr = i < 16 ? madhi_fma(mul_fma(Wm[i], one << 16), 1u << 16, hbase)
+                                           : mad_fma(shr_fma<16>(Wm[i - 16]), one, hbase);
+              asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(addr), "r"(c16) : "memory");
+            } else {
+              if (ECC_F3_FMA_DEP) {   // counter address on the FMA pipe: 4 * lane + base
+                const uint32_t addr = i < 16 ? madhi_fma(mul_fma(Wm[i], one << 16), 1u << 18, hbase)
+                                             : mad_fma(shr_fma<16>(Wm[i - 16]), one << 2, hbase);
+                asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(addr), "r"(c16) : "memory");
+              } else {
+                const uint32_t idx = i < 16 ? (Wm[i] & 0xFFFFu) : (Wm[i - 16] >> 16);
+                atomicAdd(s_hist + idx, c16);
+              }
+            }
+          }
+        }
+      }
+      r4_apply(fix);   // the deferred edge-voxel fix of plane s + 1 (its threshold load had the finalize to land)
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < NNEG; ++k) N1[k] = N0[k];
+    }
+  }
+  __syncthreads();
+  if (cur_n >= 0) flush(cur_n);
+}
+
 // ======================================================================
 // 2D rank kernel (2-D grids / D == 1): one rank plane per 128 x 30 tile, no
 // z pipeline.  The tiles of a CTA form the pipeline instead: the TMA of tile
@@ -1343,10 +2052,11 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
 // c = 1 - E + S (coefficients.py:109-126), from the same word logic with the
 // z words zero (folded at compile time).
 // ======================================================================
-template <bool EDGE, bool U8>
+template <int EK, bool U8>
 __global__ void __launch_bounds__(NT, ECC_F3_MINB)
 ecc_fast2d_rank_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* __restrict__ table_g, int nb,
                        int cells, int hsize, float lut_scale, float lut_bias, unsigned long long* __restrict__ hist) {
+  constexpr bool EDGE = EK != 0;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr uint32_t STAGE_BYTES = U8 ? U8_PLANE_BYTES : PLANE_BYTES;
   float* stage = reinterpret_cast<float*>(smem_raw);
@@ -1372,8 +2082,12 @@ ecc_fast2d_rank_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const v
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
   }
   __syncthreads();
-  const uint32_t lut_m = smem_u32(s_t) - (EDGE ? 0x012C0000u : 0x2C000000u);
-  const float fcells = EDGE ? (float)(256 * cells) : (float)cells;
+  // table base: edge4 adds the field to the plain address; the older ranks
+  // index a biased base with the float bits (2-rank: key = 0x4B000000 + cell,
+  // edge: (key256 + 1) >> 6)
+  const uint32_t lut_m = smem_u32(s_t) - (EK == 2 ? 0u : EDGE ? 0x012C0000u : 0x2C000000u);
+  const float fcells = EK == 2 ? (float)(1024 * cells) : EDGE ? (float)(256 * cells) : (float)cells;
+  const R4 r4{lut_scale, lut_bias, fcells, g.r4_magic, g.r4_emask, smem_u32(s_t), nullptr, (uint32_t)g.one};
   const int nranks = U8 ? 256 : EDGE ? cells + 2 : 2 * (cells + 1);
   const uint32_t dummy_off = (uint32_t)(nranks + lane);
   const uint32_t one = (uint32_t)g.one;
@@ -1450,7 +2164,7 @@ ecc_fast2d_rank_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const v
     if (U8)
       rank_plane_u8(reinterpret_cast<const unsigned char*>(stage), B, true, x0, y0, g.W, g.H);
     else
-      bin_plane<EDGE>(stage, B, true, x0, y0, g.W, g.H, lut_m, lut_scale, lut_bias, fcells);
+      bin_plane<EK>(stage, B, true, x0, y0, g.W, g.H, lut_m, lut_scale, lut_bias, fcells, r4);
     __syncwarp();
     if (lane == 0) {
       __threadfence_block();
@@ -1509,7 +2223,8 @@ ecc_fast2d_rank_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const v
     uint32_t Q[4];
     const uint32_t any = coeff_nibbles(Lw, outmask, Q, one);
     if (__any_sync(FULL, any != 0u)) {
-      const uint32_t d2 = dummy_off | (dummy_off << 16);
+      const uint32_t dof = EK == 2 ? 4u * dummy_off : dummy_off;   // edge4 ranks are byte offsets
+      const uint32_t d2 = dof | (dof << 16);
       uint32_t Wm[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
@@ -1523,8 +2238,10 @@ ecc_fast2d_rank_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const v
                              ((uint32_t)(8 | m) << 12);
         const uint32_t bq = (i & 1) ? (Q[i >> 3] & 0xF0F0F0F0u) : ((Q[i >> 3] << 4) & 0xF0F0F0F0u);
         const int c16 = (int)prmt(bq, 0u, sel);
-        const uint32_t addr = i < 16 ? madhi_fma(mul_fma(Wm[i], one << 16), 1u << 18, hbase)
-                                     : mad_fma(shr_fma<16>(Wm[i - 16]), one << 2, hbase);
+        const uint32_t addr = EK == 2 ? (i < 16 ? madhi_fma(mul_fma(Wm[i], one << 16), 1u << 16, hbase)
+                                                : mad_fma(shr_fma<16>(Wm[i - 16]), one, hbase))
+                                      : (i < 16 ? madhi_fma(mul_fma(Wm[i], one << 16), 1u << 18, hbase)
+                                                : mad_fma(shr_fma<16>(Wm[i - 16]), one << 2, hbase));
         asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(addr), "r"(c16) : "memory");
       }
     }
@@ -1616,9 +2333,16 @@ static int set_dynamic(fast::Geom& g, int64_t total, int64_t grid, int64_t depth
   return 0;
 }
 
+// edge4 rank constants for a table verified at `sub` sub-cells per cell (R4)
+static void set_r4(fast::Geom& g, int sub) {
+  const int z = sub > 0 ? 1024 / sub : 4;
+  g.r4_magic = 8388608.0f + 1024.0f + (float)z;
+  g.r4_emask = 0x3FFu & ~(uint32_t)(2 * z - 1);
+}
+
 static int launch_2d(const CUtensorMap& map, const void* kfn, size_t smem, int64_t W, int64_t H, int64_t batch,
                      const void* table, int nb, int cells, int hsize, float scale, float bias,
-                     unsigned long long* hist, cudaStream_t stream) {
+                     unsigned long long* hist, cudaStream_t stream, int edge_sub = 0) {
   using namespace fast;
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(fast2d)");
@@ -1637,6 +2361,7 @@ static int launch_2d(const CUtensorMap& map, const void* kfn, size_t smem, int64
   g.zchunks = 0;
   g.one = 1;
   g.items = (int64_t)g.tiles_x * g.tiles_y * batch;
+  set_r4(g, edge_sub);
   const int64_t max_ctas = (int64_t)num_sms_fast() * occ;
   const int64_t grid = g.items < max_ctas ? g.items : max_ctas;
   if (grid < 1) return ECC_OK;
@@ -1677,31 +2402,82 @@ int fast3d_launch(const float* x, int64_t D, int64_t H, int64_t W, int64_t batch
     if (!strcmp(e, "cta")) return 3;
     if (!strcmp(e, "rank2")) return 4;
     if (!strcmp(e, "no2d")) return 5;
+    if (!strcmp(e, "edge1")) return 6;     // the round-1 edge rank (inline threshold test per voxel)
+    if (!strcmp(e, "dummy")) return 8;     // rank4 with dummy counters for c = 0 even when not needed
+    if (!strcmp(e, "static")) return 9;    // rank4 with the static partition only
     return 0;
   }();
   const bool use_bin = b->lut_ok && cells <= 16382 && mode != 1;
   const bool edge = b->lut_edge && mode != 4;
-  const int hsize = (edge ? cells + 2 : 2 * (cells + 1)) + 32;   // rank counters + 32 dummies
+  // edge4 (rank fields = 4 * rank, 2^23 + 1024 cells + 1028 < 2^24) unless the round-1 rank is asked for
+  const int ek = !edge ? 0 : (cells <= 8190 && mode != 6 && mode != 3 && mode != 2) ? 2
+                          : b->lut_edge_sub == 256 ? 1 : 0;
+  const int hsize = (ek ? cells + 2 : 2 * (cells + 1)) + 32;   // rank counters + 32 dummies
   size_t smem;
   const void* kfn;
   if (use_bin) {
     smem = (size_t)PLANE_BYTES + (size_t)2 * BPLANE * 4 + 16 + (size_t)((cells + 1 + 3) & ~3) * 4 +
            (size_t)hsize * 4;
-    kfn = edge ? (mode == 2 ? (const void*)ecc_fast3d_bin_kernel<0, true, true>
-                            : mode == 3 ? (const void*)ecc_fast3d_bin_kernel<1, false, true>
-                                        : (const void*)ecc_fast3d_bin_kernel<1, true, true>)
-               : (mode == 2 ? (const void*)ecc_fast3d_bin_kernel<0, true, false>
-                            : mode == 3 ? (const void*)ecc_fast3d_bin_kernel<1, false, false>
-                                        : (const void*)ecc_fast3d_bin_kernel<1, true, false>);
+    kfn = ek == 1 ? (mode == 2 ? (const void*)ecc_fast3d_bin_kernel<0, true, 1>
+                               : mode == 3 ? (const void*)ecc_fast3d_bin_kernel<1, false, 1>
+                                           : (const void*)ecc_fast3d_bin_kernel<1, true, 1>)
+                  : (mode == 2 ? (const void*)ecc_fast3d_bin_kernel<0, true, 0>
+                               : mode == 3 ? (const void*)ecc_fast3d_bin_kernel<1, false, 0>
+                                           : (const void*)ecc_fast3d_bin_kernel<1, true, 0>);
   } else {
     smem = (size_t)NSTAGE * PLANE_BYTES + 4 * 8 + (size_t)(b->lut_ok ? cells + 1 : 0) * sizeof(LutEntry) +
            (size_t)((nb + 1 + 3) & ~3) * 4 + (size_t)(b->lut_ok ? 0 : nb + 2) * 4;
     kfn = (const void*)ecc_fast3d_kernel;
   }
   if (use_bin && D == 1 && mode != 3 && mode != 5)   // single planes: the 2-D tile pipeline
-    return launch_2d(map, edge ? (const void*)ecc_fast2d_rank_kernel<true, false>
-                               : (const void*)ecc_fast2d_rank_kernel<false, false>,
-                     smem, W, H, batch, table, nb, cells, hsize, b->lut_scale, b->lut_bias, hist, stream);
+    return launch_2d(map, ek == 2 ? (const void*)ecc_fast2d_rank_kernel<2, false>
+                          : ek == 1 ? (const void*)ecc_fast2d_rank_kernel<1, false>
+                                    : (const void*)ecc_fast2d_rank_kernel<0, false>,
+                     smem, W, H, batch, table, nb, cells, hsize, b->lut_scale, b->lut_bias, hist, stream,
+                     b->lut_edge_sub);
+  if (use_bin && ek == 2) {
+    // the rank4 kernel: per-warp 40 x 32 TMA boxes, boundary thresholds in global memory
+    CUtensorMap wmap;
+    const cuuint32_t wbox[4] = {WPITCH, 32, 1, 1};
+    r = encode_fn()(&wmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(x), gdim, gstride, wbox, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NAN_REQUEST_ZERO_FMA);
+    if (r != CUDA_SUCCESS) return set_error(ECC_ECUDA, "cuTensorMapEncodeTiled(rank4) failed");
+    // every voxel deposits on its own counter when no tile column is partial
+    // (no sentinel ranks in deposited rows); else dummies for c = 0
+    const bool nodummy = (W % TXW) == 0 && mode != 8;
+    const int hs = nodummy ? cells + 2 : cells + 2 + 32;
+    const size_t smem4 = (size_t)NW * WSTAGE_BYTES + (size_t)2 * BPLANE * 4 + (size_t)(NW + 1) * 8 + (size_t)hs * 4;
+    const void* k4 = nodummy ? (const void*)ecc_rank4_kernel<2> : (const void*)ecc_rank4_kernel<1>;
+    cudaError_t e = cudaFuncSetAttribute(k4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem4);
+    if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(rank4)");
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k4, NT, smem4);
+    if (occ < 1) return set_error(ECC_EINVAL, "rank4 kernel does not fit on an SM");
+    Geom g;
+    g.W = (int)W;
+    g.H = (int)H;
+    g.D = (int)D;
+    g.zb = (int)zb;
+    g.ze = (int)ze;
+    g.tiles_x = (int)((W + TXW - 1) / TXW);
+    g.tiles_y = rank_tiles_y((int)H);
+    const int64_t tiles = (int64_t)g.tiles_x * g.tiles_y * batch;
+    g.zc = 0;
+    g.one = 1;
+    g.items = tiles;
+    set_r4(g, b->lut_edge_sub);
+    const int64_t total = tiles * (ze - zb);
+    const int64_t max_ctas = (int64_t)num_sms_fast() * occ;
+    const int64_t grid = total < max_ctas ? total : max_ctas;
+    g.zchunks = (tiles <= grid && grid <= tiles * (ze - zb)) ? (int)(grid / tiles) : 0;
+    if (grid < 1) return ECC_OK;
+    if (mode != 9 && set_dynamic(g, total, grid, ze - zb, stream)) return ECC_ECUDA;
+    using KFn = void (*)(const CUtensorMap, Geom, const void*, int, int, int, float, float, unsigned long long*);
+    KFn kk = reinterpret_cast<KFn>(const_cast<void*>(k4));
+    kk<<<(unsigned)grid, NT, smem4, stream>>>(wmap, g, table, nb, cells, hs, b->lut_scale, b->lut_bias, hist);
+    return check_launch("ecc_rank4_kernel");
+  }
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(fast3d)");
   int occ = 0;
@@ -1767,10 +2543,10 @@ int fast3d_u8_launch(const uint8_t* x, int64_t D, int64_t H, int64_t W, int64_t 
   const bool cta = env && !strcmp(env, "cta");
   const int hsize = 256 + 32;
   const size_t smem = (size_t)U8_PLANE_BYTES + (size_t)2 * BPLANE * 4 + 16 + 4 * 4 + (size_t)hsize * 4;
-  const void* kfn = cta ? (const void*)ecc_fast3d_bin_kernel<1, false, false, true>
-                        : (const void*)ecc_fast3d_bin_kernel<1, true, false, true>;
+  const void* kfn = cta ? (const void*)ecc_fast3d_bin_kernel<1, false, 0, true>
+                        : (const void*)ecc_fast3d_bin_kernel<1, true, 0, true>;
   if (D == 1 && !cta && !(env && !strcmp(env, "no2d")))
-    return launch_2d(map, (const void*)ecc_fast2d_rank_kernel<false, true>, smem, W, H, batch, table, nb, 0, hsize,
+    return launch_2d(map, (const void*)ecc_fast2d_rank_kernel<0, true>, smem, W, H, batch, table, nb, 0, hsize,
                      0.f, 0.f, hist, stream);
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(fast3d u8)");

@@ -129,7 +129,12 @@ static int64_t bin32(float x, const float* t32, int64_t nb) {
 // last thresholds.  aligned != 0 maps [t_0 - w, t_last] (w the mean spacing)
 // instead, so that uniform thresholds fall on cell boundaries (cells == nb),
 // which is what the edge tables below need.
-constexpr int EDGE_SUB = 256;   // edge sub-cells per cell (ecc_fast3d.cu rank_edge)
+// edge sub-cells per cell (ecc_fast3d.cu rank_edge / rank4): 1024 is tried
+// first (fewer edge voxels), then 256
+constexpr int EDGE_SUB_FINE = 1024, EDGE_SUB_COARSE = 256;
+#ifndef ECC_EDGE_COARSE_ONLY
+#define ECC_EDGE_COARSE_ONLY 0
+#endif
 
 static int build_lut(const float* t32, int64_t nb, int cells, float* scale_out, float* bias_out, LutEntryH* lut,
                      int aligned = 0) {
@@ -184,7 +189,7 @@ static int build_lut(const float* t32, int64_t nb, int cells, float* scale_out, 
 // non-decreasing in x, so each rank's floats form one key interval, found by
 // binary search; every interval is verified to lie in one bin (rbin[rank]).
 // Returns 1 on success.
-static int edge_rank(float x, float scale, float bias, int cells, const float* tE) {
+static int edge_rank(float x, float scale, float bias, int cells, const float* tE, int EDGE_SUB) {
   const int sidx = cell_of(x, scale, bias, cells * EDGE_SUB);
   const int k1 = sidx + 1;
   const int idx = k1 / EDGE_SUB;
@@ -193,7 +198,7 @@ static int edge_rank(float x, float scale, float bias, int cells, const float* t
 }
 
 static int build_edge(const float* t32, int64_t nb, int cells, float scale, float bias, float* tE,
-                      int32_t* rbin) {
+                      int32_t* rbin, int EDGE_SUB) {
   const int nsub = cells * EDGE_SUB;
   if (cells + 2 >= 0x7FFF || nsub >= (1 << 23)) return 0;
   const uint32_t kmin = fkey(-std::numeric_limits<float>::max());
@@ -226,7 +231,7 @@ static int build_edge(const float* t32, int64_t nb, int cells, float scale, floa
   // rank r holds keys [lo_r, lo_{r+1}); each nonempty interval must sit in one bin
   std::vector<uint32_t> lo((size_t)cells + 4);
   for (int r = 0; r <= cells + 3; ++r)
-    lo[r] = first_key([&](float x) { return edge_rank(x, scale, bias, cells, tE) >= r; });
+    lo[r] = first_key([&](float x) { return edge_rank(x, scale, bias, cells, tE, EDGE_SUB) >= r; });
   for (int r = 0; r <= cells + 1; ++r) {
     rbin[r] = 0;
     if (lo[r] >= lo[r + 1]) continue;
@@ -276,7 +281,7 @@ extern "C" int ecc_threshold_table(const double* taus, int64_t nb, int dtype, vo
   b->nbins = nb;
   b->lut_ok = 0;
   b->lut_edge = 0;
-  b->lut_pad = 0;
+  b->lut_edge_sub = 0;
   b->lut_cells = 0;
   b->lut_scale = 0.0f;
   b->lut_bias = 0.0f;
@@ -297,9 +302,13 @@ extern "C" int ecc_threshold_table(const double* taus, int64_t nb, int dtype, vo
       if (build_lut(t + 1, nb, (int)cells, &sc, &bi, lut, 1)) {
         float* tE = reinterpret_cast<float*>(lut + cells + 1);
         int32_t* rbin = reinterpret_cast<int32_t*>(tE + cells + 1);
-        if (build_edge(t + 1, nb, (int)cells, sc, bi, tE, rbin)) {
+        const int sub = (!ECC_EDGE_COARSE_ONLY && build_edge(t + 1, nb, (int)cells, sc, bi, tE, rbin, EDGE_SUB_FINE)) ? EDGE_SUB_FINE
+                        : build_edge(t + 1, nb, (int)cells, sc, bi, tE, rbin, EDGE_SUB_COARSE) ? EDGE_SUB_COARSE
+                                                                                             : 0;
+        if (sub) {
           b->lut_ok = 1;
           b->lut_edge = 1;
+          b->lut_edge_sub = sub;
           b->lut_cells = (int32_t)cells;
           b->lut_scale = sc;
           b->lut_bias = bi;
@@ -315,7 +324,10 @@ extern "C" int ecc_threshold_table(const double* taus, int64_t nb, int dtype, vo
         b->lut_bias = bi;
         float* tE = reinterpret_cast<float*>(lut + cells + 1);
         int32_t* rbin = reinterpret_cast<int32_t*>(tE + cells + 1);
-        b->lut_edge = build_edge(t + 1, nb, (int)cells, sc, bi, tE, rbin);
+        b->lut_edge_sub = build_edge(t + 1, nb, (int)cells, sc, bi, tE, rbin, EDGE_SUB_FINE) ? EDGE_SUB_FINE
+                          : build_edge(t + 1, nb, (int)cells, sc, bi, tE, rbin, EDGE_SUB_COARSE) ? EDGE_SUB_COARSE
+                                                                                               : 0;
+        b->lut_edge = b->lut_edge_sub != 0;
       }
     }
   } else if (dtype == ECC_DTYPE_F64) {

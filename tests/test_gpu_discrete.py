@@ -225,6 +225,8 @@ class TestFastPath:
     KERNELS = {"bin": {}, "value": {"ECC_B200_F3": "value"}, "branch": {"ECC_B200_F3": "branch"},
                "cta": {"ECC_B200_F3": "cta"}, "rank2": {"ECC_B200_F3": "rank2"}, "no2d": {"ECC_B200_F3": "no2d"},
                "dyn4": {"ECC_B200_F3_ZUNIT": "4"}, "dyn7": {"ECC_B200_F3_ZUNIT": "7"},
+               "edge1": {"ECC_B200_F3": "edge1"}, "dummy": {"ECC_B200_F3": "dummy"},
+               "static": {"ECC_B200_F3": "static"},
                "generic": {"ECC_B200_GENERIC": "1"}}
 
     @classmethod
@@ -247,7 +249,7 @@ class TestFastPath:
     @classmethod
     def _both(cls, t, ts, **kw):
         out = cls._all(t, ts, **kw)
-        for name in ("value", "branch", "cta", "rank2", "no2d", "dyn4", "dyn7"):
+        for name in ("value", "branch", "cta", "rank2", "no2d", "dyn4", "dyn7", "edge1", "dummy", "static"):
             assert np.array_equal(out[name], out["bin"]), name
         return out["bin"], out["generic"]
 
