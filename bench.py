@@ -14,11 +14,18 @@ fused stencil/bin/histogram sweep + all-reduce (N>1) + prefix scan.  Inputs
 are resident in HBM and larger than L2 (512 MiB per rank vs 126 MB), so no
 flush is needed between steps.  `e2e` repeats the measurement through the
 public API with the volume copied host->device from pinned memory every step
-and the curve copied back.  `soft` reports the C3 soft-ECC forward+backward
-(128 x 1024^2, 256 thresholds, lambda 50, learnable tau/u/alpha).
+and the curve copied back.
+
+Further legs (sub-objects of the line): `north_star` (1024^3 on one GPU),
+`c5` (the 2048^3 volume z-slab sharded over the N ranks, strong scaling),
+`soft` (C3: 128 x 1024^2, 256 thresholds, lambda 50, learnable tau/u/alpha,
+forward + backward, batch-sharded) and `c4` (one 1024^3 soft item per GPU).
+Every leg is gated on the CPU oracle before its time is reported
+(`parity`), as the reference's own harness refuses to time a wrong answer
+(/root/reference/pkg/src/ecckit/bench.py:28-37, 115-117).
 
 --impl reference times the reference algorithm's CPU port (oracle/, all host
-threads) on a bounded sample of the same workload (the reference is pure
+threads) on the full C2 volume every step (the reference is pure
 Python/numpy and cannot travel to the GPU box; its C restatement is pinned
 to the reference's golden vectors, see tests/test_oracle_golden.py).
 """
@@ -120,47 +127,56 @@ def _dist_env():
 
 
 # ---------------------------------------------------------------------------
-# reference arm: the CPU port on a bounded sample
+# reference arm and CPU baselines: the CPU port (oracle/, the checker) timed
+# on the box's host cores on the same full volume
 # ---------------------------------------------------------------------------
 
-def cpu_port_sample(planes: int = 32, reps: int = 1):
-    """Time oracle/ (the C restatement of ecckit's compute_ecc, all host
-    threads) on `planes` planes of the 512^3 workload.  Returns Gvox/s."""
+def cpu_port_c2(planes: int = 512, threads: int | None = None, reps: int = 1):
+    """Time oracle/ (the C restatement of ecckit's compute_ecc) on the full
+    C2 volume (`planes` x 512 x 512 float32 counter grid, SEED, 1024 uniform
+    thresholds over [0, 1)) with `threads` OpenMP threads (None: all host
+    threads; the reference's `workers`, hard.py:184-200).  Returns
+    (Gvox/s of the best rep, threads, sample text, bins+overflow)."""
     from oracle import oracle
 
-    dims = (planes + 2, 512, 512)
+    nthreads = threads or os.cpu_count() or 1
+    oracle.set_threads(nthreads)
+    dims = (planes, 512, 512)
     x = oracle.counter_grid(SEED, dims).reshape(dims)
     taus = np.linspace(0.0, 1.0, NB + 1)[1:]
-    oracle.histogram_rows(x, 1, planes + 1, taus)  # warm-up (thread pool)
     ts = []
+    hist = None
     for _ in range(reps):
         t0 = time.perf_counter()
-        oracle.histogram_rows(x, 1, planes + 1, taus)
+        bins, ovf = oracle.histogram(x, taus)
         ts.append(time.perf_counter() - t0)
+        hist = np.concatenate([bins, [ovf]])
+    oracle.set_threads(os.cpu_count() or 1)
     vox = planes * 512 * 512
-    return vox / min(ts) / 1e9, oracle.num_threads(), f"{planes}x512x512 f32 planes of the 512^3 volume, {NB} bins"
+    return (vox / min(ts) / 1e9, nthreads,
+            f"full {planes}x512x512 f32 volume, {NB} bins, {nthreads} OpenMP threads", hist)
 
 
 def run_reference(args):
     world, rank, _ = _dist_env()
     if rank != 0:
         return
-    vals = []
-    sample = ""
-    cores = 1
+    planes = 512 * world
     for _ in range(args.warmup):
-        cpu_port_sample(planes=16)
+        cpu_port_c2(planes)
+    vals = []
+    cores, sample = 1, ""
     for _ in range(args.steps):
-        v, cores, sample = cpu_port_sample(planes=32)
+        v, cores, sample, _ = cpu_port_c2(planes)
         vals.append(v)
     value = statistics.median(vals)
-    vox_per_step = 512 * 512 * 512 * world
+    vox_per_step = 512 * 512 * planes
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": vox_per_step / (value * 1e9) * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": "C2: 3D 512^3 float32 volume, discrete ECC, 1024 uniform thresholds "
-                   "(sampled: 32 planes per step)", "volume": [512 * world, 512, 512], "bins": NB,
+                   "(full volume every step)", "volume": [planes, 512, 512], "bins": NB,
                    "parallelism": f"zslab{world}"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -168,9 +184,57 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def cpu_soft_sample(ndim: int, reps: int = 1):
+    """The oracle's soft forward + backward (soft.py:154-257, float64, all host
+    threads) on one C3 image (1024 x 1024, ndim = 2) or a 128^3 C4 sub-volume
+    (ndim = 3), B = 256, lambda = 50, alpha = 0.3.  Returns (voxels/s, threads,
+    sample text, voxels of the sample)."""
+    from oracle import oracle
+
+    rng = np.random.default_rng(SEED)
+    B, lam, alpha = 256, 50.0, 0.3
+    v = np.array([1.0, 2.0]) if ndim == 2 else np.array([1.0, 2.0, -0.5])
+    u = v / np.linalg.norm(v)
+    span = alpha * np.abs(u).sum()
+    taus = np.linspace(-span, 1.0 + span, B + 1)[1:]
+    dims = (1024, 1024) if ndim == 2 else (128, 128, 128)
+    x = rng.random(dims).astype(np.float32).astype(np.float64)
+    up = np.ones(B)
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        c = oracle.coefficients(oracle.effective_field(x, alpha, u))
+        oracle.soft_forward(x, c, lam, alpha, u, taus)
+        oracle.soft_backward(x, c, lam, alpha, u, taus, up)
+        ts.append(time.perf_counter() - t0)
+    n = int(np.prod(dims))
+    what = "one 1024x1024 C3 image" if ndim == 2 else "a 128^3 sub-volume of the C4 item"
+    return (n / min(ts), oracle.num_threads(),
+            f"{what}, B = 256, forward + backward in float64; voxels/s extrapolated linearly in voxels "
+            "(the work per (voxel, threshold) pair is uniform)", n)
+
+
 # ---------------------------------------------------------------------------
 # B200 arm
 # ---------------------------------------------------------------------------
+
+def _gate(ok: bool, what: str):
+    """The reference harness never reports a time for a wrong answer
+    (/root/reference/pkg/src/ecckit/bench.py:28-37, 115-117)."""
+    if not ok:
+        raise SystemExit(f"bench: parity gate failed ({what}); no number is reported")
+
+
+def _max_over_ranks(vals, dev, dist_on):
+    if not dist_on:
+        return vals
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor(vals, dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(v) for v in t]
+
 
 def run_b200(args):
     import torch
@@ -197,6 +261,8 @@ def run_b200(args):
     own = padded[1:-1]
     start = rank * P * H * W
     _lib.check(L.ecc_counter_grid(SEED, start, own.numel(), _lib.ptr(own), _lib.stream_ptr(own)))
+    if dist_on:   # halo planes of the global volume (timed steps exchange them again)
+        D.exchange_halos(padded)
 
     # thresholds: uniform over the global range (device min/max, grid.py:183-196)
     torch.cuda.synchronize()
@@ -223,13 +289,10 @@ def run_b200(args):
     hist = torch.empty(NB + 1, dtype=torch.int64, device=dev)
     curve = torch.empty(NB, dtype=torch.int64, device=dev)
     view, z0, z1 = (own, 0, P) if not dist_on else D.slab_view(padded)
-    dims = _lib.dims_arg(view.shape)
     # kernel-only timing: one event pair per step around the histogram kernel,
     # steps back to back (no host sync in between), read after the last one
     kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    kernel_ms = []
-
-    dims_cache = {tuple(view.shape): dims}
+    dims_cache = {}
 
     def sweep(v, a, b, out):
         dv = dims_cache.get(tuple(v.shape))
@@ -260,11 +323,18 @@ def run_b200(args):
         _lib.check(L.ecc_scan(_lib.ptr(h), 1, NB, _lib.ptr(curve), _lib.ctypes.c_void_p(stream.cuda_stream)))
         return h
 
-    # correctness gate on the real workload (size-independent properties):
-    # the full-volume curve ends at chi(box) = 1 and sums of c are 1.
+    # parity gate on the timed workload: the global histogram of the (world x
+    # 512)-plane volume equals the oracle's, bit for bit (rank 0 checks)
     h = step().cpu().numpy()
     c = curve.cpu().numpy()
-    assert int(h.sum()) == 1 and int(c[-1]) == 1, "ECC invariant violated (sum c != 1)"
+    _gate(int(h.sum()) == 1 and int(c[-1]) == 1, "C2 sum of coefficients")
+    parity = "invariants only"
+    if rank == 0 and not args.no_parity:
+        from oracle import parity as OP
+
+        want = OP.counter_slab_hist(SEED, (P * world, H, W), 0, P * world, taus.taus)
+        _gate(np.array_equal(h, want), "C2 histogram vs oracle")
+        parity = "checked: bit-exact vs the CPU oracle on the timed volume"
     checksum = int(np.bitwise_xor.reduce(c.view(np.uint64)))
 
     def barrier():
@@ -289,12 +359,7 @@ def run_b200(args):
         step(record=i)
     torch.cuda.synchronize()
     kernel_ms = [a.elapsed_time(b) for a, b in kev]
-    if dist_on:
-        t = torch.tensor([total_ms, statistics.mean(kernel_ms)], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms, kmean = float(t[0]), float(t[1])
-    else:
-        kmean = statistics.mean(kernel_ms)
+    total_ms, kmean = _max_over_ranks([total_ms, statistics.mean(kernel_ms)], dev, dist_on)
     ms_per_step = total_ms / args.steps
     vox_rank = P * H * W
     vox_total = vox_rank * world
@@ -333,7 +398,7 @@ def run_b200(args):
             api = "paper_2510_20271_b200.distributed.slab_curve"
 
         got = e2e_step()
-        assert int(got[-1]) == 1
+        _gate(int(got[-1]) == 1 and np.array_equal(got.numpy(), c), "C2 e2e curve")
         for _ in range(2):
             e2e_step()
         barrier()
@@ -343,34 +408,34 @@ def run_b200(args):
             e2e_step()
         barrier()
         e_ms = (time.perf_counter() - t0) * 1e3 / reps
-        if dist_on:
-            t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e_ms = float(t[0])
+        e_ms = _max_over_ranks([e_ms], dev, dist_on)[0]
         e2e = {"value": vox_total / (e_ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": e_ms,
                "h2d_bytes_per_step": int(host.numel() * 4) * world, "d2h_bytes_per_step": int(NB * 8) * world,
                "api": api + " (pinned host -> HBM copy inside the timed region)"}
         del host
+    del padded, own, view
+    torch.cuda.empty_cache()
 
     # --- north-star volume (1024^3 f32, 1024 bins; N = 1 only) ---------------
     ns = None
     if world == 1 and not args.no_ns:
         ns = bench_ns(args, dev)
 
-    # --- soft ECC C3 (forward + backward) -------------------------------------
-    soft = None
-    if not args.no_soft:
-        soft = bench_soft(args, dev, world, rank, dist_on)
+    # --- C5: 2048^3 z-slabs over the N ranks (strong scaling) ------------------
+    c5 = None if args.no_c5 else bench_c5(args, dev, world, rank, dist_on)
 
-    # --- C5 per-GPU slab and C4 (one 1024^3 soft item per GPU) -----------------
-    c5 = None if args.no_c5 else bench_c5_slab(args, dev, world, rank, dist_on)
+    # --- soft ECC C3 (forward + backward) and C4 (one 1024^3 item per GPU) ------
+    soft = None if args.no_soft else bench_soft(args, dev, world, rank, dist_on)
     c4 = None if args.no_soft or args.no_c4 else bench_c4(args, dev, world, rank, dist_on)
 
-    # --- CPU baseline (rank 0, N = 1) ----------------------------------------
+    # --- CPU baseline (rank 0, N = 1): the oracle port on the full C2 volume ----
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        v, cores, sample = cpu_port_sample(planes=32)
-        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
+        v, cores, sample, cpu_hist = cpu_port_c2(P)
+        v1, _, sample1, _ = cpu_port_c2(P, threads=1)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
+               "workers_1": {"value": v1, "unit": UNIT, "cores": 1, "sample": sample1},
+               "same_config": True}
 
     if rank == 0:
         line = {
@@ -383,10 +448,12 @@ def run_b200(args):
                        "l2": "input larger than L2 (512 MiB per GPU), no flush",
                        "thresholds": "given (uniform over the device min/max, computed once)",
                        "minmax_pass_ms": minmax_ms, "minmax_kernel_ms": minmax_kernel_ms,
-                       "minmax_kernel_gbs": 4.0 * own.numel() / (minmax_kernel_ms * 1e-3) / 1e9, "seed": SEED, "curve_xor_checksum": checksum},
+                       "minmax_kernel_gbs": 4.0 * vox_rank / (minmax_kernel_ms * 1e-3) / 1e9, "seed": SEED,
+                       "curve_xor_checksum": checksum},
+            "parity": parity,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
-                         "kernel": "ecc_fast3d_bin_kernel" if W % 4 == 0 else "ecc_sweep_kernel<RawSrc<float>,HistSink<float>>",
+                         "kernel": "ecc_rank4_kernel" if W % 128 == 0 else "ecc_fast3d_bin_kernel",
                          "kernel_ms": kmean, "algorithmic_bytes_per_launch": 4 * vox_rank},
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -394,9 +461,9 @@ def run_b200(args):
             "gpu_launches": (4 if world > 1 and P >= 3 else 2) * args.steps,
             "clocks": clocks.summary(),
             "north_star": ns,
+            "c5": c5,
             "soft": soft,
             "c4": c4,
-            "c5_slab": c5,
         }
         print(json.dumps(line), flush=True)
     if dist_on:
@@ -405,8 +472,8 @@ def run_b200(args):
 
 def bench_ns(args, dev):
     """The north-star case on one GPU: 1024^3 float32, 1024 uniform thresholds,
-    device-resident input (4 GiB > L2), CUDA-event timing over K steps.  The
-    curve is checked against the size-independent invariants (sum c = 1)."""
+    device-resident input (4 GiB > L2), CUDA-event timing over K steps,
+    gated bit-exact against the oracle (accumulated slab by slab)."""
     import torch
 
     import paper_2510_20271_b200 as E
@@ -419,7 +486,15 @@ def bench_ns(args, dev):
     lo, hi, _ = E.device_minmax(x)
     taus = E.thresholds_from_range(lo, hi, NB)
     curve, hist = E.ecc_discrete(x, taus, return_hist=True)
-    assert int(hist.sum()) == 1 and int(curve[-1]) == 1, "ECC invariant violated at 1024^3"
+    h = hist.cpu().numpy().reshape(-1)
+    _gate(int(h.sum()) == 1 and int(curve.reshape(-1)[-1]) == 1, "NS sum of coefficients")
+    parity = "invariants only"
+    if not args.no_parity:
+        from oracle import parity as OP
+
+        _gate(np.array_equal(h, OP.counter_slab_hist(SEED + 1, (n, n, n), 0, n, taus.taus, slab=128)),
+              "NS histogram vs oracle")
+        parity = "checked: bit-exact vs the CPU oracle on the timed 1024^3 volume"
     for _ in range(3):
         E.histogram_device(x, taus)
     torch.cuda.synchronize()
@@ -443,82 +518,155 @@ def bench_ns(args, dev):
             traffic = None
     out = {"workload": "NS: 3D 1024^3 float32, discrete ECC, 1024 uniform thresholds (device-resident)",
            "value": x.numel() / (ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": ms, "steps": steps,
+           "parity": parity,
            "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
                         "peak_source": peak_kind, "traffic": traffic,
                         "algorithmic_bytes_per_launch": 4 * x.numel()}}
-    del x
+    del x, curve, hist
     torch.cuda.empty_cache()
     return out
 
 
-def bench_c5_slab(args, dev, world, rank, dist_on=False):
-    """One GPU's share of C5 (3D 2048^3 float32, z-slabs over 8 GPUs): a
-    256 x 2048 x 2048 slab (4 GiB) of the counter-generated C5 volume (the
-    planes rank r would own in an 8-way split, r = this rank mod 8) plus its
-    two halo planes, swept by the fused kernel over its own planes
-    (ecc_histogram_range, the per-rank kernel of distributed.slab_histogram).
-    Thresholds: 1024 uniform over [0, 1) edges of the generator's range.
-    The halo exchange and the 8 KiB histogram all-reduce are timed by the
-    multi-GPU C2 line; here the slab kernel alone, CUDA events."""
+def bench_c5(args, dev, world, rank, dist_on=False):
+    """C5: the 2048^3 float32 counter volume cut into N z-slabs, one per GPU
+    (strong scaling: the total volume is fixed).  A step is the distributed
+    pipeline: halo exchange with the z-neighbours (overlapped with the
+    interior sweep), the fused slab sweep (ecc_histogram_range), the NCCL
+    all-reduce of the (B+1) int64 histogram and the scan.  1024 thresholds
+    uniform over the generator's range.  Gate: the sum invariant of the whole
+    volume, and the kernel bit-exact vs the oracle on the slab's first 64
+    planes taken as a volume of C5's 2048 x 2048 planes."""
     import torch
+    import torch.distributed as dist
 
     import paper_2510_20271_b200 as E
     from paper_2510_20271_b200 import _lib
     from paper_2510_20271_b200 import distributed as D
 
     L = _lib.lib()
-    P, H, W = 256, 2048, 2048
-    part = rank % 8
+    Dz, H, W = args.c5_depth, 2048, 2048
+    if dist_on:
+        z0, z1 = D.slab_bounds(Dz, world, rank)
+    else:
+        z0, z1 = 0, Dz
+    P = z1 - z0
     padded = D.alloc_padded_slab(P, (H, W), torch.float32, dev)
-    z0 = part * P
     lo_plane = max(z0 - 1, 0)
-    hi_plane = min(z0 + P + 1, 8 * P)
+    hi_plane = min(z1 + 1, Dz)
     first = 1 - (z0 - lo_plane)
-    view = padded[first:first + (hi_plane - lo_plane)]
-    _lib.check(L.ecc_counter_grid(SEED + 2, lo_plane * H * W, view.numel(), _lib.ptr(view), _lib.stream_ptr(view)))
+    gen = padded[first:first + (hi_plane - lo_plane)]
+    _lib.check(L.ecc_counter_grid(SEED + 2, lo_plane * H * W, gen.numel(), _lib.ptr(gen), _lib.stream_ptr(gen)))
     taus = E.thresholds_from_range(0.0, 1.0 - 2.0 ** -24, NB)
     table, binning = taus.device_table(_lib.DTYPE_F32, dev)
-    hist = torch.zeros(NB + 1, dtype=torch.int64, device=dev)
-    zlo, zhi = z0 - lo_plane, z0 - lo_plane + P
-    dims = _lib.dims_arg(view.shape)
     stream = torch.cuda.current_stream(dev)
+    curve = torch.empty(NB, dtype=torch.int64, device=dev)
+    dims_cache = {}
 
-    def run():
-        _lib.check(L.ecc_histogram_range(_lib.ptr(view), _lib.DTYPE_F32, 3, _lib.ptr(dims), 1, zlo, zhi,
-                                         _lib.ptr(table), _lib.ctypes.byref(binning), _lib.ptr(hist),
+    def slab_fn(v, a, b, t):
+        out = torch.empty(NB + 1, dtype=torch.int64, device=dev)
+        dv = dims_cache.get(tuple(v.shape))
+        if dv is None:
+            dv = dims_cache[tuple(v.shape)] = _lib.dims_arg(v.shape)
+        _lib.check(L.ecc_histogram_range(_lib.ptr(v), _lib.DTYPE_F32, 3, _lib.ptr(dv), 1, a, b, _lib.ptr(table),
+                                         _lib.ctypes.byref(binning), _lib.ptr(out),
                                          _lib.ctypes.c_void_p(stream.cuda_stream)))
+        return out
 
-    run()
-    torch.cuda.synchronize()
+    whole = padded[1:-1]
+
+    def step():
+        if dist_on:
+            h = D.slab_histogram(padded, taus, hist_fn=slab_fn)
+        else:
+            h = slab_fn(whole, 0, P, taus)
+        _lib.check(L.ecc_scan(_lib.ptr(h), 1, NB, _lib.ptr(curve), _lib.ctypes.c_void_p(stream.cuda_stream)))
+        return h
+
+    h = step().cpu().numpy()
+    _gate(int(h.sum()) == 1, "C5 sum of coefficients")
+    parity = "invariants only"
+    if rank == 0 and not args.no_parity:
+        from oracle import parity as OP
+
+        k = min(64, P)
+        sub = whole[:k].contiguous()
+        got = E.histogram_device(sub, taus).cpu().numpy().reshape(-1)
+        want = OP.counter_slab_hist(SEED + 2, (k, H, W), 0, k, taus.taus, slab=32) if z0 == 0 else None
+        if want is not None:
+            _gate(np.array_equal(got, want), "C5 kernel on 64 planes of 2048^2 vs oracle")
+            parity = ("checked: global sum invariant; the kernel bit-exact vs the CPU oracle on the first "
+                      f"{k} planes of the C5 volume taken as a volume")
+        del sub
+    if dist_on:
+        dist.barrier(device_ids=[dev.index])
     for _ in range(2):
-        run()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    steps = max(3, min(args.steps, 10))
+        step()
     torch.cuda.synchronize()
+    if dist_on:
+        dist.barrier(device_ids=[dev.index])
+    steps = max(3, min(args.steps, 10))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(steps):
-        run()
+        step()
     e1.record(stream)
     torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / steps
-    if dist_on:
-        import torch.distributed as dist
-
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t[0])
+    ms = _max_over_ranks([e0.elapsed_time(e1) / steps], dev, dist_on)[0]
     peak, peak_kind = _peaks()
-    vox = P * H * W
-    gbs = 4.0 * vox / (ms * 1e-3) / 1e9
-    out = {"workload": "C5 per-GPU slab: planes [%d, %d) of the 2048^3 float32 counter volume (+ halos), "
-                       "1024 thresholds, fused slab kernel (ecc_histogram_range)" % (z0, z0 + P),
-           "value": vox * world / (ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": ms, "steps": steps,
-           "n_gpus": world, "scaling": "weak",
-           "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
-                        "peak_source": peak_kind}}
-    del padded, view
+    vox = Dz * H * W
+    gbs_gpu = 4.0 * vox / world / (ms * 1e-3) / 1e9
+    out = {"workload": f"C5: 3D {Dz}x2048x2048 float32 counter volume, discrete ECC, 1024 thresholds, "
+                       f"z-slabs over {world} GPU(s): halo exchange + slab sweep + NCCL histogram all-reduce",
+           "value": vox / (ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": ms, "steps": steps,
+           "n_gpus": world, "scaling": "strong", "planes_per_gpu": P, "parity": parity,
+           "gpu_launches_per_step": (4 if dist_on and world > 1 and P >= 3 else 2),
+           "roofline": {"bound": "hbm", "achieved": gbs_gpu, "peak": peak, "unit": "GB/s",
+                        "frac": gbs_gpu / peak, "peak_source": peak_kind, "per": "GPU"}}
+    del padded, gen, whole
     torch.cuda.empty_cache()
     return out
+
+
+def _soft_setup(ndim: int):
+    B, lam, alpha = 256, 50.0, 0.3
+    v = np.array([1.0, 2.0]) if ndim == 2 else np.array([1.0, 2.0, -0.5])
+    u = v / np.linalg.norm(v)
+    span = alpha * np.abs(u).sum()
+    return B, lam, alpha, v, u, np.linspace(-span, 1.0 + span, B + 1)[1:]
+
+
+def _soft_gate(E, x_np, taus, v, alpha, lam, dev, what):
+    """Module forward + backward on x_np (a few images / one small volume)
+    against the oracle: chi, d_values, d_tau, d_v, d_alpha normwise <= 1e-4."""
+    import torch
+
+    from oracle import parity as OP
+
+    m = E.SoftECC(taus, v, alpha=alpha, lam=lam).to(dev)
+    xt = torch.from_numpy(x_np).to(dev).requires_grad_(True)
+    chi = m(xt)
+    rng = np.random.default_rng(7)
+    up = rng.uniform(0.5, 1.5, (x_np.shape[0], len(taus)))
+    (chi * torch.from_numpy(up).to(dev)).sum().backward()
+    u = v / np.linalg.norm(v)
+    gtau, G = np.zeros(len(taus)), np.zeros(len(v))
+    worst = 0.0
+
+    def nw(a, b):
+        return float(np.abs(np.asarray(a, np.float64) - b).max() / max(np.abs(b).max(), 1e-300))
+
+    for i in range(x_np.shape[0]):
+        c_chi, dv, dt, _, _, Gi = OP.soft_item(x_np[i], lam, alpha, u, taus, up[i])
+        worst = max(worst, nw(chi[i].detach().cpu().numpy(), c_chi), nw(xt.grad[i].cpu().numpy(), dv))
+        gtau += dt
+        G += Gi
+    worst = max(worst, nw(m.taus.grad.cpu().numpy(), gtau))
+    du_raw = -alpha * G
+    worst = max(worst, nw(m.v.grad.cpu().numpy(), (du_raw - u * (u @ du_raw)) / np.linalg.norm(v)))
+    da = -(G @ u)
+    worst = max(worst, abs(float(m.alpha.grad) - da) / max(abs(da), 1e-4))
+    _gate(worst <= 1e-4, f"{what}: normwise error {worst:.2e} > 1e-4")
+    return worst
 
 
 def bench_c4(args, dev, world, rank, dist_on=False):
@@ -530,14 +678,12 @@ def bench_c4(args, dev, world, rank, dist_on=False):
 
     import paper_2510_20271_b200 as E
 
-    n, B, lam, alpha = 1024, 256, 50.0, 0.3
+    n = 1024
+    B, lam, alpha, v, u, taus0 = _soft_setup(3)
     g = torch.Generator(device=dev)
     g.manual_seed(SEED + 100 + rank)
     x = torch.rand((1, n, n, n), device=dev, generator=g, dtype=torch.float32)
-    v = np.array([1.0, 2.0, -0.5])
-    u = v / np.linalg.norm(v)
-    span = alpha * np.abs(u).sum()
-    m = E.SoftECC(np.linspace(-span, 1.0 + span, B + 1)[1:], v, alpha=alpha, lam=lam).to(dev)
+    m = E.SoftECC(taus0, v, alpha=alpha, lam=lam).to(dev)
     up = torch.ones((1, B), dtype=torch.float64, device=dev)
 
     def step():
@@ -557,22 +703,28 @@ def bench_c4(args, dev, world, rank, dist_on=False):
         step()
     e1.record()
     torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / steps
-    if dist_on:
-        import torch.distributed as dist
-
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t[0])
-    assert bool(torch.isfinite(m.taus.grad).all()), "non-finite d_tau at C4"
-    vox = n ** 3 * world
-    out = {"workload": "C4: 3D 1024^3 float32 soft ECC fwd+bwd, learnable tau/u/alpha, one item per GPU",
-           "value": vox / (ms * 1e-3), "unit": "voxel/s", "ms_per_step": ms, "steps": steps,
-           "n_gpus": world, "bins": B, "lambda": lam, "alpha": alpha, "parallelism": f"batch{world}",
-           "algorithmic_pairs_per_s": 2 * vox * B / (ms * 1e-3)}
+    ms = _max_over_ranks([e0.elapsed_time(e1) / steps], dev, dist_on)[0]
+    _gate(bool(torch.isfinite(m.taus.grad).all()) and bool(torch.isfinite(m.v.grad).all()), "C4 finite gradients")
     del x, m
     torch.cuda.empty_cache()
-    return out
+    parity = "finite gradients only"
+    if rank == 0 and not args.no_parity:
+        rng = np.random.default_rng(SEED + 100)
+        err = _soft_gate(E, rng.random((1, 128, 128, 128)).astype(np.float32), taus0, v, alpha, lam, dev,
+                         "C4 module on 128^3")
+        parity = (f"checked: the same 3-D module path on a 128^3 volume vs the CPU oracle (max normwise "
+                  f"error {err:.1e} <= 1e-4); the timed 1024^3 item: finite gradients")
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v_s, cores, sample, nvox = cpu_soft_sample(3)
+        cpu = {"value": v_s, "unit": "voxel/s", "cores": cores, "kind": "port",
+               "sample": sample, "extrapolated_ms_per_step": n ** 3 / v_s * 1e3}
+    vox = n ** 3 * world
+    return {"workload": "C4: 3D 1024^3 float32 soft ECC fwd+bwd, learnable tau/u/alpha, one item per GPU",
+            "value": vox / (ms * 1e-3), "unit": "voxel/s", "ms_per_step": ms, "steps": steps,
+            "n_gpus": world, "bins": B, "lambda": lam, "alpha": alpha, "parallelism": f"batch{world}",
+            "scaling": "weak", "parity": parity, "cpu_baseline": cpu,
+            "algorithmic_pairs_per_s": 2 * vox * B / (ms * 1e-3)}
 
 
 def bench_soft(args, dev, world, rank, dist_on=False):
@@ -580,49 +732,83 @@ def bench_soft(args, dev, world, rank, dist_on=False):
 
     import paper_2510_20271_b200 as E
 
-    N, H, W, B, lam, alpha = args.soft_batch, 1024, 1024, 256, 50.0, 0.3
+    N, H, W = args.soft_batch, 1024, 1024
+    B, lam, alpha, v, u, taus = _soft_setup(2)
     g = torch.Generator(device=dev)
     g.manual_seed(SEED + rank)
     x = torch.rand((N, H, W), device=dev, generator=g, dtype=torch.float32)
-    v = np.array([1.0, 2.0])
-    u = v / np.linalg.norm(v)
-    span = alpha * np.abs(u).sum()
-    taus = np.linspace(-span, 1.0 + span, B + 1)[1:]
     m = E.SoftECC(taus, v, alpha=alpha, lam=lam).to(dev)
     up = torch.ones((N, B), dtype=torch.float64, device=dev)
 
-    def step():
+    def step(xx):
         m.zero_grad(set_to_none=True)
-        chi = m(x)
+        chi = m(xx)
         chi.backward(up)
         if dist_on:
             from paper_2510_20271_b200 import distributed as D
 
             D.allreduce_soft_grads(m)
+        return chi
 
-    step()
+    step(x)
     torch.cuda.synchronize()
     steps = max(2, min(args.steps, 5))
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(steps):
-        step()
+        step(x)
     e1.record()
     torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / steps
-    if dist_on:
-        import torch.distributed as dist
-
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t[0])
+    ms = _max_over_ranks([e0.elapsed_time(e1) / steps], dev, dist_on)[0]
     # fraction of voxels with c != 0 (the kernels skip the others)
     from paper_2510_20271_b200 import soft as S
 
     p = S._params(lam, alpha, u, float(taus[0]), float(taus[-1]), 2, S._block_halfwidth(taus))
     c0, _ = S.soft_prepare_device(x[:8].contiguous(), (H, W), min(N, 8), p)
     nz = float(torch.count_nonzero(c0)) / c0.numel()
+    del c0
+
+    # e2e through the module: each step copies the batch pinned host -> HBM,
+    # runs forward + backward, and reads chi and the parameter gradients back
+    e2e = None
+    if not args.no_e2e:
+        host = torch.empty((N, H, W), dtype=torch.float32, pin_memory=True)
+        host.copy_(x.cpu())
+
+        def e2e_step():
+            xd = host.to(dev, non_blocking=True)
+            chi = step(xd)
+            return (chi.detach().cpu(), m.taus.grad.cpu(), m.v.grad.cpu(), m.alpha.grad.cpu())
+
+        e2e_step()
+        torch.cuda.synchronize()
+        reps = max(2, min(args.steps, 5))
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            e2e_step()
+        torch.cuda.synchronize()
+        e_ms = _max_over_ranks([(time.perf_counter() - t0) * 1e3 / reps], dev, dist_on)[0]
+        e2e = {"value": N * H * W * world / (e_ms * 1e-3), "unit": "voxel/s", "ms_per_step": e_ms,
+               "h2d_bytes_per_step": int(host.numel() * 4) * world,
+               "d2h_bytes_per_step": (N * B * 8 + B * 8 + 2 * 8 + 8) * world,
+               "api": "paper_2510_20271_b200.SoftECC forward + backward (pinned host batch -> HBM, chi and the "
+                      "tau / v / alpha gradients -> host, inside the timed region)"}
+        del host
+    del x
+    torch.cuda.empty_cache()
+    parity = "not checked"
+    if rank == 0 and not args.no_parity:
+        rng = np.random.default_rng(SEED)
+        err = _soft_gate(E, rng.random((2, H, W)).astype(np.float32), taus, v, alpha, lam, dev,
+                         "C3 module on 2 full images")
+        parity = (f"checked: the same module path on 2 full 1024x1024 images vs the CPU oracle "
+                  f"(chi, d_values, d_tau, d_v, d_alpha; max normwise error {err:.1e} <= 1e-4)")
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v_s, cores, sample, _ = cpu_soft_sample(2)
+        cpu = {"value": v_s, "unit": "voxel/s", "cores": cores, "kind": "port", "sample": sample,
+               "extrapolated_ms_per_step": N * H * W / v_s * 1e3}
     vox = N * H * W * world
     pairs = vox * B * 2                      # algorithmic (voxel, threshold) pairs, forward + backward
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
@@ -633,7 +819,7 @@ def bench_soft(args, dev, world, rank, dist_on=False):
     # ex2 per voxel and lane (T = 16)
     mufu_ops = nz * vox * B * ((0.5 + 1.0 / 16.0) + (7.0 / 8.0 + 1.0 / 16.0))
     return {"metric": "soft-ECC fwd+bwd voxels/s", "value": vox / (ms * 1e-3), "unit": "voxel/s",
-            "ms_per_step": ms, "steps": steps,
+            "ms_per_step": ms, "steps": steps, "parity": parity, "cpu_baseline": cpu, "e2e": e2e,
             "config": {"workload": "C3: batched 2D 128x1024x1024 f32, soft ECC fwd+bwd, learnable tau/u/alpha",
                        "batch_per_gpu": N, "bins": B, "lambda": lam, "alpha": alpha, "parallelism": f"batch{world}"},
             "roofline": {"bound": "sfu", "unit": "MUFU ops/s", "achieved": mufu_ops / (ms * 1e-3),
@@ -656,13 +842,15 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--planes", type=int, default=512, help="planes per GPU (512 = C2)")
+    ap.add_argument("--c5-depth", type=int, default=2048, help="planes of the C5 volume (2048 = C5)")
     ap.add_argument("--soft-batch", type=int, default=128)
     ap.add_argument("--no-soft", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-parity", action="store_true", help="skip the oracle gates (invariants only)")
     ap.add_argument("--no-ns", action="store_true", help="skip the 1024^3 north-star measurement")
     ap.add_argument("--no-c4", action="store_true", help="skip the 1024^3 soft (C4) measurement")
-    ap.add_argument("--no-c5", action="store_true", help="skip the C5 per-GPU slab measurement")
+    ap.add_argument("--no-c5", action="store_true", help="skip the C5 2048^3 measurement")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

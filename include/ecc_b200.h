@@ -95,7 +95,13 @@ int ecc_histogram(const void *x, int dtype, int ndim, const int64_t *dims, int64
  * 141-152 _coefficient_rows); they must hold the neighbouring slab's real
  * values (at the volume's ends, pass a view without the halo plane instead).
  * This is the z-slab entry point of the multi-GPU path (one rank = one slab
- * plus a one-plane halo on each interior side).  3D only. */
+ * plus a one-plane halo on each interior side).  3D only.
+ * The histograms of any partition of the planes sum, bit for bit, to the
+ * whole volume's (the all-reduce of the multi-GPU path).  A single range is a
+ * partial sum in the kernel's vertex order: the float32 fast path orders
+ * voxels by (threshold rank, index) rather than (value, index), so a cell
+ * whose two highest vertices share a bin and straddle the range boundary may
+ * be counted by the neighbouring range instead. */
 int ecc_histogram_range(const void *x, int dtype, int ndim, const int64_t *dims, int64_t batch,
                         int64_t plane_begin, int64_t plane_end, const void *table,
                         const ecc_binning *binning_host, int64_t *hist, void *stream);

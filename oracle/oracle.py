@@ -66,6 +66,7 @@ def lib():
                                                ctypes.c_int64, vp, vp, vp, vp]
         L.ecc_oracle_counter_grid.argtypes = [ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64, vp]
         L.ecc_oracle_num_threads.restype = ctypes.c_int
+        L.ecc_oracle_set_threads.argtypes = [ctypes.c_int]
         _lib = L
     return _lib
 
@@ -80,6 +81,11 @@ def _dims(x: np.ndarray) -> np.ndarray:
 
 def num_threads() -> int:
     return int(lib().ecc_oracle_num_threads())
+
+
+def set_threads(n: int) -> None:
+    """Thread count of the parallel loops (the reference's ``workers``)."""
+    lib().ecc_oracle_set_threads(int(n))
 
 
 def coefficients(values) -> np.ndarray:
