@@ -106,6 +106,15 @@ int ecc_histogram_range(const void *x, int dtype, int ndim, const int64_t *dims,
                         int64_t plane_begin, int64_t plane_end, const void *table,
                         const ecc_binning *binning_host, int64_t *hist, void *stream);
 
+/* ecc_histogram_range plus the reference's finiteness rule (ScalarGrid,
+ * grid.py:63-64) checked on the device: *nonfinite (device int32) is set to
+ * 1 when any value read is NaN or +-Inf, else 0.  The float32 rank kernels
+ * check while they sweep (no second pass over the volume); other paths run
+ * a check pass.  plane_begin/plane_end as ecc_histogram_range (2D: 0, 1). */
+int ecc_histogram_checked(const void *x, int dtype, int ndim, const int64_t *dims, int64_t batch,
+                          int64_t plane_begin, int64_t plane_end, const void *table,
+                          const ecc_binning *binning_host, int64_t *hist, int32_t *nonfinite, void *stream);
+
 /* Inclusive prefix sum of bins[0..nbins) per batch item -> int64 curve
  * [batch][nbins] (compute_ecc, hard.py:226). */
 int ecc_scan(const int64_t *hist, int64_t batch, int64_t nbins, int64_t *curve, void *stream);
@@ -173,6 +182,36 @@ int ecc_soft_backward(const int8_t *coeffs, const float *field_c, const float *f
                       const int64_t *dims, int64_t batch, const double *taus, int64_t nbins,
                       const ecc_soft_params *params_host, const double *upstream, float *d_values, double *d_tau,
                       double *G, void *workspace, void *stream);
+
+/* Sync-free variants for the autograd module (no device->host read per
+ * call, so forward + backward can be captured in a CUDA graph or traced by
+ * torch.compile): the parameters live in DEVICE memory.
+ * ecc_soft_setup fills *params_dev from device tensors: center =
+ * (min tau + max tau) / 2, factorized = lam log2(e) h <= 40 with h the
+ * largest half-width of the 32-threshold blocks, lam, *alpha, u[0..ndim)
+ * (taus, u, alpha: device float64).  The _d entry points take that device
+ * struct instead of a host one; they launch both sigmoid modes and the one
+ * the device flag does not select exits at once, so field_lo is required. */
+int ecc_soft_setup(const double *taus, int64_t nbins, const double *u, int ndim, const double *alpha, double lam,
+                   ecc_soft_params *params_dev, void *stream);
+int ecc_soft_prepare_d(const void *x, int dtype, int ndim, const int64_t *dims, int64_t batch,
+                       const ecc_soft_params *params_dev, int8_t *coeffs, float *field_c, float *field_lo,
+                       void *stream);
+int ecc_soft_forward_d(const int8_t *coeffs, const float *field_c, const float *field_lo, int ndim,
+                       const int64_t *dims, int64_t batch, const double *taus, int64_t nbins,
+                       const ecc_soft_params *params_dev, double *chi, void *workspace, void *stream);
+int ecc_soft_backward_d(const int8_t *coeffs, const float *field_c, const float *field_lo, int ndim,
+                        const int64_t *dims, int64_t batch, const double *taus, int64_t nbins,
+                        const ecc_soft_params *params_dev, const double *upstream, float *d_values, double *d_tau,
+                        double *G, void *workspace, void *stream);
+
+/* Kernel-variant switch for A/B checks (tests, tools/): key "f3" with value
+ * default | value | branch | cta | rank2 | no2d | edge1 | dummy | static,
+ * "zunit" (forced dynamic unit in planes, "0" = automatic), "generic"
+ * ("1": every grid through the generic sweep), "soft_fwd_t" / "soft_bwd_t"
+ * (thresholds per soft lane: 8, 16, 32).  Process-wide; the production
+ * kernels are the defaults.  Returns 0 or ECC_EINVAL. */
+int ecc_set_variant(const char *key, const char *value);
 
 /* Finite-difference harness for gradient_check (soft.py:260-359), float64:
  * 4th-order central differences (soft.py:308-315) with step `step` of

@@ -31,6 +31,7 @@ from .hard import (
     device_minmax,
     ecc_discrete,
     ecc_discrete_host,
+    release_host_buffers,
     histogram_device,
     merge_histograms,
     parse_strategy,
@@ -70,7 +71,7 @@ __all__ = [
     "COEFF_RANGE", "CoefficientGrid", "Chunked", "CorruptionError", "EulerCurve", "FormatError", "FullSweep",
     "HistogramBins", "ScalarGrid", "SoftECC", "SoftECCFunction", "SoftEccParams", "SoftGradients", "ThresholdSet",
     "accumulate_histogram", "bin_index", "coefficients_device", "compute_coefficients", "compute_ecc",
-    "device_minmax", "ecc_discrete", "ecc_discrete_host", "effective_field", "flatten_index", "histogram_device", "merge_histograms",
+    "device_minmax", "ecc_discrete", "ecc_discrete_host", "release_host_buffers", "effective_field", "flatten_index", "histogram_device", "merge_histograms",
     "parse_strategy", "pixel_coordinates", "reparametrize_direction", "reparametrize_direction_jvp", "scan_device",
     "soft_ecc", "soft_ecc_backward", "thresholds_from_range", "unflatten_index", "uniform_thresholds",
     "vertex_order", "gradient_check", "MAGIC", "VERSION_COEFF", "VERSION_SCALAR", "load_grid_device", "load_slab_device",

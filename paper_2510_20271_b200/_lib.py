@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+from contextlib import contextmanager
 from pathlib import Path
 
 import numpy as np
@@ -57,6 +58,9 @@ def lib():
         L.ecc_threshold_table_bytes.restype = ctypes.c_size_t
         L.ecc_histogram.argtypes = [vp, i32, i32, vp, i64, vp, ctypes.POINTER(Binning), vp, vp]
         L.ecc_histogram_range.argtypes = [vp, i32, i32, vp, i64, i64, i64, vp, ctypes.POINTER(Binning), vp, vp]
+        if hasattr(L, "ecc_histogram_checked"):   # absent from older builds used in A/B tools
+            L.ecc_histogram_checked.argtypes = [vp, i32, i32, vp, i64, i64, i64, vp, ctypes.POINTER(Binning), vp,
+                                                vp, vp]
         L.ecc_scan.argtypes = [vp, i64, i64, vp, vp]
         L.ecc_coefficients.argtypes = [vp, i32, i32, vp, i64, vp, vp]
         L.ecc_minmax.argtypes = [vp, i32, i64, vp, vp]
@@ -72,8 +76,48 @@ def lib():
         L.ecc_counter_grid.argtypes = [ctypes.c_uint64, i64, i64, vp, vp]
         dbl = ctypes.c_double
         L.ecc_soft_fd.argtypes = [vp, vp, i32, vp, vp, i64, vp, dbl, dbl, vp, dbl, vp, vp, vp, vp]
+        if hasattr(L, "ecc_soft_setup"):
+            L.ecc_soft_setup.argtypes = [vp, i64, vp, i32, vp, dbl, vp, vp]
+            L.ecc_soft_prepare_d.argtypes = [vp, i32, i32, vp, i64, vp, vp, vp, vp, vp]
+            L.ecc_soft_forward_d.argtypes = [vp, vp, vp, i32, vp, i64, vp, i64, vp, vp, vp, vp]
+            L.ecc_soft_backward_d.argtypes = [vp, vp, vp, i32, vp, i64, vp, i64, vp, vp, vp, vp, vp, vp, vp]
         _lib = L
+        if hasattr(L, "ecc_set_variant"):
+            L.ecc_set_variant.argtypes = [ctypes.c_char_p, ctypes.c_char_p]
+            _apply_env_variants()
     return _lib
+
+
+# Kernel-variant switches (A/B checks; ecc_set_variant in the C ABI).  The
+# launchers never read the environment; for the development tools the legacy
+# ECC_B200_* variables are applied once, when the library is loaded.
+_VARIANT_DEFAULTS = {"f3": "default", "zunit": "0", "generic": "0", "soft_fwd_t": "16", "soft_bwd_t": "16"}
+_VARIANT_ENV = {"f3": "ECC_B200_F3", "zunit": "ECC_B200_F3_ZUNIT", "generic": "ECC_B200_GENERIC",
+                "soft_fwd_t": "ECC_SOFT_FWD_T", "soft_bwd_t": "ECC_SOFT_BWD_T"}
+
+
+def set_variant(key: str, value) -> None:
+    check(lib().ecc_set_variant(key.encode(), str(value).encode()))
+
+
+def _apply_env_variants() -> None:
+    for key, env in _VARIANT_ENV.items():
+        v = os.environ.get(env)
+        if v:
+            set_variant(key, v)
+
+
+@contextmanager
+def variant(**kw):
+    """Run a block with kernel variants switched (f3=..., zunit=..., generic=1,
+    soft_fwd_t=..., soft_bwd_t=...); the production defaults are restored after."""
+    for k, v in kw.items():
+        set_variant(k, v)
+    try:
+        yield
+    finally:
+        for k in kw:
+            set_variant(k, _VARIANT_DEFAULTS[k])
 
 
 def check(rc: int):

@@ -108,9 +108,10 @@ __device__ __forceinline__ int bin_of(V x, const V* __restrict__ tab, int nb, V 
     g = g < V(0) ? V(0) : g;
     g = g > V(nb) ? V(nb) : g;
     j = (int)g;
+    if (!(j >= 0 && j <= nb)) j = 0;   // NaN (non-finite grids are rejected, but must not fault)
     // tab is offset by one: tab[j+1] == tau_j
-    while (x > tab[j + 1]) ++j;   // stops at tab[nb+1] = +inf
-    while (x <= tab[j]) --j;      // stops at tab[0] = -inf
+    while (x > tab[j + 1]) ++j;            // stops at tab[nb+1] = +inf
+    while (j > 0 && x <= tab[j]) --j;      // stops at tab[0] = -inf (x = -inf: bin 0)
   } else {
     int lo = 0, hi = nb;
     while (lo < hi) {

@@ -10,6 +10,10 @@
 // subnormal comparisons (the reference's hypothesis test draws subnormals).
 #include "ecc_common.cuh"
 #include "ecc_internal.h"
+#include <algorithm>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <stdlib.h>
 
 namespace ecc {
@@ -33,6 +37,7 @@ struct RawSrc<uint8_t> {
   __device__ __forceinline__ R raw(int64_t lin) const { return (float)x[lin]; }
   __device__ __forceinline__ V make(R r, int64_t, int64_t, int64_t) const { return r; }
   __device__ __forceinline__ V at(int64_t lin, int64_t, int64_t, int64_t) const { return (float)x[lin]; }
+  __device__ __forceinline__ void init() {}
 };
 template <>
 struct RawSrc<float> {
@@ -43,6 +48,7 @@ struct RawSrc<float> {
   __device__ __forceinline__ R raw(int64_t lin) const { return x[lin]; }
   __device__ __forceinline__ V make(R r, int64_t, int64_t, int64_t) const { return r; }
   __device__ __forceinline__ V at(int64_t lin, int64_t, int64_t, int64_t) const { return x[lin]; }
+  __device__ __forceinline__ void init() {}
 };
 template <>
 struct RawSrc<double> {
@@ -53,6 +59,7 @@ struct RawSrc<double> {
   __device__ __forceinline__ R raw(int64_t lin) const { return x[lin]; }
   __device__ __forceinline__ V make(R r, int64_t, int64_t, int64_t) const { return r; }
   __device__ __forceinline__ V at(int64_t lin, int64_t, int64_t, int64_t) const { return x[lin]; }
+  __device__ __forceinline__ void init() {}
 };
 
 
@@ -67,6 +74,17 @@ struct EffSrc {
   int64_t D, H, W;
   int ndim;
   double sD, sH, sW;   // 2.0 / (d - 1) in float64 (host-computed like numpy), 0 when d == 1
+  // device-resident soft parameters (ecc_soft_setup; sync-free module path):
+  // alpha and u are read from there when the kernel starts
+  const ecc_soft_params* pd = nullptr;
+  __device__ __forceinline__ void init() {
+    if (pd) {
+      alpha = pd->alpha;
+      u0 = pd->u[0];
+      u1 = pd->u[1];
+      u2 = pd->u[2];
+    }
+  }
   // pixel_coordinates (soft.py:79-94): idx * (2/(d-1)) - 1 with two roundings; 0 for d == 1
   __device__ __forceinline__ static double crd(int64_t idx, int64_t d, double s) {
     // extents are < 2^31 (checked by the launchers), so the int32 -> f64
@@ -131,9 +149,16 @@ struct HistSink {
   V* s_tab;
   int64_t cur_item_n;
   int64_t pending;   // voxels deposited since last flush (int32 overflow guard)
+  // global mode (bin counts whose counters and table do not fit in shared
+  // memory): the table is read through L1 and every voxel adds its c to the
+  // int64 global histogram directly -- slower, but any bin count works
+  int global_mode = 0;
 
   __device__ void init(unsigned char* smem) {
     const int nb = (int)bp.nb;
+    cur_item_n = -1;
+    pending = 0;
+    if (global_mode) return;
     s_hist = reinterpret_cast<int*>(smem);
     size_t off = ((size_t)(nb + 1) * sizeof(int) + 15) & ~size_t(15);
     s_tab = reinterpret_cast<V*>(smem + off);
@@ -145,8 +170,10 @@ struct HistSink {
   static size_t smem_bytes(int64_t nb) {
     return (((size_t)(nb + 1) * sizeof(int) + 15) & ~size_t(15)) + (size_t)(nb + 2) * sizeof(V);
   }
+  // shared-memory budget of the counters + table; above it the global mode
+  static constexpr size_t kSmemMax = 120 * 1024;
   __device__ void flush() {
-    if (cur_item_n < 0) return;
+    if (cur_item_n < 0 || global_mode) return;
     const int nb = (int)bp.nb;
     unsigned long long* h = hist + cur_item_n * (nb + 1);
     for (int i = threadIdx.x; i <= nb; i += blockDim.x) {
@@ -159,6 +186,10 @@ struct HistSink {
   }
   // called by all threads at the start of a work item (after a barrier)
   __device__ void begin_item(int64_t n, int64_t voxels) {
+    if (global_mode) {
+      cur_item_n = n;
+      return;
+    }
     if (n != cur_item_n || pending + voxels > (int64_t(1) << 27)) {
       flush();
       __syncthreads();
@@ -170,8 +201,13 @@ struct HistSink {
   __device__ void end() { __syncthreads(); flush(); }
   __device__ __forceinline__ void put(int c, V value, int64_t, int64_t, int64_t, int64_t) {
     if (c != 0) {
-      int j = bin_of<V>(value, s_tab, (int)bp.nb, (V)bp.t0, (V)bp.inv_w, bp.mode);
-      atomicAdd(&s_hist[j], c);
+      if (global_mode) {
+        const int j = bin_of<V>(value, tab_g, (int)bp.nb, (V)bp.t0, (V)bp.inv_w, bp.mode);
+        atomicAdd(hist + cur_item_n * (bp.nb + 1) + j, (unsigned long long)(long long)c);
+      } else {
+        const int j = bin_of<V>(value, s_tab, (int)bp.nb, (V)bp.t0, (V)bp.inv_w, bp.mode);
+        atomicAdd(&s_hist[j], c);
+      }
     }
   }
 };
@@ -197,7 +233,10 @@ struct SoftPrepSink {
   float* __restrict__ fclo;   // optional: (f - m) - fc, for the float64-exponent direct mode
   double center;
   int64_t D, H, W;
-  __device__ void init(unsigned char*) {}
+  const ecc_soft_params* pd = nullptr;   // device-resident parameters: the centre is read there
+  __device__ void init(unsigned char*) {
+    if (pd) center = pd->center;
+  }
   static size_t smem_bytes(int64_t) { return 0; }
   __device__ void begin_item(int64_t, int64_t) {}
   __device__ void end() {}
@@ -227,6 +266,7 @@ ecc_sweep_kernel(Src src, Sink sink, Geom g) {
   V* planes = reinterpret_cast<V*>(smem_raw);                       // [NBUF][PH][PW]
   unsigned char* sink_smem = smem_raw + sizeof(V) * NBUF * PLANE;
   sink.init(sink_smem);
+  src.init();
   __syncthreads();
 
   const int tx = threadIdx.x & (TX - 1);
@@ -476,6 +516,35 @@ static Geom make_geom(const int64_t* dims3, int64_t batch, int64_t zc_hint, int6
   return g;
 }
 
+// function attribute + occupancy once per (kernel, smem bytes, device)
+static int sweep_occupancy(const void* kfn, size_t smem, int* occ) {
+  // the attribute is raised to the largest dynamic smem any launch of the
+  // kernel asked for (a smaller later setting would fail the larger launch)
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, size_t, int>, int> cache;
+  static std::map<std::pair<const void*, int>, size_t> attr;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find({kfn, smem, dev});
+  if (it != cache.end()) {
+    *occ = it->second;
+    return ECC_OK;
+  }
+  size_t& cur = attr[{kfn, dev}];
+  if (smem > 48 * 1024 && smem > cur) {
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(sweep)");
+    cur = smem;
+  }
+  int o = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kfn, NT, smem);
+  if (o < 1) return set_error(ECC_EINVAL, "sweep kernel does not fit on an SM");
+  cache[{kfn, smem, dev}] = o;
+  *occ = o;
+  return ECC_OK;
+}
+
 template <typename Src, typename Sink>
 static int launch_sweep(Src src, Sink sink, const int64_t* dims3, int64_t batch, size_t sink_smem,
                         cudaStream_t stream, int64_t zb = 0, int64_t ze = -1) {
@@ -483,13 +552,8 @@ static int launch_sweep(Src src, Sink sink, const int64_t* dims3, int64_t batch,
   using V = typename Src::V;
   const size_t smem = sizeof(V) * NBUF * PLANE + sink_smem;
   auto kfn = ecc_sweep_kernel<Src, Sink>;
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(sweep)");
-  }
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, NT, smem);
-  if (occ < 1) return set_error(ECC_EINVAL, "sweep kernel does not fit on an SM (too many thresholds?)");
+  if (int rc = sweep_occupancy(reinterpret_cast<const void*>(kfn), smem, &occ)) return rc;
   const int64_t max_ctas = (int64_t)num_sms() * occ;
   if (ze <= zb) return ECC_OK;
   Geom g = make_geom(dims3, batch, 0, max_ctas, zb, ze);
@@ -525,9 +589,21 @@ static int dims_to3(int ndim, const int64_t* dims, int64_t out[3]) {
   return ECC_OK;
 }
 
-extern "C" int ecc_histogram_range(const void* x, int dtype, int ndim, const int64_t* dims, int64_t batch,
-                                   int64_t plane_begin, int64_t plane_end, const void* table,
-                                   const ecc_binning* binning, int64_t* hist, void* stream) {
+namespace ecc {
+// non-finite check pass for the kernels that do not check while they sweep
+// (the float32 fallbacks; the production rank kernels fuse it)
+template <typename T>
+__global__ void nonfinite_kernel(const T* __restrict__ x, int64_t n, int* __restrict__ nf) {
+  bool bad = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    bad |= !isfinite((double)x[i]);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nf, 1);
+}
+}  // namespace ecc
+
+static int histogram_range_impl(const void* x, int dtype, int ndim, const int64_t* dims, int64_t batch,
+                                int64_t plane_begin, int64_t plane_end, const void* table,
+                                const ecc_binning* binning, int64_t* hist, int* nf, void* stream) {
   clear_error();
   int64_t d3[3];
   int rc = dims_to3(ndim, dims, d3);
@@ -544,6 +620,8 @@ extern "C" int ecc_histogram_range(const void* x, int dtype, int ndim, const int
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e = cudaMemsetAsync(hist, 0, sizeof(int64_t) * (size_t)batch * (size_t)(nb + 1), s);
   if (e != cudaSuccess) return set_cuda_error(e, "cudaMemsetAsync(hist)");
+  if (nf && (e = cudaMemsetAsync(nf, 0, sizeof(int), s)) != cudaSuccess)
+    return set_cuda_error(e, "cudaMemsetAsync(nonfinite flag)");
   BinParams bp;
   bp.t0 = binning->t0;
   bp.inv_w = binning->inv_w;
@@ -552,30 +630,64 @@ extern "C" int ecc_histogram_range(const void* x, int dtype, int ndim, const int
   bp.pad = 0;
   auto* h = reinterpret_cast<unsigned long long*>(hist);
   switch (dtype) {
-    case ECC_DTYPE_U8: {
-      if (fast3d_u8_eligible(x, d3[0], d3[1], d3[2], batch, nb) && !getenv("ECC_B200_GENERIC"))
+    case ECC_DTYPE_U8: {   // always finite
+      if (fast3d_u8_eligible(x, d3[0], d3[1], d3[2], batch, nb) && !variant_generic())
         return fast3d_u8_launch((const uint8_t*)x, d3[0], d3[1], d3[2], batch, plane_begin, plane_end, table,
                                 binning, h, s);
       HistSink<float> sk{(const float*)table, h, bp};
-      return launch_sweep(RawSrc<uint8_t>{(const uint8_t*)x}, sk, d3, batch, HistSink<float>::smem_bytes(nb), s,
-                          plane_begin, plane_end);
+      sk.global_mode = HistSink<float>::smem_bytes(nb) > HistSink<float>::kSmemMax;
+      return launch_sweep(RawSrc<uint8_t>{(const uint8_t*)x}, sk, d3, batch,
+                          sk.global_mode ? 0 : HistSink<float>::smem_bytes(nb), s, plane_begin, plane_end);
     }
     case ECC_DTYPE_F32: {
-      if (fast3d_eligible(x, d3[0], d3[1], d3[2], batch, nb) && !getenv("ECC_B200_GENERIC"))
-        return fast3d_launch((const float*)x, d3[0], d3[1], d3[2], batch, plane_begin, plane_end, table, binning, h,
-                             s);
-      HistSink<float> sk{(const float*)table, h, bp};
-      return launch_sweep(RawSrc<float>{(const float*)x}, sk, d3, batch, HistSink<float>::smem_bytes(nb), s,
-                          plane_begin, plane_end);
+      bool checked = false;
+      if (fast3d_eligible(x, d3[0], d3[1], d3[2], batch, nb) && !variant_generic()) {
+        rc = fast3d_launch((const float*)x, d3[0], d3[1], d3[2], batch, plane_begin, plane_end, table, binning, h, s,
+                           nf, &checked);
+      } else {
+        HistSink<float> sk{(const float*)table, h, bp};
+        sk.global_mode = HistSink<float>::smem_bytes(nb) > HistSink<float>::kSmemMax;
+        rc = launch_sweep(RawSrc<float>{(const float*)x}, sk, d3, batch,
+                          sk.global_mode ? 0 : HistSink<float>::smem_bytes(nb), s, plane_begin, plane_end);
+      }
+      if (rc || !nf || checked) return rc;
+      const int64_t n = batch * d3[0] * d3[1] * d3[2];
+      nonfinite_kernel<float><<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, s>>>(
+          (const float*)x, n, nf);
+      return check_launch("nonfinite_kernel");
     }
     case ECC_DTYPE_F64: {
       HistSink<double> sk{(const double*)table, h, bp};
-      return launch_sweep(RawSrc<double>{(const double*)x}, sk, d3, batch, HistSink<double>::smem_bytes(nb), s,
-                          plane_begin, plane_end);
+      sk.global_mode = HistSink<double>::smem_bytes(nb) > HistSink<double>::kSmemMax;
+      rc = launch_sweep(RawSrc<double>{(const double*)x}, sk, d3, batch,
+                        sk.global_mode ? 0 : HistSink<double>::smem_bytes(nb), s, plane_begin, plane_end);
+      if (rc || !nf) return rc;
+      const int64_t n = batch * d3[0] * d3[1] * d3[2];
+      nonfinite_kernel<double><<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, s>>>(
+          (const double*)x, n, nf);
+      return check_launch("nonfinite_kernel");
     }
     default:
       return set_error(ECC_EINVAL, "unsupported dtype");
   }
+}
+
+extern "C" int ecc_histogram_range(const void* x, int dtype, int ndim, const int64_t* dims, int64_t batch,
+                                   int64_t plane_begin, int64_t plane_end, const void* table,
+                                   const ecc_binning* binning, int64_t* hist, void* stream) {
+  return histogram_range_impl(x, dtype, ndim, dims, batch, plane_begin, plane_end, table, binning, hist, nullptr,
+                              stream);
+}
+
+extern "C" int ecc_histogram_checked(const void* x, int dtype, int ndim, const int64_t* dims, int64_t batch,
+                                     int64_t plane_begin, int64_t plane_end, const void* table,
+                                     const ecc_binning* binning, int64_t* hist, int32_t* nonfinite, void* stream) {
+  if (!nonfinite) {
+    clear_error();
+    return set_error(ECC_EINVAL, "null pointer argument");
+  }
+  return histogram_range_impl(x, dtype, ndim, dims, batch, plane_begin, plane_end, table, binning, hist, nonfinite,
+                              stream);
 }
 
 extern "C" int ecc_histogram(const void* x, int dtype, int ndim, const int64_t* dims, int64_t batch,
@@ -654,6 +766,8 @@ namespace ecc {
 template <typename T>
 __global__ void __launch_bounds__(256) soft_prep2d_kernel(EffSrc<T> src, double center, int8_t* __restrict__ coeffs,
                                                           float* __restrict__ fc, float* __restrict__ fclo) {
+  src.init();
+  if (src.pd) center = src.pd->center;
   // 32 x 32 outputs per CTA (8 warps x 4 rows); the 34 x 34 effective-field
   // tile is loaded with all of a thread's global loads in flight at once
   constexpr int TH = PREP_TH, TW = 32, PWD = TW + 2, PHT = TH + 2, NE = PWD * PHT, PER = (NE + 255) / 256;
@@ -699,28 +813,30 @@ __global__ void __launch_bounds__(256) soft_prep2d_kernel(EffSrc<T> src, double 
 }
 }  // namespace ecc
 
-extern "C" int ecc_soft_prepare(const void* x, int dtype, int ndim, const int64_t* dims, int64_t batch,
-                                const ecc_soft_params* p, int8_t* coeffs, float* field_c, float* field_lo,
-                                void* stream) {
+// p: host parameters, or (pd != nullptr) parameters resident on the device
+// (ecc_soft_setup); the values in *p are then placeholders
+static int soft_prepare(const void* x, int dtype, int ndim, const int64_t* dims, int64_t batch,
+                        const ecc_soft_params* p, const ecc_soft_params* pd, int8_t* coeffs, float* field_c,
+                        float* field_lo, void* stream) {
   clear_error();
   int64_t d3[3];
   int rc = dims_to3(ndim, dims, d3);
   if (rc) return rc;
   if (!x || !p || !coeffs || !field_c) return set_error(ECC_EINVAL, "null pointer argument");
   if (batch < 1) return set_error(ECC_EINVAL, "batch must be >= 1");
-  SoftPrepSink sk{coeffs, field_c, field_lo, p->center, d3[0], d3[1], d3[2]};
+  SoftPrepSink sk{coeffs, field_c, field_lo, p->center, d3[0], d3[1], d3[2], pd};
   cudaStream_t s = (cudaStream_t)stream;
   if (ndim == 2 && batch <= 65535 && (dtype == ECC_DTYPE_F32 || dtype == ECC_DTYPE_F64) &&
-      !getenv("ECC_B200_GENERIC")) {
+      !variant_generic()) {
     dim3 grid((unsigned)((d3[2] + 31) / 32), (unsigned)((d3[1] + PREP_TH - 1) / PREP_TH), (unsigned)batch);
     if (grid.y > 65535) goto generic;
     if (dtype == ECC_DTYPE_F32) {
       EffSrc<float> src{(const float*)x, p->alpha, p->u[0], p->u[1], 0.0, 1, d3[1], d3[2], 2,
-                        0.0, coord_scale(d3[1]), coord_scale(d3[2])};
+                        0.0, coord_scale(d3[1]), coord_scale(d3[2]), pd};
       soft_prep2d_kernel<float><<<grid, 256, 0, s>>>(src, p->center, coeffs, field_c, field_lo);
     } else {
       EffSrc<double> src{(const double*)x, p->alpha, p->u[0], p->u[1], 0.0, 1, d3[1], d3[2], 2,
-                         0.0, coord_scale(d3[1]), coord_scale(d3[2])};
+                         0.0, coord_scale(d3[1]), coord_scale(d3[2]), pd};
       soft_prep2d_kernel<double><<<grid, 256, 0, s>>>(src, p->center, coeffs, field_c, field_lo);
     }
     return check_launch("soft_prep2d_kernel");
@@ -728,14 +844,28 @@ extern "C" int ecc_soft_prepare(const void* x, int dtype, int ndim, const int64_
 generic:
   if (dtype == ECC_DTYPE_F32) {
     EffSrc<float> src{(const float*)x, p->alpha, p->u[0], p->u[1], p->u[2], d3[0], d3[1], d3[2], ndim,
-                      coord_scale(d3[0]), coord_scale(d3[1]), coord_scale(d3[2])};
+                      coord_scale(d3[0]), coord_scale(d3[1]), coord_scale(d3[2]), pd};
     return launch_sweep(src, sk, d3, batch, 0, s);
   } else if (dtype == ECC_DTYPE_F64) {
     EffSrc<double> src{(const double*)x, p->alpha, p->u[0], p->u[1], p->u[2], d3[0], d3[1], d3[2], ndim,
-                       coord_scale(d3[0]), coord_scale(d3[1]), coord_scale(d3[2])};
+                       coord_scale(d3[0]), coord_scale(d3[1]), coord_scale(d3[2]), pd};
     return launch_sweep(src, sk, d3, batch, 0, s);
   }
   return set_error(ECC_EINVAL, "soft path takes float32 or float64 grids");
+}
+
+extern "C" int ecc_soft_prepare(const void* x, int dtype, int ndim, const int64_t* dims, int64_t batch,
+                                const ecc_soft_params* p, int8_t* coeffs, float* field_c, float* field_lo,
+                                void* stream) {
+  return soft_prepare(x, dtype, ndim, dims, batch, p, nullptr, coeffs, field_c, field_lo, stream);
+}
+
+extern "C" int ecc_soft_prepare_d(const void* x, int dtype, int ndim, const int64_t* dims, int64_t batch,
+                                  const ecc_soft_params* params_dev, int8_t* coeffs, float* field_c, float* field_lo,
+                                  void* stream) {
+  if (!params_dev) return set_error(ECC_EINVAL, "null pointer argument");
+  const ecc_soft_params placeholder{1.0, 0.0, {0.0, 0.0, 0.0}, 0.0, 1, 0};
+  return soft_prepare(x, dtype, ndim, dims, batch, &placeholder, params_dev, coeffs, field_c, field_lo, stream);
 }
 
 namespace ecc {

@@ -30,6 +30,9 @@
 // mbarriers; one thread issues, all threads wait on the stage's parity.
 #include <cuda.h>
 #include <atomic>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <algorithm>
 #include <cudaTypedefs.h>
 #include <stdint.h>
@@ -60,6 +63,7 @@ struct Geom {
   int64_t items;
   unsigned int* wq = nullptr;   // dynamic work queue (rank kernel): next unit, zeroed before the launch
   int zunit = 0;                // planes per dynamic unit (0: static partition)
+  int* nf = nullptr;            // non-finite flag (ecc_histogram_checked), rank4 / 2-D edge4 kernels
   float r4_magic = 0.f;         // edge4 rank (R4): M = 2^23 + 1024 + z
   uint32_t r4_emask = 0;        //                  edge test mask 0x3FF & ~(2z - 1)
 };
@@ -886,6 +890,23 @@ __device__ __forceinline__ void fma2_rz(float a0, float a1, uint64_t b2, uint64_
   asm("fma.rz.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2pack(a0, a1)), "l"(b2), "l"(c2));
   asm("mov.b64 {%0, %1}, %2;" : "=r"(r0), "=r"(r1) : "l"(r));
 }
+// Non-finite detection fused into the rank pass: acc = fma(x, 0, acc) stays
+// +-0 for finite x and turns NaN for any NaN or +-Inf, on the FMA pipe (two
+// voxels per fma.rn.f32x2, ~0.5 instructions per voxel).  The kernel ORs a
+// device flag at the end (ecc_histogram_checked: ScalarGrid's finiteness
+// rule, grid.py:63-64, without a second pass over the volume).
+#ifndef ECC_R4_NF
+#define ECC_R4_NF 1
+#endif
+__device__ __forceinline__ void nf_acc2(float a, float b, uint64_t& acc2) {
+  if (ECC_R4_NF) asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc2) : "l"(f2pack(a, b)), "l"(0ull));
+}
+__device__ __forceinline__ bool nf_any(uint64_t acc2) {
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(acc2));
+  return !(a == 0.f && b == 0.f);
+}
+
 template <bool TEG>
 __device__ __forceinline__ float r4_boundary(const R4& r, uint32_t f) {   // tE[f / 4 - 1]
   if (TEG) return __ldg(r.tE_g + (f >> 2) - 1);
@@ -908,7 +929,8 @@ __device__ __forceinline__ uint32_t rank4_field(float x, const R4& r) {
 // pitch (per-warp TMA boxes) free of bank conflicts; the words go to the
 // matching (dynamic) offsets.
 template <bool CHECK, bool TEG, bool ROT>
-__device__ __forceinline__ void rank4_rowseg(const float* src, uint32_t* dw, uint32_t* de, const R4& r) {
+__device__ __forceinline__ void rank4_rowseg(const float* src, uint32_t* dw, uint32_t* de, const R4& r,
+                                             uint64_t& nfa, int nvalid) {
   const float4* s4 = reinterpret_cast<const float4*>(src);
   const uint64_t fc2 = f2pack(r.fc, r.fc), mg2 = f2pack(r.magic, r.magic);
   const int q = ROT ? (int)((threadIdx.x >> 2) & 1u) : 0;
@@ -918,6 +940,18 @@ __device__ __forceinline__ void rank4_rowseg(const float* src, uint32_t* dw, uin
     const int g = (ROT && ECC_R4_ROT) ? (gi ^ q) : gi;   // chunk pair: voxels 4g..4g+3 and 16+4g..16+4g+3
     const float4 lo = s4[g], hi = s4[4 + g];
     const float a[4] = {lo.x, lo.y, lo.z, lo.w}, b[4] = {hi.x, hi.y, hi.z, hi.w};
+    if (!CHECK) {
+      nf_acc2(lo.x, lo.y, nfa);
+      nf_acc2(lo.z, lo.w, nfa);
+      nf_acc2(hi.x, hi.y, nfa);
+      nf_acc2(hi.z, hi.w, nfa);
+    } else {   // columns past the grid hold the TMA's NaN fill
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        if (4 * g + m < nvalid) nf_acc2(a[m], 0.f, nfa);
+        if (16 + 4 * g + m < nvalid) nf_acc2(b[m], 0.f, nfa);
+      }
+    }
     uint32_t w[4];
     uint32_t em = 0;   // bits m (voxel 4g + m) and 16 + m (voxel 16 + 4g + m)
 #pragma unroll
@@ -976,10 +1010,11 @@ __device__ __forceinline__ void rank4_plane_w(const float* stage, uint32_t* B, b
     return;
   }
   const float* src = stage + row * WPITCH + 4;
+  uint64_t nfa = 0;
   if (xs + 32 > W)
-    rank4_rowseg<true, true, true>(src, dw, de, r4);
+    rank4_rowseg<true, true, true>(src, dw, de, r4, nfa, W - xs);
   else
-    rank4_rowseg<false, true, true>(src, dw, de, r4);
+    rank4_rowseg<false, true, true>(src, dw, de, r4, nfa, 32);
 }
 
 // Deferred-fix variant for the per-warp kernel.  The row is ranked without
@@ -998,8 +1033,9 @@ struct R4Row {       // what rank4_rowseg_d leaves for the fix-up decision
   uint32_t fl, fr;   // x-edge fields, not yet fixed
   bool el_e, er_e;   // x-edge voxels in edge sub-cells
 };
-template <bool CHECK>
-__device__ __forceinline__ R4Row rank4_rowseg_d(const float* src, uint32_t* dw, uint32_t* de, const R4& r) {
+template <bool CHECK, bool NF>
+__device__ __forceinline__ R4Row rank4_rowseg_d(const float* src, uint32_t* dw, uint32_t* de, const R4& r,
+                                                uint64_t& nfa, int nvalid) {
   const float4* s4 = reinterpret_cast<const float4*>(src);
   const uint64_t fc2 = f2pack(r.fc, r.fc), mg2 = f2pack(r.magic, r.magic);
   const int q = ECC_R4_ROT ? (int)((threadIdx.x >> 2) & 1u) : 0;
@@ -1012,6 +1048,19 @@ __device__ __forceinline__ R4Row rank4_rowseg_d(const float* src, uint32_t* dw, 
     const int g = gi ^ q;   // chunk pair: voxels 4g..4g+3 and 16+4g..16+4g+3 (rotated: no LDS.128 bank conflicts)
     const float4 lo = s4[g], hi = s4[4 + g];
     const float a[4] = {lo.x, lo.y, lo.z, lo.w}, b[4] = {hi.x, hi.y, hi.z, hi.w};
+    if (!NF) {
+    } else if (!CHECK) {
+      nf_acc2(lo.x, lo.y, nfa);
+      nf_acc2(lo.z, lo.w, nfa);
+      nf_acc2(hi.x, hi.y, nfa);
+      nf_acc2(hi.z, hi.w, nfa);
+    } else {   // columns past the grid hold the TMA's NaN fill
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        if (4 * g + m < nvalid) nf_acc2(a[m], 0.f, nfa);
+        if (16 + 4 * g + m < nvalid) nf_acc2(b[m], 0.f, nfa);
+      }
+    }
     uint32_t w[4], eg[4];
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
@@ -1076,8 +1125,9 @@ __device__ __forceinline__ void r4_apply(const R4Fix& fx) {
   }
 }
 // rank4_plane_w with deferred fixes
+template <bool NF>
 __device__ __forceinline__ R4Fix rank4_plane_wd(const float* stage, uint32_t* B, bool plane_in, int xs, int y0,
-                                                int W, int H, const R4& r4) {
+                                                int W, int H, const R4& r4, uint64_t& nfa) {
   const int row = threadIdx.x & 31, seg = threadIdx.x >> 5;
   uint32_t* dw = B + row * BROW + 16 * seg;
   uint32_t* de = B + BEDGE + seg * 32 + row;
@@ -1091,9 +1141,9 @@ __device__ __forceinline__ R4Fix rank4_plane_wd(const float* stage, uint32_t* B,
     for (int k = 0; k < 4; ++k) d4[k] = make_uint4(s2, s2, s2, s2);
     *de = s2;
   } else if (xs + 32 > W) {
-    o = rank4_rowseg_d<true>(src, dw, de, r4);
+    o = rank4_rowseg_d<true, NF>(src, dw, de, r4, nfa, W - xs);
   } else {
-    o = rank4_rowseg_d<false>(src, dw, de, r4);
+    o = rank4_rowseg_d<false, NF>(src, dw, de, r4, nfa, 32);
   }
   const int cnt = __popc(o.emask) + (int)o.el_e + (int)o.er_e;
   R4Fix fx{0u, 0u, 0.f, 0.f};
@@ -1227,7 +1277,8 @@ __device__ __forceinline__ void rank_plane_u8(const unsigned char* stage, uint32
 // bin the staged plane into a bin plane: warp -> x segment, lane -> row
 template <int EK>
 __device__ __forceinline__ void bin_plane(const float* stage, uint32_t* B, bool plane_in, int x0, int y0, int W,
-                                          int H, uint32_t lut_m, float sc, float bi, float fcells, const R4& r4) {
+                                          int H, uint32_t lut_m, float sc, float bi, float fcells, const R4& r4,
+                                          uint64_t& nfa) {
   constexpr bool EDGE = EK != 0;
   const int row = threadIdx.x & 31, seg = threadIdx.x >> 5;
   uint32_t* dw = B + row * BROW + 16 * seg;
@@ -1244,9 +1295,9 @@ __device__ __forceinline__ void bin_plane(const float* stage, uint32_t* B, bool 
   const float* src = stage + row * PITCH + 4 + 32 * seg;
   if (EK == 2) {   // 2-D kernel: tE in shared memory, shared 140-float stage rows
     if (xs + 32 > W)
-      rank4_rowseg<true, false, false>(src, dw, de, r4);
+      rank4_rowseg<true, false, false>(src, dw, de, r4, nfa, W - xs);
     else
-      rank4_rowseg<false, false, false>(src, dw, de, r4);
+      rank4_rowseg<false, false, false>(src, dw, de, r4, nfa, 32);
   } else if (xs + 32 > W) {
     bin_rowseg<true, EDGE>(src, dw, de, lut_m, sc, bi, fcells);
   } else {
@@ -1297,6 +1348,7 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
   const uint32_t lut_m = smem_u32(s_t) - (EK == 2 ? 0u : EDGE ? 0x012C0000u : 0x2C000000u);
   const float fcells = EK == 2 ? (float)(1024 * cells) : EDGE ? (float)(256 * cells) : (float)cells;
   const R4 r4{lut_scale, lut_bias, fcells, g.r4_magic, g.r4_emask, smem_u32(s_t), nullptr, (uint32_t)g.one};
+  uint64_t nfa = 0;   // non-finite accumulator (nf_acc2)
   const int nranks = U8 ? 256 : EDGE ? cells + 2 : 2 * (cells + 1);
   const uint32_t dummy_off = (uint32_t)(nranks + lane);   // dummy counter index (< 2^15)
   const uint32_t one = (uint32_t)g.one;
@@ -1455,7 +1507,7 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
       if (U8)
         rank_plane_u8(reinterpret_cast<const unsigned char*>(stage), bbuf + (p & 1) * BPLANE, pin, x0, y0, g.W, g.H);
       else
-        bin_plane<EK>(stage, bbuf + (p & 1) * BPLANE, pin, x0, y0, g.W, g.H, lut_m, lut_scale, lut_bias, fcells, r4);
+        bin_plane<EK>(stage, bbuf + (p & 1) * BPLANE, pin, x0, y0, g.W, g.H, lut_m, lut_scale, lut_bias, fcells, r4, nfa);
       if (WS) {
         if (pin) round_done(p);
         else __syncwarp();
@@ -1532,7 +1584,7 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
           rank_plane_u8(reinterpret_cast<const unsigned char*>(stage), bbuf + (p & 1) * BPLANE, pin, x0, y0, g.W,
                         g.H);
         else
-          bin_plane<EK>(stage, bbuf + (p & 1) * BPLANE, pin, x0, y0, g.W, g.H, lut_m, lut_scale, lut_bias, fcells, r4);
+          bin_plane<EK>(stage, bbuf + (p & 1) * BPLANE, pin, x0, y0, g.W, g.H, lut_m, lut_scale, lut_bias, fcells, r4, nfa);
         if (WS) {
           if (pin) round_done(p);
           else __syncwarp();
@@ -1656,9 +1708,10 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
   }
   __syncthreads();
   if (cur_n >= 0) flush(cur_n);
+  if (g.nf && nf_any(nfa)) atomicOr(g.nf, 1);
 }
 
-template <int DEP>
+template <int DEP, bool NF>
 __global__ void __launch_bounds__(NT, ECC_F3_MINB)
 ecc_rank4_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* __restrict__ table_g, int nb,
                  int cells, int hsize, float lut_scale, float lut_bias, unsigned long long* __restrict__ hist) {
@@ -1694,6 +1747,7 @@ ecc_rank4_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* _
   // edge: (key256 + 1) >> 6)
   // edge4 ranks, boundary thresholds read from global memory (L1) by the rare edge voxels
   const R4 r4{lut_scale, lut_bias, (float)(1024 * cells), g.r4_magic, g.r4_emask, 0u, tE_g, (uint32_t)g.one};
+  uint64_t nfa = 0;   // non-finite accumulator (nf_acc2)
   const int nranks = U8 ? 256 : EDGE ? cells + 2 : 2 * (cells + 1);
   const uint32_t dummy_off = (uint32_t)(nranks + lane);   // dummy counter index (< 2^15)
   const uint32_t one = (uint32_t)g.one;
@@ -1829,7 +1883,7 @@ ecc_rank4_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* _
       }
     };
     auto rank = [&](int p, bool pin) {
-      const R4Fix fx = rank4_plane_wd(stage, bbuf + (p & 1) * BPLANE, pin, xs_w, y0, g.W, g.H, r4);
+      const R4Fix fx = rank4_plane_wd<NF>(stage, bbuf + (p & 1) * BPLANE, pin, xs_w, y0, g.W, g.H, r4, nfa);
       __syncwarp();
       return fx;
     };
@@ -2041,6 +2095,7 @@ ecc_rank4_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* _
   }
   __syncthreads();
   if (cur_n >= 0) flush(cur_n);
+  if (g.nf && nf_any(nfa)) atomicOr(g.nf, 1);
 }
 
 // ======================================================================
@@ -2088,6 +2143,7 @@ ecc_fast2d_rank_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const v
   const uint32_t lut_m = smem_u32(s_t) - (EK == 2 ? 0u : EDGE ? 0x012C0000u : 0x2C000000u);
   const float fcells = EK == 2 ? (float)(1024 * cells) : EDGE ? (float)(256 * cells) : (float)cells;
   const R4 r4{lut_scale, lut_bias, fcells, g.r4_magic, g.r4_emask, smem_u32(s_t), nullptr, (uint32_t)g.one};
+  uint64_t nfa = 0;   // non-finite accumulator (nf_acc2)
   const int nranks = U8 ? 256 : EDGE ? cells + 2 : 2 * (cells + 1);
   const uint32_t dummy_off = (uint32_t)(nranks + lane);
   const uint32_t one = (uint32_t)g.one;
@@ -2164,7 +2220,7 @@ ecc_fast2d_rank_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const v
     if (U8)
       rank_plane_u8(reinterpret_cast<const unsigned char*>(stage), B, true, x0, y0, g.W, g.H);
     else
-      bin_plane<EK>(stage, B, true, x0, y0, g.W, g.H, lut_m, lut_scale, lut_bias, fcells, r4);
+      bin_plane<EK>(stage, B, true, x0, y0, g.W, g.H, lut_m, lut_scale, lut_bias, fcells, r4, nfa);
     __syncwarp();
     if (lane == 0) {
       __threadfence_block();
@@ -2248,6 +2304,7 @@ ecc_fast2d_rank_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const v
   }
   __syncthreads();
   if (cur_n >= 0) flush(cur_n);
+  if (g.nf && nf_any(nfa)) atomicOr(g.nf, 1);
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -2286,33 +2343,103 @@ bool fast3d_eligible(const void* x, int64_t D, int64_t H, int64_t W, int64_t bat
 #ifndef ECC_F3_DYN
 #define ECC_F3_DYN 48   // largest dynamic work unit in planes (0: static partition only)
 #endif
-// Work-queue counters of the rank kernel: a ring of slots so launches on
-// different streams never share one; each launch zeroes its slot on its own
-// stream first.
+// Work-queue counters of the rank kernels: a ring of slots per device.  A
+// slot is reused only after the launch that last used it has finished: its
+// new user's stream first waits on the event recorded after that launch
+// (a stream-ordered wait, no host synchronisation), then zeroes the slot.
+// So concurrent launches on different streams never share a live counter,
+// however many are in flight.
 __device__ unsigned int g_f3_wq[64];
+namespace {
+struct WorkRing {
+  std::mutex mu;
+  unsigned int* base = nullptr;
+  cudaEvent_t ev[64] = {};
+  bool used[64] = {};
+  unsigned next = 0;
+};
+WorkRing g_rings[64];
+thread_local int t_slot_dev = -1, t_slot = -1;
+}  // namespace
 static unsigned int* work_slot(cudaStream_t stream) {
-  // the symbol has one instance per device: cache its address per device
-  constexpr int MAXDEV = 64;
-  static std::atomic<unsigned int*> base[MAXDEV];
-  static std::atomic<unsigned> seq{0};
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess || dev < 0 || dev >= MAXDEV) {
+  if (e != cudaSuccess || dev < 0 || dev >= 64) {
     set_cuda_error(e != cudaSuccess ? e : cudaErrorInvalidDevice, "cudaGetDevice(work queue)");
     return nullptr;
   }
-  unsigned int* b = base[dev].load();
-  if (!b) {
+  WorkRing& R = g_rings[dev];
+  std::lock_guard<std::mutex> lk(R.mu);
+  if (!R.base) {
     void* p = nullptr;
     e = cudaGetSymbolAddress(&p, g_f3_wq);
     if (e != cudaSuccess) { set_cuda_error(e, "cudaGetSymbolAddress(work queue)"); return nullptr; }
-    b = static_cast<unsigned int*>(p);
-    base[dev].store(b);
+    R.base = static_cast<unsigned int*>(p);
+    for (auto& ev : R.ev)
+      if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) {
+        set_cuda_error(e, "cudaEventCreate(work queue)");
+        return nullptr;
+      }
   }
-  unsigned int* slot = b + (seq.fetch_add(1) % 64);
+  const int k = (int)(R.next++ % 64);
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(stream, &cap);
+  if (R.used[k] && cap == cudaStreamCaptureStatusNone) {
+    e = cudaStreamWaitEvent(stream, R.ev[k], 0);   // the slot's previous launch has finished
+    if (e != cudaSuccess) { set_cuda_error(e, "cudaStreamWaitEvent(work queue)"); return nullptr; }
+  }
+  unsigned int* slot = R.base + k;
   e = cudaMemsetAsync(slot, 0, sizeof(unsigned int), stream);
   if (e != cudaSuccess) { set_cuda_error(e, "cudaMemsetAsync(work queue)"); return nullptr; }
+  t_slot_dev = dev;
+  t_slot = k;
   return slot;
+}
+// after the launch that uses the slot work_slot handed out on this thread
+static int work_slot_done(cudaStream_t stream) {
+  if (t_slot < 0) return ECC_OK;
+  WorkRing& R = g_rings[t_slot_dev];
+  std::lock_guard<std::mutex> lk(R.mu);
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(stream, &cap);
+  if (cap == cudaStreamCaptureStatusNone) {
+    const cudaError_t e = cudaEventRecord(R.ev[t_slot], stream);
+    if (e != cudaSuccess) return set_cuda_error(e, "cudaEventRecord(work queue)");
+    R.used[t_slot] = true;
+  }
+  t_slot = -1;
+  return ECC_OK;
+}
+
+// Function attribute and occupancy once per (kernel, smem bytes, device):
+// the launchers issue no other driver calls per launch.
+static int kernel_occupancy(const void* kfn, size_t smem, int* occ) {
+  // the attribute is raised to the largest dynamic smem any launch of the
+  // kernel asked for (a smaller later setting would fail the larger launch)
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, size_t, int>, int> cache;
+  static std::map<std::pair<const void*, int>, size_t> attr;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find({kfn, smem, dev});
+  if (it != cache.end()) {
+    *occ = it->second;
+    return ECC_OK;
+  }
+  size_t& cur = attr[{kfn, dev}];
+  if (smem > cur) {
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(fast path)");
+    cur = smem;
+  }
+  int o = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kfn, fast::NT, smem);
+  if (e != cudaSuccess) return set_cuda_error(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+  if (o < 1) return set_error(ECC_EINVAL, "fast-path kernel does not fit on an SM");
+  cache[{kfn, smem, dev}] = o;
+  *occ = o;
+  return ECC_OK;
 }
 
 // Dynamic schedule of the rank kernel: units of P/4 planes (P = planes per
@@ -2326,7 +2453,7 @@ static int set_dynamic(fast::Geom& g, int64_t total, int64_t grid, int64_t depth
   if (!ECC_F3_DYN) return 0;
   const int64_t P = total / grid;
   int z = P >= 96 ? (int)std::min<int64_t>(ECC_F3_DYN, std::max<int64_t>(24, (P / 4) & ~7)) : 0;
-  if (const char* zu = getenv("ECC_B200_F3_ZUNIT")) z = atoi(zu);   // A/B experiments
+  if (variant_zunit() > 0) z = variant_zunit();   // A/B experiments (ecc_set_variant)
   if (z <= 0 || z >= depth) return 0;
   if (!(g.wq = work_slot(stream))) return 1;
   g.zunit = z;
@@ -2342,13 +2469,10 @@ static void set_r4(fast::Geom& g, int sub) {
 
 static int launch_2d(const CUtensorMap& map, const void* kfn, size_t smem, int64_t W, int64_t H, int64_t batch,
                      const void* table, int nb, int cells, int hsize, float scale, float bias,
-                     unsigned long long* hist, cudaStream_t stream, int edge_sub = 0) {
+                     unsigned long long* hist, cudaStream_t stream, int edge_sub = 0, int* nf = nullptr) {
   using namespace fast;
-  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(fast2d)");
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, NT, smem);
-  if (occ < 1) return set_error(ECC_EINVAL, "fast2d kernel does not fit on an SM");
+  if (int rc = kernel_occupancy(kfn, smem, &occ)) return rc;
   Geom g;
   g.W = (int)W;
   g.H = (int)H;
@@ -2361,6 +2485,7 @@ static int launch_2d(const CUtensorMap& map, const void* kfn, size_t smem, int64
   g.zchunks = 0;
   g.one = 1;
   g.items = (int64_t)g.tiles_x * g.tiles_y * batch;
+  g.nf = nf;
   set_r4(g, edge_sub);
   const int64_t max_ctas = (int64_t)num_sms_fast() * occ;
   const int64_t grid = g.items < max_ctas ? g.items : max_ctas;
@@ -2372,7 +2497,9 @@ static int launch_2d(const CUtensorMap& map, const void* kfn, size_t smem, int64
 }
 
 int fast3d_launch(const float* x, int64_t D, int64_t H, int64_t W, int64_t batch, int64_t zb, int64_t ze,
-                  const void* table, const ecc_binning* b, unsigned long long* hist, cudaStream_t stream) {
+                  const void* table, const ecc_binning* b, unsigned long long* hist, cudaStream_t stream,
+                  int* nf, bool* nf_done) {
+  *nf_done = false;
   using namespace fast;
   CUtensorMap map;
   const cuuint64_t gdim[4] = {(cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)D, (cuuint64_t)batch};
@@ -2394,19 +2521,7 @@ int fast3d_launch(const float* x, int64_t D, int64_t H, int64_t W, int64_t batch
   // ECC_B200_F3=value selects the value-order kernel, =branch a branch
   // around each reduction, =cta the CTA-barrier pipeline, =no2d the 3-D kernel
   // for single planes (A/B checks)
-  const int mode = [] {   // read per launch so tests can switch kernels in-process
-    const char* e = getenv("ECC_B200_F3");
-    if (!e) return 0;
-    if (!strcmp(e, "value")) return 1;
-    if (!strcmp(e, "branch")) return 2;
-    if (!strcmp(e, "cta")) return 3;
-    if (!strcmp(e, "rank2")) return 4;
-    if (!strcmp(e, "no2d")) return 5;
-    if (!strcmp(e, "edge1")) return 6;     // the round-1 edge rank (inline threshold test per voxel)
-    if (!strcmp(e, "dummy")) return 8;     // rank4 with dummy counters for c = 0 even when not needed
-    if (!strcmp(e, "static")) return 9;    // rank4 with the static partition only
-    return 0;
-  }();
+  const int mode = variant_f3();   // A/B checks (ecc_set_variant); 0 = production kernels
   const bool use_bin = b->lut_ok && cells <= 16382 && mode != 1;
   const bool edge = b->lut_edge && mode != 4;
   // edge4 (rank fields = 4 * rank, 2^23 + 1024 cells + 1028 < 2^24) unless the round-1 rank is asked for
@@ -2434,7 +2549,7 @@ int fast3d_launch(const float* x, int64_t D, int64_t H, int64_t W, int64_t batch
                           : ek == 1 ? (const void*)ecc_fast2d_rank_kernel<1, false>
                                     : (const void*)ecc_fast2d_rank_kernel<0, false>,
                      smem, W, H, batch, table, nb, cells, hsize, b->lut_scale, b->lut_bias, hist, stream,
-                     b->lut_edge_sub);
+                     b->lut_edge_sub, (*nf_done = (ek == 2)) ? nf : nullptr);
   if (use_bin && ek == 2) {
     // the rank4 kernel: per-warp 40 x 32 TMA boxes, boundary thresholds in global memory
     CUtensorMap wmap;
@@ -2448,12 +2563,12 @@ int fast3d_launch(const float* x, int64_t D, int64_t H, int64_t W, int64_t batch
     const bool nodummy = (W % TXW) == 0 && mode != 8;
     const int hs = nodummy ? cells + 2 : cells + 2 + 32;
     const size_t smem4 = (size_t)NW * WSTAGE_BYTES + (size_t)2 * BPLANE * 4 + (size_t)(NW + 1) * 8 + (size_t)hs * 4;
-    const void* k4 = nodummy ? (const void*)ecc_rank4_kernel<2> : (const void*)ecc_rank4_kernel<1>;
-    cudaError_t e = cudaFuncSetAttribute(k4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem4);
-    if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(rank4)");
+    // the non-finite check (ecc_histogram_checked) is a kernel variant: ~0.5
+    // FMA-pipe instructions per voxel, paid only when asked for
+    const void* k4 = nodummy ? (nf ? (const void*)ecc_rank4_kernel<2, true> : (const void*)ecc_rank4_kernel<2, false>)
+                             : (nf ? (const void*)ecc_rank4_kernel<1, true> : (const void*)ecc_rank4_kernel<1, false>);
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k4, NT, smem4);
-    if (occ < 1) return set_error(ECC_EINVAL, "rank4 kernel does not fit on an SM");
+    if (int rc = kernel_occupancy(k4, smem4, &occ)) return rc;
     Geom g;
     g.W = (int)W;
     g.H = (int)H;
@@ -2466,6 +2581,8 @@ int fast3d_launch(const float* x, int64_t D, int64_t H, int64_t W, int64_t batch
     g.zc = 0;
     g.one = 1;
     g.items = tiles;
+    g.nf = nf;
+    *nf_done = true;
     set_r4(g, b->lut_edge_sub);
     const int64_t total = tiles * (ze - zb);
     const int64_t max_ctas = (int64_t)num_sms_fast() * occ;
@@ -2476,13 +2593,11 @@ int fast3d_launch(const float* x, int64_t D, int64_t H, int64_t W, int64_t batch
     using KFn = void (*)(const CUtensorMap, Geom, const void*, int, int, int, float, float, unsigned long long*);
     KFn kk = reinterpret_cast<KFn>(const_cast<void*>(k4));
     kk<<<(unsigned)grid, NT, smem4, stream>>>(wmap, g, table, nb, cells, hs, b->lut_scale, b->lut_bias, hist);
-    return check_launch("ecc_rank4_kernel");
+    if (int rc = check_launch("ecc_rank4_kernel")) return rc;
+    return work_slot_done(stream);
   }
-  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(fast3d)");
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, NT, smem);
-  if (occ < 1) return set_error(ECC_EINVAL, "fast3d kernel does not fit on an SM");
+  if (int rc = kernel_occupancy(kfn, smem, &occ)) return rc;
   const int64_t max_ctas = (int64_t)num_sms_fast() * occ;
 
   Geom g;
@@ -2509,7 +2624,8 @@ int fast3d_launch(const float* x, int64_t D, int64_t H, int64_t W, int64_t batch
     using KFn = void (*)(const CUtensorMap, Geom, const void*, int, int, int, float, float, unsigned long long*);
     KFn k = reinterpret_cast<KFn>(const_cast<void*>(kfn));
     k<<<(unsigned)grid, NT, smem, stream>>>(map, g, table, nb, cells, hsize, b->lut_scale, b->lut_bias, hist);
-    return check_launch("ecc_fast3d_bin_kernel");
+    if (int rc = check_launch("ecc_fast3d_bin_kernel")) return rc;
+    return work_slot_done(stream);
   }
   ecc_fast3d_kernel<<<(unsigned)grid, NT, smem, stream>>>(map, g, table, nb, cells, cell_shift, b->lut_scale,
                                                             b->lut_bias, b->lut_ok, hist);
@@ -2539,20 +2655,16 @@ int fast3d_u8_launch(const uint8_t* x, int64_t D, int64_t H, int64_t W, int64_t 
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(ECC_ECUDA, "cuTensorMapEncodeTiled(u8) failed");
   const int nb = (int)b->nbins;
-  const char* env = getenv("ECC_B200_F3");
-  const bool cta = env && !strcmp(env, "cta");
+  const bool cta = variant_f3() == F3_CTA;
   const int hsize = 256 + 32;
   const size_t smem = (size_t)U8_PLANE_BYTES + (size_t)2 * BPLANE * 4 + 16 + 4 * 4 + (size_t)hsize * 4;
   const void* kfn = cta ? (const void*)ecc_fast3d_bin_kernel<1, false, 0, true>
                         : (const void*)ecc_fast3d_bin_kernel<1, true, 0, true>;
-  if (D == 1 && !cta && !(env && !strcmp(env, "no2d")))
+  if (D == 1 && !cta && variant_f3() != F3_NO2D)
     return launch_2d(map, (const void*)ecc_fast2d_rank_kernel<0, true>, smem, W, H, batch, table, nb, 0, hsize,
                      0.f, 0.f, hist, stream);
-  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(fast3d u8)");
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, NT, smem);
-  if (occ < 1) return set_error(ECC_EINVAL, "fast3d u8 kernel does not fit on an SM");
+  if (int rc = kernel_occupancy(kfn, smem, &occ)) return rc;
   const int64_t max_ctas = (int64_t)num_sms_fast() * occ;
   Geom g;
   g.W = (int)W;
@@ -2574,7 +2686,8 @@ int fast3d_u8_launch(const uint8_t* x, int64_t D, int64_t H, int64_t W, int64_t 
   using KFn = void (*)(const CUtensorMap, Geom, const void*, int, int, int, float, float, unsigned long long*);
   KFn k = reinterpret_cast<KFn>(const_cast<void*>(kfn));
   k<<<(unsigned)grid, NT, smem, stream>>>(map, g, table, nb, 0, hsize, 0.f, 0.f, hist);
-  return check_launch("ecc_fast3d_bin_kernel<u8>");
+  if (int rc = check_launch("ecc_fast3d_bin_kernel<u8>")) return rc;
+  return work_slot_done(stream);
 }
 
 }  // namespace ecc

@@ -5,6 +5,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <limits>
 #include <vector>
@@ -24,6 +25,12 @@ int set_cuda_error(cudaError_t e, const char* what) {
   return ECC_ECUDA;
 }
 void clear_error() { g_err[0] = 0; }
+
+static std::atomic<int> g_f3{0}, g_zunit{0}, g_generic{0}, g_soft_fwd_t{16}, g_soft_bwd_t{16};
+int variant_f3() { return g_f3.load(std::memory_order_relaxed); }
+int variant_zunit() { return g_zunit.load(std::memory_order_relaxed); }
+bool variant_generic() { return g_generic.load(std::memory_order_relaxed) != 0; }
+int variant_soft_t(bool bwd) { return (bwd ? g_soft_bwd_t : g_soft_fwd_t).load(std::memory_order_relaxed); }
 
 // largest float32 <= t (round toward -inf), the t32 of DESIGN.md
 static float round_down_f32(double t) {
@@ -260,6 +267,29 @@ using namespace ecc;
 
 extern "C" const char* ecc_version(void) { return "ecc_b200 0.1.0 (sm_100a)"; }
 extern "C" const char* ecc_last_error(void) { return g_err; }
+
+extern "C" int ecc_set_variant(const char* key, const char* value) {
+  clear_error();
+  if (!key || !value) return set_error(ECC_EINVAL, "null pointer argument");
+  if (!strcmp(key, "f3")) {
+    static const struct { const char* n; int m; } names[] = {
+        {"", F3_DEFAULT}, {"default", F3_DEFAULT}, {"value", F3_VALUE}, {"branch", F3_BRANCH}, {"cta", F3_CTA},
+        {"rank2", F3_RANK2}, {"no2d", F3_NO2D}, {"edge1", F3_EDGE1}, {"dummy", F3_DUMMY}, {"static", F3_STATIC}};
+    for (const auto& e : names)
+      if (!strcmp(value, e.n)) {
+        g_f3.store(e.m);
+        return ECC_OK;
+      }
+    return set_error(ECC_EINVAL, "unknown f3 variant");
+  }
+  const int v = atoi(value);
+  if (!strcmp(key, "zunit")) g_zunit.store(v > 0 ? v : 0);
+  else if (!strcmp(key, "generic")) g_generic.store(v != 0);
+  else if (!strcmp(key, "soft_fwd_t")) g_soft_fwd_t.store(v);
+  else if (!strcmp(key, "soft_bwd_t")) g_soft_bwd_t.store(v);
+  else return set_error(ECC_EINVAL, "unknown variant key");
+  return ECC_OK;
+}
 
 extern "C" double ecc_key_to_double(uint64_t k) {
   uint64_t b = (k & 0x8000000000000000ull) ? (k & 0x7fffffffffffffffull) : ~k;

@@ -14,10 +14,22 @@ inline int check_launch(const char* what) {
 }
 // float32 fast path (ecc_fast3d.cu)
 bool fast3d_eligible(const void* x, int64_t D, int64_t H, int64_t W, int64_t batch, int64_t nb);
+// nf: optional device flag set to 1 when a non-finite value is read; *nf_done
+// tells whether the kernel chosen checked (else the caller runs a check pass)
 int fast3d_launch(const float* x, int64_t D, int64_t H, int64_t W, int64_t batch, int64_t zb, int64_t ze,
-                  const void* table, const ecc_binning* b, unsigned long long* hist, cudaStream_t stream);
+                  const void* table, const ecc_binning* b, unsigned long long* hist, cudaStream_t stream,
+                  int* nf, bool* nf_done);
 // uint8 fast path (ecc_fast3d.cu): the value is the rank
 bool fast3d_u8_eligible(const void* x, int64_t D, int64_t H, int64_t W, int64_t batch, int64_t nb);
 int fast3d_u8_launch(const uint8_t* x, int64_t D, int64_t H, int64_t W, int64_t batch, int64_t zb, int64_t ze,
                      const void* table, const ecc_binning* b, unsigned long long* hist, cudaStream_t stream);
+// Kernel-variant switches for A/B checks (tests, tools/).  Set through the C
+// ABI (ecc_set_variant); read as relaxed atomics by the launchers -- no
+// getenv on the launch path.  Defaults select the production kernels.
+enum F3Mode { F3_DEFAULT = 0, F3_VALUE = 1, F3_BRANCH = 2, F3_CTA = 3, F3_RANK2 = 4, F3_NO2D = 5, F3_EDGE1 = 6,
+              F3_DUMMY = 8, F3_STATIC = 9 };
+int variant_f3();          // F3Mode
+int variant_zunit();       // forced dynamic unit (planes), 0: automatic
+bool variant_generic();    // route everything through the generic sweep
+int variant_soft_t(bool bwd);   // thresholds per lane of the soft kernels (8 / 16 / 32)
 }  // namespace ecc

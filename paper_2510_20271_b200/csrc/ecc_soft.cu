@@ -24,6 +24,9 @@
 
 #include "ecc_common.cuh"
 #include "ecc_internal.h"
+#include <mutex>
+#include <map>
+#include <tuple>
 
 namespace ecc {
 
@@ -51,6 +54,7 @@ struct SoftArgs {
   double* part;           // [N][chunks][B]
   double* gpart;          // [N][chunks][4]   (backward)
   float* dX;              // [N][n]   (backward)
+  const ecc_soft_params* pd;   // parameters resident on the device (sync-free path), else nullptr
 };
 
 __device__ __forceinline__ float ex2_approx(float x) {
@@ -307,6 +311,12 @@ __device__ __forceinline__ void pair_loop_direct(const double* __restrict__ kt, 
 template <bool BWD, bool FACT, int T>
 __global__ void __launch_bounds__(SNT, (T == 8 ? 4 : (T == 16 ? 3 : 2)))
 ecc_soft_kernel(SoftArgs a) {
+  if (a.pd) {   // device-resident parameters: both modes are launched, the other one exits here
+    if ((a.pd->factorized != 0) != FACT) return;
+    a.lam = a.pd->lam;
+    a.m = a.pd->center;
+    a.kscale = (float)(a.lam * LOG2E);
+  }
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ChunkSmem& S = *reinterpret_cast<ChunkSmem*>(smem_raw);
   unsigned char* tail = smem_raw + CHUNK_BYTES;
@@ -611,7 +621,8 @@ __global__ void ecc_soft_reduce1(const double* __restrict__ part, int64_t chunks
 }
 
 __global__ void ecc_soft_reduce2(const double* __restrict__ gpart, int groups, int nb, const double* __restrict__ up,
-                                 double lam, double* __restrict__ out) {
+                                 double lam, const ecc_soft_params* __restrict__ pd, double* __restrict__ out) {
+  if (pd) lam = pd->lam;
   const int64_t item = blockIdx.y;
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= nb) return;
@@ -669,10 +680,26 @@ extern "C" size_t ecc_soft_workspace_bytes(int ndim, const int64_t* dims, int64_
   return sizeof(double) * ((size_t)(batch * chunks) * (size_t)(nbins + 4) + (size_t)batch * RGROUPS * (size_t)nbins);
 }
 
+// cudaFuncSetAttribute once per (kernel, smem size, device): the launchers
+// stay free of per-call driver work besides the launches themselves
+static bool soft_attr_done(const void* kfn, size_t smem) {
+  // true when the kernel's attribute already covers smem; else the caller raises it
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> attr;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& cur = attr[{kfn, dev}];
+  if (smem <= cur) return true;
+  cur = smem;
+  return false;
+}
+
 template <bool BWD>
 static int soft_launch(const int8_t* coeffs, const float* fc, const float* fclo, int ndim, const int64_t* dims, int64_t batch,
                        const double* taus, int64_t nbins, const ecc_soft_params* p, const double* up, float* dX,
-                       double* out_main, double* G, void* workspace, void* stream) {
+                       double* out_main, double* G, void* workspace, void* stream,
+                       const ecc_soft_params* pd = nullptr) {
   clear_error();
   int64_t d3[3];
   int rc = soft_dims(ndim, dims, d3);
@@ -681,8 +708,9 @@ static int soft_launch(const int8_t* coeffs, const float* fc, const float* fclo,
   if (BWD && (!up || !dX || !G)) return set_error(ECC_EINVAL, "null pointer argument");
   if (batch < 1 || nbins < 1) return set_error(ECC_EINVAL, "empty soft problem");
   if (nbins > MAXB_PASS) return set_error(ECC_EINVAL, "soft path supports at most 1024 thresholds per call");
-  if (!(p->lam > 0)) return set_error(ECC_EINVAL, "sharpness must be positive");
-  if (!p->factorized && !fclo) return set_error(ECC_EINVAL, "direct mode needs the float32 field remainder");
+  if (!pd && !(p->lam > 0)) return set_error(ECC_EINVAL, "sharpness must be positive");
+  if ((pd || !p->factorized) && !fclo)
+    return set_error(ECC_EINVAL, "direct mode needs the float32 field remainder");
   const int64_t n = d3[0] * d3[1] * d3[2];
   const int64_t chunks = (n + CH - 1) / CH;
   SoftArgs a;
@@ -705,26 +733,33 @@ static int soft_launch(const int8_t* coeffs, const float* fc, const float* fclo,
   a.part = (double*)workspace;
   a.gpart = a.part + (size_t)(batch * chunks) * (size_t)nbins;
   a.dX = dX;
+  a.pd = pd;
   cudaStream_t s = (cudaStream_t)stream;
   // 16 thresholds per lane (~80 registers, 3 CTAs/SM): on 16 x 1024^2,
   // B = 256 the forward takes 522 vs 559 us and the backward 837 vs 868 us
   // compared with 32 per lane; ECC_SOFT_FWD_T / ECC_SOFT_BWD_T = 32 override
-  const char* tenv = getenv(BWD ? "ECC_SOFT_BWD_T" : "ECC_SOFT_FWD_T");
-  const int tsel = tenv ? atoi(tenv) : 16;
+  const int tsel = variant_soft_t(BWD);
   const int T = (tsel == 8 && nbins <= 8 * 32) ? 8 : (tsel <= 16 && nbins <= 16 * 32) ? 16 : 32;
-  const bool fact = p->factorized != 0;
-  auto kfn = fact ? (T == 8 ? ecc_soft_kernel<BWD, true, 8> : T == 16 ? ecc_soft_kernel<BWD, true, 16>
-                                                                        : ecc_soft_kernel<BWD, true, 32>)
-                  : (T == 8 ? ecc_soft_kernel<BWD, false, 8> : T == 16 ? ecc_soft_kernel<BWD, false, 16>
-                                                                         : ecc_soft_kernel<BWD, false, 32>);
-  const size_t smem = soft_smem(fact, T);
-  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(soft)");
   const int64_t grid = batch * chunks;
   if (grid > 0x7fffffff) return set_error(ECC_EINVAL, "soft problem too large");
-  kfn<<<(unsigned)grid, SNT, smem, s>>>(a);
-  rc = check_launch(BWD ? "ecc_soft_kernel<bwd>" : "ecc_soft_kernel<fwd>");
-  if (rc) return rc;
+  // host parameters: the one mode they select; device parameters: both modes,
+  // the kernel whose mode the device flag does not select exits at once
+  for (int mode = 0; mode < 2; ++mode) {
+    const bool fact = mode == 0;
+    if (!pd && fact != (p->factorized != 0)) continue;
+    auto kfn = fact ? (T == 8 ? ecc_soft_kernel<BWD, true, 8> : T == 16 ? ecc_soft_kernel<BWD, true, 16>
+                                                                          : ecc_soft_kernel<BWD, true, 32>)
+                    : (T == 8 ? ecc_soft_kernel<BWD, false, 8> : T == 16 ? ecc_soft_kernel<BWD, false, 16>
+                                                                           : ecc_soft_kernel<BWD, false, 32>);
+    const size_t smem = soft_smem(fact, T);
+    if (!soft_attr_done(reinterpret_cast<const void*>(kfn), smem)) {
+      cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(soft)");
+    }
+    kfn<<<(unsigned)grid, SNT, smem, s>>>(a);
+    rc = check_launch(BWD ? "ecc_soft_kernel<bwd>" : "ecc_soft_kernel<fwd>");
+    if (rc) return rc;
+  }
   const int groups = (int)(chunks < RGROUPS ? chunks : RGROUPS);
   const int64_t per_group = (chunks + groups - 1) / groups;
   double* grp = a.gpart + (size_t)(batch * chunks) * 4;
@@ -733,7 +768,7 @@ static int soft_launch(const int8_t* coeffs, const float* fc, const float* fclo,
   rc = check_launch("ecc_soft_reduce1");
   if (rc) return rc;
   dim3 g2((unsigned)((nbins + 127) / 128), (unsigned)batch);
-  ecc_soft_reduce2<<<g2, 128, 0, s>>>(grp, groups, (int)nbins, BWD ? up : nullptr, p->lam, out_main);
+  ecc_soft_reduce2<<<g2, 128, 0, s>>>(grp, groups, (int)nbins, BWD ? up : nullptr, pd ? 0.0 : p->lam, pd, out_main);
   rc = check_launch("ecc_soft_reduce2");
   if (rc) return rc;
   if (BWD) {
@@ -758,4 +793,81 @@ extern "C" int ecc_soft_backward(const int8_t* coeffs, const float* field_c, con
                                  void* stream) {
   return soft_launch<true>(coeffs, field_c, field_lo, ndim, dims, batch, taus, nbins, p, upstream, d_values, d_tau, G,
                            workspace, stream);
+}
+
+// ---------------------------------------------------------------------------
+// Device-resident soft parameters (the sync-free module path): one CTA
+// derives what the host used to compute from tau / u / alpha
+// (soft.py _params): the centre (tau_min + tau_max) / 2, the largest
+// half-width of the 32-threshold blocks, the factorised-mode flag
+// lam log2(e) halfwidth <= A_MAX, and copies lam, alpha, u.
+// ---------------------------------------------------------------------------
+namespace ecc {
+__global__ void ecc_soft_setup_kernel(const double* __restrict__ taus, int nb, const double* __restrict__ u, int ndim,
+                                      const double* __restrict__ alpha, double lam, ecc_soft_params* __restrict__ out) {
+  __shared__ double smn[256], smx[256], shw[256];
+  double mn = INFINITY, mx = -INFINITY, hw = 0.0;
+  for (int b = threadIdx.x; b * TT < nb; b += blockDim.x) {   // block b: thresholds [32 b, 32 b + 32)
+    double bmn = INFINITY, bmx = -INFINITY;
+    for (int j = b * TT; j < min(nb, (b + 1) * TT); ++j) {
+      bmn = fmin(bmn, taus[j]);
+      bmx = fmax(bmx, taus[j]);
+    }
+    mn = fmin(mn, bmn);
+    mx = fmax(mx, bmx);
+    hw = fmax(hw, 0.5 * (bmx - bmn));
+  }
+  smn[threadIdx.x] = mn;
+  smx[threadIdx.x] = mx;
+  shw[threadIdx.x] = hw;
+  __syncthreads();
+  for (int o = blockDim.x >> 1; o; o >>= 1) {
+    if (threadIdx.x < o) {
+      smn[threadIdx.x] = fmin(smn[threadIdx.x], smn[threadIdx.x + o]);
+      smx[threadIdx.x] = fmax(smx[threadIdx.x], smx[threadIdx.x + o]);
+      shw[threadIdx.x] = fmax(shw[threadIdx.x], shw[threadIdx.x + o]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    ecc_soft_params p;
+    p.lam = lam;
+    p.alpha = *alpha;
+    for (int i = 0; i < 3; ++i) p.u[i] = i < ndim ? u[i] : 0.0;
+    p.center = 0.5 * (smn[0] + smx[0]);
+    p.factorized = lam * LOG2E * shw[0] <= (double)A_MAX ? 1 : 0;
+    p.pad = 0;
+    *out = p;
+  }
+}
+}  // namespace ecc
+
+extern "C" int ecc_soft_setup(const double* taus, int64_t nbins, const double* u, int ndim, const double* alpha,
+                              double lam, ecc_soft_params* params_dev, void* stream) {
+  clear_error();
+  if (!taus || !u || !alpha || !params_dev) return set_error(ECC_EINVAL, "null pointer argument");
+  if (nbins < 1 || nbins > MAXB_PASS) return set_error(ECC_EINVAL, "soft path takes 1 to 1024 thresholds");
+  if (ndim != 2 && ndim != 3) return set_error(ECC_EINVAL, "grid must be 2D or 3D");
+  if (!(lam > 0)) return set_error(ECC_EINVAL, "sharpness must be positive");
+  ecc_soft_setup_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(taus, (int)nbins, u, ndim, alpha, lam, params_dev);
+  return check_launch("ecc_soft_setup_kernel");
+}
+
+extern "C" int ecc_soft_forward_d(const int8_t* coeffs, const float* field_c, const float* field_lo, int ndim,
+                                  const int64_t* dims, int64_t batch, const double* taus, int64_t nbins,
+                                  const ecc_soft_params* params_dev, double* chi, void* workspace, void* stream) {
+  if (!params_dev) return set_error(ECC_EINVAL, "null pointer argument");
+  const ecc_soft_params placeholder{1.0, 0.0, {0.0, 0.0, 0.0}, 0.0, 1, 0};
+  return soft_launch<false>(coeffs, field_c, field_lo, ndim, dims, batch, taus, nbins, &placeholder, nullptr, nullptr,
+                            chi, nullptr, workspace, stream, params_dev);
+}
+
+extern "C" int ecc_soft_backward_d(const int8_t* coeffs, const float* field_c, const float* field_lo, int ndim,
+                                   const int64_t* dims, int64_t batch, const double* taus, int64_t nbins,
+                                   const ecc_soft_params* params_dev, const double* upstream, float* d_values,
+                                   double* d_tau, double* G, void* workspace, void* stream) {
+  if (!params_dev) return set_error(ECC_EINVAL, "null pointer argument");
+  const ecc_soft_params placeholder{1.0, 0.0, {0.0, 0.0, 0.0}, 0.0, 1, 0};
+  return soft_launch<true>(coeffs, field_c, field_lo, ndim, dims, batch, taus, nbins, &placeholder, upstream, d_values,
+                           d_tau, G, workspace, stream, params_dev);
 }

@@ -12,6 +12,7 @@ shape [N?, (D,) H, W] in, int64 curves [N?, B] out, no host round trip.
 
 from __future__ import annotations
 
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -116,23 +117,46 @@ def _split_batch(x: torch.Tensor, ndim: int | None):
     raise ValueError(f"expected a {ndim}-D grid or a batch of them, got shape {tuple(x.shape)}")
 
 
-def histogram_device(x: torch.Tensor, taus: ThresholdSet, ndim: int | None = None) -> torch.Tensor:
-    """int64 [N, B+1] coefficient histograms (last column = overflow) of CUDA
-    grids x [N?, (D,) H, W] (uint8 / float32 / float64)."""
-    if not x.is_cuda:
-        raise ValueError("histogram_device takes a CUDA tensor")
-    x = x.contiguous()
+def _binning_bytes(b) -> torch.Tensor:
+    return torch.frombuffer(bytearray(bytes(b)), dtype=torch.uint8)
+
+
+def _binning_from(t: torch.Tensor):
+    return _lib.Binning.from_buffer_copy(t.numpy().tobytes())
+
+
+# The fused sweep and the scan as torch.library custom ops (fake
+# implementations give torch.compile the output shapes, no graph break).  The
+# threshold table is built on the host (ThresholdSet.device_table) and passed
+# in: a device table tensor plus the ecc_binning struct as a CPU byte tensor.
+@torch.library.custom_op("ecc_b200::histogram", mutates_args=())
+def _histogram_op(x: torch.Tensor, table: torch.Tensor, binning: torch.Tensor, ndim: int, nbins: int,
+                  check_finite: bool) -> tuple[torch.Tensor, torch.Tensor]:
+    """(int64 [N, B+1] histograms, int32 [1] non-finite flag) of x [N?, (D,) H, W]."""
     batch, dims, _ = _split_batch(x, ndim)
-    code = _lib.dtype_code(x)
-    table, binning = taus.device_table(code, x.device)
-    hist = torch.empty((batch, len(taus) + 1), dtype=torch.int64, device=x.device)
+    hist = torch.empty((batch, nbins + 1), dtype=torch.int64, device=x.device)
+    flag = torch.zeros(1, dtype=torch.int32, device=x.device)
     d = _lib.dims_arg(dims)
-    _lib.check(_lib.lib().ecc_histogram(_lib.ptr(x), code, len(dims), _lib.ptr(d), batch, _lib.ptr(table),
-                                        _lib.ctypes.byref(binning), _lib.ptr(hist), _lib.stream_ptr(x)))
-    return hist
+    b = _binning_from(binning)
+    L = _lib.lib()
+    if check_finite:
+        _lib.check(L.ecc_histogram_checked(_lib.ptr(x), _lib.dtype_code(x), len(dims), _lib.ptr(d), batch, 0,
+                                           dims[0] if len(dims) == 3 else 1, _lib.ptr(table), _lib.ctypes.byref(b),
+                                           _lib.ptr(hist), _lib.ptr(flag), _lib.stream_ptr(x)))
+    else:
+        _lib.check(L.ecc_histogram(_lib.ptr(x), _lib.dtype_code(x), len(dims), _lib.ptr(d), batch, _lib.ptr(table),
+                                   _lib.ctypes.byref(b), _lib.ptr(hist), _lib.stream_ptr(x)))
+    return hist, flag
 
 
-def scan_device(hist: torch.Tensor, nbins: int) -> torch.Tensor:
+@_histogram_op.register_fake
+def _(x, table, binning, ndim, nbins, check_finite):
+    batch, _, _ = _split_batch(x, ndim)
+    return x.new_empty((batch, nbins + 1), dtype=torch.int64), x.new_empty((1,), dtype=torch.int32)
+
+
+@torch.library.custom_op("ecc_b200::scan", mutates_args=())
+def _scan_op(hist: torch.Tensor, nbins: int) -> torch.Tensor:
     """Inclusive prefix over the first nbins columns -> int64 [N, B] curves."""
     batch = hist.shape[0]
     curve = torch.empty((batch, nbins), dtype=torch.int64, device=hist.device)
@@ -140,29 +164,95 @@ def scan_device(hist: torch.Tensor, nbins: int) -> torch.Tensor:
     return curve
 
 
-def ecc_discrete(x: torch.Tensor, taus, ndim: int | None = None, return_hist: bool = False):
+@_scan_op.register_fake
+def _(hist, nbins):
+    return hist.new_empty((hist.shape[0], nbins), dtype=torch.int64)
+
+
+def _hist(x: torch.Tensor, taus: ThresholdSet, ndim: int | None, check_finite: bool):
+    if not x.is_cuda:
+        raise ValueError("histogram_device takes a CUDA tensor")
+    x = x.contiguous()
+    _split_batch(x, ndim)   # validates the shape
+    table, binning = taus.device_table(_lib.dtype_code(x), x.device)
+    nd = ndim if ndim is not None else x.ndim
+    return torch.ops.ecc_b200.histogram(x, table, _binning_bytes(binning), nd, len(taus), check_finite)
+
+
+def _raise_nonfinite(flag: torch.Tensor) -> None:
+    if int(flag.item()):
+        raise ValueError("grid values must be finite (the device found NaN or Inf)")
+
+
+def histogram_device(x: torch.Tensor, taus: ThresholdSet, ndim: int | None = None,
+                     check_finite: bool = False) -> torch.Tensor:
+    """int64 [N, B+1] coefficient histograms (last column = overflow) of CUDA
+    grids x [N?, (D,) H, W] (uint8 / float32 / float64).  check_finite:
+    raise ValueError for NaN / Inf values like ScalarGrid (grid.py:63-64);
+    the float32 kernels test while they sweep, the raise reads a flag back."""
+    hist, flag = _hist(x, taus, ndim, check_finite)
+    if check_finite:
+        _raise_nonfinite(flag)
+    return hist
+
+
+def scan_device(hist: torch.Tensor, nbins: int) -> torch.Tensor:
+    """Inclusive prefix over the first nbins columns -> int64 [N, B] curves."""
+    return torch.ops.ecc_b200.scan(hist, nbins)
+
+
+def ecc_discrete(x: torch.Tensor, taus, ndim: int | None = None, return_hist: bool = False,
+                 check_finite: bool = True):
     """Torch-native batched exact ECC.
 
     x: CUDA tensor [N?, (D,) H, W] of uint8 / float32 / float64 (float32
     values are compared exactly as the reference's float64 would be).
     taus: ThresholdSet or 1-D array of strictly increasing thresholds.
     Returns int64 curves [N?, B] on the device (and the [N?, B+1] histogram).
-    Non-finite inputs are the caller's responsibility on this path (validate
-    with ScalarGrid or device_minmax).
+    NaN / Inf values raise ValueError like ScalarGrid (grid.py:63-64); the
+    check runs inside the fused sweep, and reading its flag is one small
+    device -> host copy (check_finite=False skips it: fully asynchronous).
     """
     ts = taus if isinstance(taus, ThresholdSet) else ThresholdSet(taus)
     _, _, batched = _split_batch(x, ndim)
-    hist = histogram_device(x, ts, ndim)
+    hist, flag = _hist(x, ts, ndim, check_finite)
     curve = scan_device(hist, len(ts))
+    if check_finite:
+        _raise_nonfinite(flag)
     if not batched:
         curve, hist = curve[0], hist[0]
     return (curve, hist) if return_hist else curve
 
 
 class _StreamState:
-    """Device buffers of ecc_discrete_host, cached per (shape, chunk, device)."""
+    """Device buffers of ecc_discrete_host, one cached configuration per
+    (calling thread, device stream): concurrent calls from different threads
+    or on different streams never share a buffer, and calls on one stream are
+    ordered by the stream (plus the event recorded after each call's last
+    kernel, waited on before the next call's first copy)."""
 
-    cache: dict = {}
+    _local = threading.local()
+
+    @classmethod
+    def table(cls) -> dict:
+        t = getattr(cls._local, "cache", None)
+        if t is None:
+            t = cls._local.cache = {}
+        return t
+
+    @classmethod
+    def get(cls, stream, key):
+        st = cls.table().get(stream.cuda_stream)
+        return st if st is not None and st.get("key") == key else None
+
+    @classmethod
+    def put(cls, stream, st):
+        cls.table()[stream.cuda_stream] = st   # one configuration per stream: the previous one is freed
+
+
+def release_host_buffers() -> None:
+    """Free the device buffers ecc_discrete_host keeps for this thread's streams."""
+    _StreamState.table().clear()
 
 
 RESIDENT_MAX_BYTES = 8 << 30   # ecc_discrete_host(resident=None): volumes up to this size stay in HBM
@@ -215,20 +305,22 @@ def ecc_discrete_host(x_host: torch.Tensor, taus, chunk_planes: int = 64, device
         except torch.cuda.OutOfMemoryError:
             if not auto:
                 raise
-            _StreamState.cache = {}   # no room for the whole volume: stream through the ring
+            release_host_buffers()   # no room for the whole volume: stream through the ring
             torch.cuda.empty_cache()
-    key = (x_host.dtype, cp, H, W, nb, str(dev))
-    st = _StreamState.cache.get(key)
-    if st is None:
-        st = {"bufs": [torch.empty((cp + 2, H, W), dtype=x_host.dtype, device=dev) for _ in range(2)],
-              "part": [torch.empty(nb + 1, dtype=torch.int64, device=dev) for _ in range(2)],
-              "copy": torch.cuda.Stream(dev)}
-        _StreamState.cache = {key: st}   # one cached configuration
     main = torch.cuda.current_stream(dev)
+    key = (x_host.dtype, cp, H, W, nb, str(dev))
+    st = _StreamState.get(main, key)
+    if st is None:
+        st = {"key": key, "bufs": [torch.empty((cp + 2, H, W), dtype=x_host.dtype, device=dev) for _ in range(2)],
+              "part": [torch.empty(nb + 1, dtype=torch.int64, device=dev) for _ in range(2)],
+              "copy": torch.cuda.Stream(dev), "done": None}
+        _StreamState.put(main, st)
     cs = st["copy"]
     total = torch.zeros(nb + 1, dtype=torch.int64, device=dev)
     freed = [None, None]
     cs.wait_stream(main)
+    if st["done"] is not None:
+        cs.wait_event(st["done"])   # the previous call's kernels are done with the buffers
     for c, z0 in enumerate(range(0, D, cp)):
         z1 = min(z0 + cp, D)
         lo, hi = max(z0 - 1, 0), min(z1 + 1, D)
@@ -250,6 +342,7 @@ def ecc_discrete_host(x_host: torch.Tensor, taus, chunk_planes: int = 64, device
         ev.record(main)
         freed[c % 2] = ev
     curve = scan_device(total.reshape(1, -1), nb)[0]
+    st["done"] = freed[(D - 1) // cp % 2]
     return (curve, total) if return_hist else curve
 
 
@@ -258,16 +351,18 @@ def _ecc_discrete_host_resident(x_host, ts, cp, dev, code, table, binning, retur
     nb = len(ts)
     nchunks = (D + cp - 1) // cp
     key = ("resident", x_host.dtype, D, H, W, nb, nchunks, str(dev))
-    st = _StreamState.cache.get(key)
-    if st is None:
-        st = {"vol": torch.empty((D, H, W), dtype=x_host.dtype, device=dev),
-              "parts": torch.empty((nchunks, nb + 1), dtype=torch.int64, device=dev),
-              "copy": torch.cuda.Stream(dev)}
-        _StreamState.cache = {key: st}   # one cached configuration
-    vol, parts, cs = st["vol"], st["parts"], st["copy"]
     main = torch.cuda.current_stream(dev)
+    st = _StreamState.get(main, key)
+    if st is None:
+        st = {"key": key, "vol": torch.empty((D, H, W), dtype=x_host.dtype, device=dev),
+              "parts": torch.empty((nchunks, nb + 1), dtype=torch.int64, device=dev),
+              "copy": torch.cuda.Stream(dev), "done": None}
+        _StreamState.put(main, st)
+    vol, parts, cs = st["vol"], st["parts"], st["copy"]
     d = _lib.dims_arg(vol.shape)
-    cs.wait_stream(main)   # the previous call's kernels are done with vol and parts
+    cs.wait_stream(main)
+    if st["done"] is not None:
+        cs.wait_event(st["done"])   # the previous call's kernels are done with vol and parts
     a = 0                  # planes [0, a) deposited
     for k in range(nchunks):
         z0, z1 = k * cp, min((k + 1) * cp, D)
@@ -285,6 +380,9 @@ def _ecc_discrete_host_resident(x_host, ts, cp, dev, code, table, binning, retur
             parts[k].zero_()
         a = max(a, b)
     total = parts.sum(0)
+    done = torch.cuda.Event()
+    done.record(main)
+    st["done"] = done
     curve = scan_device(total.reshape(1, -1), nb)[0]
     return (curve, total) if return_hist else curve
 

@@ -336,44 +336,124 @@ def gradient_check(grid: ScalarGrid, params: SoftEccParams, upstream=None, step:
 # PyTorch autograd surface
 # ---------------------------------------------------------------------------
 
-class SoftECCFunction(torch.autograd.Function):
+# The module path is sync-free: tau, u and alpha stay on the device, the
+# kernel parameters (centre, sigmoid mode) are derived there (ecc_soft_setup),
+# so a forward + backward issues no device -> host read and can be captured
+# in a CUDA graph.  The kernels are registered as torch.library custom ops
+# with fake (meta) implementations, so torch.compile traces through them
+# without graph breaks.
+_PARAMS_F64 = 7   # sizeof(ecc_soft_params) / 8
+
+
+@torch.library.custom_op("ecc_b200::soft_ecc_fwd", mutates_args=())
+def _soft_fwd_op(x: torch.Tensor, taus: torch.Tensor, u: torch.Tensor, alpha: torch.Tensor, lam: float,
+                 ndim: int) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor]:
+    """(chi [N, B] f64, coefficients int8, centred field f32, its remainder
+    f32, device parameters) of x [N, (D,) H, W]."""
+    from .hard import _split_batch
+
+    if not x.is_cuda:
+        raise ValueError("SoftECC takes a CUDA tensor")
+    dev = x.device
+    xs = _soft_tensor(x)
+    batch, dims, _ = _split_batch(xs, ndim)
+    taus_d = taus.detach().to(dev, torch.float64).contiguous()
+    u_d = u.detach().to(dev, torch.float64).contiguous()
+    a_d = alpha.detach().to(dev, torch.float64).reshape(1).contiguous()
+    nb = taus_d.numel()
+    L = _lib.lib()
+    st = _lib.stream_ptr(xs)
+    params = torch.empty(_PARAMS_F64, dtype=torch.float64, device=dev)
+    _lib.check(L.ecc_soft_setup(_lib.ptr(taus_d), nb, _lib.ptr(u_d), ndim, _lib.ptr(a_d), float(lam),
+                                _lib.ptr(params), st))
+    c = torch.empty(xs.shape, dtype=torch.int8, device=dev)
+    fc = torch.empty(xs.shape, dtype=torch.float32, device=dev)
+    lo = torch.empty(xs.shape, dtype=torch.float32, device=dev)
+    d = _lib.dims_arg(dims)
+    _lib.check(L.ecc_soft_prepare_d(_lib.ptr(xs), _lib.dtype_code(xs), len(dims), _lib.ptr(d), batch,
+                                    _lib.ptr(params), _lib.ptr(c), _lib.ptr(fc), _lib.ptr(lo), st))
+    chi = torch.empty((batch, nb), dtype=torch.float64, device=dev)
+    ws = _workspace(dims, batch, nb, dev)
+    _lib.check(L.ecc_soft_forward_d(_lib.ptr(c), _lib.ptr(fc), _lib.ptr(lo), len(dims), _lib.ptr(d), batch,
+                                    _lib.ptr(taus_d), nb, _lib.ptr(params), _lib.ptr(chi), _lib.ptr(ws), st))
+    return chi, c, fc, lo, params
+
+
+@_soft_fwd_op.register_fake
+def _(x, taus, u, alpha, lam, ndim):
+    from .hard import _split_batch
+
+    batch, _, _ = _split_batch(x, ndim)
+    return (x.new_empty((batch, taus.shape[0]), dtype=torch.float64), x.new_empty(x.shape, dtype=torch.int8),
+            x.new_empty(x.shape, dtype=torch.float32), x.new_empty(x.shape, dtype=torch.float32),
+            x.new_empty((_PARAMS_F64,), dtype=torch.float64))
+
+
+@torch.library.custom_op("ecc_b200::soft_ecc_bwd", mutates_args=())
+def _soft_bwd_op(c: torch.Tensor, fc: torch.Tensor, lo: torch.Tensor, params: torch.Tensor, taus: torch.Tensor,
+                 grad_chi: torch.Tensor, ndim: int) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
+    """(d_values f32 like the field, d_tau [N, B] f64, G [N, ndim] f64) for upstream grad_chi [N, B]."""
+    dims = tuple(c.shape[-ndim:])
+    batch = c.numel() // math.prod(dims)
+    dev = c.device
+    taus_d = taus.detach().to(dev, torch.float64).contiguous()
+    nb = taus_d.numel()
+    up = grad_chi.to(dev, torch.float64).reshape(batch, nb).contiguous()
+    dX = torch.empty(fc.shape, dtype=torch.float32, device=dev)
+    dtau = torch.empty((batch, nb), dtype=torch.float64, device=dev)
+    G = torch.empty((batch, ndim), dtype=torch.float64, device=dev)
+    ws = _workspace(dims, batch, nb, dev)
+    d = _lib.dims_arg(dims)
+    _lib.check(_lib.lib().ecc_soft_backward_d(_lib.ptr(c), _lib.ptr(fc), _lib.ptr(lo), ndim, _lib.ptr(d), batch,
+                                              _lib.ptr(taus_d), nb, _lib.ptr(params), _lib.ptr(up), _lib.ptr(dX),
+                                              _lib.ptr(dtau), _lib.ptr(G), _lib.ptr(ws), _lib.stream_ptr(fc)))
+    return dX, dtau, G
+
+
+@_soft_bwd_op.register_fake
+def _(c, fc, lo, params, taus, grad_chi, ndim):
+    batch = grad_chi.shape[0]
+    return (fc.new_empty(fc.shape), fc.new_empty((batch, taus.shape[0]), dtype=torch.float64),
+            fc.new_empty((batch, ndim), dtype=torch.float64))
+
+
+def _soft_setup_context(ctx, inputs, output):
+    x, taus, u, alpha, lam, ndim = inputs
+    chi, c, fc, lo, params = output
+    ctx.save_for_backward(c, fc, lo, params, taus, u, alpha)
+    ctx.ndim = ndim
+    ctx.xdtype = x.dtype
+
+
+def _soft_backward(ctx, grad_chi, _gc, _gfc, _glo, _gp):
+    c, fc, lo, params, taus, u, alpha = ctx.saved_tensors
+    dX, dtau, G = torch.ops.ecc_b200.soft_ecc_bwd(c, fc, lo, params, taus, grad_chi, ctx.ndim)
+    Gs = G.sum(0)
+    u64 = u.to(Gs.device, torch.float64)
+    gx = dX.to(ctx.xdtype) if ctx.needs_input_grad[0] else None
+    gt = dtau.sum(0).to(taus.device, taus.dtype) if ctx.needs_input_grad[1] else None
+    gu = (-alpha.to(Gs.device, torch.float64) * Gs).to(u.device, u.dtype) if ctx.needs_input_grad[2] else None
+    ga = (-(Gs * u64).sum()).to(alpha.device, alpha.dtype) if ctx.needs_input_grad[3] else None
+    return gx, gt, gu, ga, None, None
+
+
+torch.library.register_autograd("ecc_b200::soft_ecc_fwd", _soft_backward, setup_context=_soft_setup_context)
+
+
+class SoftECCFunction:
     """chi[N, B] = sum_p c_p sigmoid(lam (tau_j - X_np - alpha <u, pos_p>)).
 
     x: CUDA [N, (D,) H, W] float32/float64; taus: [B]; u: [ndim] (any norm;
     the module normalises); alpha: scalar tensor; lam: python float.
     Coefficients come from the effective field and carry no gradient
-    (SPEC.md:294; soft.py:14-19).
+    (SPEC.md:294; soft.py:14-19).  Differentiable in x, taus, u and alpha
+    through the registered custom op ``torch.ops.ecc_b200.soft_ecc_fwd``.
     """
 
     @staticmethod
-    def forward(ctx, x, taus, u, alpha, lam: float, ndim: int):
-        from .hard import _split_batch
-
-        xs = _soft_tensor(x.detach())
-        batch, dims, batched = _split_batch(xs, ndim)
-        taus_d = taus.detach().to(torch.float64).contiguous()
-        lo, hi = torch.aminmax(taus_d)
-        uh = u.detach().to(torch.float64).cpu().numpy()
-        a = float(alpha.detach())
-        p = _params(lam, a, uh, float(lo), float(hi), ndim, _block_halfwidth(taus_d))
-        c, (fc, lo) = soft_prepare_device(xs, dims, batch, p)
-        chi = soft_forward_device(c, (fc, lo), dims, batch, taus_d, p)
-        ctx.save_for_backward(c, fc, lo if lo is not None else fc.new_empty(0), taus_d, u.detach(), alpha.detach())
-        ctx.meta = (dims, batch, batched, p, x.dtype, taus.dtype)
-        return chi if batched else chi[0]
-
-    @staticmethod
-    def backward(ctx, grad_chi):
-        c, fc, lo, taus_d, u, alpha = ctx.saved_tensors
-        dims, batch, batched, p, xdtype, tdtype = ctx.meta
-        up = grad_chi.reshape(batch, -1)
-        dX, dtau, G = soft_backward_device(c, (fc, lo if lo.numel() else None), dims, batch, taus_d, p, up)
-        Gs = G.sum(0)
-        gx = dX.to(xdtype) if ctx.needs_input_grad[0] else None
-        gt = dtau.sum(0).to(tdtype) if ctx.needs_input_grad[1] else None
-        gu = (-alpha.to(torch.float64) * Gs).to(u.dtype) if ctx.needs_input_grad[2] else None
-        ga = (-(Gs * u.to(torch.float64)).sum()).to(alpha.dtype) if ctx.needs_input_grad[3] else None
-        return gx, gt, gu, ga, None, None
+    def apply(x, taus, u, alpha, lam: float, ndim: int):
+        chi = torch.ops.ecc_b200.soft_ecc_fwd(x, taus, u, alpha, float(lam), int(ndim))[0]
+        return chi if x.dim() == ndim + 1 else chi[0]
 
 
 class SoftECC(torch.nn.Module):
@@ -400,9 +480,10 @@ class SoftECC(torch.nn.Module):
         self.v = torch.nn.Parameter(v, requires_grad=learn_direction)
         self.alpha = torch.nn.Parameter(torch.tensor(float(alpha), dtype=torch.float64), requires_grad=learn_alpha)
         self.register_buffer("lam", torch.tensor(float(lam), dtype=torch.float64))
+        self._lam = float(lam)   # the kernels take lambda by value: no device read per call
 
     def direction(self) -> torch.Tensor:
         return self.v / self.v.norm()
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:
-        return SoftECCFunction.apply(x, self.taus, self.direction(), self.alpha, float(self.lam), self.ndim)
+        return SoftECCFunction.apply(x, self.taus, self.direction(), self.alpha, self._lam, self.ndim)

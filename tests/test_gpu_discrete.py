@@ -222,28 +222,22 @@ class TestFastPath:
     SHAPES = [(1, 4, 4), (3, 5, 8), (7, 31, 32), (9, 30, 36), (5, 61, 100), (33, 33, 128), (2, 64, 132),
               (17, 90, 260), (64, 31, 4), (1, 1, 64), (40, 1, 40), (65, 47, 68)]
 
-    KERNELS = {"bin": {}, "value": {"ECC_B200_F3": "value"}, "branch": {"ECC_B200_F3": "branch"},
-               "cta": {"ECC_B200_F3": "cta"}, "rank2": {"ECC_B200_F3": "rank2"}, "no2d": {"ECC_B200_F3": "no2d"},
-               "dyn4": {"ECC_B200_F3_ZUNIT": "4"}, "dyn7": {"ECC_B200_F3_ZUNIT": "7"},
-               "edge1": {"ECC_B200_F3": "edge1"}, "dummy": {"ECC_B200_F3": "dummy"},
-               "static": {"ECC_B200_F3": "static"},
-               "generic": {"ECC_B200_GENERIC": "1"}}
+    KERNELS = {"bin": {}, "value": {"f3": "value"}, "branch": {"f3": "branch"}, "cta": {"f3": "cta"},
+               "rank2": {"f3": "rank2"}, "no2d": {"f3": "no2d"}, "dyn4": {"zunit": 4}, "dyn7": {"zunit": 7},
+               "edge1": {"f3": "edge1"}, "dummy": {"f3": "dummy"}, "static": {"f3": "static"},
+               "generic": {"generic": 1}}
 
     @classmethod
     def _all(cls, t, ts, **kw):
-        """Histogram through each kernel: the bin-image TMA kernel (default when
-        the thresholds have a cell table), its branch-deposit variant, the
-        value-order TMA kernel and the generic sweep."""
-        import os
+        """Histogram through each kernel: the rank4 TMA kernel (default when
+        the thresholds have an edge table), its variants, the value-order TMA
+        kernel and the generic sweep."""
+        from paper_2510_20271_b200 import _lib
 
         out = {}
-        for name, env in cls.KERNELS.items():
-            os.environ.update(env)
-            try:
+        for name, var in cls.KERNELS.items():
+            with _lib.variant(**var):
                 out[name] = E.histogram_device(t, ts, **kw).cpu().numpy()
-            finally:
-                for k in env:
-                    del os.environ[k]
         return out
 
     @classmethod
@@ -291,17 +285,13 @@ class TestFastPath:
             assert np.array_equal(fast[0], want) and np.array_equal(gen[0], want)
 
     def test_batched(self, rng):
-        import os
+        from paper_2510_20271_b200 import _lib
 
         xs = rng.random((3, 10, 37, 44)).astype(np.float32)
         ts = E.ThresholdSet(np.linspace(0.01, 0.99, 129))
-        for zunit in (None, "3"):   # static partition, dynamic work queue (units span items)
-            if zunit:
-                os.environ["ECC_B200_F3_ZUNIT"] = zunit
-            try:
+        for zunit in (0, 3):   # static partition, dynamic work queue (units span items)
+            with _lib.variant(zunit=zunit):
                 h = E.histogram_device(torch.from_numpy(xs).cuda(), ts, ndim=3).cpu().numpy()
-            finally:
-                os.environ.pop("ECC_B200_F3_ZUNIT", None)
             for i in range(3):
                 assert np.array_equal(h[i], np.append(*oracle.histogram(xs[i], ts.taus))), (zunit, i)
 
@@ -315,12 +305,8 @@ class TestFastPath:
         t = torch.from_numpy(x).cuda()
         table, binning = ts.device_table(_lib.DTYPE_F32, t.device)
         want = np.append(*oracle.histogram(x, ts.taus))
-        import os
-
-        for zunit in (None, "2", "3"):   # static partition and the dynamic work queue
-            if zunit:
-                os.environ["ECC_B200_F3_ZUNIT"] = zunit
-            try:
+        for zunit in (0, 2, 3):   # static partition and the dynamic work queue
+            with _lib.variant(zunit=zunit):
                 total = np.zeros(65, np.int64)
                 for z0, z1 in [(0, 7), (7, 8), (8, 16), (16, 23)]:
                     lo, hi = max(0, z0 - 1), min(D, z1 + 1)
@@ -332,8 +318,6 @@ class TestFastPath:
                                                               _lib.ctypes.byref(binning), _lib.ptr(hist),
                                                               _lib.stream_ptr(view)))
                     total += hist.cpu().numpy()
-            finally:
-                os.environ.pop("ECC_B200_F3_ZUNIT", None)
             assert np.array_equal(total, want), zunit
 
     def test_large_volume_invariants(self):

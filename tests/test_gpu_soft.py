@@ -291,8 +291,6 @@ class TestPrepare2D:
     @pytest.mark.parametrize("hw,batch", [((8, 8), 1), ((37, 23), 2), ((70, 33), 3), ((1, 40), 2), ((65, 1), 1),
                                           ((100, 130), 2)])
     def test_matches_generic_sweep(self, rng, hw, batch):
-        import os
-
         for dtype, lam, hw_, alpha in ((np.float32, 50.0, 0.01, 0.3), (np.float64, 500.0, 1.0, 0.3),
                                        (np.float32, 50.0, 0.01, 0.0)):
             x = rng.random((batch,) + hw).astype(dtype)
@@ -301,11 +299,8 @@ class TestPrepare2D:
             p = E.soft._params(lam, alpha, u, -0.5, 1.5, 2, hw_)
             t = torch.from_numpy(x).cuda()
             c1, (f1, l1) = E.soft.soft_prepare_device(t, hw, batch, p)
-            os.environ["ECC_B200_GENERIC"] = "1"
-            try:
+            with E._lib.variant(generic=1):
                 c2, (f2, l2) = E.soft.soft_prepare_device(t, hw, batch, p)
-            finally:
-                del os.environ["ECC_B200_GENERIC"]
             assert torch.equal(c1, c2) and torch.equal(f1, f2), (hw, dtype, alpha)
             if l1 is not None:
                 assert torch.equal(l1, l2)

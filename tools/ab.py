@@ -1,4 +1,4 @@
-"""A/B device timings of kernel variants (ECC_B200_F3=...) on the C2/NS volumes;
+"""A/B device timings of kernel variants (f3 variants, ecc_set_variant) on the C2/NS volumes;
 every variant's histogram must equal the first one's (development aid)."""
 import os, sys
 import numpy as np
@@ -19,7 +19,7 @@ for n in sizes:
     res = {}
     for rnd in range(2):
         for v in variants:
-            os.environ["ECC_B200_F3"] = v
+            _lib.set_variant("f3", v or "default")
             h = E.histogram_device(x, ts).cpu().numpy()
             if ref is None:
                 ref = h
