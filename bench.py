@@ -317,7 +317,7 @@ def run_b200(args):
         if dist_on:
             # halo exchange in flight while the interior planes are swept, then
             # the two boundary planes, histogram all-reduce (distributed.slab_histogram)
-            h = D.slab_histogram(padded, taus, hist_fn=slab_fn)
+            h = D.slab_histogram(padded, taus, hist_fn=slab_fn, depth=P * world)
         else:
             h = sweep(view, z0, z1, hist)
         _lib.check(L.ecc_scan(_lib.ptr(h), 1, NB, _lib.ptr(curve), _lib.ctypes.c_void_p(stream.cuda_stream)))
@@ -576,7 +576,7 @@ def bench_c5(args, dev, world, rank, dist_on=False):
 
     def step():
         if dist_on:
-            h = D.slab_histogram(padded, taus, hist_fn=slab_fn)
+            h = D.slab_histogram(padded, taus, hist_fn=slab_fn, depth=Dz)
         else:
             h = slab_fn(whole, 0, P, taus)
         _lib.check(L.ecc_scan(_lib.ptr(h), 1, NB, _lib.ptr(curve), _lib.ctypes.c_void_p(stream.cuda_stream)))

@@ -29,7 +29,8 @@ import torch.distributed as dist
 
 
 def slab_bounds(depth: int, world: int, rank: int) -> tuple[int, int]:
-    """Planes [z0, z1) of rank `rank` for an even split of `depth` planes."""
+    """Planes [z0, z1) of rank `rank` for an even split of `depth` planes
+    (empty for ranks beyond `depth`; slab_histogram refuses such splits)."""
     base, extra = divmod(depth, world)
     z0 = rank * base + min(rank, extra)
     return z0, z0 + base + (1 if rank < extra else 0)
@@ -94,13 +95,19 @@ def _cuda_slab_hist(view: torch.Tensor, z0: int, z1: int, taus) -> torch.Tensor:
 
 
 def slab_histogram(padded: torch.Tensor, taus, group=None, exchange: bool = True,
-                   hist_fn: Callable | None = None, overlap: bool = True) -> torch.Tensor:
+                   hist_fn: Callable | None = None, overlap: bool = True, depth: int | None = None) -> torch.Tensor:
     """Global (B+1) int64 histogram of a z-slab-partitioned 3D volume.
 
     padded: [planes + 2, H, W] (own planes at 1..planes; halos filled here
     when `exchange`).  hist_fn(view, plane_begin, plane_end, taus) -> (B+1)
     int64 histogram of planes [plane_begin, plane_end) of the contiguous
     view; defaults to the CUDA kernel (ecc_histogram_range).
+
+    depth (the volume's plane count, optional): every rank refuses a split
+    with more ranks than planes before any collective, so all of them raise
+    together; without it only the empty rank raises (an empty
+    rank's halo slots would otherwise reach its neighbours as their boundary
+    planes).
 
     overlap (with exchange, >= 3 own planes, >1 rank): the interior planes
     [1, planes - 1) need only this rank's own data, so they are swept while
@@ -110,6 +117,8 @@ def slab_histogram(padded: torch.Tensor, taus, group=None, exchange: bool = True
     """
     fn = hist_fn or _cuda_slab_hist
     planes = padded.shape[0] - 2
+    if (depth is not None and depth < dist.get_world_size(group)) or planes < 1:
+        raise ValueError("every rank needs at least one plane (more ranks than planes in the volume)")
     if exchange and overlap and planes >= 3 and dist.get_world_size(group) > 1:
         reqs = start_halo_exchange(padded, group)
         hist = fn(padded[1:-1], 1, planes - 1, taus)
@@ -126,9 +135,10 @@ def slab_histogram(padded: torch.Tensor, taus, group=None, exchange: bool = True
     return hist
 
 
-def slab_curve(padded: torch.Tensor, taus, group=None, hist_fn: Callable | None = None) -> torch.Tensor:
+def slab_curve(padded: torch.Tensor, taus, group=None, hist_fn: Callable | None = None,
+               depth: int | None = None) -> torch.Tensor:
     """Exact int64 ECC curve [B] of the whole distributed volume (every rank)."""
-    hist = slab_histogram(padded, taus, group, hist_fn=hist_fn)
+    hist = slab_histogram(padded, taus, group, hist_fn=hist_fn, depth=depth)
     return torch.cumsum(hist[:-1], 0) if not hist.is_cuda else _scan(hist, len(taus))
 
 

@@ -259,6 +259,8 @@ def load_slab_device(path, rank: int, world: int, device=None, **kw) -> tuple[to
     h = read_header(path, VERSION_SCALAR, 4)
     if len(h.dims) != 3:
         raise ValueError("z-slab loading needs a 3D grid file")
+    if world > h.dims[0]:
+        raise ValueError(f"cannot split {h.dims[0]} planes over {world} ranks (every rank needs a plane)")
     z0, z1 = slab_bounds(h.dims[0], world, rank)
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
     padded = alloc_padded_slab(z1 - z0, h.dims[1:], torch.float32, dev)

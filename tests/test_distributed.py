@@ -86,21 +86,55 @@ def test_slab_histogram_matches_whole_volume(world, dims, dtype):
     assert q.get(timeout=5) is True
 
 
+def _soft_item_grads(x, taus, v, alpha, lam, up):
+    """(d_tau, d_v, d_alpha) of one item from the oracle (soft.py:199-257 plus
+    the alpha gradient), with the module's u = v/|v| reparametrisation."""
+    from oracle import oracle
+
+    u = v / np.linalg.norm(v)
+    c = oracle.coefficients(oracle.effective_field(x, alpha, u))
+    _, dt, _, _, G = oracle.soft_backward(x, c, lam, alpha, u, taus, up)
+    du_raw = -alpha * G
+    dv = (du_raw - u * (u @ du_raw)) / np.linalg.norm(v)
+    return dt, dv, -(G @ u)
+
+
 def _grad_worker(rank, world, port, result_q):
+    """Batch-sharded soft ECC: each rank holds a SoftECC module and its shard of
+    the batch, its parameter gradients are the shard's (computed here by the
+    CPU oracle, the per-shard kernel being test-injected as for the slabs);
+    allreduce_soft_grads must leave every rank with the full batch's."""
     import sys
 
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_2510_20271_b200 import SoftECC
     from paper_2510_20271_b200 import distributed as D
 
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     try:
-        m = torch.nn.Linear(3, 2).double()
-        for p in m.parameters():
-            p.grad = torch.full_like(p, float(rank + 1))
+        rng = np.random.default_rng(3)
+        N, B, lam, alpha = 7, 24, 20.0, 0.3
+        xs = rng.random((N, 12, 10))
+        v = np.array([1.0, 2.0])
+        taus = np.linspace(-0.4, 1.4, B)
+        up = rng.uniform(0.5, 1.5, (N, B))
+        m = SoftECC(taus, v, alpha=alpha, lam=lam)
+        i0, i1 = D.shard_batch(N, world, rank)
+        g = [np.zeros(B), np.zeros(2), 0.0]
+        for i in range(i0, i1):
+            dt, dv, da = _soft_item_grads(xs[i], taus, v, alpha, lam, up[i])
+            g = [g[0] + dt, g[1] + dv, g[2] + da]
+        m.taus.grad = torch.from_numpy(g[0])
+        m.v.grad = torch.from_numpy(g[1])
+        m.alpha.grad = torch.tensor(float(g[2]), dtype=torch.float64)
         D.allreduce_soft_grads(m)
-        want = sum(r + 1 for r in range(world))
-        ok = all(torch.all(p.grad == want) for p in m.parameters())
-        i0, i1 = D.shard_batch(10, world, rank)
+        full = [np.zeros(B), np.zeros(2), 0.0]
+        for i in range(N):
+            dt, dv, da = _soft_item_grads(xs[i], taus, v, alpha, lam, up[i])
+            full = [full[0] + dt, full[1] + dv, full[2] + da]
+        ok = (np.allclose(m.taus.grad.numpy(), full[0], rtol=1e-12, atol=1e-14)
+              and np.allclose(m.v.grad.numpy(), full[1], rtol=1e-12, atol=1e-14)
+              and abs(float(m.alpha.grad) - full[2]) <= 1e-12 * max(1.0, abs(full[2])))
         result_q.put((rank, bool(ok), i0, i1))
     finally:
         dist.destroy_process_group()
@@ -120,8 +154,44 @@ def test_soft_gradient_allreduce_and_batch_shards():
     res = sorted(q.get(timeout=5) for _ in range(world))
     assert all(ok for _, ok, _, _ in res)
     spans = [(a, b) for _, _, a, b in res]
-    assert spans[0][0] == 0 and spans[-1][1] == 10
+    assert spans[0][0] == 0 and spans[-1][1] == 7
     assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))
+
+
+def _empty_worker(rank, world, port, result_q):
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_2510_20271_b200 import distributed as D
+    from paper_2510_20271_b200.grid import ThresholdSet
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        z0, z1 = D.slab_bounds(2, world, rank)
+        padded = D.alloc_padded_slab(z1 - z0, (4, 4), torch.float32, "cpu")
+        try:
+            D.slab_histogram(padded, ThresholdSet([0.5]), hist_fn=_oracle_hist, depth=2)
+            result_q.put((rank, z1 - z0, "ran"))
+        except ValueError:
+            result_q.put((rank, z1 - z0, "refused"))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_more_ranks_than_planes_is_refused():
+    """with world > depth an empty rank would hand its neighbours
+    uninitialised halo planes; the empty rank refuses before any exchange."""
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_empty_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(60)
+    res = sorted(q.get(timeout=5) for _ in range(world))
+    assert all(how == "refused" for _, _, how in res) and any(n == 0 for _, n, _ in res)
 
 
 def test_slab_bounds_cover():
