@@ -813,6 +813,141 @@ __global__ void __launch_bounds__(256) soft_prep2d_kernel(EffSrc<T> src, double 
 }
 }  // namespace ecc
 
+namespace ecc {
+// 3-D soft prepare (C4).  The generic sweep's z-streaming tiling (32 x 16
+// outputs per work item, a 4-plane float64 ring in shared memory, a 3 x 4 x 3
+// register window per thread), specialised for the effective field: every
+// thread stages the same three (row, column) positions of each plane of an
+// item, so the position terms of the field are formed once per item and a
+// staged voxel costs only
+//   t = fma(p0(z), u0, p1(y) u1),  dot = fma(p2(x), u2, t),  f = x + alpha dot
+// -- the reference's rounding sequence (soft.py:97-101; OpenBLAS dgemv's fma
+// order), bit for bit the generic sweep's EffSrc::make -- with 32-bit index
+// and bounds arithmetic per plane.
+template <typename T>
+__global__ void __launch_bounds__(NT, 2)
+soft_prep3d_kernel(EffSrc<T> src, SoftPrepSink sk, Geom g) {
+  __shared__ double planes[NBUF][PLANE];
+  src.init();
+  sk.init(nullptr);
+  const int tx = threadIdx.x & (TX - 1);
+  const int wy = threadIdx.x >> 5;
+  const double nanv = __longlong_as_double(0x7ff8000000000000ll);
+  const int64_t HW = g.H * g.W;
+  int sry[LPT], srx[LPT];
+#pragma unroll
+  for (int k = 0; k < LPT; ++k) {
+    const int e = threadIdx.x + k * NT;
+    sry[k] = e / PW;
+    srx[k] = e - sry[k] * PW;
+  }
+  for (int64_t item = blockIdx.x; item < g.items; item += gridDim.x) {
+    int64_t r = item;
+    const int64_t tile_x = r % g.tiles_x; r /= g.tiles_x;
+    const int64_t tile_y = r % g.tiles_y; r /= g.tiles_y;
+    const int64_t zchunk = r % g.zchunks; r /= g.zchunks;
+    const int64_t n = r;
+    const int64_t x0 = tile_x * TX, y0 = tile_y * TY;
+    const int64_t zs = g.zb + zchunk * g.zc;
+    const int64_t ze = min(zs + g.zc, g.ze);
+    const T* xb = src.x + n * g.D * HW;
+    // per staged position: in-grid flag, in-plane offset, p1 u1 and p2
+    bool ok[LPT];
+    int64_t off[LPT];
+    double p1u1[LPT], p2[LPT];
+#pragma unroll
+    for (int k = 0; k < LPT; ++k) {
+      const int64_t yy = y0 - 1 + sry[k], xx = x0 - 1 + srx[k];
+      ok[k] = threadIdx.x + k * NT < PLANE && yy >= 0 && yy < g.H && xx >= 0 && xx < g.W;
+      off[k] = ok[k] ? yy * g.W + xx : 0;
+      p1u1[k] = __dmul_rn(EffSrc<T>::crd(ok[k] ? yy : 0, g.H, src.sH), src.u1);
+      p2[k] = EffSrc<T>::crd(ok[k] ? xx : 0, g.W, src.sW);
+    }
+    auto load_plane = [&](int64_t z, T (&buf)[LPT]) {
+      const bool zin = z >= 0 && z < g.D;
+#pragma unroll
+      for (int k = 0; k < LPT; ++k) buf[k] = (zin && ok[k]) ? xb[z * HW + off[k]] : T(0);
+    };
+    auto store_plane = [&](int64_t z, const T (&buf)[LPT]) {
+      double* dst = planes[(int)((z + 4) & (NBUF - 1))];
+      const bool zin = z >= 0 && z < g.D;
+      const double t0 = EffSrc<T>::crd(zin ? z : 0, g.D, src.sD);   // p0(z)
+#pragma unroll
+      for (int k = 0; k < LPT; ++k) {
+        const int e = threadIdx.x + k * NT;
+        if (e < PLANE) {
+          double v = nanv;
+          if (zin && ok[k]) {
+            v = (double)buf[k];
+            if (src.alpha != 0.0) {
+              const double dot = __fma_rn(p2[k], src.u2, __fma_rn(t0, src.u0, p1u1[k]));
+              v = __dadd_rn(v, __dmul_rn(src.alpha, dot));
+            }
+          }
+          dst[e] = v;
+        }
+      }
+    };
+    {
+      T b0[LPT], b1[LPT], b2[LPT];
+      load_plane(zs - 1, b0);
+      load_plane(zs, b1);
+      load_plane(zs + 1, b2);
+      store_plane(zs - 1, b0);
+      store_plane(zs, b1);
+      store_plane(zs + 1, b2);
+    }
+    __syncthreads();
+    double win[3][RY + 2][3];
+#pragma unroll
+    for (int pz = 0; pz < 2; ++pz) {
+      const double* sp = planes[(int)((zs - 1 + pz + 4) & (NBUF - 1))];
+#pragma unroll
+      for (int rr = 0; rr < RY + 2; ++rr)
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc) win[pz + 1][rr][cc] = sp[(RY * wy + rr) * PW + tx + cc];
+    }
+    const int64_t xg = x0 + tx;
+    for (int64_t z = zs; z < ze; ++z) {
+      T nxt[LPT];
+      const bool more = (z + 2 <= ze);
+      if (more) load_plane(z + 2, nxt);
+      const double* sp = planes[(int)((z + 1 + 4) & (NBUF - 1))];
+#pragma unroll
+      for (int rr = 0; rr < RY + 2; ++rr)
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc) {
+          win[0][rr][cc] = win[1][rr][cc];
+          win[1][rr][cc] = win[2][rr][cc];
+          win[2][rr][cc] = sp[(RY * wy + rr) * PW + tx + cc];
+        }
+#pragma unroll
+      for (int ry = 0; ry < RY; ++ry) {
+        const int64_t yg = y0 + RY * wy + ry;
+        if (xg < g.W && yg < g.H) {
+          double nb[3][3][3];
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int b = 0; b < 3; ++b)
+#pragma unroll
+              for (int c = 0; c < 3; ++c) nb[a][b][c] = win[a][ry + b][c];
+          const int c = coeff3<double>(nb);
+          const int64_t i = ((n * g.D + z) * g.H + yg) * g.W + xg;
+          sk.coeffs[i] = (int8_t)c;
+          const double d = nb[1][1][1] - sk.center;
+          const float hi = (float)d;
+          sk.fc[i] = hi;
+          if (sk.fclo) sk.fclo[i] = (float)(d - (double)hi);
+        }
+      }
+      if (more) store_plane(z + 2, nxt);
+      __syncthreads();
+    }
+  }
+}
+}  // namespace ecc
+
 // p: host parameters, or (pd != nullptr) parameters resident on the device
 // (ecc_soft_setup); the values in *p are then placeholders
 static int soft_prepare(const void* x, int dtype, int ndim, const int64_t* dims, int64_t batch,
@@ -842,6 +977,26 @@ static int soft_prepare(const void* x, int dtype, int ndim, const int64_t* dims,
     return check_launch("soft_prep2d_kernel");
   }
 generic:
+  if (ndim == 3 && !variant_generic() && (dtype == ECC_DTYPE_F32 || dtype == ECC_DTYPE_F64)) {
+    int occ = 0;
+    const void* kfn = dtype == ECC_DTYPE_F32 ? (const void*)soft_prep3d_kernel<float>
+                                             : (const void*)soft_prep3d_kernel<double>;
+    if (int rc2 = sweep_occupancy(kfn, 0, &occ)) return rc2;
+    const int64_t max_ctas = (int64_t)num_sms() * occ;
+    Geom g = make_geom(d3, batch, 0, max_ctas, 0, d3[0]);
+    const int64_t grid = g.items < max_ctas ? g.items : max_ctas;
+    if (grid < 1) return ECC_OK;
+    if (dtype == ECC_DTYPE_F32) {
+      EffSrc<float> src{(const float*)x, p->alpha, p->u[0], p->u[1], p->u[2], d3[0], d3[1], d3[2], ndim,
+                        coord_scale(d3[0]), coord_scale(d3[1]), coord_scale(d3[2]), pd};
+      soft_prep3d_kernel<float><<<(unsigned)grid, NT, 0, s>>>(src, sk, g);
+    } else {
+      EffSrc<double> src{(const double*)x, p->alpha, p->u[0], p->u[1], p->u[2], d3[0], d3[1], d3[2], ndim,
+                         coord_scale(d3[0]), coord_scale(d3[1]), coord_scale(d3[2]), pd};
+      soft_prep3d_kernel<double><<<(unsigned)grid, NT, 0, s>>>(src, sk, g);
+    }
+    return check_launch("soft_prep3d_kernel");
+  }
   if (dtype == ECC_DTYPE_F32) {
     EffSrc<float> src{(const float*)x, p->alpha, p->u[0], p->u[1], p->u[2], d3[0], d3[1], d3[2], ndim,
                       coord_scale(d3[0]), coord_scale(d3[1]), coord_scale(d3[2]), pd};

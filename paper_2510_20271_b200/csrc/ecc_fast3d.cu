@@ -758,6 +758,7 @@ __device__ __forceinline__ uint32_t qword(const BRow& R, int j) {
                         // measured slower (1024^3: 561 vs 582 Gvoxel/s, Horner chain or
                         // balanced tree): IMAD does not relieve the ALU pipe here
 #endif
+constexpr uint32_t INV55 = 0xfcfcfcfdu;   // 0x55^-1 mod 2^32
 template <int DX>
 __device__ __forceinline__ uint32_t cmp_word(const uint32_t (&PP)[16], const BRow& R, uint32_t two) {
   uint32_t d[16];
@@ -768,6 +769,19 @@ __device__ __forceinline__ uint32_t cmp_word(const uint32_t (&PP)[16], const BRo
   uint32_t m[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) m[k] = prmt(d[k], d[k + 8], 0xFBD9u);
+  if (ECC_F3_PACK == 2) {
+    // first level as LOP3 selects (m01 byte = 0x55 b0 | 0xAA b1 = 0x55 (b0 + 2 b1)),
+    // the rest on the FMA pipe: m01 + 4 m23 + 16 m45 + 64 m67 = 0x55 V exactly
+    // (as 32-bit integers), and 0x55 is odd: V = (...) * 0x55^-1 mod 2^32.
+    // 4 ALU + 4 IMAD instead of 7 ALU (the ALU pipe is the kernel's busiest)
+    const uint32_t m01 = (m[0] & 0x55555555u) | (m[1] & 0xAAAAAAAAu);
+    const uint32_t m23 = (m[2] & 0x55555555u) | (m[3] & 0xAAAAAAAAu);
+    const uint32_t m45 = (m[4] & 0x55555555u) | (m[5] & 0xAAAAAAAAu);
+    const uint32_t m67 = (m[6] & 0x55555555u) | (m[7] & 0xAAAAAAAAu);
+    const uint32_t four = two << 1, sixteen = two << 3;
+    const uint32_t a = mad_fma(m23, four, m01), b = mad_fma(m67, four, m45);
+    return mul_fma(mad_fma(b, sixteen, a), INV55);
+  }
   if (ECC_F3_PACK) {
     // sum_k m[k] 2^k = 255 V (mod 2^32), V = the wanted word (byte a, bit k =
     // voxel 8a + k; the byte sums stay below 256 so nothing carries), and 255
@@ -859,6 +873,9 @@ __device__ __forceinline__ uint32_t rank_of(float x, uint32_t m, float sc, float
 // after the row is stored.
 #ifndef ECC_R4_ROT
 #define ECC_R4_ROT 1
+#endif
+#ifndef ECC_R4_PRED
+#define ECC_R4_PRED 0
 #endif
 #ifndef ECC_R4_IDP
 #define ECC_R4_IDP 1   // deposit operands by IDP.4A / IDP.2A (FMA pipe) instead of PRMT (ALU)
@@ -2066,7 +2083,10 @@ ecc_rank4_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* _
               const uint32_t addr = ECC_R4_IDP ? dp2a_lo(i < 16 ? Ro.w[i] : Ro.w[i - 16], i < 16 ? 1u : 0x100u, hbase)
                                                : hbase + (i < 16 ? prmt(Ro.w[i], 0u, 0x4410u)
                                                                  : prmt(Ro.w[i - 16], 0u, 0x4432u));
-              asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(addr), "r"(c16) : "memory");
+              if (ECC_R4_PRED)   // c = 0 voxels skip the atomic (fewer shared-memory wavefronts, one more ALU op)
+                red_add_shared_nz(addr, c16);
+              else
+                asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(addr), "r"(c16) : "memory");
             } else if (DEP == 0) {
               const uint32_t idx = i < 16 ? (Ro.w[i] & 0xFFFFu) : (Ro.w[i - 16] >> 16);
               if (c16) atomicAdd(s_hist + idx, c16);

@@ -420,6 +420,10 @@ def _(c, fc, lo, params, taus, grad_chi, ndim):
 def _soft_setup_context(ctx, inputs, output):
     x, taus, u, alpha, lam, ndim = inputs
     chi, c, fc, lo, params = output
+    # the prepared tensors are saved state, not differentiable outputs: no
+    # zero gradients are materialised for them (~9 B per voxel of fills)
+    ctx.mark_non_differentiable(c, fc, lo, params)
+    ctx.set_materialize_grads(False)
     ctx.save_for_backward(c, fc, lo, params, taus, u, alpha)
     ctx.ndim = ndim
     ctx.xdtype = x.dtype
@@ -427,6 +431,8 @@ def _soft_setup_context(ctx, inputs, output):
 
 def _soft_backward(ctx, grad_chi, _gc, _gfc, _glo, _gp):
     c, fc, lo, params, taus, u, alpha = ctx.saved_tensors
+    if grad_chi is None:
+        return None, None, None, None, None, None
     dX, dtau, G = torch.ops.ecc_b200.soft_ecc_bwd(c, fc, lo, params, taus, grad_chi, ctx.ndim)
     Gs = G.sum(0)
     u64 = u.to(Gs.device, torch.float64)

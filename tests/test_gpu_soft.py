@@ -304,3 +304,31 @@ class TestPrepare2D:
             assert torch.equal(c1, c2) and torch.equal(f1, f2), (hw, dtype, alpha)
             if l1 is not None:
                 assert torch.equal(l1, l2)
+
+
+class TestPrepare3D:
+    """The dedicated 3-D soft prepare (soft_prep3d_kernel) against the generic
+    sweep: the same coefficients of the effective field and the same centred
+    field and remainder, bit for bit (float32 and float64 grids, ragged
+    shapes, ties, with and without the position term)."""
+
+    @pytest.mark.parametrize("dhw,batch", [((5, 6, 7), 1), ((17, 33, 40), 2), ((9, 1, 35), 1), ((1, 20, 64), 2),
+                                           ((40, 18, 31), 1)])
+    def test_matches_generic_sweep(self, rng, dhw, batch):
+        for dtype, lam, hw_, alpha in ((np.float32, 50.0, 0.01, 0.3), (np.float64, 500.0, 1.0, 0.25),
+                                       (np.float32, 50.0, 0.01, 0.0)):
+            x = rng.random((batch,) + dhw).astype(dtype)
+            x[..., ::2, :, :] = np.round(x[..., ::2, :, :] * 4) / 4       # ties in the effective field
+            u = E.reparametrize_direction([1.0, 2.0, -0.5])
+            p = E.soft._params(lam, alpha, u, -0.5, 1.5, 3, hw_)
+            t = torch.from_numpy(x).cuda()
+            c1, (f1, l1) = E.soft.soft_prepare_device(t, dhw, batch, p)
+            with E._lib.variant(generic=1):
+                c2, (f2, l2) = E.soft.soft_prepare_device(t, dhw, batch, p)
+            assert torch.equal(c1, c2) and torch.equal(f1, f2), (dhw, dtype, alpha)
+            if l1 is not None:
+                assert torch.equal(l1, l2)
+            # and the coefficients against the oracle's of the float64 field
+            xi = x[0].astype(np.float64)
+            want = oracle.coefficients(oracle.effective_field(xi, alpha, u))
+            assert np.array_equal(c1[0].cpu().numpy(), want), (dhw, dtype, alpha)
