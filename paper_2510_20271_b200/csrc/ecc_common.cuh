@@ -67,6 +67,58 @@ __device__ __forceinline__ int coeff3(const V (&v)[3][3][3]) {
   return __popc(pos | ((~neg & EVA) << 1) | ((Lm ^ 1u) << 28) | ((Lp ^ 1u) << 29)) - 13;
 }
 
+// coeff3 on float64 values with the compare results taken from sign bits:
+// bit 31 of hi(RD(q - p)) is [q <= p] and of hi(RN(q - p)) is [q < p] when
+// no value is -0 (callers canonicalise: v + 0.0); an out-of-grid NaN gives
+// +NaN, i.e. "not lower", as the IEEE compares do.  A funnel shift moves
+// each sign into its mask (one SHF per compare instead of a predicate select
+// and an OR); the masks and the count are coeff3's.
+__device__ __forceinline__ uint32_t hi_le(double q, double p) { return (uint32_t)__double2hiint(__dsub_rd(q, p)); }
+__device__ __forceinline__ uint32_t hi_lt(double q, double p) { return (uint32_t)__double2hiint(__dsub_rn(q, p)); }
+__device__ __forceinline__ uint32_t push_sign(uint32_t acc, uint32_t h) { return __funnelshift_l(h, acc, 1); }
+__device__ __forceinline__ int coeff3_sgn(const double (&v)[3][3][3]) {
+  const double p = v[1][1][1];
+  // 9-bit cyclic masks, bit 8 = bit 0 (E repeated): push E first, then bits 7 .. 0
+  const uint32_t e = hi_lt(v[1][1][2], p);
+  uint32_t P9 = e >> 31;
+  P9 = push_sign(P9, hi_le(v[1][0][2], p));   // 7 (-1,+1)
+  P9 = push_sign(P9, hi_le(v[1][0][1], p));   // 6 (-1, 0)
+  P9 = push_sign(P9, hi_le(v[1][0][0], p));   // 5 (-1,-1)
+  P9 = push_sign(P9, hi_le(v[1][1][0], p));   // 4 ( 0,-1)
+  P9 = push_sign(P9, hi_lt(v[1][2][0], p));   // 3 (+1,-1)
+  P9 = push_sign(P9, hi_lt(v[1][2][1], p));   // 2 (+1, 0)
+  P9 = push_sign(P9, hi_lt(v[1][2][2], p));   // 1 (+1,+1)
+  P9 = push_sign(P9, e);                      // 0 ( 0,+1)
+  const uint32_t em = hi_le(v[0][1][2], p);
+  uint32_t Qm9 = em >> 31;
+  Qm9 = push_sign(Qm9, hi_le(v[0][0][2], p));
+  Qm9 = push_sign(Qm9, hi_le(v[0][0][1], p));
+  Qm9 = push_sign(Qm9, hi_le(v[0][0][0], p));
+  Qm9 = push_sign(Qm9, hi_le(v[0][1][0], p));
+  Qm9 = push_sign(Qm9, hi_le(v[0][2][0], p));
+  Qm9 = push_sign(Qm9, hi_le(v[0][2][1], p));
+  Qm9 = push_sign(Qm9, hi_le(v[0][2][2], p));
+  Qm9 = push_sign(Qm9, em);
+  const uint32_t ep = hi_lt(v[2][1][2], p);
+  uint32_t Qp9 = ep >> 31;
+  Qp9 = push_sign(Qp9, hi_lt(v[2][0][2], p));
+  Qp9 = push_sign(Qp9, hi_lt(v[2][0][1], p));
+  Qp9 = push_sign(Qp9, hi_lt(v[2][0][0], p));
+  Qp9 = push_sign(Qp9, hi_lt(v[2][1][0], p));
+  Qp9 = push_sign(Qp9, hi_lt(v[2][2][0], p));
+  Qp9 = push_sign(Qp9, hi_lt(v[2][2][1], p));
+  Qp9 = push_sign(Qp9, hi_lt(v[2][2][2], p));
+  Qp9 = push_sign(Qp9, ep);
+  const uint32_t hm = hi_le(v[0][1][1], p), hp = hi_lt(v[2][1][1], p);
+  const uint32_t mLm = (uint32_t)((int32_t)hm >> 31), mLp = (uint32_t)((int32_t)hp >> 31);
+  const uint32_t W = P9 | ((P9 & Qm9 & mLm) << 9) | ((P9 & Qp9 & mLp) << 18);
+  const uint32_t sq = W & (W >> 1) & (W >> 2);
+  constexpr uint32_t EV0 = 0x55u, EV12 = (0x55u << 9) | (0x55u << 18), EVA = EV0 | EV12;
+  const uint32_t pos = (W & EV12) | (sq & EV0);
+  const uint32_t neg = (W & EV0) | (sq & EV12);
+  return __popc(pos | ((~neg & EVA) << 1) | ((~mLm & 1u) << 28) | ((~mLp & 1u) << 29)) - 13;
+}
+
 // 2D coefficient (coefficients.py:109-126 on a 3x3 window v[dy][dx]):
 // c2(P) = 1 - #lower axis neighbours + #lower quadrant triples.
 template <typename V>

@@ -813,6 +813,12 @@ __global__ void __launch_bounds__(256) soft_prep2d_kernel(EffSrc<T> src, double 
 }
 }  // namespace ecc
 
+#ifndef ECC_PREP_SGN
+#define ECC_PREP_SGN 0   // 1: coeff3_sgn (sign bits of RD/RN differences + funnel shifts) in the 3-D
+                         // soft prepare; measured slower at 1024^3 (9.87 vs 9.05 ms: the nine
+                         // chained pushes per mask are a longer dependency chain than the
+                         // independent predicate selects)
+#endif
 namespace ecc {
 // 3-D soft prepare (C4).  The generic sweep's z-streaming tiling (32 x 16
 // outputs per work item, a 4-plane float64 ring in shared memory, a 3 x 4 x 3
@@ -883,6 +889,7 @@ soft_prep3d_kernel(EffSrc<T> src, SoftPrepSink sk, Geom g) {
               const double dot = __fma_rn(p2[k], src.u2, __fma_rn(t0, src.u0, p1u1[k]));
               v = __dadd_rn(v, __dmul_rn(src.alpha, dot));
             }
+            v = __dadd_rn(v, 0.0);   // -0 -> +0 (coeff3_sgn's sign-bit compares; equal values either way)
           }
           dst[e] = v;
         }
@@ -932,7 +939,7 @@ soft_prep3d_kernel(EffSrc<T> src, SoftPrepSink sk, Geom g) {
             for (int b = 0; b < 3; ++b)
 #pragma unroll
               for (int c = 0; c < 3; ++c) nb[a][b][c] = win[a][ry + b][c];
-          const int c = coeff3<double>(nb);
+          const int c = ECC_PREP_SGN ? coeff3_sgn(nb) : coeff3<double>(nb);
           const int64_t i = ((n * g.D + z) * g.H + yg) * g.W + xg;
           sk.coeffs[i] = (int8_t)c;
           const double d = nb[1][1][1] - sk.center;
