@@ -830,8 +830,11 @@ namespace ecc {
 // -- the reference's rounding sequence (soft.py:97-101; OpenBLAS dgemv's fma
 // order), bit for bit the generic sweep's EffSrc::make -- with 32-bit index
 // and bounds arithmetic per plane.
+#ifndef ECC_PREP_MINB
+#define ECC_PREP_MINB 2
+#endif
 template <typename T>
-__global__ void __launch_bounds__(NT, 2)
+__global__ void __launch_bounds__(NT, ECC_PREP_MINB)
 soft_prep3d_kernel(EffSrc<T> src, SoftPrepSink sk, Geom g) {
   __shared__ double planes[NBUF][PLANE];
   src.init();

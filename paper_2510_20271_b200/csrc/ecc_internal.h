@@ -32,4 +32,6 @@ int variant_f3();          // F3Mode
 int variant_zunit();       // forced dynamic unit (planes), 0: automatic
 bool variant_generic();    // route everything through the generic sweep
 int variant_soft_t(bool bwd);   // thresholds per lane of the soft kernels (8 / 16 / 32)
+bool variant_soft_band();       // windowed (band-sorted) soft kernels when the thresholds allow
+int variant_soft_g();           // chunks per soft CTA, 0: automatic
 }  // namespace ecc

@@ -24,6 +24,8 @@
 
 #include "ecc_common.cuh"
 #include "ecc_internal.h"
+#include <algorithm>
+#include <type_traits>
 #include <mutex>
 #include <map>
 #include <tuple>
@@ -43,6 +45,8 @@ struct SoftArgs {
   const float* fclo;      // [N][n] f - m - fc (direct mode only)
   int64_t n;              // voxels per item
   int64_t chunks;         // ceil(n / CH)
+  int64_t G;              // chunks per CTA (a unit)
+  int64_t units;          // ceil(chunks / G): CTAs per item, partial rows per item
   int64_t D, H, W;
   int ndim;
   int nb;                 // B
@@ -55,6 +59,7 @@ struct SoftArgs {
   double* gpart;          // [N][chunks][4]   (backward)
   float* dX;              // [N][n]   (backward)
   const ecc_soft_params* pd;   // parameters resident on the device (sync-free path), else nullptr
+  int band;               // the windowed kernel was launched alongside: this one exits where it runs
 };
 
 __device__ __forceinline__ float ex2_approx(float x) {
@@ -308,6 +313,107 @@ __device__ __forceinline__ void pair_loop_direct(const double* __restrict__ kt, 
   }
 }
 
+
+// G = sum_p c_p w_p pos_p = -sum_p dX_p pos_p.  soft_chunk_G_acc adds one
+// chunk (dX was just written by this CTA; zero-coefficient voxels hold 0):
+// each thread takes a contiguous run of voxels and walks their coordinates.
+// soft_unit_G_write reduces the per-thread sums of the CTA's chunks in a
+// fixed order.
+__device__ __forceinline__ void soft_chunk_G_acc(const SoftArgs& a, int64_t item, int64_t v0, int nvox,
+                                                 double (&gacc)[3]) {
+  const int per = (CH + SNT - 1) / SNT;
+  const int i0 = threadIdx.x * per, i1 = min(i0 + per, nvox);
+  float g0 = 0.f, g1 = 0.f, g2 = 0.f;
+  if (i0 < i1) {
+    const float sH = a.H > 1 ? (float)(2.0 / (double)(a.H - 1)) : 0.f;
+    const float sW = a.W > 1 ? (float)(2.0 / (double)(a.W - 1)) : 0.f;
+    const float sD = a.D > 1 ? (float)(2.0 / (double)(a.D - 1)) : 0.f;
+    const int64_t vi = v0 + i0;
+    int64_t z = vi / (a.H * a.W), r = vi - z * a.H * a.W, y = r / a.W, x = r - y * a.W;
+    const float* dxp = a.dX + item * a.n + v0;
+    for (int i = i0; i < i1; ++i) {
+      const float d = dxp[i];
+      if (d != 0.f) {
+        const float pz = a.D > 1 ? __fmaf_rn((float)z, sD, -1.f) : 0.f;
+        const float py = a.H > 1 ? __fmaf_rn((float)y, sH, -1.f) : 0.f;
+        const float px = a.W > 1 ? __fmaf_rn((float)x, sW, -1.f) : 0.f;
+        if (a.ndim == 2) {
+          g0 = __fmaf_rn(-d, py, g0);
+          g1 = __fmaf_rn(-d, px, g1);
+        } else {
+          g0 = __fmaf_rn(-d, pz, g0);
+          g1 = __fmaf_rn(-d, py, g1);
+          g2 = __fmaf_rn(-d, px, g2);
+        }
+      }
+      if (++x == a.W) {
+        x = 0;
+        if (++y == a.H) { y = 0; ++z; }
+      }
+    }
+  }
+  gacc[0] += g0;
+  gacc[1] += g1;
+  gacc[2] += g2;
+}
+
+__device__ __forceinline__ void soft_unit_G_write(const SoftArgs& a, int64_t slotidx, const double (&gacc)[3],
+                                                  double (*s_g)[4]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double v0d = gacc[0], v1d = gacc[1], v2d = gacc[2];
+  for (int o = 16; o; o >>= 1) {
+    v0d += __shfl_xor_sync(0xffffffffu, v0d, o);
+    v1d += __shfl_xor_sync(0xffffffffu, v1d, o);
+    v2d += __shfl_xor_sync(0xffffffffu, v2d, o);
+  }
+  if (lane == 0) { s_g[warp][0] = v0d; s_g[warp][1] = v1d; s_g[warp][2] = v2d; }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    double sg = 0.0;
+    for (int w = 0; w < SNW; ++w) sg += s_g[w][threadIdx.x];
+    a.gpart[slotidx * 4 + threadIdx.x] = sg;
+  }
+}
+
+// ---- windowed ("band") mode ------------------------------------------------
+// With a sharp sigmoid most (voxel, threshold) pairs are saturated:
+// sigma(lam (tau - f)) < 2^-24 for tau < f - W and > 1 - 2^-24 for
+// tau > f + W, W = 24 ln 2 / lam.  The band kernel evaluates only a window of
+// NWB consecutive 16-threshold blocks per voxel, chosen so that every
+// threshold below it lies below f - W and every threshold above it above
+// f + W; the pairs above contribute sigma = 1 (forward: c_p per threshold,
+// summed per band and added once per chunk), those below 0, and in the
+// backward both contribute sigma (1 - sigma) = 0.  The error per skipped pair
+// is < 2^-24 -- the float32 rounding the pair loop already has (a
+// denominator 1 + a b with a b < 2^-24 rounds to 1).  Each CTA sorts its
+// non-zero voxels by window start ("band") while compacting, so a lane keeps
+// one block's factors and accumulators in registers for a whole band.  Valid
+// when the thresholds are sorted and every NWB - 1 blocks span more than 2 W
+// (band_ok, evaluated identically by this kernel and the full one, so exactly
+// one of the two does the work); for C3 / C4 (B = 256, lam = 50) the window
+// is 8 of 16 blocks.
+constexpr int BT = 16;                          // thresholds per lane block
+constexpr int NWB = 8;                          // blocks (lanes) per voxel window
+constexpr int BVW = 32 / NWB;                   // voxels per warp in flight
+constexpr int BSLOTS = SNW * BVW;               // voxel slots per CTA
+constexpr int BAND_MAXB = 368;                  // thresholds: at most 16 bands of NWB blocks
+constexpr int BAND_MAXBLK = BAND_MAXB / BT;
+constexpr int BAND_MAXBANDS = 16;               // band index: 4 bits of the voxel record
+constexpr double BAND_ZCUT = 16.635532333438686;   // 24 ln 2
+
+__device__ __forceinline__ bool band_ok(const SoftArgs& a) {
+  const int nb = a.nb, nblk = (nb + BT - 1) / BT, nbands = nblk - NWB + 1;
+  if (nb > BAND_MAXB || nbands < 2 || nbands > BAND_MAXBANDS) return false;   // uniform over the grid
+  const double w2 = 2.0 * BAND_ZCUT / a.lam * (1.0 + 1e-3);
+  bool ok = true;
+  for (int j = threadIdx.x; j + 1 < nb; j += blockDim.x) ok = ok && a.taus[j] <= a.taus[j + 1];
+  for (int b = threadIdx.x; b + 1 < nbands; b += blockDim.x)
+    ok = ok && a.taus[(b + NWB) * BT] - a.taus[(b + 1) * BT] > w2;
+  return __syncthreads_and(ok) != 0;
+}
+
+static size_t band_smem(int nb);
+
 template <bool BWD, bool FACT, int T>
 __global__ void __launch_bounds__(SNT, (T == 8 ? 4 : (T == 16 ? 3 : 2)))
 ecc_soft_kernel(SoftArgs a) {
@@ -317,6 +423,7 @@ ecc_soft_kernel(SoftArgs a) {
     a.m = a.pd->center;
     a.kscale = (float)(a.lam * LOG2E);
   }
+  if (FACT && T == BT && a.band && band_ok(a)) return;   // the band kernel does this problem
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ChunkSmem& S = *reinterpret_cast<ChunkSmem*>(smem_raw);
   unsigned char* tail = smem_raw + CHUNK_BYTES;
@@ -327,61 +434,12 @@ ecc_soft_kernel(SoftArgs a) {
   __shared__ int s_wcount[SNW];
   __shared__ double s_g[SNW][4];
 
-  const int64_t item = blockIdx.x / a.chunks;
-  const int64_t chunk = blockIdx.x % a.chunks;
-  const int64_t v0 = chunk * CH;
-  const int nvox = (int)min((int64_t)CH, a.n - v0);
-  const int8_t* cg = a.c + item * a.n + v0;
-  const float* fg = a.fc + item * a.n + v0;
+  // this CTA: chunks [c0, c1) of one item (a unit of G chunks)
+  const int64_t item = blockIdx.x / a.units;
+  const int64_t unit = blockIdx.x % a.units;
+  const int64_t c0 = unit * a.G, c1 = min(c0 + a.G, a.chunks);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
-  // ---- compaction of the chunk to c != 0 voxels (order-preserving) -------
-  // Each warp owns CITER x 32 consecutive voxels; all of its coefficient and
-  // field loads are issued up front (one memory latency, not CITER).
-  {
-    constexpr int CITER = CH / SNW / 32;
-    const int w0 = warp * (CITER * 32), w1 = min(w0 + CITER * 32, nvox);
-    int cvr[CITER];
-    float fvr[CITER];
-#pragma unroll
-    for (int it = 0; it < CITER; ++it) {
-      const int i = w0 + it * 32 + lane;
-      cvr[it] = i < w1 ? (int)cg[i] : 0;
-      fvr[it] = i < w1 ? fg[i] : 0.f;
-    }
-    int cnt = 0;
-#pragma unroll
-    for (int it = 0; it < CITER; ++it) cnt += __popc(__ballot_sync(0xffffffffu, cvr[it] != 0));
-    if (lane == 0) s_wcount[warp] = cnt;
-    __syncthreads();
-    int off = 0;
-    for (int w = 0; w < warp; ++w) off += s_wcount[w];
-    if (threadIdx.x == 0) {
-      int tot = 0;
-      for (int w = 0; w < SNW; ++w) tot += s_wcount[w];
-      S.count = tot;
-    }
-#pragma unroll
-    for (int it = 0; it < CITER; ++it) {
-      const int i = w0 + it * 32 + lane;
-      const int cv = cvr[it];
-      const unsigned m = __ballot_sync(0xffffffffu, cv != 0);
-      if (cv != 0) {
-        const int k = off + __popc(m & ((1u << lane) - 1u));
-        S.fc[k] = fvr[it];
-        if (!FACT) s_fclo[k] = a.fclo[item * a.n + v0 + i];
-        // upper half: the float32 bits of c (small integers have a zero low
-        // half), so the pair loop reads c with one AND instead of an I2F on
-        // the XU pipe that the reciprocals saturate; lower half: the voxel
-        S.pk[k] = i | (int)(__float_as_uint((float)cv) & 0xFFFF0000u);
-      } else if (BWD && i < w1) {
-        a.dX[item * a.n + v0 + i] = 0.f;
-      }
-      off += __popc(m);
-    }
-    __syncthreads();
-  }
-  const int count = S.count;
 
   // ---- lane groups: Lv lanes cover one voxel's thresholds -----------------
   const int nb = a.nb;
@@ -436,18 +494,24 @@ ecc_soft_kernel(SoftArgs a) {
   const int j0 = l * T;
   const int jl = min(j0 + T, nb) - 1;
   const double ml = (j0 < nb) ? 0.5 * (a.taus[j0] + a.taus[jl]) : a.m;
+  // the factors are (re)loaded per chunk after its compaction, so they are
+  // not live across it; the accumulators persist over the CTA's chunks
+  auto load_lane = [&]() {
 #pragma unroll
-  for (int t = 0; t < T; ++t) {
-    at[t] = FACT ? atab[j0 + t] : 0.f;
-    upv[t] = (BWD && j0 + t < nb) ? (float)a.up[item * nb + j0 + t] : 0.f;
-    acc[t] = 0.f;
-  }
+    for (int t = 0; t < T; ++t) {
+      at[t] = FACT ? atab[j0 + t] : 0.f;
+      upv[t] = (BWD && j0 + t < nb) ? (float)a.up[item * nb + j0 + t] : 0.f;
+    }
 #pragma unroll
-  for (int i = 0; i < T / 2; ++i) {
-    at2[i] = f2_pack(-at[2 * i], -at[2 * i + 1]);   // negated: see pair_loop_fact2
-    up2[i] = f2_pack(upv[2 * i], upv[2 * i + 1]);
-    acc2[i] = 0ull;
-  }
+    for (int i = 0; i < T / 2; ++i) {
+      at2[i] = f2_pack(-at[2 * i], -at[2 * i + 1]);   // negated: see pair_loop_fact2
+      up2[i] = f2_pack(upv[2 * i], upv[2 * i + 1]);
+    }
+  };
+#pragma unroll
+  for (int t = 0; t < T; ++t) acc[t] = 0.f;
+#pragma unroll
+  for (int i = 0; i < T / 2; ++i) acc2[i] = 0ull;
   const float koff = FACT ? (float)(ks * (a.m - ml)) : 0.f;   // k f_p - k m_l = k fc + koff
 
   auto voxel_w = [&](int k, bool valid) -> float {
@@ -479,6 +543,60 @@ ecc_soft_kernel(SoftArgs a) {
     return w;
   };
   const float lamf = (float)a.lam;
+  double gacc[3] = {0.0, 0.0, 0.0};
+  for (int64_t chunk = c0; chunk < c1; ++chunk) {
+  const int64_t v0 = chunk * CH;
+  const int nvox = (int)min((int64_t)CH, a.n - v0);
+  const int8_t* cg = a.c + item * a.n + v0;
+  const float* fg = a.fc + item * a.n + v0;
+  // ---- compaction of the chunk to c != 0 voxels (order-preserving) -------
+  // Each warp owns CITER x 32 consecutive voxels; all of its coefficient and
+  // field loads are issued up front (one memory latency, not CITER).
+  {
+    constexpr int CITER = CH / SNW / 32;
+    const int w0 = warp * (CITER * 32), w1 = min(w0 + CITER * 32, nvox);
+    int cvr[CITER];
+    float fvr[CITER];
+#pragma unroll
+    for (int it = 0; it < CITER; ++it) {
+      const int i = w0 + it * 32 + lane;
+      cvr[it] = i < w1 ? (int)cg[i] : 0;
+      fvr[it] = i < w1 ? fg[i] : 0.f;
+    }
+    int cnt = 0;
+#pragma unroll
+    for (int it = 0; it < CITER; ++it) cnt += __popc(__ballot_sync(0xffffffffu, cvr[it] != 0));
+    if (lane == 0) s_wcount[warp] = cnt;
+    __syncthreads();
+    int off = 0;
+    for (int w = 0; w < warp; ++w) off += s_wcount[w];
+    if (threadIdx.x == 0) {
+      int tot = 0;
+      for (int w = 0; w < SNW; ++w) tot += s_wcount[w];
+      S.count = tot;
+    }
+#pragma unroll
+    for (int it = 0; it < CITER; ++it) {
+      const int i = w0 + it * 32 + lane;
+      const int cv = cvr[it];
+      const unsigned m = __ballot_sync(0xffffffffu, cv != 0);
+      if (cv != 0) {
+        const int k = off + __popc(m & ((1u << lane) - 1u));
+        S.fc[k] = fvr[it];
+        if (!FACT) s_fclo[k] = a.fclo[item * a.n + v0 + i];
+        // upper half: the float32 bits of c (small integers have a zero low
+        // half), so the pair loop reads c with one AND instead of an I2F on
+        // the XU pipe that the reciprocals saturate; lower half: the voxel
+        S.pk[k] = i | (int)(__float_as_uint((float)cv) & 0xFFFF0000u);
+      } else if (BWD && i < w1) {
+        a.dX[item * a.n + v0 + i] = 0.f;
+      }
+      off += __popc(m);
+    }
+    __syncthreads();
+  }
+  const int count = S.count;
+  load_lane();
   int kb0 = warp * VW;
   if (BWD && FACT && Lv >= 8) {
     // deferred group reduction: 8 voxel rounds, then (Lv > 8) a butterfly
@@ -532,8 +650,10 @@ ecc_soft_kernel(SoftArgs a) {
     }
   }
 
+  __syncthreads();   // the next chunk's compaction overwrites S; dX of this chunk is visible
+  if (BWD) soft_chunk_G_acc(a, item, v0, nvox, gacc);
+  }
   // ---- fixed-order reduction of acc over the CTA's voxel slots ------------
-  __syncthreads();   // chunk arrays no longer needed (red aliases them)
   const int rowlen = Lv * T;
   if (FACT && (!BWD || ECC_BWD_PACKED)) {
 #pragma unroll
@@ -546,62 +666,357 @@ ecc_soft_kernel(SoftArgs a) {
 #pragma unroll
   for (int t = 0; t < T; ++t) red[slot * rowlen + l * T + t] = acc[t];
   __syncthreads();
-  double* out = a.part + (item * a.chunks + chunk) * nb;
+  double* out = a.part + (item * a.units + unit) * nb;
   for (int j = threadIdx.x; j < nb; j += SNT) {
     double sacc = 0.0;
     for (int q = 0; q < nslots; ++q) sacc += (double)red[q * rowlen + j];
     out[j] = sacc;
   }
 
-  if (BWD) {
-    // G = sum_p c_p w_p pos_p = -sum_p dX_p pos_p over this chunk (dX was
-    // just written by this CTA; zero-coefficient voxels hold 0).  Each thread
-    // takes a contiguous run of voxels and walks their coordinates.
-    const int per = (CH + SNT - 1) / SNT;
-    const int i0 = threadIdx.x * per, i1 = min(i0 + per, nvox);
-    float g0 = 0.f, g1 = 0.f, g2 = 0.f;
-    if (i0 < i1) {
-      const float sH = a.H > 1 ? (float)(2.0 / (double)(a.H - 1)) : 0.f;
-      const float sW = a.W > 1 ? (float)(2.0 / (double)(a.W - 1)) : 0.f;
-      const float sD = a.D > 1 ? (float)(2.0 / (double)(a.D - 1)) : 0.f;
-      const int64_t vi = v0 + i0;
-      int64_t z = vi / (a.H * a.W), r = vi - z * a.H * a.W, y = r / a.W, x = r - y * a.W;
-      const float* dxp = a.dX + item * a.n + v0;
-      for (int i = i0; i < i1; ++i) {
-        const float d = dxp[i];
-        if (d != 0.f) {
-          const float pz = a.D > 1 ? __fmaf_rn((float)z, sD, -1.f) : 0.f;
-          const float py = a.H > 1 ? __fmaf_rn((float)y, sH, -1.f) : 0.f;
-          const float px = a.W > 1 ? __fmaf_rn((float)x, sW, -1.f) : 0.f;
-          if (a.ndim == 2) {
-            g0 = __fmaf_rn(-d, py, g0);
-            g1 = __fmaf_rn(-d, px, g1);
-          } else {
-            g0 = __fmaf_rn(-d, pz, g0);
-            g1 = __fmaf_rn(-d, py, g1);
-            g2 = __fmaf_rn(-d, px, g2);
-          }
-        }
-        if (++x == a.W) {
-          x = 0;
-          if (++y == a.H) { y = 0; ++z; }
-        }
+  if (BWD) soft_unit_G_write(a, item * a.units + unit, gacc, s_g);
+}
+
+// K5/K6 windowed: see the band-mode comment above.  Per-pair arithmetic
+// (a_j, block centres, the b clamp, paired reciprocals) is the full kernel's
+// with T = 16, so evaluated pairs give the same float32 values.
+//
+// A CTA takes G consecutive chunks of one item (the per-threshold tables are
+// built once per CTA).  Per chunk each warp compacts its own 512 voxels into
+// its own region of the record array, sorted by band (a counting sort with
+// match.any groups and shared atomics) and with every band padded to a
+// multiple of four records (zero-coefficient fillers), so the warp's four
+// voxel slots of eight lanes change band together; lane o of a slot holds
+// block (band + o).  Blocks of 16 floats in shared memory are read and
+// written as four 16-byte quads whose order is swizzled by the block index,
+// so the eight lanes of a slot (consecutive blocks) hit distinct banks.
+constexpr int BPAD = 2 * BVW;                        // records per warp iteration: bands are padded to it
+constexpr int BREG = CH / SNW + (BPAD - 1) * BAND_MAXBANDS + BPAD;   // per-warp record region: fillers, prefetch slack
+
+constexpr int BSTAGE = (CH / SNW) * 5;               // per-warp staging: 512 int8 + 512 float
+
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc, int src_bytes) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(gsrc), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+__device__ __forceinline__ int bq(int blk, int q) {   // float offset of quad q of block blk
+  return blk * BT + 4 * (q ^ ((blk >> 1) & 3));
+}
+
+template <bool BWD>
+#ifndef ECC_BAND_MINB
+#define ECC_BAND_MINB 2   // 128 registers: two voxels per lane in flight, no spills
+#endif
+__global__ void __launch_bounds__(SNT, ECC_BAND_MINB) ecc_soft_band_kernel(SoftArgs a) {
+  if (a.pd) {
+    if (!a.pd->factorized) return;
+    a.lam = a.pd->lam;
+    a.m = a.pd->center;
+    a.kscale = (float)(a.lam * LOG2E);
+  }
+  if (!band_ok(a)) return;   // the full kernel does this problem
+  const int nb = a.nb, nblk = (nb + BT - 1) / BT, nbands = nblk - NWB + 1, rowlen = nblk * BT;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  int2* rec = reinterpret_cast<int2*>(smem_raw);                    // [SNW][BREG] {fc bits, voxel | band << 12 | c bits}
+  float* red = reinterpret_cast<float*>(rec + SNW * BREG);          // [BSLOTS][rowlen] per-slot partials
+  float* natab = red + BSLOTS * rowlen;                             // [rowlen] -a_j
+  float* s_up = natab + rowlen;                                     // [rowlen] (backward)
+  __shared__ float s_edge[BAND_MAXBANDS + 1], s_koff[BAND_MAXBLK], s_bc[BAND_MAXBLK], s_above[BAND_MAXBLK];
+  __shared__ int s_cnt[SNW][BAND_MAXBANDS], s_csb[BAND_MAXBANDS];
+  __shared__ double s_g[SNW][4];
+
+  const int64_t item = blockIdx.x / a.units;
+  const int64_t unit = blockIdx.x % a.units;
+  const int64_t c0 = unit * a.G, c1 = min(c0 + a.G, a.chunks);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double ks = a.lam * LOG2E;
+
+  // ---- per-threshold factors and per-block parameters (once per CTA) -------
+  for (int j = threadIdx.x; j < rowlen; j += SNT) {
+    float av = 0.f;
+    if (j < nb) {
+      const int b0 = (j / BT) * BT, b1 = min(b0 + BT, nb) - 1;
+      av = (float)exp2(-ks * (a.taus[j] - 0.5 * (a.taus[b0] + a.taus[b1])));
+    }
+    const int q = bq(j / BT, (j % BT) >> 2) + (j & 3);
+    natab[q] = -av;   // negated: see pair_loop_fact2
+    s_up[q] = (BWD && j < nb) ? (float)a.up[item * nb + j] : 0.f;
+  }
+  for (int i = threadIdx.x; i < BSLOTS * rowlen; i += SNT) red[i] = 0.f;
+  if (threadIdx.x < nblk)
+    s_koff[threadIdx.x] = (float)(ks * (a.m - 0.5 * (a.taus[threadIdx.x * BT] + a.taus[min(threadIdx.x * BT + BT, nb) - 1])));
+  if (threadIdx.x <= BAND_MAXBANDS) {
+    // band b >= 1 starts where f - m >= tau_{16 b} - m + W; +inf past the last band
+    const int b = threadIdx.x;
+    s_edge[b] = (b >= 1 && b < nbands) ? (float)(a.taus[b * BT] - a.m + BAND_ZCUT / a.lam) : INFINITY;
+  }
+  if (threadIdx.x < BAND_MAXBANDS) s_csb[threadIdx.x] = 0;
+  __syncthreads();
+  float bcv = B_MAX;
+  bool prod = false;
+  if (ECC_SOFT_PAIR & (BWD ? 2 : 1)) {
+    bool okp = true;
+    if (threadIdx.x < nblk) {
+      float amax = 0.f, dmax = 0.f;
+#pragma unroll
+      for (int t = 0; t < BT; ++t) {
+        const int tp = (BT - 2 - 2 * (t >> 1)) + (t & 1);
+        const float x0 = -natab[bq(threadIdx.x, t >> 2) + (t & 3)], x1 = -natab[bq(threadIdx.x, tp >> 2) + (tp & 3)];
+        const float l0 = x0 > 0.f ? __log2f(x0) : 0.f, l1 = x1 > 0.f ? __log2f(x1) : 0.f;
+        amax = fmaxf(amax, fabsf(l0));
+        dmax = fmaxf(dmax, l0 + l1);
+      }
+      bcv = fminf(B_MAX, 0.5f * (126.f - dmax) - 1.f);
+      okp = bcv - amax >= 24.f;
+    }
+    prod = __syncthreads_and(okp) != 0;
+  }
+  if (threadIdx.x < nblk) s_bc[threadIdx.x] = prod ? bcv : B_MAX;
+  // (made visible by the first chunk's barrier)
+
+  const int g = lane / NWB, o = lane % NWB;
+  const int slot = warp * BVW + g;
+  float* myred = red + slot * rowlen;
+  int2* wrec = rec + warp * BREG;
+  f2_t nat2[BT / 2], up2[BT / 2], acc2[BT / 2];
+  float koff = 0.f, bc = B_MAX, csum = 0.f;
+  int curb = -1;
+  auto load_block = [&](int b) {
+    const int blk = b + o;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float4 av = *reinterpret_cast<const float4*>(natab + bq(blk, q));
+      nat2[2 * q] = f2_pack(av.x, av.y);
+      nat2[2 * q + 1] = f2_pack(av.z, av.w);
+      if (BWD) {
+        const float4 uv = *reinterpret_cast<const float4*>(s_up + bq(blk, q));
+        up2[2 * q] = f2_pack(uv.x, uv.y);
+        up2[2 * q + 1] = f2_pack(uv.z, uv.w);
       }
     }
-    double v0d = g0, v1d = g1, v2d = g2;
-    for (int o = 16; o; o >>= 1) {
-      v0d += __shfl_xor_sync(0xffffffffu, v0d, o);
-      v1d += __shfl_xor_sync(0xffffffffu, v1d, o);
-      v2d += __shfl_xor_sync(0xffffffffu, v2d, o);
+#pragma unroll
+    for (int i = 0; i < BT / 2; ++i) acc2[i] = 0ull;
+    koff = s_koff[blk];
+    bc = s_bc[blk];
+  };
+  auto flush = [&]() {
+    const int blk = curb + o;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float4* p = reinterpret_cast<float4*>(myred + bq(blk, q));
+      float4 v = *p;
+      float x0, x1, x2, x3;
+      f2_unpack(acc2[2 * q], x0, x1);
+      f2_unpack(acc2[2 * q + 1], x2, x3);
+      if (BWD) { v.x -= x0; v.y -= x1; v.z -= x2; v.w -= x3; }   // the packed backward accumulates -d_tau
+      else { v.x += x0; v.y += x1; v.z += x2; v.w += x3; }
+      *p = v;
     }
-    if (lane == 0) { s_g[warp][0] = v0d; s_g[warp][1] = v1d; s_g[warp][2] = v2d; }
-    __syncthreads();
-    if (threadIdx.x < 3) {
-      double sg = 0.0;
-      for (int w = 0; w < SNW; ++w) sg += s_g[w][threadIdx.x];
-      a.gpart[(item * a.chunks + chunk) * 4 + threadIdx.x] = sg;
+    if (!BWD && o == 0) atomicAdd(&s_csb[curb], (int)csum);
+    csum = 0.f;
+  };
+  if (!BWD) {
+#pragma unroll
+    for (int i = 0; i < BT / 2; ++i) up2[i] = 0ull;
+  }
+  const float lamf = (float)a.lam;
+  double gacc[3] = {0.0, 0.0, 0.0};
+  constexpr int CITER = CH / SNW / 32;
+  // The warp's next slice of coefficients and field values is fetched into
+  // its shared staging buffer with cp.async while it sorts and walks the
+  // current one (16-byte copies: needs 16-byte aligned slices).
+  const bool staged = (a.n % 16) == 0 && (((uintptr_t)a.c | (uintptr_t)a.fc) & 15) == 0;
+  int8_t* st_c = reinterpret_cast<int8_t*>(s_up + rowlen) + warp * BSTAGE;   // [512] coefficients
+  float* st_f = reinterpret_cast<float*>(st_c + CITER * 32);                  // [512] field values
+  auto stage_issue = [&](int64_t ch) {
+    const int w0s = warp * (CITER * 32);
+    const int nv = (int)min((int64_t)CITER * 32, max((int64_t)0, min((int64_t)CH, a.n - ch * CH) - w0s));
+    const int64_t vb = item * a.n + ch * CH + w0s;
+    const int off = 16 * lane;
+    const int cb = max(0, min(16, nv - off));
+    cp_async16(st_c + off, a.c + vb + (cb ? off : 0), cb);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int fo = off + 4 * q;
+      const int fb = 4 * max(0, min(4, nv - fo));
+      cp_async16(st_f + fo, a.fc + vb + (fb ? fo : 0), fb);
+    }
+    cp_async_commit();
+  };
+  if (staged) stage_issue(c0);
+  const float e1 = s_edge[1];
+  const float einv = nbands > 2 ? (float)(nbands - 2) / (s_edge[nbands - 1] - e1) : 0.f;
+
+  for (int64_t chunk = c0; chunk < c1; ++chunk) {
+    const int64_t v0 = chunk * CH;
+    const int nvox = (int)min((int64_t)CH, a.n - v0);
+    const int8_t* cg = a.c + item * a.n + v0;
+    const float* fg = a.fc + item * a.n + v0;
+    // ---- per-warp compaction to c != 0 voxels, sorted by band (stable) -----
+    const int w0 = warp * (CITER * 32), w1 = min(w0 + CITER * 32, nvox);
+    int kvr[CITER];     // band | c << 8  (c == 0: band field 0xFF)
+    float fvr[CITER];
+    if (staged) {
+      cp_async_wait_all();
+      __syncwarp();
+#pragma unroll
+      for (int it = 0; it < CITER; ++it) {
+        const int i = w0 + it * 32 + lane;
+        const int cv = i < w1 ? (int)st_c[it * 32 + lane] : 0;
+        fvr[it] = i < w1 ? st_f[it * 32 + lane] : 0.f;
+        kvr[it] = (cv << 8) | 0xFF;
+      }
+      __syncwarp();
+      if (chunk + 1 < c1) stage_issue(chunk + 1);   // overlaps this chunk's sort and window loop
+    } else {
+#pragma unroll
+      for (int it = 0; it < CITER; ++it) {
+        const int i = w0 + it * 32 + lane;
+        const int cv = i < w1 ? (int)cg[i] : 0;
+        fvr[it] = i < w1 ? fg[i] : 0.f;
+        kvr[it] = (cv << 8) | 0xFF;
+      }
+    }
+    if (lane < BAND_MAXBANDS) s_cnt[warp][lane] = 0;
+    __syncwarp();
+#pragma unroll
+    for (int it = 0; it < CITER; ++it) {
+      const float f = fvr[it];
+      if ((kvr[it] >> 8) != 0) {
+        // band guess for near-uniform thresholds, then fixed against the edges
+        int bb = 0;
+        if (f >= e1) {
+          const float gss = __fmul_rn(f - e1, einv);
+          bb = min(1 + (gss < (float)nbands ? (int)gss : nbands), nbands - 1);
+          // one step each way covers a guess off by one; exact otherwise
+          const float lo = s_edge[bb], hi = s_edge[bb + 1], lo1 = s_edge[bb - 1];
+          if (lo > f) {
+            --bb;
+            if (lo1 > f) { while (bb > 0 && s_edge[bb] > f) --bb; }
+          } else if (hi <= f) {
+            ++bb;
+            while (s_edge[bb + 1] <= f) ++bb;
+          }
+        }
+        kvr[it] = (kvr[it] & ~0xFF) | bb;
+      }
+      const unsigned peers = __match_any_sync(0xffffffffu, kvr[it] & 0xFF);
+      if ((kvr[it] >> 8) != 0 && lane == __ffs(peers) - 1) atomicAdd(&s_cnt[warp][kvr[it] & 0xFF], __popc(peers));
+    }
+    __syncwarp();
+    int nlist;   // records in this warp's region, fillers included
+    {
+      const int c = lane < nbands ? s_cnt[warp][lane] : 0;
+      const int cpad = (c + BPAD - 1) & ~(BPAD - 1);
+      int incl = cpad;
+#pragma unroll
+      for (int sh = 1; sh < 32; sh <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, sh);
+        if (lane >= sh) incl += y;
+      }
+      // fillers at the end of each band: zero coefficient, the band's index
+      for (int q = incl - cpad + c; q < incl; ++q) wrec[q] = make_int2(0, lane << 12);
+      __syncwarp();
+      if (lane < nbands) s_cnt[warp][lane] = incl - cpad;   // start of band `lane`
+      nlist = __shfl_sync(0xffffffffu, incl, 31);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int it = 0; it < CITER; ++it) {
+      const int i = w0 + it * 32 + lane;
+      const int kv = kvr[it], cv = kv >> 8, bb = kv & 0xFF;
+      const unsigned peers = __match_any_sync(0xffffffffu, bb);
+      const int leader = __ffs(peers) - 1;
+      int old = 0;
+      if (cv != 0 && lane == leader) old = atomicAdd(&s_cnt[warp][bb], __popc(peers));
+      const int base = __shfl_sync(0xffffffffu, old, leader);
+      if (cv != 0) {
+        const int k = base + __popc(peers & ((1u << lane) - 1u));
+        wrec[k] = make_int2(__float_as_int(fvr[it]), i | (bb << 12) | (int)(__float_as_uint((float)cv) & 0xFFFF0000u));
+      } else if (BWD && i < w1) {
+        a.dX[item * a.n + v0 + i] = 0.f;
+      }
+    }
+    __syncwarp();
+    if (chunk == c0) __syncthreads();   // the per-block tables of the prologue
+
+    // ---- window loop: the warp's four slots walk its list together ---------
+    // Slot g takes records kb + 2g and kb + 2g + 1 (one 16-byte load, the
+    // next pair prefetched; the region has slack for the overrun): two
+    // independent voxels per lane and iteration.
+    auto walk = [&](auto prodtag) {
+      constexpr bool PROD = decltype(prodtag)::value;
+      int4 r = *reinterpret_cast<const int4*>(wrec + 2 * g);
+      for (int kb = 0; kb < nlist; kb += BPAD) {
+        const int4 cur = r;
+        r = *reinterpret_cast<const int4*>(wrec + kb + BPAD + 2 * g);
+        const int b = (cur.y >> 12) & 0xF;   // uniform over the warp (bands padded to BPAD)
+        if (b != curb) {
+          if (curb >= 0) flush();
+          load_block(b);
+          curb = b;
+        }
+        const float cf0 = __uint_as_float((uint32_t)cur.y & 0xFFFF0000u);
+        const float cf1 = __uint_as_float((uint32_t)cur.w & 0xFFFF0000u);
+        if (!BWD) csum += cf0 + cf1;
+        const float kf0 = fminf(fmaxf(__fmaf_rn(a.kscale, __int_as_float(cur.x), koff), -bc), bc);
+        const float kf1 = fminf(fmaxf(__fmaf_rn(a.kscale, __int_as_float(cur.z), koff), -bc), bc);
+        float w0 = 0.f, w1 = 0.f;
+        if (PROD) {
+          pair_loop_prod<BWD, BT>(nat2, up2, acc2, ex2_approx(kf0), cf0, w0);
+          pair_loop_prod<BWD, BT>(nat2, up2, acc2, ex2_approx(kf1), cf1, w1);
+        } else {
+          pair_loop_fact2<BWD, BT>(nat2, up2, acc2, ex2_approx(kf0), cf0, w0);
+          pair_loop_fact2<BWD, BT>(nat2, up2, acc2, ex2_approx(kf1), cf1, w1);
+        }
+        if (BWD) {
+#pragma unroll
+          for (int sh = NWB / 2; sh; sh >>= 1) {
+            w0 += __shfl_xor_sync(0xffffffffu, w0, sh);
+            w1 += __shfl_xor_sync(0xffffffffu, w1, sh);
+          }
+          float* dxp = a.dX + item * a.n + v0;
+          if (o == 0 && cf0 != 0.f) dxp[cur.y & 0xfff] = -cf0 * (lamf * w0);
+          if (o == 1 && cf1 != 0.f) dxp[cur.w & 0xfff] = -cf1 * (lamf * w1);
+        }
+      }
+    };
+    if (prod) walk(std::true_type{});
+    else walk(std::false_type{});
+    // flushed per chunk: the block registers are then dead during the next
+    // chunk's compaction
+    if (curb >= 0) flush();
+    curb = -1;
+    if (BWD) {
+      __syncthreads();   // dX of this chunk is visible to the CTA
+      soft_chunk_G_acc(a, item, v0, nvox, gacc);
     }
   }
+  __syncthreads();
+
+  // ---- fixed-order reduction over the CTA's slots ----------------------------
+  if (!BWD && threadIdx.x < nblk) {
+    // block J lies above the window of every band b <= J - NWB: sigma = 1
+    int cs = 0;
+    for (int b = 0; b <= (int)threadIdx.x - NWB; ++b) cs += s_csb[b];
+    s_above[threadIdx.x] = (float)cs;
+  }
+  __syncthreads();
+  double* out = a.part + (item * a.units + unit) * nb;
+  for (int j = threadIdx.x; j < nb; j += SNT) {
+    const int q = bq(j / BT, (j % BT) >> 2) + (j & 3);
+    double sacc = BWD ? 0.0 : (double)s_above[j / BT];
+    for (int sl = 0; sl < BSLOTS; ++sl) sacc += (double)red[sl * rowlen + q];
+    out[j] = sacc;
+  }
+  if (BWD) soft_unit_G_write(a, item * a.units + unit, gacc, s_g);
+}
+
+static size_t band_smem(int nb) {
+  const size_t rowlen = (size_t)((nb + BT - 1) / BT) * BT;
+  return sizeof(int2) * SNW * BREG + sizeof(float) * ((size_t)BSLOTS + 2) * rowlen + (size_t)SNW * BSTAGE;
 }
 
 // K7: out[b][j] = scale_j * sum_c part[b][c][j] in a fixed order: stage 1
@@ -698,14 +1113,14 @@ static bool soft_attr_done(const void* kfn, size_t smem) {
 template <bool BWD>
 static int soft_launch(const int8_t* coeffs, const float* fc, const float* fclo, int ndim, const int64_t* dims, int64_t batch,
                        const double* taus, int64_t nbins, const ecc_soft_params* p, const double* up, float* dX,
-                       double* out_main, double* G, void* workspace, void* stream,
+                       double* out_main, double* G_out, void* workspace, void* stream,
                        const ecc_soft_params* pd = nullptr) {
   clear_error();
   int64_t d3[3];
   int rc = soft_dims(ndim, dims, d3);
   if (rc) return rc;
   if (!coeffs || !fc || !taus || !p || !out_main || !workspace) return set_error(ECC_EINVAL, "null pointer argument");
-  if (BWD && (!up || !dX || !G)) return set_error(ECC_EINVAL, "null pointer argument");
+  if (BWD && (!up || !dX || !G_out)) return set_error(ECC_EINVAL, "null pointer argument");
   if (batch < 1 || nbins < 1) return set_error(ECC_EINVAL, "empty soft problem");
   if (nbins > MAXB_PASS) return set_error(ECC_EINVAL, "soft path supports at most 1024 thresholds per call");
   if (!pd && !(p->lam > 0)) return set_error(ECC_EINVAL, "sharpness must be positive");
@@ -734,16 +1149,41 @@ static int soft_launch(const int8_t* coeffs, const float* fc, const float* fclo,
   a.gpart = a.part + (size_t)(batch * chunks) * (size_t)nbins;
   a.dX = dX;
   a.pd = pd;
+  a.band = 0;
   cudaStream_t s = (cudaStream_t)stream;
   // 16 thresholds per lane (~80 registers, 3 CTAs/SM): on 16 x 1024^2,
   // B = 256 the forward takes 522 vs 559 us and the backward 837 vs 868 us
   // compared with 32 per lane; ECC_SOFT_FWD_T / ECC_SOFT_BWD_T = 32 override
   const int tsel = variant_soft_t(BWD);
   const int T = (tsel == 8 && nbins <= 8 * 32) ? 8 : (tsel <= 16 && nbins <= 16 * 32) ? 16 : 32;
-  const int64_t grid = batch * chunks;
+  // G chunks per CTA: the per-CTA tables and partial rows are amortised
+  // over G chunks while keeping ~6 waves of 3 CTAs per SM
+  int64_t G = variant_soft_g();
+  if (G <= 0) G = std::max<int64_t>(1, std::min<int64_t>(16, batch * chunks / (148 * 3 * 6)));
+  G = std::min<int64_t>(G, chunks);
+  const int64_t units = (chunks + G - 1) / G;
+  a.G = G;
+  a.units = units;
+  const int64_t grid = batch * units;
   if (grid > 0x7fffffff) return set_error(ECC_EINVAL, "soft problem too large");
   // host parameters: the one mode they select; device parameters: both modes,
   // the kernel whose mode the device flag does not select exits at once
+  // band kernel alongside the full factorised one (each CTA of both decides
+  // band_ok identically; exactly one of them works)
+  const int nblk = (int)((nbins + BT - 1) / BT);
+  a.band = (T == BT && variant_soft_band() && nbins <= BAND_MAXB && nblk - NWB + 1 >= 2 && nblk - NWB + 1 <= BAND_MAXBANDS &&
+            (pd || p->factorized)) ? 1 : 0;
+  if (a.band) {
+    auto kfn = ecc_soft_band_kernel<BWD>;
+    const size_t smem = band_smem((int)nbins);
+    if (!soft_attr_done(reinterpret_cast<const void*>(kfn), smem)) {
+      cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(soft band)");
+    }
+    kfn<<<(unsigned)grid, SNT, smem, s>>>(a);
+    rc = check_launch(BWD ? "ecc_soft_band_kernel<bwd>" : "ecc_soft_band_kernel<fwd>");
+    if (rc) return rc;
+  }
   for (int mode = 0; mode < 2; ++mode) {
     const bool fact = mode == 0;
     if (!pd && fact != (p->factorized != 0)) continue;
@@ -760,11 +1200,11 @@ static int soft_launch(const int8_t* coeffs, const float* fc, const float* fclo,
     rc = check_launch(BWD ? "ecc_soft_kernel<bwd>" : "ecc_soft_kernel<fwd>");
     if (rc) return rc;
   }
-  const int groups = (int)(chunks < RGROUPS ? chunks : RGROUPS);
-  const int64_t per_group = (chunks + groups - 1) / groups;
+  const int groups = (int)(units < RGROUPS ? units : RGROUPS);
+  const int64_t per_group = (units + groups - 1) / groups;
   double* grp = a.gpart + (size_t)(batch * chunks) * 4;
   dim3 g1((unsigned)((nbins + 127) / 128), (unsigned)groups, (unsigned)batch);
-  ecc_soft_reduce1<<<g1, 128, 0, s>>>(a.part, chunks, (int)nbins, per_group, grp);
+  ecc_soft_reduce1<<<g1, 128, 0, s>>>(a.part, units, (int)nbins, per_group, grp);
   rc = check_launch("ecc_soft_reduce1");
   if (rc) return rc;
   dim3 g2((unsigned)((nbins + 127) / 128), (unsigned)batch);
@@ -772,7 +1212,7 @@ static int soft_launch(const int8_t* coeffs, const float* fc, const float* fclo,
   rc = check_launch("ecc_soft_reduce2");
   if (rc) return rc;
   if (BWD) {
-    ecc_soft_reduce_g<<<(unsigned)batch, 256, 0, s>>>(a.gpart, chunks, ndim, G);
+    ecc_soft_reduce_g<<<(unsigned)batch, 256, 0, s>>>(a.gpart, units, ndim, G_out);
     rc = check_launch("ecc_soft_reduce_g");
   }
   return rc;

@@ -113,6 +113,7 @@ def _oracle_case(rng, dims, B, lam, alpha, u):
 
 class TestOracleParity:
     @pytest.mark.parametrize("dims,B,lam", [((128, 96), 256, 50.0), ((24, 20, 16), 256, 50.0),
+                                           ((97, 83), 256, 50.0), ((19, 23, 17), 256, 50.0),   # band kernel, n % 16 != 0
                                            ((64, 64), 1024, 50.0), ((40, 40), 37, 1e4), ((50, 30), 7, 0.5)])
     def test_forward_backward(self, rng, dims, B, lam):
         alpha = 0.3
@@ -141,6 +142,60 @@ class TestOracleParity:
         a = E.soft_ecc(g, c, p).values
         b = E.soft_ecc(g, c, p).values
         assert a.tobytes() == b.tobytes()
+
+
+def _module_outputs(m, x, up):
+    xs = x.clone().requires_grad_(True)
+    m.zero_grad()
+    chi = m(xs)
+    (chi * up).sum().backward()
+    return [chi.detach().cpu().numpy(), xs.grad.cpu().numpy(), m.taus.grad.cpu().numpy(), m.v.grad.cpu().numpy(),
+            m.alpha.grad.cpu().numpy()]
+
+
+class TestBandKernel:
+    """The windowed soft kernels (ecc_soft.cu band mode: a 128-threshold window
+    per voxel, saturated pairs taken as sigma = 0 / 1 with error < 2^-24)
+    against the full kernels: same outputs to float32 rounding, over odd
+    sizes (direct loads instead of the staged cp.async slices), several
+    chunks per CTA, 2-D and 3-D."""
+
+    @pytest.mark.parametrize("shape,v", [((3, 97, 83), [1.0, 2.0]), ((6, 128, 160), [1.0, 2.0]),
+                                         ((2, 33, 31, 29), [1.0, 2.0, -0.5]), ((1, 64, 64, 64), [1.0, 2.0, -0.5])])
+    @pytest.mark.parametrize("g", [0, 1, 3])
+    def test_matches_full_kernels(self, rng, shape, v, g):
+        from paper_2510_20271_b200 import _lib
+
+        B, lam, alpha = 256, 50.0, 0.3
+        u = np.asarray(v) / np.linalg.norm(v)
+        span = alpha * np.abs(u).sum()
+        taus = np.linspace(-span, 1.0 + span, B + 1)[1:]
+        m = E.SoftECC(taus, v, alpha=alpha, lam=lam).cuda()
+        x = torch.from_numpy(rng.random(shape).astype(np.float32)).cuda()
+        up = torch.from_numpy(rng.uniform(0.5, 1.5, (shape[0], B))).cuda()
+        with _lib.variant(soft_band=0, soft_g=g):
+            full = _module_outputs(m, x, up)
+        with _lib.variant(soft_band=1, soft_g=g):
+            band = _module_outputs(m, x, up)
+        for name, a, b in zip(("chi", "dX", "dtau", "dv"), band, full):
+            assert normwise(a, b) <= 1e-5, name
+        assert abs(float(band[4]) - float(full[4])) <= 1e-5 * max(abs(float(full[4])), 1e-3)
+
+    def test_unsorted_thresholds_fall_back(self, rng):
+        """Learnable thresholds may leave sorted order: the band kernels then
+        step aside and the full ones run (band_ok)."""
+        B, lam, alpha = 256, 50.0, 0.3
+        v = np.array([1.0, 2.0])
+        u = v / np.linalg.norm(v)
+        taus = np.linspace(-0.5, 1.5, B)
+        perm = rng.permutation(B)
+        m = E.SoftECC(taus[perm], v, alpha=alpha, lam=lam).cuda()
+        x = rng.random((2, 48, 40)).astype(np.float32)
+        chi = m(torch.from_numpy(x).cuda()).detach().cpu().numpy()
+        for i in range(2):
+            xi = x[i].astype(np.float64)
+            c = oracle.coefficients(oracle.effective_field(xi, alpha, u))
+            assert normwise(chi[i], oracle.soft_forward(xi, c, lam, alpha, u, taus[perm])) <= TOL
 
 
 class TestModule:
