@@ -813,11 +813,19 @@ def bench_soft(args, dev, world, rank, dist_on=False):
     pairs = vox * B * 2                      # algorithmic (voxel, threshold) pairs, forward + backward
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     mufu_peak = 16 * sms * 1.965e9 * world   # MUFU.RCP lane-ops/s (15.9/clk/SM measured, tools/microbench)
-    # MUFU work actually issued: the kernels evaluate only c != 0 voxels; the
-    # forward takes one reciprocal per two pairs (paired denominators), the
-    # backward 7/8 per pair (1/8 as Newton steps on the FMA pipe); plus one
-    # ex2 per voxel and lane (T = 16)
-    mufu_ops = nz * vox * B * ((0.5 + 1.0 / 16.0) + (7.0 / 8.0 + 1.0 / 16.0))
+    # MUFU work actually issued: the kernels evaluate only c != 0 voxels, and
+    # with the band kernels only a window of `win` thresholds per voxel (the
+    # saturated pairs outside it are exact 0 / 1 to 2^-24); both passes take
+    # one reciprocal per two pairs (paired denominators) -- the full backward
+    # 7/8 per pair (1/8 as Newton steps on the FMA pipe); plus one ex2 per
+    # voxel and lane (T = 16)
+    from paper_2510_20271_b200.soft import band_window
+
+    win = band_window(taus, lam)
+    if win < B:
+        mufu_ops = nz * vox * win * 2 * (0.5 + 1.0 / 16.0)
+    else:
+        mufu_ops = nz * vox * B * ((0.5 + 1.0 / 16.0) + (7.0 / 8.0 + 1.0 / 16.0))
     return {"metric": "soft-ECC fwd+bwd voxels/s", "value": vox / (ms * 1e-3), "unit": "voxel/s",
             "ms_per_step": ms, "steps": steps, "parity": parity, "cpu_baseline": cpu, "e2e": e2e,
             "config": {"workload": "C3: batched 2D 128x1024x1024 f32, soft ECC fwd+bwd, learnable tau/u/alpha",
@@ -825,6 +833,7 @@ def bench_soft(args, dev, world, rank, dist_on=False):
             "roofline": {"bound": "sfu", "unit": "MUFU ops/s", "achieved": mufu_ops / (ms * 1e-3),
                          "peak": mufu_peak, "frac": mufu_ops / (ms * 1e-3) / mufu_peak,
                          "nonzero_fraction": nz, "algorithmic_pairs_per_s": pairs / (ms * 1e-3),
+                         "window_thresholds": win,
                          # one MUFU per (voxel, threshold) pair per pass bounds fwd+bwd at
                          # mufu_peak / (2 B) voxels/s; skipping c = 0 voxels and pairing reciprocals beat it
                          "survey_sfu_bound_voxel_s": mufu_peak / (2 * B),

@@ -706,6 +706,10 @@ __device__ __forceinline__ int bq(int blk, int q) {   // float offset of quad q 
 }
 
 template <bool BWD>
+#ifndef ECC_BAND_PAIR
+#define ECC_BAND_PAIR 3   // paired reciprocals in both band kernels (backward: 4.82 vs 5.05 ms on 128 x 1024^2;
+                          // with two voxels per lane in flight the longer chain no longer costs)
+#endif
 #ifndef ECC_BAND_MINB
 #define ECC_BAND_MINB 2   // 128 registers: two voxels per lane in flight, no spills
 #endif
@@ -756,7 +760,7 @@ __global__ void __launch_bounds__(SNT, ECC_BAND_MINB) ecc_soft_band_kernel(SoftA
   __syncthreads();
   float bcv = B_MAX;
   bool prod = false;
-  if (ECC_SOFT_PAIR & (BWD ? 2 : 1)) {
+  if (ECC_BAND_PAIR & (BWD ? 2 : 1)) {
     bool okp = true;
     if (threadIdx.x < nblk) {
       float amax = 0.f, dmax = 0.f;

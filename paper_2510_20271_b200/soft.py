@@ -129,6 +129,32 @@ def _block_halfwidth(taus) -> float:
     return max(0.5 * float(t[i:i + _TT].max() - t[i:i + _TT].min()) for i in range(0, t.size, _TT))
 
 
+# windowed ("band") kernels, ecc_soft.cu band_ok: 16-threshold blocks, an
+# 8-block window per voxel, at most 16 bands, saturation cut 24 ln 2
+_BAND_T, _BAND_NWB, _BAND_MAXB, _BAND_MAXBANDS = 16, 8, 368, 16
+_BAND_ZCUT = 24.0 * math.log(2.0)
+
+
+def band_window(taus, lam: float) -> int:
+    """Thresholds the soft kernels evaluate per voxel: the 128-threshold window
+    of the band kernels when their condition holds (sorted thresholds, every 7
+    blocks spanning more than 2 * 24 ln 2 / lam, factorised mode; the device
+    decides the same way), else all of them.  For reporting (bench.py)."""
+    t = np.asarray(taus.detach().cpu() if isinstance(taus, torch.Tensor) else taus, dtype=np.float64).ravel()
+    nb = t.size
+    nblk = -(-nb // _BAND_T)
+    nbands = nblk - _BAND_NWB + 1
+    if nb > _BAND_MAXB or nbands < 2 or nbands > _BAND_MAXBANDS or not np.all(t[:-1] <= t[1:]):
+        return nb
+    if lam * _LOG2E * _block_halfwidth(t) > _FACTOR_LIMIT:
+        return nb
+    w2 = 2.0 * _BAND_ZCUT / lam * (1.0 + 1e-3)
+    for b in range(nbands - 1):
+        if not t[(b + _BAND_NWB) * _BAND_T] - t[(b + 1) * _BAND_T] > w2:
+            return nb
+    return _BAND_NWB * _BAND_T
+
+
 def _params(lam: float, alpha: float, u, tau_lo: float, tau_hi: float, ndim: int, halfwidth: float | None = None
             ) -> _lib.SoftParams:
     p = _lib.SoftParams()
