@@ -191,7 +191,8 @@ int ecc_soft_backward(const int8_t *coeffs, const float *field_c, const float *f
  * largest half-width of the 32-threshold blocks, lam, *alpha, u[0..ndim)
  * (taus, u, alpha: device float64).  The _d entry points take that device
  * struct instead of a host one; they launch both sigmoid modes and the one
- * the device flag does not select exits at once, so field_lo is required. */
+ * the device flag does not select exits at once, so field_lo is required
+ * (ecc_soft_prepare_d writes it only when the flag selects the direct mode). */
 int ecc_soft_setup(const double *taus, int64_t nbins, const double *u, int ndim, const double *alpha, double lam,
                    ecc_soft_params *params_dev, void *stream);
 int ecc_soft_prepare_d(const void *x, int dtype, int ndim, const int64_t *dims, int64_t batch,

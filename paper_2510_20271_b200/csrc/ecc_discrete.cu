@@ -235,7 +235,10 @@ struct SoftPrepSink {
   int64_t D, H, W;
   const ecc_soft_params* pd = nullptr;   // device-resident parameters: the centre is read there
   __device__ void init(unsigned char*) {
-    if (pd) center = pd->center;
+    if (pd) {
+      center = pd->center;
+      if (pd->factorized) fclo = nullptr;   // only the direct mode reads the remainders
+    }
   }
   static size_t smem_bytes(int64_t) { return 0; }
   __device__ void begin_item(int64_t, int64_t) {}
@@ -767,7 +770,10 @@ template <typename T>
 __global__ void __launch_bounds__(256) soft_prep2d_kernel(EffSrc<T> src, double center, int8_t* __restrict__ coeffs,
                                                           float* __restrict__ fc, float* __restrict__ fclo) {
   src.init();
-  if (src.pd) center = src.pd->center;
+  if (src.pd) {
+    center = src.pd->center;
+    if (src.pd->factorized) fclo = nullptr;   // only the direct mode reads the remainders
+  }
   // 32 x 32 outputs per CTA (8 warps x 4 rows); the 34 x 34 effective-field
   // tile is loaded with all of a thread's global loads in flight at once
   constexpr int TH = PREP_TH, TW = 32, PWD = TW + 2, PHT = TH + 2, NE = PWD * PHT, PER = (NE + 255) / 256;
