@@ -92,10 +92,11 @@ def lib():
 # launchers never read the environment; for the development tools the legacy
 # ECC_B200_* variables are applied once, when the library is loaded.
 _VARIANT_DEFAULTS = {"f3": "default", "zunit": "0", "generic": "0", "soft_fwd_t": "16", "soft_bwd_t": "16",
-                     "soft_band": "1", "soft_g": "0"}
+                     "soft_band": "1", "soft_g": "0", "soft_prep": "0"}
 _VARIANT_ENV = {"f3": "ECC_B200_F3", "zunit": "ECC_B200_F3_ZUNIT", "generic": "ECC_B200_GENERIC",
                 "soft_fwd_t": "ECC_SOFT_FWD_T", "soft_bwd_t": "ECC_SOFT_BWD_T",
-                "soft_band": "ECC_SOFT_BAND", "soft_g": "ECC_SOFT_G"}
+                "soft_band": "ECC_SOFT_BAND", "soft_g": "ECC_SOFT_G",
+                "soft_prep": "ECC_SOFT_PREP"}
 
 
 def set_variant(key: str, value) -> None:
@@ -112,7 +113,7 @@ def _apply_env_variants() -> None:
 @contextmanager
 def variant(**kw):
     """Run a block with kernel variants switched (f3=..., zunit=..., generic=1,
-    soft_fwd_t=..., soft_bwd_t=..., soft_band=0/1, soft_g=chunks per CTA); the production defaults are restored after."""
+    soft_fwd_t=..., soft_bwd_t=..., soft_band=0/1, soft_g=chunks per CTA, soft_prep=1 (old 3-D prepare)); the production defaults are restored after."""
     for k, v in kw.items():
         set_variant(k, v)
     try:

@@ -8,6 +8,18 @@
 
 namespace ecc {
 
+
+// ---------------------------------------------------------------------------
+// cp.async (LDGSTS): global -> shared copies that bypass the registers;
+// src_bytes < the copy size zero-fills the rest (0: nothing is read).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc, int src_bytes) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(gsrc), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
 // ---------------------------------------------------------------------------
 // Lower-star Euler coefficient of one voxel from its 3x3x3 neighbourhood.
 //

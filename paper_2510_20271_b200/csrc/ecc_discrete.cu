@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <map>
 #include <mutex>
+#include <type_traits>
 #include <tuple>
 #include <stdlib.h>
 
@@ -856,6 +857,9 @@ soft_prep3d_kernel(EffSrc<T> src, SoftPrepSink sk, Geom g) {
     sry[k] = e / PW;
     srx[k] = e - sry[k] * PW;
   }
+  // the remainder output is selected once (uniform), not per voxel
+  auto run = [&](auto lotag) {
+  constexpr bool LO = decltype(lotag)::value;
   for (int64_t item = blockIdx.x; item < g.items; item += gridDim.x) {
     int64_t r = item;
     const int64_t tile_x = r % g.tiles_x; r /= g.tiles_x;
@@ -880,9 +884,11 @@ soft_prep3d_kernel(EffSrc<T> src, SoftPrepSink sk, Geom g) {
     }
     auto load_plane = [&](int64_t z, T (&buf)[LPT]) {
       const bool zin = z >= 0 && z < g.D;
+      const T* zp = xb + z * HW;
 #pragma unroll
-      for (int k = 0; k < LPT; ++k) buf[k] = (zin && ok[k]) ? xb[z * HW + off[k]] : T(0);
+      for (int k = 0; k < LPT; ++k) buf[k] = (zin && ok[k]) ? zp[off[k]] : T(0);
     };
+    // alpha = 0 needs no branch: v + 0 * dot == v (dot is finite)
     auto store_plane = [&](int64_t z, const T (&buf)[LPT]) {
       double* dst = planes[(int)((z + 4) & (NBUF - 1))];
       const bool zin = z >= 0 && z < g.D;
@@ -890,17 +896,11 @@ soft_prep3d_kernel(EffSrc<T> src, SoftPrepSink sk, Geom g) {
 #pragma unroll
       for (int k = 0; k < LPT; ++k) {
         const int e = threadIdx.x + k * NT;
-        if (e < PLANE) {
-          double v = nanv;
-          if (zin && ok[k]) {
-            v = (double)buf[k];
-            if (src.alpha != 0.0) {
-              const double dot = __fma_rn(p2[k], src.u2, __fma_rn(t0, src.u0, p1u1[k]));
-              v = __dadd_rn(v, __dmul_rn(src.alpha, dot));
-            }
-            v = __dadd_rn(v, 0.0);   // -0 -> +0 (coeff3_sgn's sign-bit compares; equal values either way)
-          }
-          dst[e] = v;
+        if (k < LPT - 1 || e < PLANE) {
+          const double dot = __fma_rn(p2[k], src.u2, __fma_rn(t0, src.u0, p1u1[k]));
+          // -0 -> +0 (coeff3_sgn's sign-bit compares; equal values either way)
+          const double v = __dadd_rn(__dadd_rn((double)buf[k], __dmul_rn(src.alpha, dot)), 0.0);
+          dst[e] = (zin && ok[k]) ? v : nanv;
         }
       }
     };
@@ -924,6 +924,15 @@ soft_prep3d_kernel(EffSrc<T> src, SoftPrepSink sk, Geom g) {
         for (int cc = 0; cc < 3; ++cc) win[pz + 1][rr][cc] = sp[(RY * wy + rr) * PW + tx + cc];
     }
     const int64_t xg = x0 + tx;
+    const int64_t yb = y0 + RY * wy;
+    // outputs of this thread: (z, yb + ry, xg); pointers advance by a plane
+    const int64_t i0 = ((n * g.D + zs) * g.H + yb) * g.W + xg;
+    int8_t* cp = sk.coeffs + i0;
+    float* fp = sk.fc + i0;
+    float* lp = LO ? sk.fclo + i0 : nullptr;
+    bool inb[RY];
+#pragma unroll
+    for (int ry = 0; ry < RY; ++ry) inb[ry] = xg < g.W && yb + ry < g.H;
     for (int64_t z = zs; z < ze; ++z) {
       T nxt[LPT];
       const bool more = (z + 2 <= ze);
@@ -939,26 +948,391 @@ soft_prep3d_kernel(EffSrc<T> src, SoftPrepSink sk, Geom g) {
         }
 #pragma unroll
       for (int ry = 0; ry < RY; ++ry) {
-        const int64_t yg = y0 + RY * wy + ry;
-        if (xg < g.W && yg < g.H) {
-          double nb[3][3][3];
+        double nb[3][3][3];
 #pragma unroll
-          for (int a = 0; a < 3; ++a)
+        for (int a = 0; a < 3; ++a)
 #pragma unroll
-            for (int b = 0; b < 3; ++b)
+          for (int b = 0; b < 3; ++b)
 #pragma unroll
-              for (int c = 0; c < 3; ++c) nb[a][b][c] = win[a][ry + b][c];
-          const int c = ECC_PREP_SGN ? coeff3_sgn(nb) : coeff3<double>(nb);
-          const int64_t i = ((n * g.D + z) * g.H + yg) * g.W + xg;
-          sk.coeffs[i] = (int8_t)c;
-          const double d = nb[1][1][1] - sk.center;
-          const float hi = (float)d;
-          sk.fc[i] = hi;
-          if (sk.fclo) sk.fclo[i] = (float)(d - (double)hi);
+            for (int c = 0; c < 3; ++c) nb[a][b][c] = win[a][ry + b][c];
+        const int c = ECC_PREP_SGN ? coeff3_sgn(nb) : coeff3<double>(nb);
+        const double d = nb[1][1][1] - sk.center;
+        const float hi = (float)d;
+        if (inb[ry]) {
+          cp[ry * g.W] = (int8_t)c;
+          fp[ry * g.W] = hi;
+          if (LO) lp[ry * g.W] = (float)(d - (double)hi);
         }
       }
+      cp += HW;
+      fp += HW;
+      if (LO) lp += HW;
       if (more) store_plane(z + 2, nxt);
       __syncthreads();
+    }
+  }
+  };
+  if (sk.fclo) run(std::true_type{});
+  else run(std::false_type{});
+}
+}  // namespace ecc
+
+namespace ecc {
+// ---------------------------------------------------------------------------
+// 3-D soft prepare, row-word formulation (C4; the default for float32 /
+// float64 grids).  One warp per work item: a tile of 30 rows x 28 columns
+// streamed over a z-chunk.  Lane l owns row y0 - 1 + l (lanes 0 and 31 are
+// halo rows: their words serve the neighbours, they write nothing) and walks
+// the 30 voxels x0 - 1 .. x0 + 28 of its row once per plane, comparing each
+// with its 13 "positive" neighbours (first non-zero offset component +1).
+// The sign of RN(q - p) is [q < p] exactly (a difference of distinct doubles
+// never rounds to zero; values are canonicalised, -0 -> +0), and a funnel
+// shift pushes it into a 32-bit word per direction (bit j = voxel x0 - 1 + j,
+// the two end voxels included).  The 13 "negative" relations are the
+// complements of the neighbours' positive ones -- [q <= p] = !(p < q) -- taken
+// from the lane above (SHFL), the previous plane's words and the shifted own
+// words, so each pair of voxels is compared once instead of twice.  The
+// lower-star coefficient c = 1 - E + S - C (coefficients.py:109-138) is then
+// evaluated bit-sliced on the 26 words -- squares and cubes are ANDs, the
+// count a carry-save adder tree -- 32 voxels per instruction, and spread to
+// bytes.  Out-of-grid positions hold +inf: never lower, and !(p < +inf) is
+// false, so the complements stay right.  A tile whose effective field holds a
+// non-finite value is redone voxel by voxel with the IEEE compares (coeff3's
+// NaN semantics, the generic sweep's result).
+// ---------------------------------------------------------------------------
+#ifndef ECC_RW_UNR
+#define ECC_RW_UNR 4   // unroll of the staging loops (rows): 1 / 2 / 4 / 8 measured 7.19 / 6.92 / 6.87 / 6.99 ms
+#endif
+#ifndef ECC_RW_LA
+#define ECC_RW_LA 5    // look-ahead of the plane walk's column reads: 1 / 2 / 3 / 5 measured 6.90 / 6.72 / 6.72 / 6.62 ms
+#endif
+#define ECC_RW_PRAGMA(x) _Pragma(#x)
+#define ECC_RW_PRAGMA2(n) ECC_RW_PRAGMA(unroll n)
+#define ECC_RW_UNROLL ECC_RW_PRAGMA2(ECC_RW_UNR)
+constexpr int RWR = 34;      // staged rows: y0 - 2 .. y0 + 31
+constexpr int RWC = 32;      // staged columns: x0 - 2 .. x0 + 29, one per lane
+constexpr int RWLD = 33;     // row stride in doubles (odd: lanes reading one column hit distinct banks)
+constexpr int RWOUT = 30;    // output rows per tile (lanes 1 .. 30)
+constexpr int RWX = 28;      // output columns per tile: x0 .. x0 + 27
+
+template <typename T>
+struct RwSmem {
+  double eff[2][RWR * RWLD];   // effective field of planes z (slot z & 1) and z + 1
+  T raw[RWR * RWC];            // the next plane's raw values (cp.async)
+  double p1u1[RWR];            // per staged row: crd(y) * u1
+  double q[RWR];               // per staged row of the plane being staged: fma(crd(z), u0, p1u1)
+};
+
+__device__ __forceinline__ void fa3(uint32_t a, uint32_t b, uint32_t c, uint32_t& s, uint32_t& cy) {
+  s = a ^ b ^ c;
+  cy = (a & b) | (c & (a ^ b));
+}
+__device__ __forceinline__ uint32_t spread4(uint32_t n) { return (n * 0x00204081u) & 0x01010101u; }
+
+template <typename T>
+__device__ __forceinline__ void cp_async_t(void* sdst, const T* gsrc, bool in) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(sdst);
+  if (sizeof(T) == 4)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(d), "l"(gsrc), "r"(in ? 4 : 0) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(gsrc), "r"(in ? 8 : 0) : "memory");
+}
+
+// Words: bit j of a lane's direction word is the voxel x0 - 1 + j of its row
+// (j = 0 .. 29: the 28 outputs and one halo voxel each side), so the shifted
+// reads of the negative relations are single shifts.
+template <typename T>
+__global__ void __launch_bounds__(32) soft_prep3d_rw_kernel(EffSrc<T> src, SoftPrepSink sk, int64_t batch,
+                                                            int64_t tiles_x, int64_t tiles_y, int64_t zc,
+                                                            int64_t zchunks) {
+  __shared__ __align__(16) RwSmem<T> S;
+  src.init();
+  sk.init(nullptr);
+  const int lane = threadIdx.x;
+  const int64_t D = sk.D, H = sk.H, W = sk.W, HW = H * W;
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  int64_t r = blockIdx.x;
+  const int64_t tile_x = r % tiles_x; r /= tiles_x;
+  const int64_t tile_y = r % tiles_y; r /= tiles_y;
+  const int64_t zchunk = r % zchunks; r /= zchunks;
+  const int64_t n = r;
+  if (n >= batch) return;
+  const int64_t x0 = tile_x * RWX, y0 = tile_y * RWOUT;
+  const int64_t zs = zchunk * zc, ze = min(zs + zc, D);
+  const T* xb = src.x + n * D * HW;
+  // tile and halo inside the grid in x and y: no per-value range checks
+  const bool inner = x0 >= 2 && x0 + RWC - 2 <= W && y0 >= 2 && y0 + RWR - 2 <= H;
+
+  const int64_t gx = x0 - 2 + lane;   // this lane's staged column
+  const bool cok = gx >= 0 && gx < W;
+  const double p2 = EffSrc<T>::crd(cok ? gx : 0, W, src.sW);
+  for (int row = lane; row < RWR; row += 32) {
+    const int64_t gy = y0 - 2 + row;
+    S.p1u1[row] = __dmul_rn(EffSrc<T>::crd(gy >= 0 && gy < H ? gy : 0, H, src.sH), src.u1);
+  }
+  __syncwarp();
+
+  auto issue = [&](int64_t zp) {   // cp.async plane zp's raw values (zero-filled outside the grid)
+    const bool zin = zp >= 0 && zp < D;
+    if (inner && zin) {
+      const T* rp = xb + zp * HW + (y0 - 2) * W + gx;
+ECC_RW_UNROLL
+      for (int row = 0; row < RWR; ++row, rp += W) cp_async_t(&S.raw[row * RWC + lane], rp, true);
+    } else {
+      const T* pl = xb + (zin ? zp : 0) * HW;
+ECC_RW_UNROLL
+      for (int row = 0; row < RWR; ++row) {
+        const int64_t gy = y0 - 2 + row;
+        const bool in = zin && cok && gy >= 0 && gy < H;
+        cp_async_t(&S.raw[row * RWC + lane], pl + (in ? gy * W + gx : 0), in);
+      }
+    }
+    cp_async_commit();
+  };
+  uint32_t badhi = 0;   // max of the exponent fields of the effective field: 0x7ff00000 = non-finite
+  auto convert = [&](int64_t zp) {   // raw -> effective field (the generic sweep's rounding sequence)
+    cp_async_wait_all();
+    const bool zin = zp >= 0 && zp < D;
+    const double t0 = EffSrc<T>::crd(zin ? zp : 0, D, src.sD);
+    for (int row = lane; row < RWR; row += 32) S.q[row] = __fma_rn(t0, src.u0, S.p1u1[row]);
+    __syncwarp();
+    double* dst = S.eff[(int)(zp & 1)];
+    if (inner && zin) {
+ECC_RW_UNROLL
+      for (int row = 0; row < RWR; ++row) {
+        const double dot = __fma_rn(p2, src.u2, S.q[row]);
+        const double v = __dadd_rn(__dadd_rn((double)S.raw[row * RWC + lane], __dmul_rn(src.alpha, dot)), 0.0);
+        badhi = max(badhi, (uint32_t)__double2hiint(v) & 0x7ff00000u);
+        dst[row * RWLD + lane] = v;
+      }
+    } else {
+ECC_RW_UNROLL
+      for (int row = 0; row < RWR; ++row) {
+        const int64_t gy = y0 - 2 + row;
+        const bool in = zin && cok && gy >= 0 && gy < H;
+        const double dot = __fma_rn(p2, src.u2, S.q[row]);
+        const double v = __dadd_rn(__dadd_rn((double)S.raw[row * RWC + lane], __dmul_rn(src.alpha, dot)), 0.0);
+        if (in) badhi = max(badhi, (uint32_t)__double2hiint(v) & 0x7ff00000u);
+        dst[row * RWLD + lane] = in ? v : inf;   // outside the grid: never lower
+      }
+    }
+    __syncwarp();
+  };
+
+  // one plane walk: the 13 positive-direction words of this lane's row, plus
+  // the centred field stores of output planes
+  const int sr = lane + 1;
+  const int64_t gyl = y0 - 1 + lane;
+  const bool rowout = lane >= 1 && lane <= RWOUT && gyl < H;
+  const bool fullx = x0 + RWX <= W && (W & 3) == 0;
+  auto walk = [&](int64_t z, uint32_t (&Wd)[13], bool out, int64_t obase, auto lotag) {
+    constexpr bool LO = decltype(lotag)::value;
+    const double* a = S.eff[(int)(z & 1)] + sr * RWLD;
+    const double* b = S.eff[(int)(z & 1)] + (sr + 1) * RWLD;
+    const double* c0 = S.eff[(int)((z + 1) & 1)] + (sr - 1) * RWLD;
+    const double* c1 = S.eff[(int)((z + 1) & 1)] + sr * RWLD;
+    const double* c2 = S.eff[(int)((z + 1) & 1)] + (sr + 1) * RWLD;
+    double av[RWC], bv[RWC], c0v[RWC], c1v[RWC], c2v[RWC];
+    // columns are read ECC_RW_LA steps ahead of their first use
+#pragma unroll
+    for (int j = RWC - 1; j >= RWC - 1 - ECC_RW_LA; --j) {
+      av[j] = a[j]; bv[j] = b[j]; c0v[j] = c0[j]; c1v[j] = c1[j]; c2v[j] = c2[j];
+    }
+    float f4[4], l4[4];
+    const bool wr = out && rowout;
+#pragma unroll
+    for (int sc = RWC - 2; sc >= 1; --sc) {   // voxel x0 - 2 + sc, bit sc - 1
+      if (sc - ECC_RW_LA >= 0) {
+        const int j = sc - ECC_RW_LA;
+        av[j] = a[j]; bv[j] = b[j]; c0v[j] = c0[j]; c1v[j] = c1[j]; c2v[j] = c2[j];
+      }
+      const double p = av[sc];
+      const double qv[13] = {av[sc + 1], bv[sc - 1], bv[sc], bv[sc + 1], c0v[sc - 1], c0v[sc], c0v[sc + 1],
+                             c1v[sc - 1], c1v[sc], c1v[sc + 1], c2v[sc - 1], c2v[sc], c2v[sc + 1]};
+#pragma unroll
+      for (int d = 0; d < 13; ++d) {
+        const uint32_t h = (uint32_t)__double2hiint(__dsub_rn(qv[d], p));   // bit 31 = [q < p]
+        Wd[d] = __funnelshift_l(h, Wd[d], 1);
+      }
+      if (sc >= 2 && sc <= RWX + 1) {
+        const int i = sc - 2;   // voxel x0 + i
+        const double dd = p - sk.center;
+        f4[i & 3] = (float)dd;
+        if (LO) l4[i & 3] = (float)(dd - (double)f4[i & 3]);
+        if ((i & 3) == 0 && wr) {
+          float* fp = sk.fc + obase + i;
+          float* lp = LO ? sk.fclo + obase + i : nullptr;
+          if (fullx) {
+            *reinterpret_cast<float4*>(fp) = make_float4(f4[0], f4[1], f4[2], f4[3]);
+            if (LO) *reinterpret_cast<float4*>(lp) = make_float4(l4[0], l4[1], l4[2], l4[3]);
+          } else {
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+              if (x0 + i + t < W) {
+                fp[t] = f4[t];
+                if (LO) lp[t] = l4[t];
+              }
+          }
+        }
+      }
+    }
+  };
+
+  auto tile = [&](auto lotag) {
+    // prologue: planes zs - 1 and zs staged; the walk of plane zs - 1 gives
+    // the previous-plane words
+    issue(zs - 1);
+    convert(zs - 1);
+    issue(zs);
+    convert(zs);
+    issue(zs + 1);
+    uint32_t Wd[13], Pz[9];
+    walk(zs - 1, Wd, false, 0, lotag);
+#pragma unroll
+    for (int d = 0; d < 9; ++d) Pz[d] = Wd[4 + d];
+    int64_t obase = ((n * D + zs) * H + gyl) * W + x0;
+    for (int64_t z = zs; z < ze; ++z, obase += HW) {
+      // planes z, z + 1 staged (z + 1 goes into the slot of z - 1, done with)
+      convert(z + 1);
+      if (z + 2 <= ze) issue(z + 2);
+      walk(z, Wd, true, obase, lotag);
+      // ---- negative relations from the neighbours' positive ones ----------
+      // lane above (row r - 1), this plane: directions (0, +1, dx)
+      const uint32_t u1 = __shfl_up_sync(0xffffffffu, Wd[1], 1), u2 = __shfl_up_sync(0xffffffffu, Wd[2], 1),
+                     u3 = __shfl_up_sync(0xffffffffu, Wd[3], 1);
+      // previous plane: rows r + 1 (dy = -1), r (dy = 0), r - 1 (dy = +1)
+      uint32_t pd[9];
+#pragma unroll
+      for (int t = 0; t < 3; ++t) {
+        pd[t] = __shfl_down_sync(0xffffffffu, Pz[t], 1);        // (1, -1, dx) of row r + 1
+        pd[3 + t] = Pz[3 + t];                                  // (1,  0, dx) of row r
+        pd[6 + t] = __shfl_up_sync(0xffffffffu, Pz[6 + t], 1);  // (1, +1, dx) of row r - 1
+      }
+      // output bit i (voxel x0 + i) reads the source voxel x0 + i - dx, bit i - dx + 1
+      auto neg = [](uint32_t w, int dx) -> uint32_t { return ~(w >> (1 - dx)); };
+      // L[dz][dy][dx] (offset + 1): the neighbour precedes p; bit i = voxel x0 + i
+      uint32_t L[3][3][3];
+      L[1][1][2] = Wd[0] >> 1;
+      L[1][1][0] = neg(Wd[0], +1);
+#pragma unroll
+      for (int dx = -1; dx <= 1; ++dx) {
+        L[1][2][dx + 1] = Wd[2 + dx] >> 1;
+        const uint32_t uw = dx < 0 ? u1 : dx == 0 ? u2 : u3;
+        L[1][0][1 - dx] = neg(uw, dx);
+      }
+#pragma unroll
+      for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+        for (int dx = -1; dx <= 1; ++dx) {
+          const int d = 3 * (dy + 1) + (dx + 1);
+          L[2][dy + 1][dx + 1] = Wd[4 + d] >> 1;
+          L[0][1 - dy][1 - dx] = neg(pd[d], dx);
+        }
+      // ---- bit-sliced lower-star count: c + 13 = #squares + #(not edges) + #(not cubes)
+      uint32_t in[26];
+      int k = 0;
+      uint32_t sxy[2][2], sxz[2][2], syz[2][2];
+#pragma unroll
+      for (int a1 = 0; a1 < 2; ++a1)
+#pragma unroll
+        for (int b1 = 0; b1 < 2; ++b1) {
+          const int A = 2 * a1, B = 2 * b1;
+          sxy[a1][b1] = L[1][A][1] & L[1][1][B] & L[1][A][B];
+          sxz[a1][b1] = L[A][1][1] & L[1][1][B] & L[A][1][B];
+          syz[a1][b1] = L[A][1][1] & L[1][B][1] & L[A][B][1];
+          in[k++] = sxy[a1][b1];
+          in[k++] = sxz[a1][b1];
+          in[k++] = syz[a1][b1];
+        }
+      in[k++] = ~L[1][1][0]; in[k++] = ~L[1][1][2]; in[k++] = ~L[1][0][1];
+      in[k++] = ~L[1][2][1]; in[k++] = ~L[0][1][1]; in[k++] = ~L[2][1][1];
+#pragma unroll
+      for (int zz = 0; zz < 2; ++zz)
+#pragma unroll
+        for (int yy = 0; yy < 2; ++yy)
+#pragma unroll
+          for (int xx = 0; xx < 2; ++xx)
+            in[k++] = ~(sxy[yy][xx] & sxz[zz][xx] & syz[zz][yy] & L[2 * zz][2 * yy][2 * xx]);
+      uint32_t s8[8], k8[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) fa3(in[3 * t], in[3 * t + 1], in[3 * t + 2], s8[t], k8[t]);
+      uint32_t t0, m0, t1, m1, t2, m2, u0, n0;
+      fa3(s8[0], s8[1], s8[2], t0, m0);
+      fa3(s8[3], s8[4], s8[5], t1, m1);
+      fa3(s8[6], s8[7], in[24], t2, m2);
+      fa3(t0, t1, t2, u0, n0);
+      const uint32_t b0 = u0 ^ in[25], n1 = u0 & in[25];
+      uint32_t a0, e0, a1, e1, a2, e2, a3, e3, bb, f0, b1, f1;
+      fa3(k8[0], k8[1], k8[2], a0, e0);
+      fa3(k8[3], k8[4], k8[5], a1, e1);
+      fa3(k8[6], k8[7], m0, a2, e2);
+      fa3(m1, m2, n0, a3, e3);
+      fa3(a0, a1, a2, bb, f0);
+      fa3(bb, a3, n1, b1, f1);
+      uint32_t g0, h0, g1, h1, b3, b4;
+      fa3(e0, e1, e2, g0, h0);
+      fa3(e3, f0, f1, g1, h1);
+      const uint32_t b2 = g0 ^ g1, h2 = g0 & g1;
+      fa3(h0, h1, h2, b3, b4);
+      // c = (c + 13) - 13: add 19 (10011b) modulo 32, 5-bit two's complement
+      const uint32_t c0 = b0;
+      const uint32_t s0 = ~b0;
+      const uint32_t s1 = ~(b1 ^ c0), c1 = b1 | c0;
+      const uint32_t s2 = b2 ^ c1, c2 = b2 & c1;
+      const uint32_t s3 = b3 ^ c2, c3 = b3 & c2;
+      const uint32_t s4 = ~(b4 ^ c3);
+      if (rowout) {
+        int8_t* cp = sk.coeffs + obase;
+#pragma unroll
+        for (int g = 0; g < RWX / 4; ++g) {
+          const int sh = 4 * g;
+          const uint32_t wv = spread4((s0 >> sh) & 15u) | (spread4((s1 >> sh) & 15u) << 1) |
+                              (spread4((s2 >> sh) & 15u) << 2) | (spread4((s3 >> sh) & 15u) << 3) |
+                              (spread4((s4 >> sh) & 15u) * 0xF0u);
+          if (fullx) {
+            reinterpret_cast<uint32_t*>(cp)[g] = wv;
+          } else {
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+              if (x0 + 4 * g + t < W) cp[4 * g + t] = (int8_t)(wv >> (8 * t));
+          }
+        }
+      }
+#pragma unroll
+      for (int d = 0; d < 9; ++d) Pz[d] = Wd[4 + d];
+    }
+  };
+  if (sk.fclo) tile(std::true_type{});
+  else tile(std::false_type{});
+
+  // a non-finite effective field: redo the tile voxel by voxel with the IEEE
+  // compares (out-of-grid neighbours NaN, as coeff3 expects)
+  if (__any_sync(0xffffffffu, badhi == 0x7ff00000u)) {
+    const double nanv = __longlong_as_double(0x7ff8000000000000ll);
+    const int64_t xg = x0 + lane;
+    if (lane < RWX && xg < W) {
+      for (int64_t z = zs; z < ze; ++z)
+        for (int ry = 0; ry < RWOUT; ++ry) {
+          const int64_t yg = y0 + ry;
+          if (yg >= H) break;
+          double nb[3][3][3];
+#pragma unroll
+          for (int a1 = 0; a1 < 3; ++a1)
+#pragma unroll
+            for (int b1 = 0; b1 < 3; ++b1)
+#pragma unroll
+              for (int c1 = 0; c1 < 3; ++c1) {
+                const int64_t zz = z + a1 - 1, yy = yg + b1 - 1, xx = xg + c1 - 1;
+                const bool in = zz >= 0 && zz < D && yy >= 0 && yy < H && xx >= 0 && xx < W;
+                nb[a1][b1][c1] = in ? src.at(n * D * HW + (zz * H + yy) * W + xx, zz, yy, xx) : nanv;
+              }
+          const int64_t i = ((n * D + z) * H + yg) * W + xg;
+          sk.coeffs[i] = (int8_t)coeff3<double>(nb);
+          const double dd = nb[1][1][1] - sk.center;
+          const float hf = (float)dd;
+          sk.fc[i] = hf;
+          if (sk.fclo) sk.fclo[i] = (float)(dd - (double)hf);
+        }
     }
   }
 }
@@ -993,6 +1367,29 @@ static int soft_prepare(const void* x, int dtype, int ndim, const int64_t* dims,
     return check_launch("soft_prep2d_kernel");
   }
 generic:
+  if (ndim == 3 && !variant_generic() && !variant_soft_prep_old() && (dtype == ECC_DTYPE_F32 || dtype == ECC_DTYPE_F64) &&
+      d3[1] < (1ll << 30) && d3[2] < (1ll << 30)) {
+    // row-word kernel: one warp per 30 x 28 tile and z-chunk; the chunk is
+    // shortened until there are ~4 waves of 9 resident warps per SM
+    const int64_t tiles_x = (d3[2] + RWX - 1) / RWX, tiles_y = (d3[1] + RWOUT - 1) / RWOUT;
+    const int64_t tiles = tiles_x * tiles_y * batch;
+    int64_t zc = 64;
+    while (zc > 8 && tiles * ((d3[0] + zc - 1) / zc) < (int64_t)num_sms() * 9 * 4) zc >>= 1;
+    if (zc > d3[0]) zc = d3[0];
+    const int64_t zchunks = (d3[0] + zc - 1) / zc;
+    const int64_t grid = tiles * zchunks;
+    if (grid > 0x7fffffff) return set_error(ECC_EINVAL, "grid too large for the 3-D prepare");
+    if (dtype == ECC_DTYPE_F32) {
+      EffSrc<float> src{(const float*)x, p->alpha, p->u[0], p->u[1], p->u[2], d3[0], d3[1], d3[2], ndim,
+                        coord_scale(d3[0]), coord_scale(d3[1]), coord_scale(d3[2]), pd};
+      soft_prep3d_rw_kernel<float><<<(unsigned)grid, 32, 0, s>>>(src, sk, batch, tiles_x, tiles_y, zc, zchunks);
+    } else {
+      EffSrc<double> src{(const double*)x, p->alpha, p->u[0], p->u[1], p->u[2], d3[0], d3[1], d3[2], ndim,
+                         coord_scale(d3[0]), coord_scale(d3[1]), coord_scale(d3[2]), pd};
+      soft_prep3d_rw_kernel<double><<<(unsigned)grid, 32, 0, s>>>(src, sk, batch, tiles_x, tiles_y, zc, zchunks);
+    }
+    return check_launch("soft_prep3d_rw_kernel");
+  }
   if (ndim == 3 && !variant_generic() && (dtype == ECC_DTYPE_F32 || dtype == ECC_DTYPE_F64)) {
     int occ = 0;
     const void* kfn = dtype == ECC_DTYPE_F32 ? (const void*)soft_prep3d_kernel<float>

@@ -26,13 +26,14 @@ int set_cuda_error(cudaError_t e, const char* what) {
 }
 void clear_error() { g_err[0] = 0; }
 
-static std::atomic<int> g_f3{0}, g_zunit{0}, g_generic{0}, g_soft_fwd_t{16}, g_soft_bwd_t{16}, g_soft_band{1}, g_soft_g{0};
+static std::atomic<int> g_f3{0}, g_zunit{0}, g_generic{0}, g_soft_fwd_t{16}, g_soft_bwd_t{16}, g_soft_band{1}, g_soft_g{0}, g_soft_prep{0};
 int variant_f3() { return g_f3.load(std::memory_order_relaxed); }
 int variant_zunit() { return g_zunit.load(std::memory_order_relaxed); }
 bool variant_generic() { return g_generic.load(std::memory_order_relaxed) != 0; }
 int variant_soft_t(bool bwd) { return (bwd ? g_soft_bwd_t : g_soft_fwd_t).load(std::memory_order_relaxed); }
 bool variant_soft_band() { return g_soft_band.load(std::memory_order_relaxed) != 0; }
 int variant_soft_g() { return g_soft_g.load(std::memory_order_relaxed); }
+bool variant_soft_prep_old() { return g_soft_prep.load(std::memory_order_relaxed) != 0; }
 
 // largest float32 <= t (round toward -inf), the t32 of DESIGN.md
 static float round_down_f32(double t) {
@@ -291,6 +292,7 @@ extern "C" int ecc_set_variant(const char* key, const char* value) {
   else if (!strcmp(key, "soft_bwd_t")) g_soft_bwd_t.store(v);
   else if (!strcmp(key, "soft_band")) g_soft_band.store(v != 0);
   else if (!strcmp(key, "soft_g")) g_soft_g.store(v > 0 ? v : 0);
+  else if (!strcmp(key, "soft_prep")) g_soft_prep.store(v != 0);
   else return set_error(ECC_EINVAL, "unknown variant key");
   return ECC_OK;
 }

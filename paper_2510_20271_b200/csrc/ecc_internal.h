@@ -34,4 +34,5 @@ bool variant_generic();    // route everything through the generic sweep
 int variant_soft_t(bool bwd);   // thresholds per lane of the soft kernels (8 / 16 / 32)
 bool variant_soft_band();       // windowed (band-sorted) soft kernels when the thresholds allow
 int variant_soft_g();           // chunks per soft CTA, 0: automatic
+bool variant_soft_prep_old();   // 3-D soft prepare: the per-voxel tile kernel instead of the row-word one
 }  // namespace ecc

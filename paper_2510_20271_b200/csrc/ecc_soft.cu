@@ -694,12 +694,6 @@ constexpr int BREG = CH / SNW + (BPAD - 1) * BAND_MAXBANDS + BPAD;   // per-warp
 
 constexpr int BSTAGE = (CH / SNW) * 5;               // per-warp staging: 512 int8 + 512 float
 
-__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc, int src_bytes) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(sdst);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(gsrc), "r"(src_bytes) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
 __device__ __forceinline__ int bq(int blk, int q) {   // float offset of quad q of block blk
   return blk * BT + 4 * (q ^ ((blk >> 1) & 3));

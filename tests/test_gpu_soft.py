@@ -387,3 +387,35 @@ class TestPrepare3D:
             xi = x[0].astype(np.float64)
             want = oracle.coefficients(oracle.effective_field(xi, alpha, u))
             assert np.array_equal(c1[0].cpu().numpy(), want), (dhw, dtype, alpha)
+
+    @pytest.mark.parametrize("dhw", [(33, 64, 70), (64, 61, 96), (9, 95, 33)])
+    def test_row_word_kernel_vs_tile_kernel(self, rng, dhw):
+        """The row-word prepare (default) against the per-voxel tile kernel
+        (soft_prep=1) on several tiles, chunks and ragged edges, with ties."""
+        u = E.reparametrize_direction([1.0, 2.0, -0.5])
+        for dtype, alpha in ((np.float32, 0.3), (np.float64, 0.25), (np.float32, 0.0)):
+            x = rng.random((2,) + dhw).astype(dtype)
+            x[:, :, ::3, :] = np.round(x[:, :, ::3, :] * 8) / 8
+            p = E.soft._params(50.0, alpha, u, -0.5, 1.5, 3, 0.01)
+            t = torch.from_numpy(x).cuda()
+            c1, (f1, _) = E.soft.soft_prepare_device(t, dhw, 2, p)
+            with E._lib.variant(soft_prep=1):
+                c2, (f2, _) = E.soft.soft_prepare_device(t, dhw, 2, p)
+            assert torch.equal(c1, c2) and torch.equal(f1, f2), (dhw, dtype, alpha)
+
+    def test_nonfinite_tiles_fall_back(self, rng):
+        """A non-finite effective field: the tile is redone with the IEEE
+        compares, matching the generic sweep bit for bit."""
+        dhw = (12, 40, 70)
+        x = rng.random((1,) + dhw).astype(np.float32)
+        x[0, 5, 7, 9] = np.nan
+        x[0, 11, 39, 69] = np.inf
+        x[0, 0, 0, 40] = -np.inf
+        u = E.reparametrize_direction([1.0, 2.0, -0.5])
+        p = E.soft._params(50.0, 0.3, u, -0.5, 1.5, 3, 0.01)
+        t = torch.from_numpy(x).cuda()
+        c1, (f1, _) = E.soft.soft_prepare_device(t, dhw, 1, p)
+        with E._lib.variant(generic=1):
+            c2, (f2, _) = E.soft.soft_prepare_device(t, dhw, 1, p)
+        assert torch.equal(c1, c2)
+        assert torch.equal(f1.view(torch.int32), f2.view(torch.int32))
