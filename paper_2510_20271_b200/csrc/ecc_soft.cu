@@ -314,15 +314,14 @@ __device__ __forceinline__ void pair_loop_direct(const double* __restrict__ kt, 
 }
 
 
-// G = sum_p c_p w_p pos_p = -sum_p dX_p pos_p.  soft_chunk_G_acc adds one
-// chunk (dX was just written by this CTA; zero-coefficient voxels hold 0):
-// each thread takes a contiguous run of voxels and walks their coordinates.
+// G = sum_p c_p w_p pos_p = -sum_p dX_p pos_p.  soft_run_G_acc adds the
+// voxels [i0, i1) of a chunk (their dX just written by this CTA or warp;
+// zero-coefficient voxels hold 0), walking their coordinates;
+// soft_chunk_G_acc gives each thread a contiguous run of the chunk.
 // soft_unit_G_write reduces the per-thread sums of the CTA's chunks in a
 // fixed order.
-__device__ __forceinline__ void soft_chunk_G_acc(const SoftArgs& a, int64_t item, int64_t v0, int nvox,
-                                                 double (&gacc)[3]) {
-  const int per = (CH + SNT - 1) / SNT;
-  const int i0 = threadIdx.x * per, i1 = min(i0 + per, nvox);
+__device__ __forceinline__ void soft_run_G_acc(const SoftArgs& a, int64_t item, int64_t v0, int i0, int i1,
+                                               double (&gacc)[3]) {
   float g0 = 0.f, g1 = 0.f, g2 = 0.f;
   if (i0 < i1) {
     const float sH = a.H > 1 ? (float)(2.0 / (double)(a.H - 1)) : 0.f;
@@ -355,6 +354,12 @@ __device__ __forceinline__ void soft_chunk_G_acc(const SoftArgs& a, int64_t item
   gacc[0] += g0;
   gacc[1] += g1;
   gacc[2] += g2;
+}
+__device__ __forceinline__ void soft_chunk_G_acc(const SoftArgs& a, int64_t item, int64_t v0, int nvox,
+                                                 double (&gacc)[3]) {
+  const int per = (CH + SNT - 1) / SNT;
+  const int i0 = threadIdx.x * per;
+  soft_run_G_acc(a, item, v0, i0, min(i0 + per, nvox), gacc);
 }
 
 __device__ __forceinline__ void soft_unit_G_write(const SoftArgs& a, int64_t slotidx, const double (&gacc)[3],
@@ -704,6 +709,12 @@ template <bool BWD>
 #define ECC_BAND_PAIR 3   // paired reciprocals in both band kernels (backward: 4.82 vs 5.05 ms on 128 x 1024^2;
                           // with two voxels per lane in flight the longer chain no longer costs)
 #endif
+#ifndef ECC_BAND_DEFER
+#define ECC_BAND_DEFER 1   // deferred w reduction (reduce-scatter over 8 voxels): backward 4.41 vs 4.99 ms (128 x 1024^2)
+#endif
+#ifndef ECC_BAND_WARPG
+#define ECC_BAND_WARPG 0   // G per warp slice without the CTA barrier: measured slower (5.28 vs 4.41 ms)
+#endif
 #ifndef ECC_BAND_MINB
 #define ECC_BAND_MINB 2   // 128 registers: two voxels per lane in flight, no spills
 #endif
@@ -947,7 +958,9 @@ __global__ void __launch_bounds__(SNT, ECC_BAND_MINB) ecc_soft_band_kernel(SoftA
     auto walk = [&](auto prodtag) {
       constexpr bool PROD = decltype(prodtag)::value;
       int4 r = *reinterpret_cast<const int4*>(wrec + 2 * g);
-      for (int kb = 0; kb < nlist; kb += BPAD) {
+      // one warp iteration: records kb + 2g, kb + 2g + 1 of each slot; w0 / w1
+      // are this lane's partial w of the two voxels (backward)
+      auto iter = [&](int kb, float& w0, float& w1) {
         const int4 cur = r;
         r = *reinterpret_cast<const int4*>(wrec + kb + BPAD + 2 * g);
         const int b = (cur.y >> 12) & 0xF;   // uniform over the warp (bands padded to BPAD)
@@ -961,7 +974,6 @@ __global__ void __launch_bounds__(SNT, ECC_BAND_MINB) ecc_soft_band_kernel(SoftA
         if (!BWD) csum += cf0 + cf1;
         const float kf0 = fminf(fmaxf(__fmaf_rn(a.kscale, __int_as_float(cur.x), koff), -bc), bc);
         const float kf1 = fminf(fmaxf(__fmaf_rn(a.kscale, __int_as_float(cur.z), koff), -bc), bc);
-        float w0 = 0.f, w1 = 0.f;
         if (PROD) {
           pair_loop_prod<BWD, BT>(nat2, up2, acc2, ex2_approx(kf0), cf0, w0);
           pair_loop_prod<BWD, BT>(nat2, up2, acc2, ex2_approx(kf1), cf1, w1);
@@ -969,15 +981,54 @@ __global__ void __launch_bounds__(SNT, ECC_BAND_MINB) ecc_soft_band_kernel(SoftA
           pair_loop_fact2<BWD, BT>(nat2, up2, acc2, ex2_approx(kf0), cf0, w0);
           pair_loop_fact2<BWD, BT>(nat2, up2, acc2, ex2_approx(kf1), cf1, w1);
         }
-        if (BWD) {
+      };
+      if (!BWD) {
+        for (int kb = 0; kb < nlist; kb += BPAD) {
+          float w0 = 0.f, w1 = 0.f;
+          iter(kb, w0, w1);
+        }
+      } else if (!ECC_BAND_DEFER) {
+        float* dxp = a.dX + item * a.n + v0;
+        for (int kb = 0; kb < nlist; kb += BPAD) {
+          float w0 = 0.f, w1 = 0.f;
+          iter(kb, w0, w1);
 #pragma unroll
           for (int sh = NWB / 2; sh; sh >>= 1) {
             w0 += __shfl_xor_sync(0xffffffffu, w0, sh);
             w1 += __shfl_xor_sync(0xffffffffu, w1, sh);
           }
-          float* dxp = a.dX + item * a.n + v0;
-          if (o == 0 && cf0 != 0.f) dxp[cur.y & 0xfff] = -cf0 * (lamf * w0);
-          if (o == 1 && cf1 != 0.f) dxp[cur.w & 0xfff] = -cf1 * (lamf * w1);
+          const int ry0 = wrec[kb + 2 * g].y, ry1 = wrec[kb + 2 * g + 1].y;
+          const float cf0 = __uint_as_float((uint32_t)ry0 & 0xFFFF0000u), cf1 = __uint_as_float((uint32_t)ry1 & 0xFFFF0000u);
+          if (o == 0 && cf0 != 0.f) dxp[ry0 & 0xfff] = -cf0 * (lamf * w0);
+          if (o == 1 && cf1 != 0.f) dxp[ry1 & 0xfff] = -cf1 * (lamf * w1);
+        }
+      } else {
+        // w of 8 voxels (4 iterations) reduced at once: a reduce-scatter over
+        // the slot's 8 lanes (7 shuffles instead of 24) leaves lane o with the
+        // sum of voxel o of the group, which it writes
+        float* dxp = a.dX + item * a.n + v0;
+        for (int kb0 = 0; kb0 < nlist; kb0 += 4 * BPAD) {
+          float wv[8];
+#pragma unroll
+          for (int gi = 0; gi < 4; ++gi) {
+            wv[2 * gi] = wv[2 * gi + 1] = 0.f;
+            if (kb0 + gi * BPAD < nlist) iter(kb0 + gi * BPAD, wv[2 * gi], wv[2 * gi + 1]);
+          }
+#pragma unroll
+          for (int sh = 4, nn = 4; sh; sh >>= 1, nn >>= 1) {
+            const bool upper = (o & sh) != 0;
+#pragma unroll
+            for (int i = 0; i < nn; ++i) {
+              const float mine = upper ? wv[nn + i] : wv[i];
+              const float give = upper ? wv[i] : wv[nn + i];
+              wv[i] = mine + __shfl_xor_sync(0xffffffffu, give, sh);
+            }
+          }
+          if (kb0 + (o >> 1) * BPAD < nlist) {
+            const int ry = wrec[kb0 + (o >> 1) * BPAD + 2 * g + (o & 1)].y;
+            const float cf = __uint_as_float((uint32_t)ry & 0xFFFF0000u);
+            if (cf != 0.f) dxp[ry & 0xfff] = -cf * (lamf * wv[0]);
+          }
         }
       }
     };
@@ -987,7 +1038,12 @@ __global__ void __launch_bounds__(SNT, ECC_BAND_MINB) ecc_soft_band_kernel(SoftA
     // chunk's compaction
     if (curb >= 0) flush();
     curb = -1;
-    if (BWD) {
+    if (BWD && ECC_BAND_WARPG) {
+      // G over this warp's slice: its dX were all written by this warp
+      __syncwarp();
+      const int i0 = w0 + 16 * lane;
+      soft_run_G_acc(a, item, v0, i0, min(i0 + 16, w1), gacc);
+    } else if (BWD) {
       __syncthreads();   // dX of this chunk is visible to the CTA
       soft_chunk_G_acc(a, item, v0, nvox, gacc);
     }
