@@ -911,9 +911,17 @@ __global__ void __launch_bounds__(SNT, ECC_BAND_MINB) ecc_soft_band_kernel(SoftA
         }
         kvr[it] = (kvr[it] & ~0xFF) | bb;
       }
-      const unsigned peers = __match_any_sync(0xffffffffu, kvr[it] & 0xFF);
-      if ((kvr[it] >> 8) != 0 && lane == __ffs(peers) - 1) atomicAdd(&s_cnt[warp][kvr[it] & 0xFF], __popc(peers));
     }
+    // band groups of all iterations first (independent MATCHes in flight),
+    // then the counts.  The backward, whose window loop needs more registers,
+    // recomputes the groups in the scatter instead of keeping them (spills).
+    constexpr bool KEEP = !BWD;
+    unsigned pvr[CITER];
+#pragma unroll
+    for (int it = 0; it < CITER; ++it) pvr[it] = __match_any_sync(0xffffffffu, kvr[it] & 0xFF);
+#pragma unroll
+    for (int it = 0; it < CITER; ++it)
+      if ((kvr[it] >> 8) != 0 && lane == __ffs(pvr[it]) - 1) atomicAdd(&s_cnt[warp][kvr[it] & 0xFF], __popc(pvr[it]));
     __syncwarp();
     int nlist;   // records in this warp's region, fillers included
     {
@@ -932,15 +940,23 @@ __global__ void __launch_bounds__(SNT, ECC_BAND_MINB) ecc_soft_band_kernel(SoftA
       nlist = __shfl_sync(0xffffffffu, incl, 31);
     }
     __syncwarp();
+    // slots: each band group's leader reserves its records (the atomics of all
+    // iterations in flight), then every member stores at its rank
+    int oldv[CITER];
+    if (KEEP) {
+#pragma unroll
+      for (int it = 0; it < CITER; ++it) {
+        const int bb = kvr[it] & 0xFF;
+        oldv[it] = ((kvr[it] >> 8) != 0 && lane == __ffs(pvr[it]) - 1) ? atomicAdd(&s_cnt[warp][bb], __popc(pvr[it])) : 0;
+      }
+    }
 #pragma unroll
     for (int it = 0; it < CITER; ++it) {
       const int i = w0 + it * 32 + lane;
       const int kv = kvr[it], cv = kv >> 8, bb = kv & 0xFF;
-      const unsigned peers = __match_any_sync(0xffffffffu, bb);
-      const int leader = __ffs(peers) - 1;
-      int old = 0;
-      if (cv != 0 && lane == leader) old = atomicAdd(&s_cnt[warp][bb], __popc(peers));
-      const int base = __shfl_sync(0xffffffffu, old, leader);
+      const unsigned peers = KEEP ? pvr[it] : __match_any_sync(0xffffffffu, bb);
+      if (!KEEP) oldv[it] = (cv != 0 && lane == __ffs(peers) - 1) ? atomicAdd(&s_cnt[warp][bb], __popc(peers)) : 0;
+      const int base = __shfl_sync(0xffffffffu, oldv[it], __ffs(peers) - 1);
       if (cv != 0) {
         const int k = base + __popc(peers & ((1u << lane) - 1u));
         wrec[k] = make_int2(__float_as_int(fvr[it]), i | (bb << 12) | (int)(__float_as_uint((float)cv) & 0xFFFF0000u));
