@@ -198,13 +198,20 @@ int ecc_soft_setup(const double *taus, int64_t nbins, const double *u, int ndim,
 int ecc_soft_prepare_d(const void *x, int dtype, int ndim, const int64_t *dims, int64_t batch,
                        const ecc_soft_params *params_dev, int8_t *coeffs, float *field_c, float *field_lo,
                        void *stream);
+/* records (optional, ecc_soft_records_bytes; NULL: none): when the windowed
+ * ("band") kernels run, the forward stores each warp's band-sorted non-zero
+ * voxels there and the backward of the same inputs reads them instead of
+ * compacting and sorting again (the kernels decide on the device; with the
+ * full kernels the buffer is ignored). */
+size_t ecc_soft_records_bytes(int ndim, const int64_t *dims, int64_t batch);
 int ecc_soft_forward_d(const int8_t *coeffs, const float *field_c, const float *field_lo, int ndim,
                        const int64_t *dims, int64_t batch, const double *taus, int64_t nbins,
-                       const ecc_soft_params *params_dev, double *chi, void *workspace, void *stream);
+                       const ecc_soft_params *params_dev, double *chi, void *workspace, void *records,
+                       void *stream);
 int ecc_soft_backward_d(const int8_t *coeffs, const float *field_c, const float *field_lo, int ndim,
                         const int64_t *dims, int64_t batch, const double *taus, int64_t nbins,
                         const ecc_soft_params *params_dev, const double *upstream, float *d_values, double *d_tau,
-                        double *G, void *workspace, void *stream);
+                        double *G, void *workspace, const void *records, void *stream);
 
 /* Kernel-variant switch for A/B checks (tests, tools/): key "f3" with value
  * default | value | branch | cta | rank2 | no2d | edge1 | dummy | static,

@@ -79,8 +79,11 @@ def lib():
         if hasattr(L, "ecc_soft_setup"):
             L.ecc_soft_setup.argtypes = [vp, i64, vp, i32, vp, dbl, vp, vp]
             L.ecc_soft_prepare_d.argtypes = [vp, i32, i32, vp, i64, vp, vp, vp, vp, vp]
-            L.ecc_soft_forward_d.argtypes = [vp, vp, vp, i32, vp, i64, vp, i64, vp, vp, vp, vp]
-            L.ecc_soft_backward_d.argtypes = [vp, vp, vp, i32, vp, i64, vp, i64, vp, vp, vp, vp, vp, vp, vp]
+            L.ecc_soft_forward_d.argtypes = [vp, vp, vp, i32, vp, i64, vp, i64, vp, vp, vp, vp, vp]
+            L.ecc_soft_backward_d.argtypes = [vp, vp, vp, i32, vp, i64, vp, i64, vp, vp, vp, vp, vp, vp, vp, vp]
+        if hasattr(L, "ecc_soft_records_bytes"):
+            L.ecc_soft_records_bytes.argtypes = [i32, vp, i64]
+            L.ecc_soft_records_bytes.restype = ctypes.c_size_t
         _lib = L
         if hasattr(L, "ecc_set_variant"):
             L.ecc_set_variant.argtypes = [ctypes.c_char_p, ctypes.c_char_p]

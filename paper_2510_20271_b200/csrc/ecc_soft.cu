@@ -60,6 +60,8 @@ struct SoftArgs {
   float* dX;              // [N][n]   (backward)
   const ecc_soft_params* pd;   // parameters resident on the device (sync-free path), else nullptr
   int band;               // the windowed kernel was launched alongside: this one exits where it runs
+  int2* recs;             // band kernels: the forward's band-sorted records [N][chunks][SNW][BREG], or nullptr
+  int* rcnt;              //   and their counts [N][chunks][SNW]; the backward reads them instead of sorting
 };
 
 __device__ __forceinline__ float ex2_approx(float x) {
@@ -836,7 +838,7 @@ __global__ void __launch_bounds__(SNT, ECC_BAND_MINB) ecc_soft_band_kernel(SoftA
   // The warp's next slice of coefficients and field values is fetched into
   // its shared staging buffer with cp.async while it sorts and walks the
   // current one (16-byte copies: needs 16-byte aligned slices).
-  const bool staged = (a.n % 16) == 0 && (((uintptr_t)a.c | (uintptr_t)a.fc) & 15) == 0;
+  const bool staged = !(BWD && a.recs) && (a.n % 16) == 0 && (((uintptr_t)a.c | (uintptr_t)a.fc) & 15) == 0;
   int8_t* st_c = reinterpret_cast<int8_t*>(s_up + rowlen) + warp * BSTAGE;   // [512] coefficients
   float* st_f = reinterpret_cast<float*>(st_c + CITER * 32);                  // [512] field values
   auto stage_issue = [&](int64_t ch) {
@@ -865,106 +867,121 @@ __global__ void __launch_bounds__(SNT, ECC_BAND_MINB) ecc_soft_band_kernel(SoftA
     const float* fg = a.fc + item * a.n + v0;
     // ---- per-warp compaction to c != 0 voxels, sorted by band (stable) -----
     const int w0 = warp * (CITER * 32), w1 = min(w0 + CITER * 32, nvox);
-    int kvr[CITER];     // band | c << 8  (c == 0: band field 0xFF)
-    float fvr[CITER];
-    if (staged) {
-      cp_async_wait_all();
+    int nlist = 0;   // records in this warp's region, fillers included
+    const int64_t rbase = (item * a.chunks + chunk) * SNW + warp;   // saved records of this warp and chunk
+    if (BWD && a.recs) {
+      // the forward's sorted records: no compaction, no sort
+      nlist = a.rcnt[rbase];
+      const int4* src4 = reinterpret_cast<const int4*>(a.recs + rbase * BREG);
+      for (int q = lane; q < nlist / 2; q += 32) reinterpret_cast<int4*>(wrec)[q] = src4[q];
+      for (int i = w0 + lane; i < w1; i += 32) a.dX[item * a.n + v0 + i] = 0.f;   // c = 0 voxels
       __syncwarp();
-#pragma unroll
-      for (int it = 0; it < CITER; ++it) {
-        const int i = w0 + it * 32 + lane;
-        const int cv = i < w1 ? (int)st_c[it * 32 + lane] : 0;
-        fvr[it] = i < w1 ? st_f[it * 32 + lane] : 0.f;
-        kvr[it] = (cv << 8) | 0xFF;
-      }
-      __syncwarp();
-      if (chunk + 1 < c1) stage_issue(chunk + 1);   // overlaps this chunk's sort and window loop
     } else {
-#pragma unroll
+      int kvr[CITER];     // band | c << 8  (c == 0: band field 0xFF)
+      float fvr[CITER];
+      if (staged) {
+        cp_async_wait_all();
+        __syncwarp();
+  #pragma unroll
+        for (int it = 0; it < CITER; ++it) {
+          const int i = w0 + it * 32 + lane;
+          const int cv = i < w1 ? (int)st_c[it * 32 + lane] : 0;
+          fvr[it] = i < w1 ? st_f[it * 32 + lane] : 0.f;
+          kvr[it] = (cv << 8) | 0xFF;
+        }
+        __syncwarp();
+        if (chunk + 1 < c1) stage_issue(chunk + 1);   // overlaps this chunk's sort and window loop
+      } else {
+  #pragma unroll
+        for (int it = 0; it < CITER; ++it) {
+          const int i = w0 + it * 32 + lane;
+          const int cv = i < w1 ? (int)cg[i] : 0;
+          fvr[it] = i < w1 ? fg[i] : 0.f;
+          kvr[it] = (cv << 8) | 0xFF;
+        }
+      }
+      if (lane < BAND_MAXBANDS) s_cnt[warp][lane] = 0;
+      __syncwarp();
+  #pragma unroll
+      for (int it = 0; it < CITER; ++it) {
+        const float f = fvr[it];
+        if ((kvr[it] >> 8) != 0) {
+          // band guess for near-uniform thresholds, then fixed against the edges
+          int bb = 0;
+          if (f >= e1) {
+            const float gss = __fmul_rn(f - e1, einv);
+            bb = min(1 + (gss < (float)nbands ? (int)gss : nbands), nbands - 1);
+            // one step each way covers a guess off by one; exact otherwise
+            const float lo = s_edge[bb], hi = s_edge[bb + 1], lo1 = s_edge[bb - 1];
+            if (lo > f) {
+              --bb;
+              if (lo1 > f) { while (bb > 0 && s_edge[bb] > f) --bb; }
+            } else if (hi <= f) {
+              ++bb;
+              while (s_edge[bb + 1] <= f) ++bb;
+            }
+          }
+          kvr[it] = (kvr[it] & ~0xFF) | bb;
+        }
+      }
+      // band groups of all iterations first (independent MATCHes in flight),
+      // then the counts.  The backward, whose window loop needs more registers,
+      // recomputes the groups in the scatter instead of keeping them (spills).
+      constexpr bool KEEP = !BWD;
+      unsigned pvr[CITER];
+  #pragma unroll
+      for (int it = 0; it < CITER; ++it) pvr[it] = __match_any_sync(0xffffffffu, kvr[it] & 0xFF);
+  #pragma unroll
+      for (int it = 0; it < CITER; ++it)
+        if ((kvr[it] >> 8) != 0 && lane == __ffs(pvr[it]) - 1) atomicAdd(&s_cnt[warp][kvr[it] & 0xFF], __popc(pvr[it]));
+      __syncwarp();
+      {
+        const int c = lane < nbands ? s_cnt[warp][lane] : 0;
+        const int cpad = (c + BPAD - 1) & ~(BPAD - 1);
+        int incl = cpad;
+  #pragma unroll
+        for (int sh = 1; sh < 32; sh <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, sh);
+          if (lane >= sh) incl += y;
+        }
+        // fillers at the end of each band: zero coefficient, the band's index
+        for (int q = incl - cpad + c; q < incl; ++q) wrec[q] = make_int2(0, lane << 12);
+        __syncwarp();
+        if (lane < nbands) s_cnt[warp][lane] = incl - cpad;   // start of band `lane`
+        nlist = __shfl_sync(0xffffffffu, incl, 31);
+      }
+      __syncwarp();
+      // slots: each band group's leader reserves its records (the atomics of all
+      // iterations in flight), then every member stores at its rank
+      int oldv[CITER];
+      if (KEEP) {
+  #pragma unroll
+        for (int it = 0; it < CITER; ++it) {
+          const int bb = kvr[it] & 0xFF;
+          oldv[it] = ((kvr[it] >> 8) != 0 && lane == __ffs(pvr[it]) - 1) ? atomicAdd(&s_cnt[warp][bb], __popc(pvr[it])) : 0;
+        }
+      }
+  #pragma unroll
       for (int it = 0; it < CITER; ++it) {
         const int i = w0 + it * 32 + lane;
-        const int cv = i < w1 ? (int)cg[i] : 0;
-        fvr[it] = i < w1 ? fg[i] : 0.f;
-        kvr[it] = (cv << 8) | 0xFF;
-      }
-    }
-    if (lane < BAND_MAXBANDS) s_cnt[warp][lane] = 0;
-    __syncwarp();
-#pragma unroll
-    for (int it = 0; it < CITER; ++it) {
-      const float f = fvr[it];
-      if ((kvr[it] >> 8) != 0) {
-        // band guess for near-uniform thresholds, then fixed against the edges
-        int bb = 0;
-        if (f >= e1) {
-          const float gss = __fmul_rn(f - e1, einv);
-          bb = min(1 + (gss < (float)nbands ? (int)gss : nbands), nbands - 1);
-          // one step each way covers a guess off by one; exact otherwise
-          const float lo = s_edge[bb], hi = s_edge[bb + 1], lo1 = s_edge[bb - 1];
-          if (lo > f) {
-            --bb;
-            if (lo1 > f) { while (bb > 0 && s_edge[bb] > f) --bb; }
-          } else if (hi <= f) {
-            ++bb;
-            while (s_edge[bb + 1] <= f) ++bb;
-          }
+        const int kv = kvr[it], cv = kv >> 8, bb = kv & 0xFF;
+        const unsigned peers = KEEP ? pvr[it] : __match_any_sync(0xffffffffu, bb);
+        if (!KEEP) oldv[it] = (cv != 0 && lane == __ffs(peers) - 1) ? atomicAdd(&s_cnt[warp][bb], __popc(peers)) : 0;
+        const int base = __shfl_sync(0xffffffffu, oldv[it], __ffs(peers) - 1);
+        if (cv != 0) {
+          const int k = base + __popc(peers & ((1u << lane) - 1u));
+          wrec[k] = make_int2(__float_as_int(fvr[it]), i | (bb << 12) | (int)(__float_as_uint((float)cv) & 0xFFFF0000u));
+        } else if (BWD && i < w1) {
+          a.dX[item * a.n + v0 + i] = 0.f;
         }
-        kvr[it] = (kvr[it] & ~0xFF) | bb;
       }
-    }
-    // band groups of all iterations first (independent MATCHes in flight),
-    // then the counts.  The backward, whose window loop needs more registers,
-    // recomputes the groups in the scatter instead of keeping them (spills).
-    constexpr bool KEEP = !BWD;
-    unsigned pvr[CITER];
-#pragma unroll
-    for (int it = 0; it < CITER; ++it) pvr[it] = __match_any_sync(0xffffffffu, kvr[it] & 0xFF);
-#pragma unroll
-    for (int it = 0; it < CITER; ++it)
-      if ((kvr[it] >> 8) != 0 && lane == __ffs(pvr[it]) - 1) atomicAdd(&s_cnt[warp][kvr[it] & 0xFF], __popc(pvr[it]));
-    __syncwarp();
-    int nlist;   // records in this warp's region, fillers included
-    {
-      const int c = lane < nbands ? s_cnt[warp][lane] : 0;
-      const int cpad = (c + BPAD - 1) & ~(BPAD - 1);
-      int incl = cpad;
-#pragma unroll
-      for (int sh = 1; sh < 32; sh <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, sh);
-        if (lane >= sh) incl += y;
-      }
-      // fillers at the end of each band: zero coefficient, the band's index
-      for (int q = incl - cpad + c; q < incl; ++q) wrec[q] = make_int2(0, lane << 12);
       __syncwarp();
-      if (lane < nbands) s_cnt[warp][lane] = incl - cpad;   // start of band `lane`
-      nlist = __shfl_sync(0xffffffffu, incl, 31);
-    }
-    __syncwarp();
-    // slots: each band group's leader reserves its records (the atomics of all
-    // iterations in flight), then every member stores at its rank
-    int oldv[CITER];
-    if (KEEP) {
-#pragma unroll
-      for (int it = 0; it < CITER; ++it) {
-        const int bb = kvr[it] & 0xFF;
-        oldv[it] = ((kvr[it] >> 8) != 0 && lane == __ffs(pvr[it]) - 1) ? atomicAdd(&s_cnt[warp][bb], __popc(pvr[it])) : 0;
+      if (!BWD && a.recs) {   // kept for the backward
+        int4* dst4 = reinterpret_cast<int4*>(a.recs + rbase * BREG);
+        for (int q = lane; q < nlist / 2; q += 32) dst4[q] = reinterpret_cast<const int4*>(wrec)[q];
+        if (lane == 0) a.rcnt[rbase] = nlist;
       }
     }
-#pragma unroll
-    for (int it = 0; it < CITER; ++it) {
-      const int i = w0 + it * 32 + lane;
-      const int kv = kvr[it], cv = kv >> 8, bb = kv & 0xFF;
-      const unsigned peers = KEEP ? pvr[it] : __match_any_sync(0xffffffffu, bb);
-      if (!KEEP) oldv[it] = (cv != 0 && lane == __ffs(peers) - 1) ? atomicAdd(&s_cnt[warp][bb], __popc(peers)) : 0;
-      const int base = __shfl_sync(0xffffffffu, oldv[it], __ffs(peers) - 1);
-      if (cv != 0) {
-        const int k = base + __popc(peers & ((1u << lane) - 1u));
-        wrec[k] = make_int2(__float_as_int(fvr[it]), i | (bb << 12) | (int)(__float_as_uint((float)cv) & 0xFFFF0000u));
-      } else if (BWD && i < w1) {
-        a.dX[item * a.n + v0 + i] = 0.f;
-      }
-    }
-    __syncwarp();
     if (chunk == c0) __syncthreads();   // the per-block tables of the prologue
 
     // ---- window loop: the warp's four slots walk its list together ---------
@@ -1184,7 +1201,7 @@ template <bool BWD>
 static int soft_launch(const int8_t* coeffs, const float* fc, const float* fclo, int ndim, const int64_t* dims, int64_t batch,
                        const double* taus, int64_t nbins, const ecc_soft_params* p, const double* up, float* dX,
                        double* out_main, double* G_out, void* workspace, void* stream,
-                       const ecc_soft_params* pd = nullptr) {
+                       const ecc_soft_params* pd = nullptr, void* records = nullptr) {
   clear_error();
   int64_t d3[3];
   int rc = soft_dims(ndim, dims, d3);
@@ -1220,6 +1237,8 @@ static int soft_launch(const int8_t* coeffs, const float* fc, const float* fclo,
   a.dX = dX;
   a.pd = pd;
   a.band = 0;
+  a.recs = reinterpret_cast<int2*>(records);
+  a.rcnt = records ? reinterpret_cast<int*>(a.recs + (size_t)(batch * chunks) * SNW * BREG) : nullptr;
   cudaStream_t s = (cudaStream_t)stream;
   // 16 thresholds per lane (~80 registers, 3 CTAs/SM): on 16 x 1024^2,
   // B = 256 the forward takes 522 vs 559 us and the backward 837 vs 868 us
@@ -1286,6 +1305,14 @@ static int soft_launch(const int8_t* coeffs, const float* fc, const float* fclo,
     rc = check_launch("ecc_soft_reduce_g");
   }
   return rc;
+}
+
+// band-sorted records kept from the forward for the backward (module path)
+extern "C" size_t ecc_soft_records_bytes(int ndim, const int64_t* dims, int64_t batch) {
+  int64_t d3[3];
+  if (soft_dims(ndim, dims, d3)) return 0;
+  const int64_t chunks = (d3[0] * d3[1] * d3[2] + CH - 1) / CH;
+  return (size_t)(batch * chunks) * SNW * (sizeof(int2) * BREG + sizeof(int));
 }
 
 extern "C" int ecc_soft_forward(const int8_t* coeffs, const float* field_c, const float* field_lo, int ndim,
@@ -1365,19 +1392,20 @@ extern "C" int ecc_soft_setup(const double* taus, int64_t nbins, const double* u
 
 extern "C" int ecc_soft_forward_d(const int8_t* coeffs, const float* field_c, const float* field_lo, int ndim,
                                   const int64_t* dims, int64_t batch, const double* taus, int64_t nbins,
-                                  const ecc_soft_params* params_dev, double* chi, void* workspace, void* stream) {
+                                  const ecc_soft_params* params_dev, double* chi, void* workspace, void* records,
+                                  void* stream) {
   if (!params_dev) return set_error(ECC_EINVAL, "null pointer argument");
   const ecc_soft_params placeholder{1.0, 0.0, {0.0, 0.0, 0.0}, 0.0, 1, 0};
   return soft_launch<false>(coeffs, field_c, field_lo, ndim, dims, batch, taus, nbins, &placeholder, nullptr, nullptr,
-                            chi, nullptr, workspace, stream, params_dev);
+                            chi, nullptr, workspace, stream, params_dev, records);
 }
 
 extern "C" int ecc_soft_backward_d(const int8_t* coeffs, const float* field_c, const float* field_lo, int ndim,
                                    const int64_t* dims, int64_t batch, const double* taus, int64_t nbins,
                                    const ecc_soft_params* params_dev, const double* upstream, float* d_values,
-                                   double* d_tau, double* G, void* workspace, void* stream) {
+                                   double* d_tau, double* G, void* workspace, const void* records, void* stream) {
   if (!params_dev) return set_error(ECC_EINVAL, "null pointer argument");
   const ecc_soft_params placeholder{1.0, 0.0, {0.0, 0.0, 0.0}, 0.0, 1, 0};
   return soft_launch<true>(coeffs, field_c, field_lo, ndim, dims, batch, taus, nbins, &placeholder, upstream, d_values,
-                           d_tau, G, workspace, stream, params_dev);
+                           d_tau, G, workspace, stream, params_dev, const_cast<void*>(records));
 }

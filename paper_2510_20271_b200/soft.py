@@ -20,6 +20,7 @@ Parity contract: normwise relative error <= 1e-4 (max|a-b| / max|b|).
 from __future__ import annotations
 
 import math
+from typing import Optional
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -371,11 +372,20 @@ def gradient_check(grid: ScalarGrid, params: SoftEccParams, upstream=None, step:
 _PARAMS_F64 = 7   # sizeof(ecc_soft_params) / 8
 
 
+def _records_bytes(dims, batch: int) -> int:
+    d = _lib.dims_arg(dims)
+    return int(_lib.lib().ecc_soft_records_bytes(len(dims), _lib.ptr(d), batch))
+
+
 @torch.library.custom_op("ecc_b200::soft_ecc_fwd", mutates_args=())
 def _soft_fwd_op(x: torch.Tensor, taus: torch.Tensor, u: torch.Tensor, alpha: torch.Tensor, lam: float,
-                 ndim: int) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor]:
+                 ndim: int, keep: bool = False
+                 ) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor]:
     """(chi [N, B] f64, coefficients int8, centred field f32, its remainder
-    f32, device parameters) of x [N, (D,) H, W]."""
+    f32, device parameters, band records) of x [N, (D,) H, W].  keep: a
+    backward will follow -- the windowed kernels then keep their band-sorted
+    records (ecc_soft_records_bytes, ~10 B per voxel) so the backward skips
+    its compaction and sort; else the records tensor is empty."""
     from .hard import _split_batch
 
     if not x.is_cuda:
@@ -400,24 +410,28 @@ def _soft_fwd_op(x: torch.Tensor, taus: torch.Tensor, u: torch.Tensor, alpha: to
                                     _lib.ptr(params), _lib.ptr(c), _lib.ptr(fc), _lib.ptr(lo), st))
     chi = torch.empty((batch, nb), dtype=torch.float64, device=dev)
     ws = _workspace(dims, batch, nb, dev)
+    recs = torch.empty(_records_bytes(dims, batch) if keep else 0, dtype=torch.uint8, device=dev)
     _lib.check(L.ecc_soft_forward_d(_lib.ptr(c), _lib.ptr(fc), _lib.ptr(lo), len(dims), _lib.ptr(d), batch,
-                                    _lib.ptr(taus_d), nb, _lib.ptr(params), _lib.ptr(chi), _lib.ptr(ws), st))
-    return chi, c, fc, lo, params
+                                    _lib.ptr(taus_d), nb, _lib.ptr(params), _lib.ptr(chi), _lib.ptr(ws),
+                                    _lib.ptr(recs) if keep else None, st))
+    return chi, c, fc, lo, params, recs
 
 
 @_soft_fwd_op.register_fake
-def _(x, taus, u, alpha, lam, ndim):
+def _(x, taus, u, alpha, lam, ndim, keep=False):
     from .hard import _split_batch
 
-    batch, _, _ = _split_batch(x, ndim)
+    batch, dims, _ = _split_batch(x, ndim)
     return (x.new_empty((batch, taus.shape[0]), dtype=torch.float64), x.new_empty(x.shape, dtype=torch.int8),
             x.new_empty(x.shape, dtype=torch.float32), x.new_empty(x.shape, dtype=torch.float32),
-            x.new_empty((_PARAMS_F64,), dtype=torch.float64))
+            x.new_empty((_PARAMS_F64,), dtype=torch.float64),
+            x.new_empty((_records_bytes(dims, batch) if keep else 0,), dtype=torch.uint8))
 
 
 @torch.library.custom_op("ecc_b200::soft_ecc_bwd", mutates_args=())
 def _soft_bwd_op(c: torch.Tensor, fc: torch.Tensor, lo: torch.Tensor, params: torch.Tensor, taus: torch.Tensor,
-                 grad_chi: torch.Tensor, ndim: int) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
+                 grad_chi: torch.Tensor, ndim: int, recs: Optional[torch.Tensor] = None
+                 ) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
     """(d_values f32 like the field, d_tau [N, B] f64, G [N, ndim] f64) for upstream grad_chi [N, B]."""
     dims = tuple(c.shape[-ndim:])
     batch = c.numel() // math.prod(dims)
@@ -430,43 +444,44 @@ def _soft_bwd_op(c: torch.Tensor, fc: torch.Tensor, lo: torch.Tensor, params: to
     G = torch.empty((batch, ndim), dtype=torch.float64, device=dev)
     ws = _workspace(dims, batch, nb, dev)
     d = _lib.dims_arg(dims)
+    rp = _lib.ptr(recs) if recs is not None and recs.numel() > 0 else None
     _lib.check(_lib.lib().ecc_soft_backward_d(_lib.ptr(c), _lib.ptr(fc), _lib.ptr(lo), ndim, _lib.ptr(d), batch,
                                               _lib.ptr(taus_d), nb, _lib.ptr(params), _lib.ptr(up), _lib.ptr(dX),
-                                              _lib.ptr(dtau), _lib.ptr(G), _lib.ptr(ws), _lib.stream_ptr(fc)))
+                                              _lib.ptr(dtau), _lib.ptr(G), _lib.ptr(ws), rp, _lib.stream_ptr(fc)))
     return dX, dtau, G
 
 
 @_soft_bwd_op.register_fake
-def _(c, fc, lo, params, taus, grad_chi, ndim):
+def _(c, fc, lo, params, taus, grad_chi, ndim, recs=None):
     batch = grad_chi.shape[0]
     return (fc.new_empty(fc.shape), fc.new_empty((batch, taus.shape[0]), dtype=torch.float64),
             fc.new_empty((batch, ndim), dtype=torch.float64))
 
 
 def _soft_setup_context(ctx, inputs, output):
-    x, taus, u, alpha, lam, ndim = inputs
-    chi, c, fc, lo, params = output
+    x, taus, u, alpha, lam, ndim, keep = inputs
+    chi, c, fc, lo, params, recs = output
     # the prepared tensors are saved state, not differentiable outputs: no
     # zero gradients are materialised for them (~9 B per voxel of fills)
-    ctx.mark_non_differentiable(c, fc, lo, params)
+    ctx.mark_non_differentiable(c, fc, lo, params, recs)
     ctx.set_materialize_grads(False)
-    ctx.save_for_backward(c, fc, lo, params, taus, u, alpha)
+    ctx.save_for_backward(c, fc, lo, params, taus, u, alpha, recs)
     ctx.ndim = ndim
     ctx.xdtype = x.dtype
 
 
-def _soft_backward(ctx, grad_chi, _gc, _gfc, _glo, _gp):
-    c, fc, lo, params, taus, u, alpha = ctx.saved_tensors
+def _soft_backward(ctx, grad_chi, _gc, _gfc, _glo, _gp, _gr):
+    c, fc, lo, params, taus, u, alpha, recs = ctx.saved_tensors
     if grad_chi is None:
-        return None, None, None, None, None, None
-    dX, dtau, G = torch.ops.ecc_b200.soft_ecc_bwd(c, fc, lo, params, taus, grad_chi, ctx.ndim)
+        return None, None, None, None, None, None, None
+    dX, dtau, G = torch.ops.ecc_b200.soft_ecc_bwd(c, fc, lo, params, taus, grad_chi, ctx.ndim, recs)
     Gs = G.sum(0)
     u64 = u.to(Gs.device, torch.float64)
     gx = dX.to(ctx.xdtype) if ctx.needs_input_grad[0] else None
     gt = dtau.sum(0).to(taus.device, taus.dtype) if ctx.needs_input_grad[1] else None
     gu = (-alpha.to(Gs.device, torch.float64) * Gs).to(u.device, u.dtype) if ctx.needs_input_grad[2] else None
     ga = (-(Gs * u64).sum()).to(alpha.device, alpha.dtype) if ctx.needs_input_grad[3] else None
-    return gx, gt, gu, ga, None, None
+    return gx, gt, gu, ga, None, None, None
 
 
 torch.library.register_autograd("ecc_b200::soft_ecc_fwd", _soft_backward, setup_context=_soft_setup_context)
@@ -484,7 +499,8 @@ class SoftECCFunction:
 
     @staticmethod
     def apply(x, taus, u, alpha, lam: float, ndim: int):
-        chi = torch.ops.ecc_b200.soft_ecc_fwd(x, taus, u, alpha, float(lam), int(ndim))[0]
+        keep = torch.is_grad_enabled() and any(t.requires_grad for t in (x, taus, u, alpha))
+        chi = torch.ops.ecc_b200.soft_ecc_fwd(x, taus, u, alpha, float(lam), int(ndim), keep)[0]
         return chi if x.dim() == ndim + 1 else chi[0]
 
 
