@@ -63,6 +63,7 @@ from .soft import (
     reparametrize_direction_jvp,
     soft_ecc,
     soft_ecc_backward,
+    soft_step_host,
 )
 
 __version__ = "0.1.0"
@@ -73,7 +74,7 @@ __all__ = [
     "accumulate_histogram", "bin_index", "coefficients_device", "compute_coefficients", "compute_ecc",
     "device_minmax", "ecc_discrete", "ecc_discrete_host", "release_host_buffers", "effective_field", "flatten_index", "histogram_device", "merge_histograms",
     "parse_strategy", "pixel_coordinates", "reparametrize_direction", "reparametrize_direction_jvp", "scan_device",
-    "soft_ecc", "soft_ecc_backward", "thresholds_from_range", "unflatten_index", "uniform_thresholds",
+    "soft_ecc", "soft_ecc_backward", "soft_step_host", "thresholds_from_range", "unflatten_index", "uniform_thresholds",
     "vertex_order", "gradient_check", "MAGIC", "VERSION_COEFF", "VERSION_SCALAR", "load_grid_device", "load_slab_device",
     "read_coefficients", "read_curve", "read_grid", "save_grid_device", "write_coefficients", "write_curve",
     "write_grid",

@@ -535,3 +535,47 @@ class SoftECC(torch.nn.Module):
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         return SoftECCFunction.apply(x, self.taus, self.direction(), self.alpha, self._lam, self.ndim)
+
+
+def soft_step_host(module: SoftECC, host_x: torch.Tensor, upstream: torch.Tensor | None = None,
+                   micro: int = 16) -> torch.Tensor:
+    """Forward + backward of ``module`` on a batch held in (pinned) host
+    memory, with the host -> device copies overlapped with the compute.
+
+    The batch is cut into micro-batches of ``micro`` items: micro-batch k + 1
+    is copied on a side stream while k runs forward and backward on the
+    current stream (two device buffers; a buffer is refilled only after the
+    compute that read it).  The loss is a sum over items, so the parameter
+    gradients accumulated over the micro-batches are the full batch's.
+    upstream: d loss / d chi [N, B] (default ones).  Returns chi [N, B] on
+    the device (enqueued; nothing here synchronises the host).
+    """
+    if host_x.is_cuda:
+        raise ValueError("soft_step_host takes a host tensor (pin it for asynchronous copies)")
+    dev = module.taus.device
+    n = host_x.shape[0]
+    micro = max(1, min(int(micro), n))
+    cur = torch.cuda.current_stream(dev)
+    side = torch.cuda.Stream(dev)
+    bufs = [torch.empty((micro,) + tuple(host_x.shape[1:]), dtype=host_x.dtype, device=dev) for _ in range(2)]
+    freed = [None, None]
+    chis = []
+    for k, i0 in enumerate(range(0, n, micro)):
+        i1 = min(n, i0 + micro)
+        buf = bufs[k % 2][: i1 - i0]
+        with torch.cuda.stream(side):
+            if freed[k % 2] is not None:
+                side.wait_event(freed[k % 2])
+            buf.copy_(host_x[i0:i1], non_blocking=True)
+            ready = torch.cuda.Event()
+            ready.record(side)
+        cur.wait_event(ready)
+        buf.record_stream(cur)
+        chi = module(buf)
+        up = torch.ones_like(chi) if upstream is None else upstream[i0:i1].to(dev, chi.dtype, non_blocking=True)
+        chi.backward(up)
+        chis.append(chi.detach())
+        done = torch.cuda.Event()
+        done.record(cur)
+        freed[k % 2] = done
+    return torch.cat(chis)

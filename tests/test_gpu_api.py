@@ -204,3 +204,22 @@ def test_sharded_gradients_sum_to_full_batch():
         a = sum(getattr(p, name).grad for p in parts)
         b = getattr(full, name).grad
         assert normwise(a.cpu().numpy(), b.cpu().numpy()) <= 1e-12, name
+
+
+def test_soft_step_host_matches_device_batch():
+    """soft_step_host (micro-batches copied from pinned host memory while the
+    previous one computes) gives the full batch's chi and gradients."""
+    x = torch.rand((7, 96, 80))
+    up = torch.rand((7, 64), dtype=torch.float64, device="cuda")
+    ref = E.SoftECC(np.linspace(-0.4, 1.4, 64), [1.0, 2.0], alpha=0.3, lam=50.0).cuda()
+    chi_ref = ref(x.cuda())
+    (chi_ref * up).sum().backward()
+    m = E.SoftECC(np.linspace(-0.4, 1.4, 64), [1.0, 2.0], alpha=0.3, lam=50.0).cuda()
+    chi = E.soft_step_host(m, x.pin_memory(), up, micro=3)
+    torch.cuda.synchronize()
+    assert normwise(chi.cpu().numpy(), chi_ref.detach().cpu().numpy()) <= 1e-12
+    for name in ("taus", "v", "alpha"):
+        assert normwise(getattr(m, name).grad.cpu().numpy(), getattr(ref, name).grad.cpu().numpy()) <= 1e-12, name
+    with pytest.raises(ValueError):
+        E.soft_step_host(m, x.cuda())
+
