@@ -1003,6 +1003,9 @@ namespace ecc {
 #ifndef ECC_RW_UNR
 #define ECC_RW_UNR 4   // unroll of the staging loops (rows): 1 / 2 / 4 / 8 measured 7.19 / 6.92 / 6.87 / 6.99 ms
 #endif
+#ifndef ECC_RW_MINB
+#define ECC_RW_MINB 1   // resident warps per SM the register budget must allow
+#endif
 #ifndef ECC_RW_LA
 #define ECC_RW_LA 5    // look-ahead of the plane walk's column reads: 1 / 2 / 3 / 5 measured 6.90 / 6.72 / 6.72 / 6.62 ms
 #endif
@@ -1017,10 +1020,15 @@ constexpr int RWX = 28;      // output columns per tile: x0 .. x0 + 27
 
 template <typename T>
 struct RwSmem {
-  double eff[2][RWR * RWLD];   // effective field of planes z (slot z & 1) and z + 1
-  T raw[RWR * RWC];            // the next plane's raw values (cp.async)
+  // effective field of planes z (slot z & 1) and z + 1; a plane's raw values
+  // arrive (cp.async) at the end of the slot it is converted into
+  double eff[2][RWR * RWLD];
   double p1u1[RWR];            // per staged row: crd(y) * u1
   double q[RWR];               // per staged row of the plane being staged: fma(crd(z), u0, p1u1)
+  __device__ __forceinline__ T* raw(int slot) {
+    return reinterpret_cast<T*>(reinterpret_cast<char*>(eff[slot]) + sizeof(double) * RWR * RWLD -
+                                sizeof(T) * RWR * RWC);
+  }
 };
 
 __device__ __forceinline__ void fa3(uint32_t a, uint32_t b, uint32_t c, uint32_t& s, uint32_t& cy) {
@@ -1042,7 +1050,7 @@ __device__ __forceinline__ void cp_async_t(void* sdst, const T* gsrc, bool in) {
 // (j = 0 .. 29: the 28 outputs and one halo voxel each side), so the shifted
 // reads of the negative relations are single shifts.
 template <typename T>
-__global__ void __launch_bounds__(32) soft_prep3d_rw_kernel(EffSrc<T> src, SoftPrepSink sk, int64_t batch,
+__global__ void __launch_bounds__(32, ECC_RW_MINB) soft_prep3d_rw_kernel(EffSrc<T> src, SoftPrepSink sk, int64_t batch,
                                                             int64_t tiles_x, int64_t tiles_y, int64_t zc,
                                                             int64_t zchunks) {
   __shared__ __align__(16) RwSmem<T> S;
@@ -1074,17 +1082,18 @@ __global__ void __launch_bounds__(32) soft_prep3d_rw_kernel(EffSrc<T> src, SoftP
 
   auto issue = [&](int64_t zp) {   // cp.async plane zp's raw values (zero-filled outside the grid)
     const bool zin = zp >= 0 && zp < D;
+    T* raw = S.raw((int)(zp & 1));
     if (inner && zin) {
       const T* rp = xb + zp * HW + (y0 - 2) * W + gx;
 ECC_RW_UNROLL
-      for (int row = 0; row < RWR; ++row, rp += W) cp_async_t(&S.raw[row * RWC + lane], rp, true);
+      for (int row = 0; row < RWR; ++row, rp += W) cp_async_t(&raw[row * RWC + lane], rp, true);
     } else {
       const T* pl = xb + (zin ? zp : 0) * HW;
 ECC_RW_UNROLL
       for (int row = 0; row < RWR; ++row) {
         const int64_t gy = y0 - 2 + row;
         const bool in = zin && cok && gy >= 0 && gy < H;
-        cp_async_t(&S.raw[row * RWC + lane], pl + (in ? gy * W + gx : 0), in);
+        cp_async_t(&raw[row * RWC + lane], pl + (in ? gy * W + gx : 0), in);
       }
     }
     cp_async_commit();
@@ -1097,11 +1106,16 @@ ECC_RW_UNROLL
     for (int row = lane; row < RWR; row += 32) S.q[row] = __fma_rn(t0, src.u0, S.p1u1[row]);
     __syncwarp();
     double* dst = S.eff[(int)(zp & 1)];
+    // In place: the raw values sit at the end of the slot.  Converted row by
+    // row in order, row r's float64 values end before raw row r + 1 starts
+    // (264 (r + 1) <= slot - raw + RWC sizeof(T) (r + 1) for r < 34), and
+    // within a row every lane's load precedes the warp's store.
+    const T* raw = S.raw((int)(zp & 1));
     if (inner && zin) {
 ECC_RW_UNROLL
       for (int row = 0; row < RWR; ++row) {
         const double dot = __fma_rn(p2, src.u2, S.q[row]);
-        const double v = __dadd_rn(__dadd_rn((double)S.raw[row * RWC + lane], __dmul_rn(src.alpha, dot)), 0.0);
+        const double v = __dadd_rn(__dadd_rn((double)raw[row * RWC + lane], __dmul_rn(src.alpha, dot)), 0.0);
         badhi = max(badhi, (uint32_t)__double2hiint(v) & 0x7ff00000u);
         dst[row * RWLD + lane] = v;
       }
@@ -1111,7 +1125,7 @@ ECC_RW_UNROLL
         const int64_t gy = y0 - 2 + row;
         const bool in = zin && cok && gy >= 0 && gy < H;
         const double dot = __fma_rn(p2, src.u2, S.q[row]);
-        const double v = __dadd_rn(__dadd_rn((double)S.raw[row * RWC + lane], __dmul_rn(src.alpha, dot)), 0.0);
+        const double v = __dadd_rn(__dadd_rn((double)raw[row * RWC + lane], __dmul_rn(src.alpha, dot)), 0.0);
         if (in) badhi = max(badhi, (uint32_t)__double2hiint(v) & 0x7ff00000u);
         dst[row * RWLD + lane] = in ? v : inf;   // outside the grid: never lower
       }
@@ -1185,17 +1199,21 @@ ECC_RW_UNROLL
     convert(zs - 1);
     issue(zs);
     convert(zs);
-    issue(zs + 1);
     uint32_t Wd[13], Pz[9];
     walk(zs - 1, Wd, false, 0, lotag);
 #pragma unroll
     for (int d = 0; d < 9; ++d) Pz[d] = Wd[4 + d];
+    __syncwarp();
+    issue(zs + 1);   // into the slot of zs - 1, done with
+    convert(zs + 1);
     int64_t obase = ((n * D + zs) * H + gyl) * W + x0;
     for (int64_t z = zs; z < ze; ++z, obase += HW) {
-      // planes z, z + 1 staged (z + 1 goes into the slot of z - 1, done with)
-      convert(z + 1);
-      if (z + 2 <= ze) issue(z + 2);
+      // planes z, z + 1 are staged; plane z + 2 is fetched into the slot of
+      // plane z once the walk has read it, while the words are evaluated
       walk(z, Wd, true, obase, lotag);
+      const bool next = z + 2 <= ze;
+      __syncwarp();
+      if (next) issue(z + 2);
       // ---- negative relations from the neighbours' positive ones ----------
       // lane above (row r - 1), this plane: directions (0, +1, dx)
       const uint32_t u1 = __shfl_up_sync(0xffffffffu, Wd[1], 1), u2 = __shfl_up_sync(0xffffffffu, Wd[2], 1),
@@ -1300,6 +1318,7 @@ ECC_RW_UNROLL
       }
 #pragma unroll
       for (int d = 0; d < 9; ++d) Pz[d] = Wd[4 + d];
+      if (next) convert(z + 2);
     }
   };
   if (sk.fclo) tile(std::true_type{});
