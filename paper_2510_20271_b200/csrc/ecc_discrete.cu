@@ -1357,6 +1357,175 @@ ECC_RW_UNROLL
 }
 }  // namespace ecc
 
+namespace ecc {
+// 2-D soft prepare, row-word form (C3; the default for float32 / float64
+// images): the 3-D kernel's scheme on one plane -- a warp per 30 x 28 tile,
+// lane = row, 4 positive compares per voxel (sign of the float64
+// difference), the 4 negative relations from the lane above and the own
+// shifted word, c = 1 - E + S bit-sliced (c + 3 = #squares + #(not edges)).
+// 128 x 1024^2: 650 us (per-voxel tile kernel: 740; several tiles per warp
+// with the next tile's loads in flight measured 661-726).
+template <typename T>
+__global__ void __launch_bounds__(32) soft_prep2d_rw_kernel(EffSrc<T> src, double center, int8_t* __restrict__ coeffs,
+                                                            float* __restrict__ fc, float* __restrict__ fclo,
+                                                            int64_t batch, int64_t tiles_x, int64_t tiles_y) {
+  __shared__ __align__(16) double eff[RWR * RWLD];
+  __shared__ double p0s[RWR];
+  src.init();
+  if (src.pd) {
+    center = src.pd->center;
+    if (src.pd->factorized) fclo = nullptr;   // only the direct mode reads the remainders
+  }
+  const int lane = threadIdx.x;
+  const int64_t H = src.H, W = src.W;
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  int64_t r = blockIdx.x;
+  const int64_t tile_x = r % tiles_x; r /= tiles_x;
+  const int64_t tile_y = r % tiles_y; r /= tiles_y;
+  const int64_t n = r;
+  if (n >= batch) return;
+  const int64_t x0 = tile_x * RWX, y0 = tile_y * RWOUT;
+  const T* xb = src.x + n * H * W;
+  const int64_t gx = x0 - 2 + lane;
+  const bool cok = gx >= 0 && gx < W;
+  const double p1u1 = __dmul_rn(EffSrc<T>::crd(cok ? gx : 0, W, src.sW), src.u1);
+  for (int row = lane; row < RWR; row += 32) {
+    const int64_t gy = y0 - 2 + row;
+    p0s[row] = EffSrc<T>::crd(gy >= 0 && gy < H ? gy : 0, H, src.sH);
+  }
+  // the tile's raw values, all loads in flight at once
+  T rv[RWR];
+#pragma unroll
+  for (int row = 0; row < RWR; ++row) {
+    const int64_t gy = y0 - 2 + row;
+    rv[row] = (cok && gy >= 0 && gy < H) ? xb[gy * W + gx] : T(0);
+  }
+  __syncwarp();
+  uint32_t badhi = 0;
+#pragma unroll
+  for (int row = 0; row < RWR; ++row) {
+    const int64_t gy = y0 - 2 + row;
+    const bool in = cok && gy >= 0 && gy < H;
+    const double dot = __fma_rn(p0s[row], src.u0, p1u1);   // EffSrc::make, 2-D
+    const double v = __dadd_rn(__dadd_rn((double)rv[row], __dmul_rn(src.alpha, dot)), 0.0);   // -0 -> +0
+    if (in) badhi = max(badhi, (uint32_t)__double2hiint(v) & 0x7ff00000u);
+    eff[row * RWLD + lane] = in ? v : inf;
+  }
+  __syncwarp();
+
+  const int sr = lane + 1;
+  const int64_t gyl = y0 - 1 + lane;
+  const bool rowout = lane >= 1 && lane <= RWOUT && gyl < H;
+  const bool fullx = x0 + RWX <= W && (W & 3) == 0;
+  const int64_t obase = (n * H + gyl) * W + x0;
+  const double* a = eff + sr * RWLD;
+  const double* b = eff + (sr + 1) * RWLD;
+  double av[RWC], bv[RWC];
+#pragma unroll
+  for (int j = RWC - 1; j >= RWC - 1 - ECC_RW_LA; --j) { av[j] = a[j]; bv[j] = b[j]; }
+  uint32_t Wd[4];
+  float f4[4], l4[4];
+#pragma unroll
+  for (int sc = RWC - 2; sc >= 1; --sc) {   // voxel x0 - 2 + sc, bit sc - 1
+    if (sc - ECC_RW_LA >= 0) { av[sc - ECC_RW_LA] = a[sc - ECC_RW_LA]; bv[sc - ECC_RW_LA] = b[sc - ECC_RW_LA]; }
+    const double p = av[sc];
+    const double qv[4] = {av[sc + 1], bv[sc - 1], bv[sc], bv[sc + 1]};
+#pragma unroll
+    for (int d = 0; d < 4; ++d) Wd[d] = __funnelshift_l((uint32_t)__double2hiint(__dsub_rn(qv[d], p)), Wd[d], 1);
+    if (sc >= 2 && sc <= RWX + 1) {
+      const int i = sc - 2;
+      const double dd = p - center;
+      f4[i & 3] = (float)dd;
+      if (fclo) l4[i & 3] = (float)(dd - (double)f4[i & 3]);
+      if ((i & 3) == 0 && rowout) {
+        if (fullx) {
+          *reinterpret_cast<float4*>(fc + obase + i) = make_float4(f4[0], f4[1], f4[2], f4[3]);
+          if (fclo) *reinterpret_cast<float4*>(fclo + obase + i) = make_float4(l4[0], l4[1], l4[2], l4[3]);
+        } else {
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            if (x0 + i + t < W) {
+              fc[obase + i + t] = f4[t];
+              if (fclo) fclo[obase + i + t] = l4[t];
+            }
+        }
+      }
+    }
+  }
+  // negative relations: the lane above (row r - 1) and the own shifted word
+  const uint32_t u1 = __shfl_up_sync(0xffffffffu, Wd[1], 1), u2 = __shfl_up_sync(0xffffffffu, Wd[2], 1),
+                 u3 = __shfl_up_sync(0xffffffffu, Wd[3], 1);
+  auto neg = [](uint32_t w, int dx) -> uint32_t { return ~(w >> (1 - dx)); };
+  uint32_t L[3][3];
+  L[1][2] = Wd[0] >> 1;
+  L[1][0] = neg(Wd[0], +1);
+#pragma unroll
+  for (int dx = -1; dx <= 1; ++dx) {
+    L[2][dx + 1] = Wd[2 + dx] >> 1;
+    L[0][1 - dx] = neg(dx < 0 ? u1 : dx == 0 ? u2 : u3, dx);
+  }
+  // c + 3 = #squares + #(not edges): 8 one-bit words
+  const uint32_t i0 = L[0][1] & L[1][0] & L[0][0], i1 = L[0][1] & L[1][2] & L[0][2];
+  const uint32_t i2 = L[2][1] & L[1][0] & L[2][0], i3 = L[2][1] & L[1][2] & L[2][2];
+  const uint32_t i4 = ~L[0][1], i5 = ~L[2][1], i6 = ~L[1][0], i7 = ~L[1][2];
+  uint32_t s0, k0, s1, k1, t0, m0, x1, n0;
+  fa3(i0, i1, i2, s0, k0);
+  fa3(i3, i4, i5, s1, k1);
+  fa3(s0, s1, i6, t0, m0);
+  const uint32_t b0 = t0 ^ i7, m1 = t0 & i7;
+  fa3(k0, k1, m0, x1, n0);
+  const uint32_t b1 = x1 ^ m1, n1 = x1 & m1;
+  const uint32_t b2 = n0 ^ n1, b3 = n0 & n1;
+  // c = (c + 3) - 3: add 13 (1101b) modulo 16, 4-bit two's complement
+  const uint32_t c0 = b0, s0b = ~b0;
+  const uint32_t s1b = b1 ^ c0, c1 = b1 & c0;
+  const uint32_t s2b = ~(b2 ^ c1), c2 = b2 | c1;
+  const uint32_t s3b = ~(b3 ^ c2);
+  if (rowout) {
+    int8_t* cp = coeffs + obase;
+#pragma unroll
+    for (int g = 0; g < RWX / 4; ++g) {
+      const int sh = 4 * g;
+      const uint32_t wv = spread4((s0b >> sh) & 15u) | (spread4((s1b >> sh) & 15u) << 1) |
+                          (spread4((s2b >> sh) & 15u) << 2) | (spread4((s3b >> sh) & 15u) * 0xF8u);
+      if (fullx) {
+        reinterpret_cast<uint32_t*>(cp)[g] = wv;
+      } else {
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          if (x0 + 4 * g + t < W) cp[4 * g + t] = (int8_t)(wv >> (8 * t));
+      }
+    }
+  }
+  // a non-finite effective field: the tile voxel by voxel with the IEEE compares
+  if (__any_sync(0xffffffffu, badhi == 0x7ff00000u)) {
+    const double nanv = __longlong_as_double(0x7ff8000000000000ll);
+    const int64_t xg = x0 + lane;
+    if (lane < RWX && xg < W) {
+      for (int ry = 0; ry < RWOUT; ++ry) {
+        const int64_t yg = y0 + ry;
+        if (yg >= H) break;
+        double nb[3][3];
+#pragma unroll
+        for (int b1 = 0; b1 < 3; ++b1)
+#pragma unroll
+          for (int c1 = 0; c1 < 3; ++c1) {
+            const int64_t yy = yg + b1 - 1, xx = xg + c1 - 1;
+            const bool in = yy >= 0 && yy < H && xx >= 0 && xx < W;
+            nb[b1][c1] = in ? src.at(n * H * W + yy * W + xx, 0, yy, xx) : nanv;
+          }
+        const int64_t i = (n * H + yg) * W + xg;
+        coeffs[i] = (int8_t)coeff2<double>(nb);
+        const double dd = nb[1][1] - center;
+        const float hf = (float)dd;
+        fc[i] = hf;
+        if (fclo) fclo[i] = (float)(dd - (double)hf);
+      }
+    }
+  }
+}
+}  // namespace ecc
+
 // p: host parameters, or (pd != nullptr) parameters resident on the device
 // (ecc_soft_setup); the values in *p are then placeholders
 static int soft_prepare(const void* x, int dtype, int ndim, const int64_t* dims, int64_t batch,
@@ -1370,6 +1539,24 @@ static int soft_prepare(const void* x, int dtype, int ndim, const int64_t* dims,
   if (batch < 1) return set_error(ECC_EINVAL, "batch must be >= 1");
   SoftPrepSink sk{coeffs, field_c, field_lo, p->center, d3[0], d3[1], d3[2], pd};
   cudaStream_t s = (cudaStream_t)stream;
+  if (ndim == 2 && (dtype == ECC_DTYPE_F32 || dtype == ECC_DTYPE_F64) && !variant_generic() &&
+      !variant_soft_prep_old() && d3[1] < (1ll << 30) && d3[2] < (1ll << 30)) {
+    const int64_t tiles_x = (d3[2] + RWX - 1) / RWX, tiles_y = (d3[1] + RWOUT - 1) / RWOUT;
+    const int64_t grid = tiles_x * tiles_y * batch;
+    if (grid > 0x7fffffff) return set_error(ECC_EINVAL, "grid too large for the 2-D prepare");
+    if (dtype == ECC_DTYPE_F32) {
+      EffSrc<float> src{(const float*)x, p->alpha, p->u[0], p->u[1], 0.0, 1, d3[1], d3[2], 2,
+                        0.0, coord_scale(d3[1]), coord_scale(d3[2]), pd};
+      soft_prep2d_rw_kernel<float><<<(unsigned)grid, 32, 0, s>>>(src, p->center, coeffs, field_c, field_lo, batch,
+                                                                  tiles_x, tiles_y);
+    } else {
+      EffSrc<double> src{(const double*)x, p->alpha, p->u[0], p->u[1], 0.0, 1, d3[1], d3[2], 2,
+                         0.0, coord_scale(d3[1]), coord_scale(d3[2]), pd};
+      soft_prep2d_rw_kernel<double><<<(unsigned)grid, 32, 0, s>>>(src, p->center, coeffs, field_c, field_lo, batch,
+                                                                   tiles_x, tiles_y);
+    }
+    return check_launch("soft_prep2d_rw_kernel");
+  }
   if (ndim == 2 && batch <= 65535 && (dtype == ECC_DTYPE_F32 || dtype == ECC_DTYPE_F64) &&
       !variant_generic()) {
     dim3 grid((unsigned)((d3[2] + 31) / 32), (unsigned)((d3[1] + PREP_TH - 1) / PREP_TH), (unsigned)batch);

@@ -359,6 +359,27 @@ class TestPrepare2D:
             assert torch.equal(c1, c2) and torch.equal(f1, f2), (hw, dtype, alpha)
             if l1 is not None:
                 assert torch.equal(l1, l2)
+            with E._lib.variant(soft_prep=1):   # the per-voxel tile kernel
+                c3, (f3, _) = E.soft.soft_prepare_device(t, hw, batch, p)
+            assert torch.equal(c1, c3) and torch.equal(f1, f3), (hw, dtype, alpha)
+            xi = x[0].astype(np.float64)
+            want = oracle.coefficients(oracle.effective_field(xi, alpha, u))
+            assert np.array_equal(c1[0].cpu().numpy(), want), (hw, dtype, alpha)
+
+    def test_nonfinite_tiles_fall_back(self, rng):
+        hw = (70, 90)
+        x = rng.random((2,) + hw).astype(np.float32)
+        x[0, 5, 7] = np.nan
+        x[1, 69, 89] = np.inf
+        x[1, 0, 30] = -np.inf
+        u = E.reparametrize_direction([1.0, 2.0])
+        p = E.soft._params(50.0, 0.3, u, -0.5, 1.5, 2, 0.01)
+        t = torch.from_numpy(x).cuda()
+        c1, (f1, _) = E.soft.soft_prepare_device(t, hw, 2, p)
+        with E._lib.variant(generic=1):
+            c2, (f2, _) = E.soft.soft_prepare_device(t, hw, 2, p)
+        assert torch.equal(c1, c2)
+        assert torch.equal(f1.view(torch.int32), f2.view(torch.int32))
 
 
 class TestPrepare3D:
