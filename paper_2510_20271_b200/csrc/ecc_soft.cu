@@ -411,6 +411,7 @@ constexpr double BAND_ZCUT = 16.635532333438686;   // 24 ln 2
 __device__ __forceinline__ bool band_ok(const SoftArgs& a) {
   const int nb = a.nb, nblk = (nb + BT - 1) / BT, nbands = nblk - NWB + 1;
   if (nb > BAND_MAXB || nbands < 2 || nbands > BAND_MAXBANDS) return false;   // uniform over the grid
+  if (a.W >= (1 << 22) || a.H >= (1 << 22) || a.D >= (1 << 22)) return false;   // fused G's 2^23 conversions
   const double w2 = 2.0 * BAND_ZCUT / a.lam * (1.0 + 1e-3);
   bool ok = true;
   for (int j = threadIdx.x; j + 1 < nb; j += blockDim.x) ok = ok && a.taus[j] <= a.taus[j + 1];
@@ -702,6 +703,9 @@ constexpr int BREG = CH / SNW + (BPAD - 1) * BAND_MAXBANDS + BPAD;   // per-warp
 constexpr int BSTAGE = (CH / SNW) * 5;               // per-warp staging: 512 int8 + 512 float
 
 
+// exact float of 0 <= i < 2^23 without an I2F (XU pipe)
+__device__ __forceinline__ float i2f23(int i) { return __int_as_float(0x4B000000 | i) - 8388608.f; }
+
 __device__ __forceinline__ int bq(int blk, int q) {   // float offset of quad q of block blk
   return blk * BT + 4 * (q ^ ((blk >> 1) & 3));
 }
@@ -713,6 +717,9 @@ template <bool BWD>
 #endif
 #ifndef ECC_BAND_DEFER
 #define ECC_BAND_DEFER 1   // deferred w reduction (reduce-scatter over 8 voxels): backward 4.41 vs 4.99 ms (128 x 1024^2)
+#endif
+#ifndef ECC_BAND_GFUSE
+#define ECC_BAND_GFUSE 1   // G accumulated where dX is written (no per-chunk barrier and re-read)
 #endif
 #ifndef ECC_BAND_WARPG
 #define ECC_BAND_WARPG 0   // G per warp slice without the CTA barrier: measured slower (5.28 vs 4.41 ms)
@@ -835,6 +842,11 @@ __global__ void __launch_bounds__(SNT, ECC_BAND_MINB) ecc_soft_band_kernel(SoftA
   const float lamf = (float)a.lam;
   double gacc[3] = {0.0, 0.0, 0.0};
   constexpr int CITER = CH / SNW / 32;
+  const int Wi = (int)a.W, Hi = (int)a.H;
+  const float invW = 1.0f / (float)a.W;
+  const float sHf = a.H > 1 ? (float)(2.0 / (double)(a.H - 1)) : 0.f;
+  const float sWf = a.W > 1 ? (float)(2.0 / (double)(a.W - 1)) : 0.f;
+  const float sDf = a.D > 1 ? (float)(2.0 / (double)(a.D - 1)) : 0.f;
   // The warp's next slice of coefficients and field values is fetched into
   // its shared staging buffer with cp.async while it sorts and walks the
   // current one (16-byte copies: needs 16-byte aligned slices).
@@ -984,6 +996,15 @@ __global__ void __launch_bounds__(SNT, ECC_BAND_MINB) ecc_soft_band_kernel(SoftA
     }
     if (chunk == c0) __syncthreads();   // the per-block tables of the prologue
 
+    // fused G (backward): this chunk's first voxel in (z, y, x) and per-lane sums
+    float gf0 = 0.f, gf1 = 0.f, gf2 = 0.f;
+    int cx0 = 0, cy0 = 0, cz0 = 0;
+    if (BWD && ECC_BAND_GFUSE) {
+      const int64_t zq = v0 / (a.H * a.W), rq = v0 - zq * a.H * a.W, yq = rq / a.W;
+      cz0 = (int)zq;
+      cy0 = (int)yq;
+      cx0 = (int)(rq - yq * a.W);
+    }
     // ---- window loop: the warp's four slots walk its list together ---------
     // Slot g takes records kb + 2g and kb + 2g + 1 (one 16-byte load, the
     // next pair prefetched; the region has slack for the overrun): two
@@ -1060,7 +1081,35 @@ __global__ void __launch_bounds__(SNT, ECC_BAND_MINB) ecc_soft_band_kernel(SoftA
           if (kb0 + (o >> 1) * BPAD < nlist) {
             const int ry = wrec[kb0 + (o >> 1) * BPAD + 2 * g + (o & 1)].y;
             const float cf = __uint_as_float((uint32_t)ry & 0xFFFF0000u);
-            if (cf != 0.f) dxp[ry & 0xfff] = -cf * (lamf * wv[0]);
+            if (cf != 0.f) {
+              const float d = -cf * (lamf * wv[0]);
+              const int idx = ry & 0xfff;
+              dxp[idx] = d;
+              if (ECC_BAND_GFUSE) {
+                // G -= d pos(voxel): coordinates from the chunk's first voxel
+                // (quotient by W through a float estimate, corrected exactly)
+                // (ints below 2^23 converted by the 2^23 magic add: no XU
+                // instructions next to the reciprocals)
+                const int t = cx0 + idx;
+                int q = __float_as_int(__fmaf_rn(i2f23(t), invW, 8388608.f)) - 0x4B000000;
+                int xx = t - q * Wi;
+                if (xx < 0) { --q; xx += Wi; }
+                if (xx >= Wi) { ++q; xx -= Wi; }
+                int yy = cy0 + q, zz = cz0;
+                while (yy >= Hi) { yy -= Hi; ++zz; }
+                const float px = a.W > 1 ? __fmaf_rn(i2f23(xx), sWf, -1.f) : 0.f;
+                const float py = a.H > 1 ? __fmaf_rn(i2f23(yy), sHf, -1.f) : 0.f;
+                if (a.ndim == 2) {
+                  gf0 = __fmaf_rn(-d, py, gf0);
+                  gf1 = __fmaf_rn(-d, px, gf1);
+                } else {
+                  const float pz = a.D > 1 ? __fmaf_rn(i2f23(zz), sDf, -1.f) : 0.f;
+                  gf0 = __fmaf_rn(-d, pz, gf0);
+                  gf1 = __fmaf_rn(-d, py, gf1);
+                  gf2 = __fmaf_rn(-d, px, gf2);
+                }
+              }
+            }
           }
         }
       }
@@ -1071,7 +1120,11 @@ __global__ void __launch_bounds__(SNT, ECC_BAND_MINB) ecc_soft_band_kernel(SoftA
     // chunk's compaction
     if (curb >= 0) flush();
     curb = -1;
-    if (BWD && ECC_BAND_WARPG) {
+    if (BWD && ECC_BAND_GFUSE) {
+      gacc[0] += gf0;
+      gacc[1] += gf1;
+      gacc[2] += gf2;
+    } else if (BWD && ECC_BAND_WARPG) {
       // G over this warp's slice: its dX were all written by this warp
       __syncwarp();
       const int i0 = w0 + 16 * lane;
