@@ -506,6 +506,40 @@ def bench_ns(args, dev):
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
+    e2e = None
+    if not args.no_e2e:
+        # the 4 GiB volume pinned host -> HBM in 64-plane chunks through
+        # ecc_discrete_host (the planes on the device are deposited while the
+        # next chunk is copied), curve -> host
+        host = torch.empty(x.shape, dtype=torch.float32, pin_memory=True)
+        host.copy_(x.cpu())
+        want = curve.cpu().numpy().reshape(-1)
+        got = E.ecc_discrete_host(host, taus, chunk_planes=64).cpu().numpy().reshape(-1)
+        _gate(np.array_equal(got, want), "NS e2e curve")
+        t0 = time.perf_counter()
+        for _ in range(2):
+            E.ecc_discrete_host(host, taus, chunk_planes=64).cpu()
+        e_ms = (time.perf_counter() - t0) * 1e3 / 2
+        e2e = {"value": x.numel() / (e_ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": e_ms,
+               "h2d_bytes_per_step": int(host.numel() * 4), "d2h_bytes_per_step": NB * 8,
+               "api": "paper_2510_20271_b200.ecc_discrete_host (64-plane chunks, pinned host -> HBM inside the "
+                      "timed region)"}
+        del host
+    cpu = None
+    if not args.no_cpu:
+        # the CPU port on a bounded sample of the same workload: 64 planes of
+        # 1024 x 1024 (all host threads), per-voxel rate
+        from oracle import oracle
+
+        oracle.set_threads(os.cpu_count() or 1)
+        xs = oracle.counter_grid(SEED + 1, (64, n, n)).reshape(64, n, n)
+        t0 = time.perf_counter()
+        oracle.histogram(xs, taus.taus)
+        v_cpu = xs.size / (time.perf_counter() - t0) / 1e9
+        cpu = {"value": v_cpu, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "port",
+               "sample": f"64 planes of the 1024^2 NS counter volume, {NB} bins, all host threads (per-voxel rate)",
+               "extrapolated_ms_per_step": x.numel() / (v_cpu * 1e9) * 1e3}
+        del xs
     peak, peak_kind = _peaks()
     gbs = 4.0 * x.numel() / (ms * 1e-3) / 1e9
     traffic = None
@@ -518,7 +552,7 @@ def bench_ns(args, dev):
             traffic = None
     out = {"workload": "NS: 3D 1024^3 float32, discrete ECC, 1024 uniform thresholds (device-resident)",
            "value": x.numel() / (ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": ms, "steps": steps,
-           "parity": parity,
+           "parity": parity, "e2e": e2e, "cpu_baseline": cpu,
            "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
                         "peak_source": peak_kind, "traffic": traffic,
                         "algorithmic_bytes_per_launch": 4 * x.numel()}}
@@ -621,9 +655,28 @@ def bench_c5(args, dev, world, rank, dist_on=False):
            "n_gpus": world, "scaling": "strong", "planes_per_gpu": P, "parity": parity,
            "gpu_launches_per_step": (4 if dist_on and world > 1 and P >= 3 else 2),
            "roofline": {"bound": "hbm", "achieved": gbs_gpu, "peak": peak, "unit": "GB/s",
-                        "frac": gbs_gpu / peak, "peak_source": peak_kind, "per": "GPU"}}
+                        "frac": gbs_gpu / peak, "peak_source": peak_kind, "per": "GPU"},
+           "e2e": None,
+           "e2e_note": ("not measured for C5: a rank's slab (32 GiB at N = 1) would have to sit in pinned host "
+                        "memory; the host -> HBM path of a slab is the C2 leg's e2e (ecc_discrete_host / "
+                        "distributed.slab_curve)")}
     del padded, gen, whole
     torch.cuda.empty_cache()
+    if rank == 0 and not args.no_cpu:
+        # the CPU port on a bounded sample of the same workload: 16 planes of
+        # 2048 x 2048 (all host threads), per-voxel rate
+        from oracle import oracle
+
+        oracle.set_threads(os.cpu_count() or 1)
+        xs = oracle.counter_grid(SEED + 2, (16, H, W)).reshape(16, H, W)
+        t0 = time.perf_counter()
+        oracle.histogram(xs, np.linspace(0.0, 1.0 - 2.0 ** -24, NB))
+        v_cpu = xs.size / (time.perf_counter() - t0) / 1e9
+        out["cpu_baseline"] = {"value": v_cpu, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "port",
+                               "sample": f"16 planes of the 2048^2 C5 counter volume, {NB} bins, all host threads "
+                                         "(per-voxel rate)",
+                               "extrapolated_ms_per_step": vox / (v_cpu * 1e9) * 1e3}
+        del xs
     return out
 
 
@@ -705,6 +758,44 @@ def bench_c4(args, dev, world, rank, dist_on=False):
     torch.cuda.synchronize()
     ms = _max_over_ranks([e0.elapsed_time(e1) / steps], dev, dist_on)[0]
     _gate(bool(torch.isfinite(m.taus.grad).all()) and bool(torch.isfinite(m.v.grad).all()), "C4 finite gradients")
+    # MUFU work issued (as the C3 leg): c != 0 voxels only, the band window
+    from paper_2510_20271_b200 import soft as S
+    from paper_2510_20271_b200.soft import band_window
+
+    p = S._params(lam, alpha, u, float(taus0[0]), float(taus0[-1]), 3, S._block_halfwidth(taus0))
+    c0, _ = S.soft_prepare_device(x[:, :128].contiguous(), (128, n, n), 1, p)
+    nz = float(torch.count_nonzero(c0)) / c0.numel()
+    del c0
+    win = band_window(taus0, lam)
+    # e2e through soft_step_host: the item pinned host -> HBM, forward + backward,
+    # chi and the parameter gradients -> host (one item per GPU: no overlap)
+    e2e = None
+    if not args.no_e2e:
+        host = torch.empty(x.shape, dtype=torch.float32, pin_memory=True)
+        host.copy_(x.cpu())
+
+        def e2e_step():
+            m.zero_grad(set_to_none=True)
+            chi = E.soft_step_host(m, host, up, micro=1)
+            if dist_on:
+                from paper_2510_20271_b200 import distributed as D
+
+                D.allreduce_soft_grads(m)
+            return (chi.cpu(), m.taus.grad.cpu(), m.v.grad.cpu(), m.alpha.grad.cpu())
+
+        e2e_step()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        e_ms = _max_over_ranks([(time.perf_counter() - t0) * 1e3 / 2], dev, dist_on)[0]
+        e2e = {"value": n ** 3 * world / (e_ms * 1e-3), "unit": "voxel/s", "ms_per_step": e_ms,
+               "h2d_bytes_per_step": int(host.numel() * 4) * world,
+               "d2h_bytes_per_step": (B * 8 + B * 8 + 3 * 8 + 8) * world,
+               "api": "paper_2510_20271_b200.soft_step_host (the 1024^3 item pinned host -> HBM, SoftECC forward + "
+                      "backward, chi and the tau / v / alpha gradients -> host, inside the timed region)"}
+        del host
     del x, m
     torch.cuda.empty_cache()
     parity = "finite gradients only"
@@ -720,10 +811,22 @@ def bench_c4(args, dev, world, rank, dist_on=False):
         cpu = {"value": v_s, "unit": "voxel/s", "cores": cores, "kind": "port",
                "sample": sample, "extrapolated_ms_per_step": n ** 3 / v_s * 1e3}
     vox = n ** 3 * world
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    mufu_peak = 16 * sms * 1.965e9 * world
+    if win < B:
+        mufu_ops = nz * vox * win * 2 * (0.5 + 1.0 / 16.0)
+    else:
+        mufu_ops = nz * vox * B * ((0.5 + 1.0 / 16.0) + (7.0 / 8.0 + 1.0 / 16.0))
     return {"workload": "C4: 3D 1024^3 float32 soft ECC fwd+bwd, learnable tau/u/alpha, one item per GPU",
             "value": vox / (ms * 1e-3), "unit": "voxel/s", "ms_per_step": ms, "steps": steps,
             "n_gpus": world, "bins": B, "lambda": lam, "alpha": alpha, "parallelism": f"batch{world}",
-            "scaling": "weak", "parity": parity, "cpu_baseline": cpu,
+            "scaling": "weak", "parity": parity, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": {"bound": "sfu", "unit": "MUFU ops/s", "achieved": mufu_ops / (ms * 1e-3),
+                         "peak": mufu_peak, "frac": mufu_ops / (ms * 1e-3) / mufu_peak,
+                         "nonzero_fraction": nz, "window_thresholds": win,
+                         "algorithmic_pairs_per_s": 2 * vox * B / (ms * 1e-3),
+                         "survey_sfu_bound_voxel_s": mufu_peak / (2 * B),
+                         "peak_source": "MUFU.RCP 15.9 lane-ops/SM-clk (tools/microbench/pipes.cu) x SMs x 1.965 GHz"},
             "algorithmic_pairs_per_s": 2 * vox * B / (ms * 1e-3)}
 
 
