@@ -105,3 +105,21 @@ def test_engine_fails_loudly_without_gpu():
         pytest.skip("GPU present")
     with pytest.raises(RuntimeError):
         E.compute_ecc(E.ScalarGrid([[1.0, 2.0]]), E.ThresholdSet([1.0, 2.0]))
+
+
+def test_band_window_condition():
+    """The windowed soft kernels' condition (soft.band_window mirrors
+    ecc_soft.cu band_ok): C3's / C4's thresholds get a 128-threshold window;
+    unsorted, too dense for the window, too few or too many thresholds, or
+    a soft sigmoid (small lambda) fall back to all thresholds."""
+    from paper_2510_20271_b200.soft import band_window
+
+    span = 0.3 * (3.0 / np.sqrt(5.0))
+    taus = np.linspace(-span, 1.0 + span, 257)[1:]
+    assert band_window(taus, 50.0) == 128
+    assert band_window(taus[::-1], 50.0) == 256               # unsorted
+    assert band_window(taus, 5.0) == 256                      # W = 24 ln2 / lam wider than 7 blocks
+    assert band_window(np.linspace(0, 1, 64), 50.0) == 64     # fewer than NWB + 2 blocks
+    assert band_window(np.linspace(0, 1, 1024), 500.0) == 1024   # more than 16 bands
+    assert band_window(np.linspace(0, 1, 368), 500.0) == 128
+
