@@ -1393,23 +1393,44 @@ __global__ void __launch_bounds__(32) soft_prep2d_rw_kernel(EffSrc<T> src, doubl
     const int64_t gy = y0 - 2 + row;
     p0s[row] = EffSrc<T>::crd(gy >= 0 && gy < H ? gy : 0, H, src.sH);
   }
-  // the tile's raw values, all loads in flight at once
+  // the tile's raw values, all loads in flight at once (interior tiles: a
+  // pointer walk without per-row range checks)
   T rv[RWR];
+  const bool inner = x0 >= 2 && x0 + RWC - 2 <= W && y0 >= 2 && y0 + RWR - 2 <= H;
+  if (inner) {
+    const T* rp = xb + (y0 - 2) * W + gx;
 #pragma unroll
-  for (int row = 0; row < RWR; ++row) {
-    const int64_t gy = y0 - 2 + row;
-    rv[row] = (cok && gy >= 0 && gy < H) ? xb[gy * W + gx] : T(0);
+    for (int row = 0; row < RWR; ++row, rp += W) rv[row] = *rp;
+  } else {
+#pragma unroll
+    for (int row = 0; row < RWR; ++row) {
+      const int64_t gy = y0 - 2 + row;
+      rv[row] = (cok && gy >= 0 && gy < H) ? xb[gy * W + gx] : T(0);
+    }
   }
   __syncwarp();
-  uint32_t badhi = 0;
+  double p0r[RWR];   // every row's p0 read before the conversion chain starts
 #pragma unroll
-  for (int row = 0; row < RWR; ++row) {
-    const int64_t gy = y0 - 2 + row;
-    const bool in = cok && gy >= 0 && gy < H;
-    const double dot = __fma_rn(p0s[row], src.u0, p1u1);   // EffSrc::make, 2-D
-    const double v = __dadd_rn(__dadd_rn((double)rv[row], __dmul_rn(src.alpha, dot)), 0.0);   // -0 -> +0
-    if (in) badhi = max(badhi, (uint32_t)__double2hiint(v) & 0x7ff00000u);
-    eff[row * RWLD + lane] = in ? v : inf;
+  for (int row = 0; row < RWR; ++row) p0r[row] = p0s[row];
+  uint32_t badhi = 0;
+  if (inner) {
+#pragma unroll
+    for (int row = 0; row < RWR; ++row) {
+      const double dot = __fma_rn(p0r[row], src.u0, p1u1);   // EffSrc::make, 2-D
+      const double v = __dadd_rn(__dadd_rn((double)rv[row], __dmul_rn(src.alpha, dot)), 0.0);   // -0 -> +0
+      badhi = max(badhi, (uint32_t)__double2hiint(v) & 0x7ff00000u);
+      eff[row * RWLD + lane] = v;
+    }
+  } else {
+#pragma unroll
+    for (int row = 0; row < RWR; ++row) {
+      const int64_t gy = y0 - 2 + row;
+      const bool in = cok && gy >= 0 && gy < H;
+      const double dot = __fma_rn(p0r[row], src.u0, p1u1);   // EffSrc::make, 2-D
+      const double v = __dadd_rn(__dadd_rn((double)rv[row], __dmul_rn(src.alpha, dot)), 0.0);   // -0 -> +0
+      if (in) badhi = max(badhi, (uint32_t)__double2hiint(v) & 0x7ff00000u);
+      eff[row * RWLD + lane] = in ? v : inf;
+    }
   }
   __syncwarp();
 
