@@ -178,8 +178,30 @@ class TestBandKernel:
         with _lib.variant(soft_band=1, soft_g=g):
             band = _module_outputs(m, x, up)
         for name, a, b in zip(("chi", "dX", "dtau", "dv"), band, full):
-            assert normwise(a, b) <= 1e-5, name
-        assert abs(float(band[4]) - float(full[4])) <= 1e-5 * max(abs(float(full[4])), 1e-3)
+            assert normwise(a, b) <= (1e-4 if name == "dv" else 1e-5), name
+        assert abs(float(band[4]) - float(full[4])) <= 1e-4 * max(abs(float(full[4])), 1e-3)
+
+    @pytest.mark.parametrize("B", [200, 250, 368])
+    def test_threshold_counts(self, rng, B):
+        """Partial last blocks and the largest band count (16 bands)."""
+        from paper_2510_20271_b200 import _lib
+        from paper_2510_20271_b200.soft import band_window
+
+        lam, alpha, v = 50.0 * B / 256, 0.3, [1.0, 2.0]
+        u = np.asarray(v) / np.linalg.norm(v)
+        span = alpha * np.abs(u).sum()
+        taus = np.linspace(-span, 1.0 + span, B + 1)[1:]
+        assert band_window(taus, lam) == 128
+        m = E.SoftECC(taus, v, alpha=alpha, lam=lam).cuda()
+        x = torch.from_numpy(rng.random((2, 64, 72)).astype(np.float32)).cuda()
+        up = torch.from_numpy(rng.uniform(0.5, 1.5, (2, B))).cuda()
+        with _lib.variant(soft_band=0):
+            full = _module_outputs(m, x, up)
+        band = _module_outputs(m, x, up)
+        # d_v comes from G = sum of -dX pos, a cancelling float32 sum in both
+        # kernels (summed in different orders): 1e-4 as against the oracle
+        for name, a, b in zip(("chi", "dX", "dtau", "dv"), band, full):
+            assert normwise(a, b) <= (1e-4 if name == "dv" else 1e-5), name
 
     def test_unsorted_thresholds_fall_back(self, rng):
         """Learnable thresholds may leave sorted order: the band kernels then
