@@ -261,7 +261,11 @@ __device__ __forceinline__ void pair_loop_fact2(const f2_t (&nat)[T / 2], const 
 // kernel falls back to pair_loop_fact2 when that margin is not met.
 // Negated factors as in pair_loop_fact2 (nd = -d): forward sigma = nd' *
 // rcp(-P), backward -sigma = nd' * rcp(P).
-template <bool BWD, int T>
+#ifndef ECC_PROD_UNP
+#define ECC_PROD_UNP 2   // band backward: slot pairs (of T / 4) kept unpaired -- one MUFU per pair, fewer FMA-pipe
+                         // ops; balances the two pipes (0 / 1 / 2 / 3 / 4: 3.50 / 3.42 / 3.39 / 3.45 / 3.55 ms, 128 x 1024^2)
+#endif
+template <bool BWD, int T, int UNP = 0>
 __device__ __forceinline__ void pair_loop_prod(const f2_t (&nat)[T / 2], const f2_t (&up)[T / 2], f2_t (&acc)[T / 2],
                                                float b, float cf, float& w) {
   const f2_t b2 = f2_pack(b, b), mone2 = f2_pack(-1.f, -1.f), cf2 = f2_pack(cf, cf);
@@ -270,6 +274,14 @@ __device__ __forceinline__ void pair_loop_prod(const f2_t (&nat)[T / 2], const f
   for (int i = 0; i < T / 4; ++i) {
     const int ip = T / 2 - 1 - i;
     const f2_t nd = fma2(nat[i], b2, mone2), ndp = fma2(nat[ip], b2, mone2);
+    if (i < UNP) {   // unpaired: rcp(-den) = sigma, rcp(den)... (as pair_loop_fact2)
+      float dx, dy, ex, ey;
+      f2_unpack(nd, dx, dy);
+      f2_unpack(ndp, ex, ey);
+      r[i] = BWD ? f2_pack(rcp_approx(dx), rcp_approx(dy)) : f2_pack(rcp_approx(-dx), rcp_approx(-dy));
+      r[ip] = BWD ? f2_pack(rcp_approx(ex), rcp_approx(ey)) : f2_pack(rcp_approx(-ex), rcp_approx(-ey));
+      continue;
+    }
     float px, py;
     f2_unpack(mul2(nd, ndp), px, py);   // d d' > 0
     const f2_t R = BWD ? f2_pack(rcp_approx(px), rcp_approx(py)) : f2_pack(rcp_approx(-px), rcp_approx(-py));
@@ -1029,8 +1041,8 @@ __global__ void __launch_bounds__(SNT, ECC_BAND_MINB) ecc_soft_band_kernel(SoftA
         const float kf0 = fminf(fmaxf(__fmaf_rn(a.kscale, __int_as_float(cur.x), koff), -bc), bc);
         const float kf1 = fminf(fmaxf(__fmaf_rn(a.kscale, __int_as_float(cur.z), koff), -bc), bc);
         if (PROD) {
-          pair_loop_prod<BWD, BT>(nat2, up2, acc2, ex2_approx(kf0), cf0, w0);
-          pair_loop_prod<BWD, BT>(nat2, up2, acc2, ex2_approx(kf1), cf1, w1);
+          pair_loop_prod<BWD, BT, BWD ? ECC_PROD_UNP : 0>(nat2, up2, acc2, ex2_approx(kf0), cf0, w0);
+          pair_loop_prod<BWD, BT, BWD ? ECC_PROD_UNP : 0>(nat2, up2, acc2, ex2_approx(kf1), cf1, w1);
         } else {
           pair_loop_fact2<BWD, BT>(nat2, up2, acc2, ex2_approx(kf0), cf0, w0);
           pair_loop_fact2<BWD, BT>(nat2, up2, acc2, ex2_approx(kf1), cf1, w1);
