@@ -261,6 +261,10 @@ __device__ __forceinline__ void pair_loop_fact2(const f2_t (&nat)[T / 2], const 
 // kernel falls back to pair_loop_fact2 when that margin is not met.
 // Negated factors as in pair_loop_fact2 (nd = -d): forward sigma = nd' *
 // rcp(-P), backward -sigma = nd' * rcp(P).
+#ifndef ECC_BAND_EX2_FMA
+#define ECC_BAND_EX2_FMA 0   // band forward: 2^kf on the FMA pipe instead of MUFU.EX2 (measured slower: C4 module
+                             // forward 3.99 vs 3.87 ms)
+#endif
 #ifndef ECC_PROD_UNP
 #define ECC_PROD_UNP 2   // band backward: slot pairs (of T / 4) kept unpaired -- one MUFU per pair, fewer FMA-pipe
                          // ops; balances the two pipes (0 / 1 / 2 / 3 / 4: 3.50 / 3.42 / 3.39 / 3.45 / 3.55 ms, 128 x 1024^2)
@@ -1041,8 +1045,10 @@ __global__ void __launch_bounds__(SNT, ECC_BAND_MINB) ecc_soft_band_kernel(SoftA
         const float kf0 = fminf(fmaxf(__fmaf_rn(a.kscale, __int_as_float(cur.x), koff), -bc), bc);
         const float kf1 = fminf(fmaxf(__fmaf_rn(a.kscale, __int_as_float(cur.z), koff), -bc), bc);
         if (PROD) {
-          pair_loop_prod<BWD, BT, BWD ? ECC_PROD_UNP : 0>(nat2, up2, acc2, ex2_approx(kf0), cf0, w0);
-          pair_loop_prod<BWD, BT, BWD ? ECC_PROD_UNP : 0>(nat2, up2, acc2, ex2_approx(kf1), cf1, w1);
+          const float b0 = (!BWD && ECC_BAND_EX2_FMA) ? ex2_fma(kf0) : ex2_approx(kf0);
+          const float b1 = (!BWD && ECC_BAND_EX2_FMA) ? ex2_fma(kf1) : ex2_approx(kf1);
+          pair_loop_prod<BWD, BT, BWD ? ECC_PROD_UNP : 0>(nat2, up2, acc2, b0, cf0, w0);
+          pair_loop_prod<BWD, BT, BWD ? ECC_PROD_UNP : 0>(nat2, up2, acc2, b1, cf1, w1);
         } else {
           pair_loop_fact2<BWD, BT>(nat2, up2, acc2, ex2_approx(kf0), cf0, w0);
           pair_loop_fact2<BWD, BT>(nat2, up2, acc2, ex2_approx(kf1), cf1, w1);
