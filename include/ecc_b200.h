@@ -202,7 +202,7 @@ int ecc_soft_prepare_d(const void *x, int dtype, int ndim, const int64_t *dims, 
  * ("band") kernels run, the forward stores each warp's band-sorted non-zero
  * voxels there and the backward of the same inputs reads them instead of
  * compacting and sorting again (the kernels decide on the device; with the
- * full kernels the buffer is ignored). */
+ * full kernels the buffer is ignored).  16-byte aligned. */
 size_t ecc_soft_records_bytes(int ndim, const int64_t *dims, int64_t batch);
 int ecc_soft_forward_d(const int8_t *coeffs, const float *field_c, const float *field_lo, int ndim,
                        const int64_t *dims, int64_t batch, const double *taus, int64_t nbins,

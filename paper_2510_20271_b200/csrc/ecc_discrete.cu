@@ -1138,7 +1138,10 @@ ECC_RW_UNROLL
   const int sr = lane + 1;
   const int64_t gyl = y0 - 1 + lane;
   const bool rowout = lane >= 1 && lane <= RWOUT && gyl < H;
-  const bool fullx = x0 + RWX <= W && (W & 3) == 0;
+  // vector stores (float4 field, 4-byte coefficient words) need whole,
+  // aligned rows: caller buffers of the C ABI may be arbitrary
+  const bool fullx = x0 + RWX <= W && (W & 3) == 0 &&
+                     (((uintptr_t)sk.fc | (uintptr_t)sk.fclo) & 15) == 0 && ((uintptr_t)sk.coeffs & 3) == 0;
   auto walk = [&](int64_t z, uint32_t (&Wd)[13], bool out, int64_t obase, auto lotag) {
     constexpr bool LO = decltype(lotag)::value;
     const double* a = S.eff[(int)(z & 1)] + sr * RWLD;
@@ -1437,7 +1440,8 @@ __global__ void __launch_bounds__(32) soft_prep2d_rw_kernel(EffSrc<T> src, doubl
   const int sr = lane + 1;
   const int64_t gyl = y0 - 1 + lane;
   const bool rowout = lane >= 1 && lane <= RWOUT && gyl < H;
-  const bool fullx = x0 + RWX <= W && (W & 3) == 0;
+  const bool fullx = x0 + RWX <= W && (W & 3) == 0 && (((uintptr_t)fc | (uintptr_t)fclo) & 15) == 0 &&
+                     ((uintptr_t)coeffs & 3) == 0;   // vector stores: whole, aligned rows
   const int64_t obase = (n * H + gyl) * W + x0;
   const double* a = eff + sr * RWLD;
   const double* b = eff + (sr + 1) * RWLD;

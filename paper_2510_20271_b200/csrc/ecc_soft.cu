@@ -1308,6 +1308,7 @@ static int soft_launch(const int8_t* coeffs, const float* fc, const float* fclo,
   a.dX = dX;
   a.pd = pd;
   a.band = 0;
+  if (((uintptr_t)records & 15) != 0) return set_error(ECC_EINVAL, "the records buffer must be 16-byte aligned");
   a.recs = reinterpret_cast<int2*>(records);
   a.rcnt = records ? reinterpret_cast<int*>(a.recs + (size_t)(batch * chunks) * SNW * BREG) : nullptr;
   cudaStream_t s = (cudaStream_t)stream;
