@@ -16,7 +16,7 @@ def run():
     _lib.check(_lib.lib().ecc_histogram(_lib.ptr(x), _lib.DTYPE_F32, 3, _lib.ptr(d), 1, _lib.ptr(table),
                                         _lib.ctypes.byref(binning), _lib.ptr(hist), _lib.stream_ptr(x)))
 for rnd in range(2):
-    for z in [0, 4, 6, 8, 10, 12, 16, 24, 32]:
+    for z in ([int(v) for v in sys.argv[2].split(",")] if len(sys.argv) > 2 else [0, 4, 6, 8, 10, 12, 16, 24, 32]):
         with _lib.variant(zunit=z):
             for _ in range(3): run()
             torch.cuda.synchronize()
