@@ -217,8 +217,11 @@ int ecc_soft_backward_d(const int8_t *coeffs, const float *field_c, const float 
  * default | value | branch | cta | rank2 | no2d | edge1 | dummy | static,
  * "zunit" (forced dynamic unit in planes, "0" = automatic), "generic"
  * ("1": every grid through the generic sweep), "soft_fwd_t" / "soft_bwd_t"
- * (thresholds per soft lane: 8, 16, 32).  Process-wide; the production
- * kernels are the defaults.  Returns 0 or ECC_EINVAL. */
+ * (thresholds per soft lane: 8, 16, 32), "soft_band" ("0": the full soft
+ * kernels even where the windowed ones apply), "soft_g" (chunks per soft
+ * CTA, "0" = automatic), "soft_prep" ("1": the per-voxel tile prepare
+ * instead of the row-word one).  Process-wide; the production kernels are
+ * the defaults.  Returns 0 or ECC_EINVAL. */
 int ecc_set_variant(const char *key, const char *value);
 
 /* Finite-difference harness for gradient_check (soft.py:260-359), float64:
