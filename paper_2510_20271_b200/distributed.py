@@ -5,7 +5,7 @@ one per rank.  Coefficients need a one-plane halo on each interior side
 (the index tie-break is translation invariant, coefficients.py:141-152),
 histograms are exactly additive (hard.py:99-118).  So a step is
     halo exchange (send first/last plane to the z-neighbours)
-    -> fused sweep over the own planes (ecc_histogram_range)
+    -> one fused sweep over the own planes (ecc_histogram_range)
     -> all_reduce(SUM) of the (B+1) int64 histogram
     -> prefix scan.
 At the two ends of the volume the missing halo plane is simply left out of
@@ -95,7 +95,7 @@ def _cuda_slab_hist(view: torch.Tensor, z0: int, z1: int, taus) -> torch.Tensor:
 
 
 def slab_histogram(padded: torch.Tensor, taus, group=None, exchange: bool = True,
-                   hist_fn: Callable | None = None, overlap: bool = True, depth: int | None = None) -> torch.Tensor:
+                   hist_fn: Callable | None = None, overlap: bool = False, depth: int | None = None) -> torch.Tensor:
     """Global (B+1) int64 histogram of a z-slab-partitioned 3D volume.
 
     padded: [planes + 2, H, W] (own planes at 1..planes; halos filled here
@@ -113,7 +113,11 @@ def slab_histogram(padded: torch.Tensor, taus, group=None, exchange: bool = True
     [1, planes - 1) need only this rank's own data, so they are swept while
     the halo planes are in flight; the two boundary planes follow once the
     halos have arrived.  Histograms are additive over plane ranges, so the
-    sum equals the single sweep bit for bit.
+    sum equals the single sweep bit for bit.  Off by default: a one-plane
+    sweep is a whole launch (setup, counter zeroing and flush of every
+    CTA), 31.6 us at 512^2 planes against 240 us for the 512-plane slab
+    (tools/plane_sweep.py), while the two halo planes cross NVLink in a few
+    microseconds -- exchanging first and sweeping once is cheaper.
     """
     fn = hist_fn or _cuda_slab_hist
     planes = padded.shape[0] - 2

@@ -55,10 +55,10 @@ def _worker(rank, world, port, dims, nbins, dtype, result_q):
             hist = D.slab_histogram(padded, taus, hist_fn=lambda v, a, b, t: torch.from_numpy(
                 oracle.histogram_rows(v.numpy().astype(np.float64), a, b, t.taus)))
         else:
-            hist = D.slab_histogram(padded, taus, hist_fn=_oracle_hist)   # interior sweep overlaps the exchange
+            hist = D.slab_histogram(padded, taus, hist_fn=_oracle_hist, overlap=True)   # interior sweep overlaps the exchange
             padded[0] = np.nan
             padded[-1] = np.nan
-            flat = D.slab_histogram(padded, taus, hist_fn=_oracle_hist, overlap=False)
+            flat = D.slab_histogram(padded, taus, hist_fn=_oracle_hist)   # exchange, then one sweep (default)
             assert torch.equal(hist, flat)
         curve = D.slab_curve(padded, taus, hist_fn=_oracle_hist if dtype != "u8" else
                              (lambda v, a, b, t: torch.from_numpy(
