@@ -1772,33 +1772,35 @@ ecc_rank4_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* _
   const uint32_t hbase = smem_u32(s_hist);
   // fold the rank counters (16 c per voxel) into the global bins: rank v is
   // bin b(v / 2) + v % 2; runs of ranks with the same bin are summed first
+  // Every CTA flushes at the end of the kernel, so the flush is on the
+  // critical path: a thread's counters and their bins are read eight at a
+  // time (loads in flight together, not one dependent chain per counter),
+  // then summed in runs of equal bins into one atomic per run.
   auto flush = [&](int64_t item) {
     unsigned long long* h = hist + item * (nb + 1);
     const int per = (nranks + NT - 1) / NT;
     const int v0 = threadIdx.x * per, v1 = min(v0 + per, nranks);
     long long acc = 0;
     int cur = -1;
-    for (int v = v0; v < v1; ++v) {
-      const int c = s_hist[v];
-      s_hist[v] = 0;
-      if (!c) continue;
-      int bin;
-      if (U8) {   // searchsorted-left of the value over the float32 thresholds
-        int lo = 0, hi = nb;
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (tab_g[mid + 1] < (float)v) lo = mid + 1; else hi = mid;
+    for (int vb = v0; vb < v1; vb += 8) {
+      int cv[8], bv[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) cv[k] = vb + k < v1 ? s_hist[vb + k] : 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        bv[k] = cv[k] ? rbin_g[vb + k] : -1;
+        if (vb + k < v1) s_hist[vb + k] = 0;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (!cv[k]) continue;
+        if (bv[k] != cur) {
+          if (cur >= 0 && acc) atomicAdd(h + cur, (unsigned long long)(acc >> 4));
+          cur = bv[k];
+          acc = 0;
         }
-        bin = lo;
-      } else {
-        bin = EDGE ? rbin_g[v] : lut_g[v >> 1].b + (v & 1);
+        acc += cv[k];
       }
-      if (bin != cur) {
-        if (cur >= 0 && acc) atomicAdd(h + cur, (unsigned long long)(acc >> 4));
-        cur = bin;
-        acc = 0;
-      }
-      acc += c;
     }
     if (cur >= 0 && acc) atomicAdd(h + cur, (unsigned long long)(acc >> 4));
   };
@@ -2114,7 +2116,9 @@ ecc_rank4_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* _
     }
   }
   __syncthreads();
+#ifndef ECC_F3_NOFLUSH_AB
   if (cur_n >= 0) flush(cur_n);
+#endif
   if (g.nf && nf_any(nfa)) atomicOr(g.nf, 1);
 }
 
