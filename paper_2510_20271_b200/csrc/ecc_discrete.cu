@@ -1369,7 +1369,10 @@ namespace ecc {
 // 128 x 1024^2: 650 us (per-voxel tile kernel: 740; several tiles per warp
 // with the next tile's loads in flight measured 661-726).
 template <typename T>
-__global__ void __launch_bounds__(32) soft_prep2d_rw_kernel(EffSrc<T> src, double center, int8_t* __restrict__ coeffs,
+#ifndef ECC_RW2_MINB
+#define ECC_RW2_MINB 1   // resident warps per SM the register budget must allow (16: -3 %, 20 / 24: spills, slower)
+#endif
+__global__ void __launch_bounds__(32, ECC_RW2_MINB) soft_prep2d_rw_kernel(EffSrc<T> src, double center, int8_t* __restrict__ coeffs,
                                                             float* __restrict__ fc, float* __restrict__ fclo,
                                                             int64_t batch, int64_t tiles_x, int64_t tiles_y) {
   __shared__ __align__(16) double eff[RWR * RWLD];
