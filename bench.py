@@ -680,6 +680,21 @@ def bench_c5(args, dev, world, rank, dist_on=False):
     return out
 
 
+def _soft_pipe_ops(nz: float, vox: int, B: int, win: int):
+    """(MUFU ops, FMA-pipe lane ops) the soft kernels issue per fwd+bwd step.
+    Band kernels (win < B): only c != 0 voxels and the window's pairs; the
+    forward pairs every two reciprocals (0.5 MUFU + 3.5 lane-FMA per pair),
+    the backward keeps half of its slot pairs unpaired (0.75 MUFU + 4.75
+    lane-FMA per pair); one ex2 per voxel and lane (1/16 per pair).  Full
+    kernels: all B thresholds, forward paired, backward 7/8 of the pairs on
+    MUFU (ecc_soft.cu)."""
+    if win < B:
+        pairs = nz * vox * win
+        return pairs * ((0.5 + 1.0 / 16.0) + (0.75 + 1.0 / 16.0)), pairs * (3.5 + 4.75)
+    pairs = nz * vox * B
+    return pairs * ((0.5 + 1.0 / 16.0) + (7.0 / 8.0 + 1.0 / 16.0)), pairs * (3.5 + 5.0)
+
+
 def _soft_setup(ndim: int):
     B, lam, alpha = 256, 50.0, 0.3
     v = np.array([1.0, 2.0]) if ndim == 2 else np.array([1.0, 2.0, -0.5])
@@ -813,10 +828,8 @@ def bench_c4(args, dev, world, rank, dist_on=False):
     vox = n ** 3 * world
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     mufu_peak = 16 * sms * 1.965e9 * world
-    if win < B:
-        mufu_ops = nz * vox * win * 2 * (0.5 + 1.0 / 16.0)
-    else:
-        mufu_ops = nz * vox * B * ((0.5 + 1.0 / 16.0) + (7.0 / 8.0 + 1.0 / 16.0))
+    mufu_ops, fma_ops = _soft_pipe_ops(nz, vox, B, win)
+    fma_peak = 116.5 * sms * 1.965e9 * world   # FFMA lane-ops/s (tools/microbench/pipes.cu)
     return {"workload": "C4: 3D 1024^3 float32 soft ECC fwd+bwd, learnable tau/u/alpha, one item per GPU",
             "value": vox / (ms * 1e-3), "unit": "voxel/s", "ms_per_step": ms, "steps": steps,
             "n_gpus": world, "bins": B, "lambda": lam, "alpha": alpha, "parallelism": f"batch{world}",
@@ -824,6 +837,7 @@ def bench_c4(args, dev, world, rank, dist_on=False):
             "roofline": {"bound": "sfu", "unit": "MUFU ops/s", "achieved": mufu_ops / (ms * 1e-3),
                          "peak": mufu_peak, "frac": mufu_ops / (ms * 1e-3) / mufu_peak,
                          "nonzero_fraction": nz, "window_thresholds": win,
+                         "fma_pipe_frac": fma_ops / (ms * 1e-3) / fma_peak,
                          "algorithmic_pairs_per_s": 2 * vox * B / (ms * 1e-3),
                          "survey_sfu_bound_voxel_s": mufu_peak / (2 * B),
                          "peak_source": "MUFU.RCP 15.9 lane-ops/SM-clk (tools/microbench/pipes.cu) x SMs x 1.965 GHz"},
@@ -923,19 +937,15 @@ def bench_soft(args, dev, world, rank, dist_on=False):
     pairs = vox * B * 2                      # algorithmic (voxel, threshold) pairs, forward + backward
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     mufu_peak = 16 * sms * 1.965e9 * world   # MUFU.RCP lane-ops/s (15.9/clk/SM measured, tools/microbench)
-    # MUFU work actually issued: the kernels evaluate only c != 0 voxels, and
-    # with the band kernels only a window of `win` thresholds per voxel (the
-    # saturated pairs outside it are exact 0 / 1 to 2^-24); both passes take
-    # one reciprocal per two pairs (paired denominators) -- the full backward
-    # 7/8 per pair (1/8 as Newton steps on the FMA pipe); plus one ex2 per
-    # voxel and lane (T = 16)
+    # MUFU and FMA-pipe work actually issued (_soft_pipe_ops): the kernels
+    # evaluate only c != 0 voxels, and with the band kernels only a window of
+    # `win` thresholds per voxel (the saturated pairs outside it are exact
+    # 0 / 1 to 2^-24)
     from paper_2510_20271_b200.soft import band_window
 
     win = band_window(taus, lam)
-    if win < B:
-        mufu_ops = nz * vox * win * 2 * (0.5 + 1.0 / 16.0)
-    else:
-        mufu_ops = nz * vox * B * ((0.5 + 1.0 / 16.0) + (7.0 / 8.0 + 1.0 / 16.0))
+    mufu_ops, fma_ops = _soft_pipe_ops(nz, vox, B, win)
+    fma_peak = 116.5 * sms * 1.965e9 * world   # FFMA lane-ops/s (tools/microbench/pipes.cu)
     return {"metric": "soft-ECC fwd+bwd voxels/s", "value": vox / (ms * 1e-3), "unit": "voxel/s",
             "ms_per_step": ms, "steps": steps, "parity": parity, "cpu_baseline": cpu, "e2e": e2e,
             "config": {"workload": "C3: batched 2D 128x1024x1024 f32, soft ECC fwd+bwd, learnable tau/u/alpha",
@@ -943,7 +953,7 @@ def bench_soft(args, dev, world, rank, dist_on=False):
             "roofline": {"bound": "sfu", "unit": "MUFU ops/s", "achieved": mufu_ops / (ms * 1e-3),
                          "peak": mufu_peak, "frac": mufu_ops / (ms * 1e-3) / mufu_peak,
                          "nonzero_fraction": nz, "algorithmic_pairs_per_s": pairs / (ms * 1e-3),
-                         "window_thresholds": win,
+                         "window_thresholds": win, "fma_pipe_frac": fma_ops / (ms * 1e-3) / fma_peak,
                          # one MUFU per (voxel, threshold) pair per pass bounds fwd+bwd at
                          # mufu_peak / (2 B) voxels/s; skipping c = 0 voxels and pairing reciprocals beat it
                          "survey_sfu_bound_voxel_s": mufu_peak / (2 * B),
