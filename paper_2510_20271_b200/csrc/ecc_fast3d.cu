@@ -1728,6 +1728,20 @@ ecc_fast3d_bin_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const vo
   if (g.nf && nf_any(nfa)) atomicOr(g.nf, 1);
 }
 
+#ifdef ECC_R4_TRACE
+// development trace (never in the production build): per CTA its SM, entry
+// time, first plane ranked, each warp's loop end and the flush end
+__device__ unsigned long long g_r4_trace[8 * 8192];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define R4_TRACE(k, v) do { if (blockIdx.x < 8192) g_r4_trace[8 * blockIdx.x + (k)] = (v); } while (0)
+#else
+#define R4_TRACE(k, v) do { } while (0)
+#endif
+
 template <int DEP, bool NF>
 __global__ void __launch_bounds__(NT, ECC_F3_MINB)
 ecc_rank4_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* __restrict__ table_g, int nb,
@@ -1742,6 +1756,15 @@ ecc_rank4_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* _
   int* s_hist = reinterpret_cast<int*>(bars + NW + 1);                          // cells + 2 ranks (+ 32 dummies), 16 c
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#ifdef ECC_R4_TRACE
+  if (threadIdx.x == 0) {
+    unsigned sm;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(sm));
+    R4_TRACE(0, sm);
+    R4_TRACE(1, gtimer());
+  }
+  bool traced_first = false;
+#endif
   const float* tab_g = reinterpret_cast<const float*>(table_g);
   const LutEntry* lut_g = reinterpret_cast<const LutEntry*>(tab_g + ((nb + 2 + 1) & ~1));
   // edge mode: boundary thresholds and the rank -> bin map follow the cell table
@@ -1924,6 +1947,10 @@ ecc_rank4_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* _
     r4_apply(rank(zs, true));
     __syncwarp();
     if (zs + 1 <= ze && zs + 1 < g.D) issue(zs + 1);
+#ifdef ECC_R4_TRACE
+    if (!traced_first && threadIdx.x == 0) R4_TRACE(2, gtimer());
+    traced_first = true;
+#endif
 
     // per-thread validity (rows / columns of this tile)
     const int y = y0 - 1 + lane;
@@ -2115,11 +2142,18 @@ ecc_rank4_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* _
       for (int k = 0; k < NNEG; ++k) N1[k] = N0[k];
     }
   }
+#ifdef ECC_R4_TRACE
+  if (lane == 0) R4_TRACE(3 + warp, gtimer());
+#endif
   __syncthreads();
 #ifndef ECC_F3_NOFLUSH_AB
   if (cur_n >= 0) flush(cur_n);
 #endif
   if (g.nf && nf_any(nfa)) atomicOr(g.nf, 1);
+#ifdef ECC_R4_TRACE
+  __syncthreads();
+  if (threadIdx.x == 0) R4_TRACE(7, gtimer());
+#endif
 }
 
 // ======================================================================
@@ -2715,3 +2749,9 @@ int fast3d_u8_launch(const uint8_t* x, int64_t D, int64_t H, int64_t W, int64_t 
 }
 
 }  // namespace ecc
+
+#ifdef ECC_R4_TRACE
+extern "C" int ecc_r4_trace_read(void* dst, size_t bytes) {
+  return cudaMemcpyFromSymbol(dst, ecc::fast::g_r4_trace, bytes) == cudaSuccess ? 0 : 1;
+}
+#endif
