@@ -740,6 +740,9 @@ template <bool BWD>
 #ifndef ECC_BAND_WARPG
 #define ECC_BAND_WARPG 0   // G per warp slice without the CTA barrier: measured slower (5.28 vs 4.41 ms)
 #endif
+#ifndef ECC_BAND_BALLOT
+#define ECC_BAND_BALLOT 1   // band sort from ballots (0: MATCH groups + shared-memory atomics)
+#endif
 #ifndef ECC_BAND_MINB
 #define ECC_BAND_MINB 2   // 128 registers: two voxels per lane in flight, no spills
 #endif
@@ -928,8 +931,10 @@ __global__ void __launch_bounds__(SNT, ECC_BAND_MINB) ecc_soft_band_kernel(SoftA
           kvr[it] = (cv << 8) | 0xFF;
         }
       }
+#if !ECC_BAND_BALLOT
       if (lane < BAND_MAXBANDS) s_cnt[warp][lane] = 0;
       __syncwarp();
+#endif
   #pragma unroll
       for (int it = 0; it < CITER; ++it) {
         const float f = fvr[it];
@@ -952,6 +957,56 @@ __global__ void __launch_bounds__(SNT, ECC_BAND_MINB) ecc_soft_band_kernel(SoftA
           kvr[it] = (kvr[it] & ~0xFF) | bb;
         }
       }
+#if ECC_BAND_BALLOT
+      // Stable counting sort by band from five ballots per iteration (valid,
+      // band bits 0..3): lane b holds band b's voxel mask, so the counts, the
+      // slots and each voxel's peers come from popc / shfl -- no MATCH, no
+      // shared-memory atomics.
+      const uint32_t FULLM = 0xffffffffu;
+      const uint32_t lm0 = (lane & 1) ? ~0u : 0u, lm1 = (lane & 2) ? ~0u : 0u;
+      const uint32_t lm2 = (lane & 4) ? ~0u : 0u, lm3 = (lane & 8) ? ~0u : 0u;
+      auto band_mask = [&](int kv) -> uint32_t {   // voxels of band `lane` in one iteration
+        const uint32_t V = __ballot_sync(FULLM, (kv >> 8) != 0);
+        const uint32_t B0 = __ballot_sync(FULLM, kv & 1), B1 = __ballot_sync(FULLM, kv & 2);
+        const uint32_t B2 = __ballot_sync(FULLM, kv & 4), B3 = __ballot_sync(FULLM, kv & 8);
+        return V & ~(B0 ^ lm0) & ~(B1 ^ lm1) & ~(B2 ^ lm2) & ~(B3 ^ lm3);
+      };
+      int pos;
+      __syncwarp();   // the previous chunk's walk is done with wrec
+      {
+        int run = 0;
+  #pragma unroll
+        for (int it = 0; it < CITER; ++it) run += __popc(band_mask(kvr[it]));
+        const int c = lane < nbands ? run : 0;
+        const int cpad = (c + BPAD - 1) & ~(BPAD - 1);
+        int incl = cpad;
+  #pragma unroll
+        for (int sh = 1; sh < 32; sh <<= 1) {
+          const int y = __shfl_up_sync(FULLM, incl, sh);
+          if (lane >= sh) incl += y;
+        }
+        // fillers at the end of each band: zero coefficient, the band's index
+        for (int q = incl - cpad + c; q < incl; ++q) wrec[q] = make_int2(0, lane << 12);
+        pos = incl - cpad;   // next slot of band `lane`
+        nlist = __shfl_sync(FULLM, incl, 31);
+      }
+      const uint32_t ltmask = (1u << lane) - 1u;
+  #pragma unroll
+      for (int it = 0; it < CITER; ++it) {
+        const uint32_t M = band_mask(kvr[it]);
+        const int i = w0 + it * 32 + lane;
+        const int kv = kvr[it], cv = kv >> 8, bb = kv & 0xFF;
+        const uint32_t peers = __shfl_sync(FULLM, M, bb & 31);
+        const int base = __shfl_sync(FULLM, pos, bb & 31);
+        if (cv != 0) {
+          const int k = base + __popc(peers & ltmask);
+          wrec[k] = make_int2(__float_as_int(fvr[it]), i | (bb << 12) | (int)(__float_as_uint((float)cv) & 0xFFFF0000u));
+        } else if (BWD && i < w1) {
+          a.dX[item * a.n + v0 + i] = 0.f;
+        }
+        pos += __popc(M);
+      }
+#else
       // band groups of all iterations first (independent MATCHes in flight),
       // then the counts.  The backward, whose window loop needs more registers,
       // recomputes the groups in the scatter instead of keeping them (spills).
@@ -1003,6 +1058,7 @@ __global__ void __launch_bounds__(SNT, ECC_BAND_MINB) ecc_soft_band_kernel(SoftA
           a.dX[item * a.n + v0 + i] = 0.f;
         }
       }
+#endif
       __syncwarp();
       if (!BWD && a.recs) {   // kept for the backward
         int4* dst4 = reinterpret_cast<int4*>(a.recs + rbase * BREG);
