@@ -203,6 +203,29 @@ class TestBandKernel:
         for name, a, b in zip(("chi", "dX", "dtau", "dv"), band, full):
             assert normwise(a, b) <= (1e-4 if name == "dv" else 1e-5), name
 
+    @pytest.mark.parametrize("shape,v", [((3, 97, 83), [1.0, 2.0]), ((2, 33, 31, 29), [1.0, 2.0, -0.5])])
+    def test_records_reuse_bit_identical(self, rng, shape, v):
+        """The backward that reads the forward's band-sorted records and the one
+        that compacts and sorts again see the same records in the same order,
+        so d_values, d_tau and G agree bit for bit."""
+        B, lam, alpha = 256, 50.0, 0.3
+        u = np.asarray(v) / np.linalg.norm(v)
+        span = alpha * np.abs(u).sum()
+        taus = torch.from_numpy(np.linspace(-span, 1.0 + span, B + 1)[1:]).cuda()
+        x = torch.from_numpy(rng.random(shape).astype(np.float32)).cuda()
+        ud = torch.from_numpy(u).cuda()
+        al = torch.tensor(alpha, dtype=torch.float64, device="cuda")
+        nd = len(shape) - 1
+        chi, c, fc, lo, params, recs = torch.ops.ecc_b200.soft_ecc_fwd(x, taus, ud, al, lam, nd, True)
+        assert recs.numel() > 0
+        chi0 = torch.ops.ecc_b200.soft_ecc_fwd(x, taus, ud, al, lam, nd, False)[0]
+        assert torch.equal(chi, chi0)   # keeping the records does not change the forward
+        up = torch.from_numpy(rng.uniform(0.5, 1.5, (shape[0], B))).cuda()
+        with_recs = torch.ops.ecc_b200.soft_ecc_bwd(c, fc, lo, params, taus, up, nd, recs)
+        resorted = torch.ops.ecc_b200.soft_ecc_bwd(c, fc, lo, params, taus, up, nd, None)
+        for a, b in zip(with_recs, resorted):
+            assert torch.equal(a, b)
+
     def test_unsorted_thresholds_fall_back(self, rng):
         """Learnable thresholds may leave sorted order: the band kernels then
         step aside and the full ones run (band_ok)."""
