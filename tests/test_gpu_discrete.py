@@ -378,6 +378,25 @@ class TestBinKernelLimits:
         assert np.array_equal(fast[0], want) and np.array_equal(gen[0], want)
 
 
+class TestSyntheticKinds:
+    """The smooth synthetic kinds of SURVEY §8(d) through the rank4 kernel
+    (1024 uniform thresholds, W % 128 == 0): gaussian blobs (c = 0 almost
+    everywhere, neighbouring rows share ranks -- the hot-counter pattern of
+    the deposits) and the radial gradient (ranks tie along shells), at a
+    static-partition depth and a dynamic-schedule depth."""
+
+    @pytest.mark.parametrize("kind", ["gaussian-blobs", "radial-gradient"])
+    @pytest.mark.parametrize("dims", [(48, 96, 128), (160, 64, 128)])
+    def test_bit_exact(self, kind, dims):
+        from paper_2510_20271_b200.synthetic import SyntheticSpec, generate_array
+
+        x = generate_array(SyntheticSpec(kind, dims, seed=3))
+        g = E.ScalarGrid(torch.from_numpy(x).cuda())
+        ts = E.uniform_thresholds(g, 1024)
+        got = E.histogram_device(torch.from_numpy(x).cuda(), ts).cpu().numpy().reshape(-1)
+        assert np.array_equal(got, np.append(*oracle.histogram(x, ts.taus)))
+
+
 class TestEdgeRanking:
     """Edge-table ranking (power-of-two bin counts): voxels sitting exactly on
     thresholds, one ulp either side, at the range ends and outside the range."""
