@@ -740,6 +740,9 @@ template <bool BWD>
 #ifndef ECC_BAND_WARPG
 #define ECC_BAND_WARPG 0   // G per warp slice without the CTA barrier: measured slower (5.28 vs 4.41 ms)
 #endif
+#ifndef ECC_BAND_RPF
+#define ECC_BAND_RPF 1   // backward: prefetch the next chunk's records into the staging area
+#endif
 #ifndef ECC_BAND_BALLOT
 #define ECC_BAND_BALLOT 1   // band sort from ballots (0: MATCH groups + shared-memory atomics)
 #endif
@@ -888,6 +891,19 @@ __global__ void __launch_bounds__(SNT, ECC_BAND_MINB) ecc_soft_band_kernel(SoftA
     cp_async_commit();
   };
   if (staged) stage_issue(c0);
+  // Backward with the forward's records: the first RPF records of the warp's
+  // next chunk are fetched into the (otherwise idle) staging area with
+  // cp.async while the current chunk walks, so only the rest of a chunk's
+  // records is read with the walk waiting (a fixed count: no wait on the
+  // next chunk's record count; the region holds BREG records, all in bounds).
+  constexpr int RPF = ECC_BAND_RPF ? (BSTAGE / 16) * 2 : 0;   // records (8 B) that fit the staging area
+  int4* rpf = reinterpret_cast<int4*>(st_c);
+  auto rpf_issue = [&](int64_t ch) {
+    const int4* src4 = reinterpret_cast<const int4*>(a.recs + ((item * a.chunks + ch) * SNW + warp) * BREG);
+    for (int q = lane; q < RPF / 2; q += 32) cp_async16(rpf + q, src4 + q, 16);
+    cp_async_commit();
+  };
+  if (BWD && a.recs && RPF && c0 < c1) rpf_issue(c0);
   const float e1 = s_edge[1];
   const float einv = nbands > 2 ? (float)(nbands - 2) / (s_edge[nbands - 1] - e1) : 0.f;
 
@@ -904,7 +920,16 @@ __global__ void __launch_bounds__(SNT, ECC_BAND_MINB) ecc_soft_band_kernel(SoftA
       // the forward's sorted records: no compaction, no sort
       nlist = a.rcnt[rbase];
       const int4* src4 = reinterpret_cast<const int4*>(a.recs + rbase * BREG);
-      for (int q = lane; q < nlist / 2; q += 32) reinterpret_cast<int4*>(wrec)[q] = src4[q];
+      int pre = 0;
+      if (RPF) {   // the prefetched head of the list, then the next chunk's head
+        pre = min(nlist, RPF) / 2;
+        cp_async_wait_all();
+        __syncwarp();
+        for (int q = lane; q < pre; q += 32) reinterpret_cast<int4*>(wrec)[q] = rpf[q];
+        __syncwarp();
+        if (chunk + 1 < c1) rpf_issue(chunk + 1);
+      }
+      for (int q = pre + lane; q < nlist / 2; q += 32) reinterpret_cast<int4*>(wrec)[q] = src4[q];
       for (int i = w0 + lane; i < w1; i += 32) a.dX[item * a.n + v0 + i] = 0.f;   // c = 0 voxels
       __syncwarp();
     } else {
