@@ -19,6 +19,7 @@ Parity contract: normwise relative error <= 1e-4 (max|a-b| / max|b|).
 
 from __future__ import annotations
 
+import functools
 import math
 from typing import Optional
 from dataclasses import dataclass, field
@@ -487,6 +488,15 @@ def _soft_backward(ctx, grad_chi, _gc, _gfc, _glo, _gp, _gr):
 torch.library.register_autograd("ecc_b200::soft_ecc_fwd", _soft_backward, setup_context=_soft_setup_context)
 
 
+@functools.lru_cache(maxsize=None)
+def _total_memory_idx(index: int) -> int:
+    return int(torch.cuda.get_device_properties(index).total_memory)
+
+
+def _total_memory(device: torch.device) -> int:
+    return _total_memory_idx(device.index if device.index is not None else torch.cuda.current_device())
+
+
 class SoftECCFunction:
     """chi[N, B] = sum_p c_p sigmoid(lam (tau_j - X_np - alpha <u, pos_p>)).
 
@@ -497,9 +507,17 @@ class SoftECCFunction:
     through the registered custom op ``torch.ops.ecc_b200.soft_ecc_fwd``.
     """
 
+    # band records are kept for the backward while they stay below this
+    # fraction of the device's memory (~10 B per voxel on top of the 9 B of
+    # saved coefficients and field); above it the backward re-sorts instead
+    RECORDS_MEMORY_FRACTION = 0.125
+
     @staticmethod
     def apply(x, taus, u, alpha, lam: float, ndim: int):
         keep = torch.is_grad_enabled() and any(t.requires_grad for t in (x, taus, u, alpha))
+        if keep and x.is_cuda:
+            cap = _total_memory(x.device) * SoftECCFunction.RECORDS_MEMORY_FRACTION
+            keep = 10 * x.numel() <= cap
         chi = torch.ops.ecc_b200.soft_ecc_fwd(x, taus, u, alpha, float(lam), int(ndim), keep)[0]
         return chi if x.dim() == ndim + 1 else chi[0]
 

@@ -226,6 +226,23 @@ class TestBandKernel:
         for a, b in zip(with_recs, resorted):
             assert torch.equal(a, b)
 
+    def test_records_memory_cap(self, rng, monkeypatch):
+        """Above the records memory cap the module keeps no records and the
+        backward re-sorts: the same gradients, bit for bit."""
+        from paper_2510_20271_b200.soft import SoftECCFunction
+
+        B, v = 256, [1.0, 2.0]
+        u = np.asarray(v) / np.linalg.norm(v)
+        span = 0.3 * np.abs(u).sum()
+        m = E.SoftECC(np.linspace(-span, 1.0 + span, B + 1)[1:], v, alpha=0.3, lam=50.0).cuda()
+        x = torch.from_numpy(rng.random((2, 96, 80)).astype(np.float32)).cuda()
+        up = torch.from_numpy(rng.uniform(0.5, 1.5, (2, B))).cuda()
+        kept = _module_outputs(m, x, up)
+        monkeypatch.setattr(SoftECCFunction, "RECORDS_MEMORY_FRACTION", 0.0)
+        resorted = _module_outputs(m, x, up)
+        for a, b in zip(kept, resorted):
+            assert np.array_equal(a, b)
+
     def test_unsorted_thresholds_fall_back(self, rng):
         """Learnable thresholds may leave sorted order: the band kernels then
         step aside and the full ones run (band_ok)."""
