@@ -1747,7 +1747,7 @@ __global__ void __launch_bounds__(NT, ECC_F3_MINB)
 ecc_rank4_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, const void* __restrict__ table_g, int nb,
                  int cells, int hsize, float lut_scale, float lut_bias, unsigned long long* __restrict__ hist) {
   constexpr int EK = 2;
-  constexpr bool EDGE = true, WS = true, U8 = false;
+  constexpr bool EDGE = true, U8 = false;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* stage_all = reinterpret_cast<float*>(smem_raw);                         // NW per-warp staged planes (TMA)
   uint32_t* bbuf = reinterpret_cast<uint32_t*>(smem_raw + NW * WSTAGE_BYTES);     // two rank planes

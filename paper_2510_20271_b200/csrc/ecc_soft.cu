@@ -764,7 +764,10 @@ __global__ void __launch_bounds__(SNT, ECC_BAND_MINB) ecc_soft_band_kernel(SoftA
   float* natab = red + BSLOTS * rowlen;                             // [rowlen] -a_j
   float* s_up = natab + rowlen;                                     // [rowlen] (backward)
   __shared__ float s_edge[BAND_MAXBANDS + 1], s_koff[BAND_MAXBLK], s_bc[BAND_MAXBLK], s_above[BAND_MAXBLK];
-  __shared__ int s_cnt[SNW][BAND_MAXBANDS], s_csb[BAND_MAXBANDS];
+#if !ECC_BAND_BALLOT
+  __shared__ int s_cnt[SNW][BAND_MAXBANDS];
+#endif
+  __shared__ int s_csb[BAND_MAXBANDS];
   __shared__ double s_g[SNW][4];
 
   const int64_t item = blockIdx.x / a.units;
