@@ -213,6 +213,28 @@ int ecc_soft_backward_d(const int8_t *coeffs, const float *field_c, const float 
                         const ecc_soft_params *params_dev, const double *upstream, float *d_values, double *d_tau,
                         double *G, void *workspace, const void *records, void *stream);
 
+/* Streaming a 3-D item in z-slabs (the host -> device copy overlapped with
+ * the prepare and the forward; soft.py soft_ecc_fwd_host).  Same semantics as
+ * ecc_soft_prepare_d / ecc_soft_forward_d restricted to part of the work:
+ * ecc_soft_prepare_range_d writes the coefficients and fields of output
+ * planes [plane_begin, plane_end) of a 3-D grid (reading the planes
+ * plane_begin - 1 and plane_end as halos, which must be resident);
+ * ecc_soft_units reports the forward's work split (chunks of 4096 voxels per
+ * unit, units per item); ecc_soft_forward_range_d runs units [unit_begin,
+ * unit_end) of every item (their voxels must be prepared) and, with finish
+ * != 0, reduces all units' partial rows into chi -- call it with finish once,
+ * after every unit ran.  Replaces the single-shot path of soft.py:154-196
+ * (soft_ecc) for streamed inputs; the results are those of the single-shot
+ * entry points. */
+int ecc_soft_prepare_range_d(const void *x, int dtype, int ndim, const int64_t *dims, int64_t batch,
+                             const ecc_soft_params *params_dev, int8_t *coeffs, float *field_c, float *field_lo,
+                             int64_t plane_begin, int64_t plane_end, void *stream);
+int ecc_soft_units(int ndim, const int64_t *dims, int64_t batch, int64_t *chunks_per_unit, int64_t *units);
+int ecc_soft_forward_range_d(const int8_t *coeffs, const float *field_c, const float *field_lo, int ndim,
+                             const int64_t *dims, int64_t batch, const double *taus, int64_t nbins,
+                             const ecc_soft_params *params_dev, double *chi, void *workspace, void *records,
+                             int64_t unit_begin, int64_t unit_end, int finish, void *stream);
+
 /* Kernel-variant switch for A/B checks (tests, tools/): key "f3" with value
  * default | value | branch | cta | rank2 | no2d | edge1 | dummy | static,
  * "zunit" (forced dynamic unit in planes, "0" = automatic), "generic"

@@ -84,6 +84,11 @@ def lib():
         if hasattr(L, "ecc_soft_records_bytes"):
             L.ecc_soft_records_bytes.argtypes = [i32, vp, i64]
             L.ecc_soft_records_bytes.restype = ctypes.c_size_t
+        if hasattr(L, "ecc_soft_forward_range_d"):
+            L.ecc_soft_prepare_range_d.argtypes = [vp, i32, i32, vp, i64, vp, vp, vp, vp, i64, i64, vp]
+            L.ecc_soft_units.argtypes = [i32, vp, i64, vp, vp]
+            L.ecc_soft_forward_range_d.argtypes = [vp, vp, vp, i32, vp, i64, vp, i64, vp, vp, vp, vp, i64, i64, i32,
+                                                   vp]
         _lib = L
         if hasattr(L, "ecc_set_variant"):
             L.ecc_set_variant.argtypes = [ctypes.c_char_p, ctypes.c_char_p]

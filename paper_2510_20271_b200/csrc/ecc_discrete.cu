@@ -1052,7 +1052,7 @@ __device__ __forceinline__ void cp_async_t(void* sdst, const T* gsrc, bool in) {
 template <typename T>
 __global__ void __launch_bounds__(32, ECC_RW_MINB) soft_prep3d_rw_kernel(EffSrc<T> src, SoftPrepSink sk, int64_t batch,
                                                             int64_t tiles_x, int64_t tiles_y, int64_t zc,
-                                                            int64_t zchunks) {
+                                                            int64_t zchunks, int64_t zb, int64_t zlim) {
   __shared__ __align__(16) RwSmem<T> S;
   src.init();
   sk.init(nullptr);
@@ -1066,7 +1066,7 @@ __global__ void __launch_bounds__(32, ECC_RW_MINB) soft_prep3d_rw_kernel(EffSrc<
   const int64_t n = r;
   if (n >= batch) return;
   const int64_t x0 = tile_x * RWX, y0 = tile_y * RWOUT;
-  const int64_t zs = zchunk * zc, ze = min(zs + zc, D);
+  const int64_t zs = zb + zchunk * zc, ze = min(zs + zc, zlim);   // output planes [zb, zlim) (halo planes read)
   const T* xb = src.x + n * D * HW;
   // tile and halo inside the grid in x and y: no per-value range checks
   const bool inner = x0 >= 2 && x0 + RWC - 2 <= W && y0 >= 2 && y0 + RWR - 2 <= H;
@@ -1556,6 +1556,35 @@ __global__ void __launch_bounds__(32, ECC_RW2_MINB) soft_prep2d_rw_kernel(EffSrc
 
 // p: host parameters, or (pd != nullptr) parameters resident on the device
 // (ecc_soft_setup); the values in *p are then placeholders
+
+// the row-word 3-D prepare of output planes [zb, zlim) (the planes zb - 1 and
+// zlim are read as halos): one warp per 30 x 28 tile and z-chunk; the chunk
+// is shortened until there are ~4 waves of 9 resident warps per SM
+static int soft_prep3d_rw_launch(const void* x, int dtype, const int64_t* d3, int64_t batch, const ecc_soft_params* p,
+                                 const ecc_soft_params* pd, const SoftPrepSink& sk, int64_t zb, int64_t zlim,
+                                 cudaStream_t s) {
+  const int64_t tiles_x = (d3[2] + RWX - 1) / RWX, tiles_y = (d3[1] + RWOUT - 1) / RWOUT;
+  const int64_t tiles = tiles_x * tiles_y * batch;
+  const int64_t depth = zlim - zb;
+  if (depth <= 0) return ECC_OK;
+  int64_t zc = 64;
+  while (zc > 8 && tiles * ((depth + zc - 1) / zc) < (int64_t)num_sms() * 9 * 4) zc >>= 1;
+  if (zc > depth) zc = depth;
+  const int64_t zchunks = (depth + zc - 1) / zc;
+  const int64_t grid = tiles * zchunks;
+  if (grid > 0x7fffffff) return set_error(ECC_EINVAL, "grid too large for the 3-D prepare");
+  if (dtype == ECC_DTYPE_F32) {
+    EffSrc<float> src{(const float*)x, p->alpha, p->u[0], p->u[1], p->u[2], d3[0], d3[1], d3[2], 3,
+                      coord_scale(d3[0]), coord_scale(d3[1]), coord_scale(d3[2]), pd};
+    soft_prep3d_rw_kernel<float><<<(unsigned)grid, 32, 0, s>>>(src, sk, batch, tiles_x, tiles_y, zc, zchunks, zb, zlim);
+  } else {
+    EffSrc<double> src{(const double*)x, p->alpha, p->u[0], p->u[1], p->u[2], d3[0], d3[1], d3[2], 3,
+                       coord_scale(d3[0]), coord_scale(d3[1]), coord_scale(d3[2]), pd};
+    soft_prep3d_rw_kernel<double><<<(unsigned)grid, 32, 0, s>>>(src, sk, batch, tiles_x, tiles_y, zc, zchunks, zb, zlim);
+  }
+  return check_launch("soft_prep3d_rw_kernel");
+}
+
 static int soft_prepare(const void* x, int dtype, int ndim, const int64_t* dims, int64_t batch,
                         const ecc_soft_params* p, const ecc_soft_params* pd, int8_t* coeffs, float* field_c,
                         float* field_lo, void* stream) {
@@ -1602,28 +1631,8 @@ static int soft_prepare(const void* x, int dtype, int ndim, const int64_t* dims,
   }
 generic:
   if (ndim == 3 && !variant_generic() && !variant_soft_prep_old() && (dtype == ECC_DTYPE_F32 || dtype == ECC_DTYPE_F64) &&
-      d3[1] < (1ll << 30) && d3[2] < (1ll << 30)) {
-    // row-word kernel: one warp per 30 x 28 tile and z-chunk; the chunk is
-    // shortened until there are ~4 waves of 9 resident warps per SM
-    const int64_t tiles_x = (d3[2] + RWX - 1) / RWX, tiles_y = (d3[1] + RWOUT - 1) / RWOUT;
-    const int64_t tiles = tiles_x * tiles_y * batch;
-    int64_t zc = 64;
-    while (zc > 8 && tiles * ((d3[0] + zc - 1) / zc) < (int64_t)num_sms() * 9 * 4) zc >>= 1;
-    if (zc > d3[0]) zc = d3[0];
-    const int64_t zchunks = (d3[0] + zc - 1) / zc;
-    const int64_t grid = tiles * zchunks;
-    if (grid > 0x7fffffff) return set_error(ECC_EINVAL, "grid too large for the 3-D prepare");
-    if (dtype == ECC_DTYPE_F32) {
-      EffSrc<float> src{(const float*)x, p->alpha, p->u[0], p->u[1], p->u[2], d3[0], d3[1], d3[2], ndim,
-                        coord_scale(d3[0]), coord_scale(d3[1]), coord_scale(d3[2]), pd};
-      soft_prep3d_rw_kernel<float><<<(unsigned)grid, 32, 0, s>>>(src, sk, batch, tiles_x, tiles_y, zc, zchunks);
-    } else {
-      EffSrc<double> src{(const double*)x, p->alpha, p->u[0], p->u[1], p->u[2], d3[0], d3[1], d3[2], ndim,
-                         coord_scale(d3[0]), coord_scale(d3[1]), coord_scale(d3[2]), pd};
-      soft_prep3d_rw_kernel<double><<<(unsigned)grid, 32, 0, s>>>(src, sk, batch, tiles_x, tiles_y, zc, zchunks);
-    }
-    return check_launch("soft_prep3d_rw_kernel");
-  }
+      d3[1] < (1ll << 30) && d3[2] < (1ll << 30))
+    return soft_prep3d_rw_launch(x, dtype, d3, batch, p, pd, sk, 0, d3[0], s);
   if (ndim == 3 && !variant_generic() && (dtype == ECC_DTYPE_F32 || dtype == ECC_DTYPE_F64)) {
     int occ = 0;
     const void* kfn = dtype == ECC_DTYPE_F32 ? (const void*)soft_prep3d_kernel<float>
@@ -1668,6 +1677,24 @@ extern "C" int ecc_soft_prepare_d(const void* x, int dtype, int ndim, const int6
   if (!params_dev) return set_error(ECC_EINVAL, "null pointer argument");
   const ecc_soft_params placeholder{1.0, 0.0, {0.0, 0.0, 0.0}, 0.0, 1, 0};
   return soft_prepare(x, dtype, ndim, dims, batch, &placeholder, params_dev, coeffs, field_c, field_lo, stream);
+}
+
+extern "C" int ecc_soft_prepare_range_d(const void* x, int dtype, int ndim, const int64_t* dims, int64_t batch,
+                                        const ecc_soft_params* params_dev, int8_t* coeffs, float* field_c,
+                                        float* field_lo, int64_t plane_begin, int64_t plane_end, void* stream) {
+  clear_error();
+  int64_t d3[3];
+  int rc = dims_to3(ndim, dims, d3);
+  if (rc) return rc;
+  if (!x || !params_dev || !coeffs || !field_c) return set_error(ECC_EINVAL, "null pointer argument");
+  if (ndim != 3 || batch < 1) return set_error(ECC_EINVAL, "plane ranges are for 3-D grids");
+  if (dtype != ECC_DTYPE_F32 && dtype != ECC_DTYPE_F64) return set_error(ECC_EINVAL, "soft path takes float32 or float64 grids");
+  if (plane_begin < 0 || plane_end > d3[0] || plane_begin > plane_end) return set_error(ECC_EINVAL, "plane range out of bounds");
+  if (d3[1] >= (1ll << 30) || d3[2] >= (1ll << 30)) return set_error(ECC_EINVAL, "grid too large for the 3-D prepare");
+  const ecc_soft_params placeholder{1.0, 0.0, {0.0, 0.0, 0.0}, 0.0, 1, 0};
+  SoftPrepSink sk{coeffs, field_c, field_lo, placeholder.center, d3[0], d3[1], d3[2], params_dev};
+  return soft_prep3d_rw_launch(x, dtype, d3, batch, &placeholder, params_dev, sk, plane_begin, plane_end,
+                               (cudaStream_t)stream);
 }
 
 namespace ecc {

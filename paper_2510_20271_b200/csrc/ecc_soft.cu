@@ -62,6 +62,8 @@ struct SoftArgs {
   int band;               // the windowed kernel was launched alongside: this one exits where it runs
   int2* recs;             // band kernels: the forward's band-sorted records [N][chunks][SNW][BREG], or nullptr
   int* rcnt;              //   and their counts [N][chunks][SNW]; the backward reads them instead of sorting
+  int64_t unit0 = 0;      // this launch's first unit (units [unit0, unit0 + lunits) of every item)
+  int64_t lunits = 0;     // units per item in this launch (== units unless a unit range is launched)
 };
 
 __device__ __forceinline__ float ex2_approx(float x) {
@@ -459,8 +461,8 @@ ecc_soft_kernel(SoftArgs a) {
   __shared__ double s_g[SNW][4];
 
   // this CTA: chunks [c0, c1) of one item (a unit of G chunks)
-  const int64_t item = blockIdx.x / a.units;
-  const int64_t unit = blockIdx.x % a.units;
+  const int64_t item = blockIdx.x / a.lunits;
+  const int64_t unit = a.unit0 + blockIdx.x % a.lunits;
   const int64_t c0 = unit * a.G, c1 = min(c0 + a.G, a.chunks);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
@@ -770,8 +772,8 @@ __global__ void __launch_bounds__(SNT, ECC_BAND_MINB) ecc_soft_band_kernel(SoftA
   __shared__ int s_csb[BAND_MAXBANDS];
   __shared__ double s_g[SNW][4];
 
-  const int64_t item = blockIdx.x / a.units;
-  const int64_t unit = blockIdx.x % a.units;
+  const int64_t item = blockIdx.x / a.lunits;
+  const int64_t unit = a.unit0 + blockIdx.x % a.lunits;
   const int64_t c0 = unit * a.G, c1 = min(c0 + a.G, a.chunks);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double ks = a.lam * LOG2E;
@@ -1352,11 +1354,20 @@ static bool soft_attr_done(const void* kfn, size_t smem) {
   return false;
 }
 
+// G chunks per CTA: the per-CTA tables and partial rows are amortised over G
+// chunks while keeping ~6 waves of 3 CTAs per SM
+static int64_t soft_units_G(int64_t batch, int64_t chunks) {
+  int64_t G = variant_soft_g();
+  if (G <= 0) G = std::max<int64_t>(1, std::min<int64_t>(16, batch * chunks / (148 * 3 * 6)));
+  return std::max<int64_t>(1, std::min<int64_t>(G, chunks));
+}
+
 template <bool BWD>
 static int soft_launch(const int8_t* coeffs, const float* fc, const float* fclo, int ndim, const int64_t* dims, int64_t batch,
                        const double* taus, int64_t nbins, const ecc_soft_params* p, const double* up, float* dX,
                        double* out_main, double* G_out, void* workspace, void* stream,
-                       const ecc_soft_params* pd = nullptr, void* records = nullptr) {
+                       const ecc_soft_params* pd = nullptr, void* records = nullptr, int64_t unit_begin = 0,
+                       int64_t unit_end = -1, bool finish = true) {
   clear_error();
   int64_t d3[3];
   int rc = soft_dims(ndim, dims, d3);
@@ -1403,14 +1414,17 @@ static int soft_launch(const int8_t* coeffs, const float* fc, const float* fclo,
   const int T = (tsel == 8 && nbins <= 8 * 32) ? 8 : (tsel <= 16 && nbins <= 16 * 32) ? 16 : 32;
   // G chunks per CTA: the per-CTA tables and partial rows are amortised
   // over G chunks while keeping ~6 waves of 3 CTAs per SM
-  int64_t G = variant_soft_g();
-  if (G <= 0) G = std::max<int64_t>(1, std::min<int64_t>(16, batch * chunks / (148 * 3 * 6)));
-  G = std::min<int64_t>(G, chunks);
+  const int64_t G = soft_units_G(batch, chunks);
   const int64_t units = (chunks + G - 1) / G;
   a.G = G;
   a.units = units;
-  const int64_t grid = batch * units;
+  if (unit_end < 0) unit_end = units;
+  if (unit_begin < 0 || unit_end > units || unit_begin > unit_end) return set_error(ECC_EINVAL, "unit range out of bounds");
+  a.unit0 = unit_begin;
+  a.lunits = unit_end - unit_begin;
+  const int64_t grid = batch * a.lunits;
   if (grid > 0x7fffffff) return set_error(ECC_EINVAL, "soft problem too large");
+  if (grid > 0) {
   // host parameters: the one mode they select; device parameters: both modes,
   // the kernel whose mode the device flag does not select exits at once
   // band kernel alongside the full factorised one (each CTA of both decides
@@ -1445,6 +1459,8 @@ static int soft_launch(const int8_t* coeffs, const float* fc, const float* fclo,
     rc = check_launch(BWD ? "ecc_soft_kernel<bwd>" : "ecc_soft_kernel<fwd>");
     if (rc) return rc;
   }
+  }
+  if (!finish) return ECC_OK;
   const int groups = (int)(units < RGROUPS ? units : RGROUPS);
   const int64_t per_group = (units + groups - 1) / groups;
   double* grp = a.gpart + (size_t)(batch * chunks) * 4;
@@ -1554,6 +1570,29 @@ extern "C" int ecc_soft_forward_d(const int8_t* coeffs, const float* field_c, co
   const ecc_soft_params placeholder{1.0, 0.0, {0.0, 0.0, 0.0}, 0.0, 1, 0};
   return soft_launch<false>(coeffs, field_c, field_lo, ndim, dims, batch, taus, nbins, &placeholder, nullptr, nullptr,
                             chi, nullptr, workspace, stream, params_dev, records);
+}
+
+extern "C" int ecc_soft_units(int ndim, const int64_t* dims, int64_t batch, int64_t* chunks_per_unit,
+                              int64_t* units) {
+  clear_error();
+  int64_t d3[3];
+  if (int rc = soft_dims(ndim, dims, d3)) return rc;
+  if (!chunks_per_unit || !units) return set_error(ECC_EINVAL, "null pointer argument");
+  const int64_t chunks = (d3[0] * d3[1] * d3[2] + CH - 1) / CH;
+  const int64_t G = soft_units_G(batch, chunks);
+  *chunks_per_unit = G;
+  *units = (chunks + G - 1) / G;
+  return ECC_OK;
+}
+
+extern "C" int ecc_soft_forward_range_d(const int8_t* coeffs, const float* field_c, const float* field_lo, int ndim,
+                                        const int64_t* dims, int64_t batch, const double* taus, int64_t nbins,
+                                        const ecc_soft_params* params_dev, double* chi, void* workspace, void* records,
+                                        int64_t unit_begin, int64_t unit_end, int finish, void* stream) {
+  if (!params_dev) return set_error(ECC_EINVAL, "null pointer argument");
+  const ecc_soft_params placeholder{1.0, 0.0, {0.0, 0.0, 0.0}, 0.0, 1, 0};
+  return soft_launch<false>(coeffs, field_c, field_lo, ndim, dims, batch, taus, nbins, &placeholder, nullptr, nullptr,
+                            chi, nullptr, workspace, stream, params_dev, records, unit_begin, unit_end, finish != 0);
 }
 
 extern "C" int ecc_soft_backward_d(const int8_t* coeffs, const float* field_c, const float* field_lo, int ndim,

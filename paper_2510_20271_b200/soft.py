@@ -429,6 +429,104 @@ def _(x, taus, u, alpha, lam, ndim, keep=False):
             x.new_empty((_records_bytes(dims, batch) if keep else 0,), dtype=torch.uint8))
 
 
+CHUNK_VOXELS = 4096   # ecc_soft.cu CH: voxels per forward chunk
+
+
+@torch.library.custom_op("ecc_b200::soft_ecc_fwd_host", mutates_args=())
+def _soft_fwd_host_op(x_host: torch.Tensor, taus: torch.Tensor, u: torch.Tensor, alpha: torch.Tensor, lam: float,
+                      ndim: int, keep: bool = False, slab: int = 64
+                      ) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor]:
+    """soft_ecc_fwd of one 3-D item held in (pinned) host memory, streamed:
+    the item goes to the device in z-slabs of ``slab`` planes on a side stream
+    while the planes already resident are prepared (ecc_soft_prepare_range_d:
+    a plane needs its successor as halo) and the forward runs over the units
+    whose voxels are prepared (ecc_soft_forward_range_d); the partial rows are
+    reduced once at the end.  The outputs are soft_ecc_fwd's for the copied
+    item (the same kernels on the same voxels).  Other shapes are copied
+    whole and take soft_ecc_fwd."""
+    from .hard import _split_batch
+
+    if x_host.is_cuda:
+        raise ValueError("soft_ecc_fwd_host takes a host tensor")
+    dev = taus.device
+    if dev.type != "cuda":
+        raise ValueError("the thresholds must be on the CUDA device the item is streamed to")
+    xs = _soft_tensor(x_host)
+    batch, dims, _ = _split_batch(xs, ndim)
+    L = _lib.lib()
+    if ndim != 3 or batch != 1 or not hasattr(L, "ecc_soft_forward_range_d"):
+        return _soft_fwd_op(xs.to(dev, non_blocking=True), taus, u, alpha, lam, ndim, keep)
+    D, H, W = dims
+    taus_d = taus.detach().to(dev, torch.float64).contiguous()
+    u_d = u.detach().to(dev, torch.float64).contiguous()
+    a_d = alpha.detach().to(dev, torch.float64).reshape(1).contiguous()
+    nb = taus_d.numel()
+    cur = torch.cuda.current_stream(dev)
+    st = _lib.ctypes.c_void_p(cur.cuda_stream)
+    params = torch.empty(_PARAMS_F64, dtype=torch.float64, device=dev)
+    _lib.check(L.ecc_soft_setup(_lib.ptr(taus_d), nb, _lib.ptr(u_d), ndim, _lib.ptr(a_d), float(lam),
+                                _lib.ptr(params), st))
+    xd = torch.empty(xs.shape, dtype=xs.dtype, device=dev)
+    c = torch.empty(xs.shape, dtype=torch.int8, device=dev)
+    fc = torch.empty(xs.shape, dtype=torch.float32, device=dev)
+    lo = torch.empty(xs.shape, dtype=torch.float32, device=dev)
+    chi = torch.empty((1, nb), dtype=torch.float64, device=dev)
+    ws = _workspace(dims, 1, nb, dev)
+    recs = torch.empty(_records_bytes(dims, 1) if keep else 0, dtype=torch.uint8, device=dev)
+    d = _lib.dims_arg(dims)
+    g = (_lib.ctypes.c_int64 * 2)()
+    _lib.check(L.ecc_soft_units(3, _lib.ptr(d), 1, _lib.ctypes.byref(g, 0), _lib.ctypes.byref(g, 8)))
+    per_unit, units = int(g[0]) * CHUNK_VOXELS, int(g[1])
+    xv, dv = xs.reshape(D, H, W), xd.view(D, H, W)
+    slab = max(1, int(slab))
+    side = torch.cuda.Stream(dev)
+    side.wait_stream(cur)   # the device buffer's allocation is ordered before the copies
+    ready = []
+    with torch.cuda.stream(side):
+        for z0 in range(0, D, slab):
+            z1 = min(D, z0 + slab)
+            dv[z0:z1].copy_(xv[z0:z1], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(side)
+            ready.append((z1, ev))
+    rp = _lib.ptr(recs) if keep else None
+    prepared, done = 0, 0
+    for z1, ev in ready:
+        cur.wait_event(ev)
+        p_end = D if z1 == D else z1 - 1   # plane z1 - 1 waits for its halo z1
+        if p_end > prepared:
+            _lib.check(L.ecc_soft_prepare_range_d(_lib.ptr(xd), _lib.dtype_code(xd), 3, _lib.ptr(d), 1,
+                                                  _lib.ptr(params), _lib.ptr(c), _lib.ptr(fc), _lib.ptr(lo),
+                                                  prepared, p_end, st))
+            prepared = p_end
+        ready_units = units if prepared == D else (prepared * H * W) // per_unit
+        if ready_units > done and ready_units < units:
+            _lib.check(L.ecc_soft_forward_range_d(_lib.ptr(c), _lib.ptr(fc), _lib.ptr(lo), 3, _lib.ptr(d), 1,
+                                                  _lib.ptr(taus_d), nb, _lib.ptr(params), _lib.ptr(chi),
+                                                  _lib.ptr(ws), rp, done, ready_units, 0, st))
+            done = ready_units
+    _lib.check(L.ecc_soft_forward_range_d(_lib.ptr(c), _lib.ptr(fc), _lib.ptr(lo), 3, _lib.ptr(d), 1,
+                                          _lib.ptr(taus_d), nb, _lib.ptr(params), _lib.ptr(chi), _lib.ptr(ws), rp,
+                                          done, units, 1, st))
+    if xs.dim() == ndim:
+        chi = chi.reshape(1, nb)
+    return chi, c, fc, lo, params, recs
+
+
+@_soft_fwd_host_op.register_fake
+def _(x_host, taus, u, alpha, lam, ndim, keep=False, slab=64):
+    from .hard import _split_batch
+
+    batch, dims, _ = _split_batch(x_host, ndim)
+    dev = taus.device
+    return (torch.empty((batch, taus.shape[0]), dtype=torch.float64, device=dev),
+            torch.empty(x_host.shape, dtype=torch.int8, device=dev),
+            torch.empty(x_host.shape, dtype=torch.float32, device=dev),
+            torch.empty(x_host.shape, dtype=torch.float32, device=dev),
+            torch.empty((_PARAMS_F64,), dtype=torch.float64, device=dev),
+            torch.empty((_records_bytes(dims, batch) if keep else 0,), dtype=torch.uint8, device=dev))
+
+
 @torch.library.custom_op("ecc_b200::soft_ecc_bwd", mutates_args=())
 def _soft_bwd_op(c: torch.Tensor, fc: torch.Tensor, lo: torch.Tensor, params: torch.Tensor, taus: torch.Tensor,
                  grad_chi: torch.Tensor, ndim: int, recs: Optional[torch.Tensor] = None
@@ -486,6 +584,19 @@ def _soft_backward(ctx, grad_chi, _gc, _gfc, _glo, _gp, _gr):
 
 
 torch.library.register_autograd("ecc_b200::soft_ecc_fwd", _soft_backward, setup_context=_soft_setup_context)
+
+
+def _soft_host_setup_context(ctx, inputs, output):
+    _soft_setup_context(ctx, inputs[:7], output)
+
+
+def _soft_host_backward(ctx, *grads):
+    g = _soft_backward(ctx, *grads)
+    return (None,) + tuple(g[1:]) + (None,)   # no gradient for the host item; none for slab
+
+
+torch.library.register_autograd("ecc_b200::soft_ecc_fwd_host", _soft_host_backward,
+                                setup_context=_soft_host_setup_context)
 
 
 @functools.lru_cache(maxsize=None)
@@ -556,7 +667,7 @@ class SoftECC(torch.nn.Module):
 
 
 def soft_step_host(module: SoftECC, host_x: torch.Tensor, upstream: torch.Tensor | None = None,
-                   micro: int = 16) -> torch.Tensor:
+                   micro: int = 16, slab_planes: int = 32) -> torch.Tensor:
     """Forward + backward of ``module`` on a batch held in (pinned) host
     memory, with the host -> device copies overlapped with the compute.
 
@@ -566,12 +677,27 @@ def soft_step_host(module: SoftECC, host_x: torch.Tensor, upstream: torch.Tensor
     compute that read it).  The loss is a sum over items, so the parameter
     gradients accumulated over the micro-batches are the full batch's.
     upstream: d loss / d chi [N, B] (default ones).  Returns chi [N, B] on
-    the device (enqueued; nothing here synchronises the host).
+    the device (enqueued; nothing here synchronises the host).  A single 3-D
+    item ([1, D, H, W]) is streamed in z-slabs of ``slab_planes`` planes
+    instead (``soft_ecc_fwd_host``): its prepare and forward start on the
+    first planes while the rest is still being copied.
     """
     if host_x.is_cuda:
         raise ValueError("soft_step_host takes a host tensor (pin it for asynchronous copies)")
     dev = module.taus.device
     n = host_x.shape[0]
+    if module.ndim == 3 and host_x.dim() == 4 and n == 1 and dev.type == "cuda":
+        # one 3-D item: streamed in z-slabs, the prepare and the forward of the
+        # resident planes overlapping the rest of the copy
+        keep = torch.is_grad_enabled() and any(
+            t.requires_grad for t in (module.taus, module.v, module.alpha))
+        if keep:
+            keep = 10 * host_x.numel() <= _total_memory(dev) * SoftECCFunction.RECORDS_MEMORY_FRACTION
+        chi = torch.ops.ecc_b200.soft_ecc_fwd_host(host_x, module.taus, module.direction(), module.alpha,
+                                                    module._lam, 3, keep, slab_planes)[0]
+        up = torch.ones_like(chi) if upstream is None else upstream.to(dev, chi.dtype, non_blocking=True)
+        chi.backward(up)
+        return chi.detach()
     micro = max(1, min(int(micro), n))
     cur = torch.cuda.current_stream(dev)
     side = torch.cuda.Stream(dev)
