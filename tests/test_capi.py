@@ -168,3 +168,19 @@ def test_threshold_table_large_power_of_two_stays_in_buffer(nb):
     assert rc == 0
     assert np.all(buf[nbytes // 4:] == np.float32(1.2345)), "threshold table wrote past its reported size"
     assert b.lut_cells <= (1 << 16)
+
+
+@pytest.mark.parametrize("dims,batch", [((70, 48, 64), 1), ((1024, 1024, 1024), 1), ((5, 7), 3), ((96, 80), 128)])
+def test_soft_units_cover_the_chunks(L, dims, batch):
+    """ecc_soft_units (host-only): G chunks of 4096 voxels per unit, the units
+    of an item cover its chunks exactly once -- the split the streamed forward
+    (ecc_soft_forward_range_d) walks; G follows the launcher's rule."""
+    d = (ctypes.c_int64 * len(dims))(*dims)
+    g, u = ctypes.c_int64(), ctypes.c_int64()
+    assert L.ecc_soft_units(len(dims), d, batch, ctypes.byref(g), ctypes.byref(u)) == 0
+    chunks = -(-int(np.prod(dims)) // 4096)
+    G, units = g.value, u.value
+    assert 1 <= G <= 16 and G <= chunks
+    assert G == max(1, min(16, batch * chunks // (148 * 3 * 6), chunks))
+    assert units == -(-chunks // G) and (units - 1) * G < chunks <= units * G
+    assert L.ecc_soft_units(len(dims), d, batch, None, ctypes.byref(u)) != 0
