@@ -783,8 +783,8 @@ def bench_c4(args, dev, world, rank, dist_on=False):
     del c0
     win = band_window(taus0, lam)
     # e2e through soft_step_host: the item pinned host -> HBM (streamed in
-    # z-slabs under the prepare and the forward), backward, chi and the
-    # parameter gradients -> host
+    # z-slabs under the prepare, forward and backward of the resident
+    # planes), chi and the parameter gradients -> host
     e2e = None
     if not args.no_e2e:
         host = torch.empty(x.shape, dtype=torch.float32, pin_memory=True)
@@ -809,10 +809,9 @@ def bench_c4(args, dev, world, rank, dist_on=False):
         e2e = {"value": n ** 3 * world / (e_ms * 1e-3), "unit": "voxel/s", "ms_per_step": e_ms,
                "h2d_bytes_per_step": int(host.numel() * 4) * world,
                "d2h_bytes_per_step": (B * 8 + B * 8 + 3 * 8 + 8) * world,
-               "api": "paper_2510_20271_b200.soft_step_host (the 1024^3 item pinned host -> HBM in z-slabs of 32 "
-                      "planes, the prepare and the forward of the resident planes overlapping the rest of the copy "
-                      "(soft_ecc_fwd_host), then the backward; chi and the tau / v / alpha gradients -> host, inside "
-                      "the timed region)"}
+               "api": "paper_2510_20271_b200.soft_step_host (the 1024^3 item pinned host -> HBM in z-slabs of 16 "
+                      "planes; the prepare, forward and backward of the resident planes overlap the rest of the "
+                      "copy; chi and the tau / v / alpha gradients -> host, inside the timed region)"}
         del host
     del x, m
     torch.cuda.empty_cache()

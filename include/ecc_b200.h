@@ -234,6 +234,17 @@ int ecc_soft_forward_range_d(const int8_t *coeffs, const float *field_c, const f
                              const int64_t *dims, int64_t batch, const double *taus, int64_t nbins,
                              const ecc_soft_params *params_dev, double *chi, void *workspace, void *records,
                              int64_t unit_begin, int64_t unit_end, int finish, void *stream);
+/* The backward of a unit range (upstream given up front, so a unit's
+ * backward can follow its forward before the rest of the item arrived);
+ * d_values of the range's voxels, the d_tau and G partial rows of its units,
+ * reduced into d_tau and G on the call with finish.  Use a workspace apart
+ * from the forward's while both are in flight (the partial rows share the
+ * layout). */
+int ecc_soft_backward_range_d(const int8_t *coeffs, const float *field_c, const float *field_lo, int ndim,
+                              const int64_t *dims, int64_t batch, const double *taus, int64_t nbins,
+                              const ecc_soft_params *params_dev, const double *upstream, float *d_values,
+                              double *d_tau, double *G, void *workspace, const void *records, int64_t unit_begin,
+                              int64_t unit_end, int finish, void *stream);
 
 /* Kernel-variant switch for A/B checks (tests, tools/): key "f3" with value
  * default | value | branch | cta | rank2 | no2d | edge1 | dummy | static,

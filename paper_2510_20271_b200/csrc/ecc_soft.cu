@@ -1604,3 +1604,15 @@ extern "C" int ecc_soft_backward_d(const int8_t* coeffs, const float* field_c, c
   return soft_launch<true>(coeffs, field_c, field_lo, ndim, dims, batch, taus, nbins, &placeholder, upstream, d_values,
                            d_tau, G, workspace, stream, params_dev, const_cast<void*>(records));
 }
+
+extern "C" int ecc_soft_backward_range_d(const int8_t* coeffs, const float* field_c, const float* field_lo, int ndim,
+                                         const int64_t* dims, int64_t batch, const double* taus, int64_t nbins,
+                                         const ecc_soft_params* params_dev, const double* upstream, float* d_values,
+                                         double* d_tau, double* G, void* workspace, const void* records,
+                                         int64_t unit_begin, int64_t unit_end, int finish, void* stream) {
+  if (!params_dev) return set_error(ECC_EINVAL, "null pointer argument");
+  const ecc_soft_params placeholder{1.0, 0.0, {0.0, 0.0, 0.0}, 0.0, 1, 0};
+  return soft_launch<true>(coeffs, field_c, field_lo, ndim, dims, batch, taus, nbins, &placeholder, upstream, d_values,
+                           d_tau, G, workspace, stream, params_dev, const_cast<void*>(records), unit_begin, unit_end,
+                           finish != 0);
+}

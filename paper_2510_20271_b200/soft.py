@@ -432,31 +432,19 @@ def _(x, taus, u, alpha, lam, ndim, keep=False):
 CHUNK_VOXELS = 4096   # ecc_soft.cu CH: voxels per forward chunk
 
 
-@torch.library.custom_op("ecc_b200::soft_ecc_fwd_host", mutates_args=())
-def _soft_fwd_host_op(x_host: torch.Tensor, taus: torch.Tensor, u: torch.Tensor, alpha: torch.Tensor, lam: float,
-                      ndim: int, keep: bool = False, slab: int = 64
-                      ) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor]:
-    """soft_ecc_fwd of one 3-D item held in (pinned) host memory, streamed:
-    the item goes to the device in z-slabs of ``slab`` planes on a side stream
-    while the planes already resident are prepared (ecc_soft_prepare_range_d:
-    a plane needs its successor as halo) and the forward runs over the units
-    whose voxels are prepared (ecc_soft_forward_range_d); the partial rows are
-    reduced once at the end.  The outputs are soft_ecc_fwd's for the copied
-    item (the same kernels on the same voxels).  Other shapes are copied
-    whole and take soft_ecc_fwd."""
-    from .hard import _split_batch
-
-    if x_host.is_cuda:
-        raise ValueError("soft_ecc_fwd_host takes a host tensor")
+def _stream_3d_item(xs: torch.Tensor, taus, u, alpha, lam: float, keep: bool, slab: int, upstream=None):
+    """The streamed forward (and, with ``upstream`` [1, B], the backward) of
+    one 3-D item in host memory xs [1?, D, H, W]: z-slabs of ``slab`` planes
+    are copied on a side stream; after each slab the compute stream prepares
+    the planes whose successor (their halo) has arrived, runs the forward over
+    the units whose voxels are prepared and, with an upstream, their backward
+    (a unit's backward needs only its own forward records, not chi).  The
+    partial rows are reduced once at the end.  Returns (chi, c, fc, lo,
+    params, recs, (dX, dtau, G) or None)."""
     dev = taus.device
-    if dev.type != "cuda":
-        raise ValueError("the thresholds must be on the CUDA device the item is streamed to")
-    xs = _soft_tensor(x_host)
-    batch, dims, _ = _split_batch(xs, ndim)
     L = _lib.lib()
-    if ndim != 3 or batch != 1 or not hasattr(L, "ecc_soft_forward_range_d"):
-        return _soft_fwd_op(xs.to(dev, non_blocking=True), taus, u, alpha, lam, ndim, keep)
-    D, H, W = dims
+    D, H, W = xs.shape[-3:]
+    dims = (D, H, W)
     taus_d = taus.detach().to(dev, torch.float64).contiguous()
     u_d = u.detach().to(dev, torch.float64).contiguous()
     a_d = alpha.detach().to(dev, torch.float64).reshape(1).contiguous()
@@ -464,7 +452,7 @@ def _soft_fwd_host_op(x_host: torch.Tensor, taus: torch.Tensor, u: torch.Tensor,
     cur = torch.cuda.current_stream(dev)
     st = _lib.ctypes.c_void_p(cur.cuda_stream)
     params = torch.empty(_PARAMS_F64, dtype=torch.float64, device=dev)
-    _lib.check(L.ecc_soft_setup(_lib.ptr(taus_d), nb, _lib.ptr(u_d), ndim, _lib.ptr(a_d), float(lam),
+    _lib.check(L.ecc_soft_setup(_lib.ptr(taus_d), nb, _lib.ptr(u_d), 3, _lib.ptr(a_d), float(lam),
                                 _lib.ptr(params), st))
     xd = torch.empty(xs.shape, dtype=xs.dtype, device=dev)
     c = torch.empty(xs.shape, dtype=torch.int8, device=dev)
@@ -473,6 +461,13 @@ def _soft_fwd_host_op(x_host: torch.Tensor, taus: torch.Tensor, u: torch.Tensor,
     chi = torch.empty((1, nb), dtype=torch.float64, device=dev)
     ws = _workspace(dims, 1, nb, dev)
     recs = torch.empty(_records_bytes(dims, 1) if keep else 0, dtype=torch.uint8, device=dev)
+    bwd = None
+    if upstream is not None:
+        up = upstream.to(dev, torch.float64).reshape(1, nb).contiguous()
+        bwd = (torch.empty(xs.shape, dtype=torch.float32, device=dev),
+               torch.empty((1, nb), dtype=torch.float64, device=dev),
+               torch.empty((1, 3), dtype=torch.float64, device=dev))
+        ws_b = _workspace(dims, 1, nb, dev)   # the backward's partial rows apart from the forward's
     d = _lib.dims_arg(dims)
     g = (_lib.ctypes.c_int64 * 2)()
     _lib.check(L.ecc_soft_units(3, _lib.ptr(d), 1, _lib.ctypes.byref(g, 0), _lib.ctypes.byref(g, 8)))
@@ -490,6 +485,14 @@ def _soft_fwd_host_op(x_host: torch.Tensor, taus: torch.Tensor, u: torch.Tensor,
             ev.record(side)
             ready.append((z1, ev))
     rp = _lib.ptr(recs) if keep else None
+    fields = (_lib.ptr(c), _lib.ptr(fc), _lib.ptr(lo), 3, _lib.ptr(d), 1, _lib.ptr(taus_d), nb, _lib.ptr(params))
+
+    def run(u0, u1, finish):
+        _lib.check(L.ecc_soft_forward_range_d(*fields, _lib.ptr(chi), _lib.ptr(ws), rp, u0, u1, finish, st))
+        if bwd is not None:
+            _lib.check(L.ecc_soft_backward_range_d(*fields, _lib.ptr(up), _lib.ptr(bwd[0]), _lib.ptr(bwd[1]),
+                                                   _lib.ptr(bwd[2]), _lib.ptr(ws_b), rp, u0, u1, finish, st))
+
     prepared, done = 0, 0
     for z1, ev in ready:
         cur.wait_event(ev)
@@ -500,16 +503,34 @@ def _soft_fwd_host_op(x_host: torch.Tensor, taus: torch.Tensor, u: torch.Tensor,
                                                   prepared, p_end, st))
             prepared = p_end
         ready_units = units if prepared == D else (prepared * H * W) // per_unit
-        if ready_units > done and ready_units < units:
-            _lib.check(L.ecc_soft_forward_range_d(_lib.ptr(c), _lib.ptr(fc), _lib.ptr(lo), 3, _lib.ptr(d), 1,
-                                                  _lib.ptr(taus_d), nb, _lib.ptr(params), _lib.ptr(chi),
-                                                  _lib.ptr(ws), rp, done, ready_units, 0, st))
+        if done < ready_units < units:
+            run(done, ready_units, 0)
             done = ready_units
-    _lib.check(L.ecc_soft_forward_range_d(_lib.ptr(c), _lib.ptr(fc), _lib.ptr(lo), 3, _lib.ptr(d), 1,
-                                          _lib.ptr(taus_d), nb, _lib.ptr(params), _lib.ptr(chi), _lib.ptr(ws), rp,
-                                          done, units, 1, st))
-    if xs.dim() == ndim:
-        chi = chi.reshape(1, nb)
+    run(done, units, 1)
+    return chi, c, fc, lo, params, recs, bwd
+
+
+@torch.library.custom_op("ecc_b200::soft_ecc_fwd_host", mutates_args=())
+def _soft_fwd_host_op(x_host: torch.Tensor, taus: torch.Tensor, u: torch.Tensor, alpha: torch.Tensor, lam: float,
+                      ndim: int, keep: bool = False, slab: int = 64
+                      ) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor]:
+    """soft_ecc_fwd of one 3-D item held in (pinned) host memory, streamed in
+    z-slabs (``_stream_3d_item``): the prepare and the forward of the planes
+    already resident overlap the rest of the copy.  The outputs are
+    soft_ecc_fwd's for the copied item (the same kernels on the same voxels).
+    Other shapes are copied whole and take soft_ecc_fwd."""
+    from .hard import _split_batch
+
+    if x_host.is_cuda:
+        raise ValueError("soft_ecc_fwd_host takes a host tensor")
+    dev = taus.device
+    if dev.type != "cuda":
+        raise ValueError("the thresholds must be on the CUDA device the item is streamed to")
+    xs = _soft_tensor(x_host)
+    batch, dims, _ = _split_batch(xs, ndim)
+    if ndim != 3 or batch != 1 or not hasattr(_lib.lib(), "ecc_soft_backward_range_d"):
+        return _soft_fwd_op(xs.to(dev, non_blocking=True), taus, u, alpha, lam, ndim, keep)
+    chi, c, fc, lo, params, recs, _ = _stream_3d_item(xs, taus, u, alpha, lam, keep, slab)
     return chi, c, fc, lo, params, recs
 
 
@@ -667,7 +688,7 @@ class SoftECC(torch.nn.Module):
 
 
 def soft_step_host(module: SoftECC, host_x: torch.Tensor, upstream: torch.Tensor | None = None,
-                   micro: int = 16, slab_planes: int = 32) -> torch.Tensor:
+                   micro: int = 16, slab_planes: int = 16) -> torch.Tensor:
     """Forward + backward of ``module`` on a batch held in (pinned) host
     memory, with the host -> device copies overlapped with the compute.
 
@@ -679,8 +700,10 @@ def soft_step_host(module: SoftECC, host_x: torch.Tensor, upstream: torch.Tensor
     upstream: d loss / d chi [N, B] (default ones).  Returns chi [N, B] on
     the device (enqueued; nothing here synchronises the host).  A single 3-D
     item ([1, D, H, W]) is streamed in z-slabs of ``slab_planes`` planes
-    instead (``soft_ecc_fwd_host``): its prepare and forward start on the
-    first planes while the rest is still being copied.
+    instead (``_stream_3d_item``): its prepare, forward and -- the upstream
+    being known -- backward run on the planes already resident while the
+    rest is still being copied; chi and the gradients are the device path's,
+    bit for bit.
     """
     if host_x.is_cuda:
         raise ValueError("soft_step_host takes a host tensor (pin it for asynchronous copies)")
@@ -689,15 +712,36 @@ def soft_step_host(module: SoftECC, host_x: torch.Tensor, upstream: torch.Tensor
     if module.ndim == 3 and host_x.dim() == 4 and n == 1 and dev.type == "cuda":
         # one 3-D item: streamed in z-slabs, the prepare and the forward of the
         # resident planes overlapping the rest of the copy
-        keep = torch.is_grad_enabled() and any(
-            t.requires_grad for t in (module.taus, module.v, module.alpha))
-        if keep:
-            keep = 10 * host_x.numel() <= _total_memory(dev) * SoftECCFunction.RECORDS_MEMORY_FRACTION
-        chi = torch.ops.ecc_b200.soft_ecc_fwd_host(host_x, module.taus, module.direction(), module.alpha,
-                                                    module._lam, 3, keep, slab_planes)[0]
-        up = torch.ones_like(chi) if upstream is None else upstream.to(dev, chi.dtype, non_blocking=True)
-        chi.backward(up)
-        return chi.detach()
+        # resident planes, and -- the upstream being given -- the backward of
+        # each unit right after its forward; the parameter gradients are those
+        # of SoftECCFunction's backward (soft_ecc_bwd + autograd through u = v/|v|)
+        params = [t for t in (module.taus, module.v, module.alpha) if t.requires_grad]
+        grad = torch.is_grad_enabled() and bool(params)
+        keep = grad and 10 * host_x.numel() <= _total_memory(dev) * SoftECCFunction.RECORDS_MEMORY_FRACTION
+        up = None
+        if grad:
+            nb = module.taus.numel()
+            up = (torch.ones((1, nb), dtype=torch.float64, device=dev) if upstream is None
+                  else upstream.to(dev, torch.float64, non_blocking=True).reshape(1, nb))
+        with torch.no_grad():
+            u = module.direction()
+            chi, *_, bwd = _stream_3d_item(_soft_tensor(host_x), module.taus, u, module.alpha, module._lam,
+                                           keep, slab_planes, up)
+        if grad:
+            _, dtau, G = bwd
+            Gs = G.sum(0)
+            outs, grads = [], []
+            if module.taus.requires_grad:
+                outs.append(module.taus)
+                grads.append(dtau.sum(0).to(module.taus.dtype))
+            if module.v.requires_grad:
+                outs.append(module.direction())
+                grads.append((-module.alpha.detach().to(torch.float64) * Gs).to(module.v.dtype))
+            if module.alpha.requires_grad:
+                outs.append(module.alpha)
+                grads.append((-(Gs * u.to(torch.float64)).sum()).to(module.alpha.dtype))
+            torch.autograd.backward(outs, grads)
+        return chi
     micro = max(1, min(int(micro), n))
     cur = torch.cuda.current_stream(dev)
     side = torch.cuda.Stream(dev)
