@@ -896,10 +896,10 @@ def bench_soft(args, dev, world, rank, dist_on=False):
         host.copy_(x.cpu())
 
         def e2e_step():
-            # micro-batches of 16 images: the next one's copy overlaps this one's
-            # forward + backward (soft_step_host); gradients accumulate to the batch's
+            # groups of 4 images: the next group's copy overlaps this group's
+            # prepare, forward and backward (soft_step_host)
             m.zero_grad(set_to_none=True)
-            chi = E.soft_step_host(m, host, up, micro=16)
+            chi = E.soft_step_host(m, host, up, micro=4)
             if dist_on:
                 from paper_2510_20271_b200 import distributed as D
 
@@ -917,9 +917,9 @@ def bench_soft(args, dev, world, rank, dist_on=False):
         e2e = {"value": N * H * W * world / (e_ms * 1e-3), "unit": "voxel/s", "ms_per_step": e_ms,
                "h2d_bytes_per_step": int(host.numel() * 4) * world,
                "d2h_bytes_per_step": (N * B * 8 + B * 8 + 2 * 8 + 8) * world,
-               "api": "paper_2510_20271_b200.soft_step_host: SoftECC forward + backward over micro-batches of 16 "
-                      "images, each copied pinned host -> HBM while the previous one computes; chi and the "
-                      "tau / v / alpha gradients -> host, inside the timed region"}
+               "api": "paper_2510_20271_b200.soft_step_host: the batch copied pinned host -> HBM in groups of 4 "
+                      "images, each group's prepare, forward and backward running while the next is copied; chi "
+                      "and the tau / v / alpha gradients -> host, inside the timed region"}
         del host
     del x
     torch.cuda.empty_cache()

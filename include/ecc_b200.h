@@ -221,9 +221,13 @@ int ecc_soft_backward_d(const int8_t *coeffs, const float *field_c, const float 
  * plane_begin - 1 and plane_end as halos, which must be resident);
  * ecc_soft_units reports the forward's work split (chunks of 4096 voxels per
  * unit, units per item); ecc_soft_forward_range_d runs units [unit_begin,
- * unit_end) of every item (their voxels must be prepared) and, with finish
- * != 0, reduces all units' partial rows into chi -- call it with finish once,
- * after every unit ran.  Replaces the single-shot path of soft.py:154-196
+ * unit_end) of items [item_begin, item_end) (their voxels must be prepared;
+ * the buffers are the whole batch's) and, with finish != 0, reduces all
+ * items' and units' partial rows into chi -- call it with finish once, after
+ * every unit ran.  chunks_per_unit: 0 = the launcher's rule for the whole
+ * batch (ecc_soft_units), else that many chunks per unit -- the same value
+ * on every call of one pass (small item ranges fill the GPU with smaller
+ * units).  Replaces the single-shot path of soft.py:154-196
  * (soft_ecc) for streamed inputs; the results are those of the single-shot
  * entry points. */
 int ecc_soft_prepare_range_d(const void *x, int dtype, int ndim, const int64_t *dims, int64_t batch,
@@ -233,7 +237,8 @@ int ecc_soft_units(int ndim, const int64_t *dims, int64_t batch, int64_t *chunks
 int ecc_soft_forward_range_d(const int8_t *coeffs, const float *field_c, const float *field_lo, int ndim,
                              const int64_t *dims, int64_t batch, const double *taus, int64_t nbins,
                              const ecc_soft_params *params_dev, double *chi, void *workspace, void *records,
-                             int64_t unit_begin, int64_t unit_end, int finish, void *stream);
+                             int64_t chunks_per_unit, int64_t item_begin, int64_t item_end, int64_t unit_begin,
+                             int64_t unit_end, int finish, void *stream);
 /* The backward of a unit range (upstream given up front, so a unit's
  * backward can follow its forward before the rest of the item arrived);
  * d_values of the range's voxels, the d_tau and G partial rows of its units,
@@ -243,7 +248,8 @@ int ecc_soft_forward_range_d(const int8_t *coeffs, const float *field_c, const f
 int ecc_soft_backward_range_d(const int8_t *coeffs, const float *field_c, const float *field_lo, int ndim,
                               const int64_t *dims, int64_t batch, const double *taus, int64_t nbins,
                               const ecc_soft_params *params_dev, const double *upstream, float *d_values,
-                              double *d_tau, double *G, void *workspace, const void *records, int64_t unit_begin,
+                              double *d_tau, double *G, void *workspace, const void *records,
+                              int64_t chunks_per_unit, int64_t item_begin, int64_t item_end, int64_t unit_begin,
                               int64_t unit_end, int finish, void *stream);
 
 /* Kernel-variant switch for A/B checks (tests, tools/): key "f3" with value

@@ -64,6 +64,7 @@ struct SoftArgs {
   int* rcnt;              //   and their counts [N][chunks][SNW]; the backward reads them instead of sorting
   int64_t unit0 = 0;      // this launch's first unit (units [unit0, unit0 + lunits) of every item)
   int64_t lunits = 0;     // units per item in this launch (== units unless a unit range is launched)
+  int64_t item0 = 0;      // this launch's first item (items [item0, item0 + gridDim.x / lunits))
 };
 
 __device__ __forceinline__ float ex2_approx(float x) {
@@ -461,7 +462,7 @@ ecc_soft_kernel(SoftArgs a) {
   __shared__ double s_g[SNW][4];
 
   // this CTA: chunks [c0, c1) of one item (a unit of G chunks)
-  const int64_t item = blockIdx.x / a.lunits;
+  const int64_t item = a.item0 + blockIdx.x / a.lunits;
   const int64_t unit = a.unit0 + blockIdx.x % a.lunits;
   const int64_t c0 = unit * a.G, c1 = min(c0 + a.G, a.chunks);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -772,7 +773,7 @@ __global__ void __launch_bounds__(SNT, ECC_BAND_MINB) ecc_soft_band_kernel(SoftA
   __shared__ int s_csb[BAND_MAXBANDS];
   __shared__ double s_g[SNW][4];
 
-  const int64_t item = blockIdx.x / a.lunits;
+  const int64_t item = a.item0 + blockIdx.x / a.lunits;
   const int64_t unit = a.unit0 + blockIdx.x % a.lunits;
   const int64_t c0 = unit * a.G, c1 = min(c0 + a.G, a.chunks);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1367,7 +1368,8 @@ static int soft_launch(const int8_t* coeffs, const float* fc, const float* fclo,
                        const double* taus, int64_t nbins, const ecc_soft_params* p, const double* up, float* dX,
                        double* out_main, double* G_out, void* workspace, void* stream,
                        const ecc_soft_params* pd = nullptr, void* records = nullptr, int64_t unit_begin = 0,
-                       int64_t unit_end = -1, bool finish = true) {
+                       int64_t unit_end = -1, bool finish = true, int64_t item_begin = 0, int64_t item_end = -1,
+                       int64_t G_force = 0) {
   clear_error();
   int64_t d3[3];
   int rc = soft_dims(ndim, dims, d3);
@@ -1414,7 +1416,7 @@ static int soft_launch(const int8_t* coeffs, const float* fc, const float* fclo,
   const int T = (tsel == 8 && nbins <= 8 * 32) ? 8 : (tsel <= 16 && nbins <= 16 * 32) ? 16 : 32;
   // G chunks per CTA: the per-CTA tables and partial rows are amortised
   // over G chunks while keeping ~6 waves of 3 CTAs per SM
-  const int64_t G = soft_units_G(batch, chunks);
+  const int64_t G = G_force > 0 ? std::min<int64_t>(G_force, chunks) : soft_units_G(batch, chunks);
   const int64_t units = (chunks + G - 1) / G;
   a.G = G;
   a.units = units;
@@ -1422,7 +1424,10 @@ static int soft_launch(const int8_t* coeffs, const float* fc, const float* fclo,
   if (unit_begin < 0 || unit_end > units || unit_begin > unit_end) return set_error(ECC_EINVAL, "unit range out of bounds");
   a.unit0 = unit_begin;
   a.lunits = unit_end - unit_begin;
-  const int64_t grid = batch * a.lunits;
+  if (item_end < 0) item_end = batch;
+  if (item_begin < 0 || item_end > batch || item_begin > item_end) return set_error(ECC_EINVAL, "item range out of bounds");
+  a.item0 = item_begin;
+  const int64_t grid = (item_end - item_begin) * a.lunits;
   if (grid > 0x7fffffff) return set_error(ECC_EINVAL, "soft problem too large");
   if (grid > 0) {
   // host parameters: the one mode they select; device parameters: both modes,
@@ -1588,11 +1593,13 @@ extern "C" int ecc_soft_units(int ndim, const int64_t* dims, int64_t batch, int6
 extern "C" int ecc_soft_forward_range_d(const int8_t* coeffs, const float* field_c, const float* field_lo, int ndim,
                                         const int64_t* dims, int64_t batch, const double* taus, int64_t nbins,
                                         const ecc_soft_params* params_dev, double* chi, void* workspace, void* records,
+                                        int64_t chunks_per_unit, int64_t item_begin, int64_t item_end,
                                         int64_t unit_begin, int64_t unit_end, int finish, void* stream) {
   if (!params_dev) return set_error(ECC_EINVAL, "null pointer argument");
   const ecc_soft_params placeholder{1.0, 0.0, {0.0, 0.0, 0.0}, 0.0, 1, 0};
   return soft_launch<false>(coeffs, field_c, field_lo, ndim, dims, batch, taus, nbins, &placeholder, nullptr, nullptr,
-                            chi, nullptr, workspace, stream, params_dev, records, unit_begin, unit_end, finish != 0);
+                            chi, nullptr, workspace, stream, params_dev, records, unit_begin, unit_end, finish != 0,
+                            item_begin, item_end, chunks_per_unit);
 }
 
 extern "C" int ecc_soft_backward_d(const int8_t* coeffs, const float* field_c, const float* field_lo, int ndim,
@@ -1609,10 +1616,11 @@ extern "C" int ecc_soft_backward_range_d(const int8_t* coeffs, const float* fiel
                                          const int64_t* dims, int64_t batch, const double* taus, int64_t nbins,
                                          const ecc_soft_params* params_dev, const double* upstream, float* d_values,
                                          double* d_tau, double* G, void* workspace, const void* records,
+                                         int64_t chunks_per_unit, int64_t item_begin, int64_t item_end,
                                          int64_t unit_begin, int64_t unit_end, int finish, void* stream) {
   if (!params_dev) return set_error(ECC_EINVAL, "null pointer argument");
   const ecc_soft_params placeholder{1.0, 0.0, {0.0, 0.0, 0.0}, 0.0, 1, 0};
   return soft_launch<true>(coeffs, field_c, field_lo, ndim, dims, batch, taus, nbins, &placeholder, upstream, d_values,
                            d_tau, G, workspace, stream, params_dev, const_cast<void*>(records), unit_begin, unit_end,
-                           finish != 0);
+                           finish != 0, item_begin, item_end, chunks_per_unit);
 }

@@ -488,10 +488,11 @@ def _stream_3d_item(xs: torch.Tensor, taus, u, alpha, lam: float, keep: bool, sl
     fields = (_lib.ptr(c), _lib.ptr(fc), _lib.ptr(lo), 3, _lib.ptr(d), 1, _lib.ptr(taus_d), nb, _lib.ptr(params))
 
     def run(u0, u1, finish):
-        _lib.check(L.ecc_soft_forward_range_d(*fields, _lib.ptr(chi), _lib.ptr(ws), rp, u0, u1, finish, st))
+        _lib.check(L.ecc_soft_forward_range_d(*fields, _lib.ptr(chi), _lib.ptr(ws), rp, 0, 0, 1, u0, u1, finish,
+                                              st))
         if bwd is not None:
             _lib.check(L.ecc_soft_backward_range_d(*fields, _lib.ptr(up), _lib.ptr(bwd[0]), _lib.ptr(bwd[1]),
-                                                   _lib.ptr(bwd[2]), _lib.ptr(ws_b), rp, u0, u1, finish, st))
+                                                   _lib.ptr(bwd[2]), _lib.ptr(ws_b), rp, 0, 0, 1, u0, u1, finish, st))
 
     prepared, done = 0, 0
     for z1, ev in ready:
@@ -508,6 +509,91 @@ def _stream_3d_item(xs: torch.Tensor, taus, u, alpha, lam: float, keep: bool, sl
             done = ready_units
     run(done, units, 1)
     return chi, c, fc, lo, params, recs, bwd
+
+
+def _stream_batch(xs: torch.Tensor, ndim: int, taus, u, alpha, lam: float, keep: bool, group: int, upstream):
+    """The streamed forward + backward of a batch xs [N, (D,) H, W] in host
+    memory, item groups of ``group`` copied on a side stream; each group is
+    prepared (ecc_soft_prepare_d on the group's items) and its forward and
+    backward run (ecc_soft_forward_range_d / ecc_soft_backward_range_d over
+    the group's item range, the whole batch's buffers) while the next group
+    is copied; the partial rows are reduced once at the end.  Returns (chi
+    [N, B], dtau [N, B], G [N, ndim])."""
+    dev = taus.device
+    L = _lib.lib()
+    n = xs.shape[0]
+    dims = tuple(xs.shape[1:])
+    nvox = math.prod(dims)
+    taus_d = taus.detach().to(dev, torch.float64).contiguous()
+    u_d = u.detach().to(dev, torch.float64).contiguous()
+    a_d = alpha.detach().to(dev, torch.float64).reshape(1).contiguous()
+    nb = taus_d.numel()
+    cur = torch.cuda.current_stream(dev)
+    st = _lib.ctypes.c_void_p(cur.cuda_stream)
+    params = torch.empty(_PARAMS_F64, dtype=torch.float64, device=dev)
+    _lib.check(L.ecc_soft_setup(_lib.ptr(taus_d), nb, _lib.ptr(u_d), ndim, _lib.ptr(a_d), float(lam),
+                                _lib.ptr(params), st))
+    xd = torch.empty(xs.shape, dtype=xs.dtype, device=dev)
+    c = torch.empty(xs.shape, dtype=torch.int8, device=dev)
+    fc = torch.empty(xs.shape, dtype=torch.float32, device=dev)
+    lo = torch.empty(xs.shape, dtype=torch.float32, device=dev)
+    chi = torch.empty((n, nb), dtype=torch.float64, device=dev)
+    dX = torch.empty(xs.shape, dtype=torch.float32, device=dev)
+    dtau = torch.empty((n, nb), dtype=torch.float64, device=dev)
+    G = torch.empty((n, ndim), dtype=torch.float64, device=dev)
+    ws, ws_b = _workspace(dims, n, nb, dev), _workspace(dims, n, nb, dev)
+    recs = torch.empty(_records_bytes(dims, n) if keep else 0, dtype=torch.uint8, device=dev)
+    rp = _lib.ptr(recs) if keep else None
+    up = upstream.to(dev, torch.float64).reshape(n, nb).contiguous()
+    d = _lib.dims_arg(dims)
+    group = max(1, int(group))
+    # units sized for one group's launch (a group alone must fill the GPU);
+    # the same split on every call of the pass
+    g = (_lib.ctypes.c_int64 * 2)()
+    _lib.check(L.ecc_soft_units(ndim, _lib.ptr(d), min(group, n), _lib.ctypes.byref(g, 0),
+                                _lib.ctypes.byref(g, 8)))
+    gcu, units = int(g[0]), int(g[1])
+    side = torch.cuda.Stream(dev)
+    side.wait_stream(cur)
+    ready = []
+    with torch.cuda.stream(side):
+        for i0 in range(0, n, group):
+            i1 = min(n, i0 + group)
+            xd[i0:i1].copy_(xs[i0:i1], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(side)
+            ready.append((i0, i1, ev))
+    fields = (_lib.ptr(c), _lib.ptr(fc), _lib.ptr(lo), ndim, _lib.ptr(d), n, _lib.ptr(taus_d), nb, _lib.ptr(params))
+    bw = (_lib.ptr(up), _lib.ptr(dX), _lib.ptr(dtau), _lib.ptr(G), _lib.ptr(ws_b), rp)
+    for i0, i1, ev in ready:
+        cur.wait_event(ev)
+        _lib.check(L.ecc_soft_prepare_d(_lib.ptr(xd[i0]), _lib.dtype_code(xd), ndim, _lib.ptr(d), i1 - i0,
+                                        _lib.ptr(params), _lib.ptr(c[i0]), _lib.ptr(fc[i0]), _lib.ptr(lo[i0]), st))
+        _lib.check(L.ecc_soft_forward_range_d(*fields, _lib.ptr(chi), _lib.ptr(ws), rp, gcu, i0, i1, 0, units, 0,
+                                              st))
+        _lib.check(L.ecc_soft_backward_range_d(*fields, *bw, gcu, i0, i1, 0, units, 0, st))
+    _lib.check(L.ecc_soft_forward_range_d(*fields, _lib.ptr(chi), _lib.ptr(ws), rp, gcu, n, n, 0, units, 1, st))
+    _lib.check(L.ecc_soft_backward_range_d(*fields, *bw, gcu, n, n, 0, units, 1, st))
+    return chi, dtau, G
+
+
+def _accumulate_param_grads(module, u, dtau, G) -> None:
+    """The parameter gradients SoftECCFunction's backward gives for (d_tau, G)
+    of a batch: d_tau summed over items, d_u = -alpha sum G (then autograd
+    through u = v/|v|), d_alpha = -<sum G, u>; accumulated into .grad."""
+    Gs = G.sum(0)
+    outs, grads = [], []
+    if module.taus.requires_grad:
+        outs.append(module.taus)
+        grads.append(dtau.sum(0).to(module.taus.dtype))
+    if module.v.requires_grad:
+        outs.append(module.direction())
+        grads.append((-module.alpha.detach().to(torch.float64) * Gs).to(module.v.dtype))
+    if module.alpha.requires_grad:
+        outs.append(module.alpha)
+        grads.append((-(Gs * u.to(torch.float64)).sum()).to(module.alpha.dtype))
+    if outs:
+        torch.autograd.backward(outs, grads)
 
 
 @torch.library.custom_op("ecc_b200::soft_ecc_fwd_host", mutates_args=())
@@ -688,22 +774,22 @@ class SoftECC(torch.nn.Module):
 
 
 def soft_step_host(module: SoftECC, host_x: torch.Tensor, upstream: torch.Tensor | None = None,
-                   micro: int = 16, slab_planes: int = 16) -> torch.Tensor:
+                   micro: int = 4, slab_planes: int = 16) -> torch.Tensor:
     """Forward + backward of ``module`` on a batch held in (pinned) host
     memory, with the host -> device copies overlapped with the compute.
 
-    The batch is cut into micro-batches of ``micro`` items: micro-batch k + 1
-    is copied on a side stream while k runs forward and backward on the
-    current stream (two device buffers; a buffer is refilled only after the
-    compute that read it).  The loss is a sum over items, so the parameter
-    gradients accumulated over the micro-batches are the full batch's.
+    The items go to the device in groups of ``micro`` on a side stream; as
+    each group arrives its prepare, forward and backward run (the upstream is
+    given, so no item waits for another's chi) over the whole batch's
+    buffers, and the partial rows are reduced once at the end
+    (``_stream_batch``).  A single 3-D item ([1, D, H, W]) is streamed in
+    z-slabs of ``slab_planes`` planes instead (``_stream_3d_item``).  Either
+    way chi and the parameter gradients (accumulated into ``.grad``) are the
+    device path's, bit for bit.  Without gradients (or an older library) the
+    batch runs in micro-batches of ``micro`` items through the module, the
+    next one copied while the current one computes.
     upstream: d loss / d chi [N, B] (default ones).  Returns chi [N, B] on
-    the device (enqueued; nothing here synchronises the host).  A single 3-D
-    item ([1, D, H, W]) is streamed in z-slabs of ``slab_planes`` planes
-    instead (``_stream_3d_item``): its prepare, forward and -- the upstream
-    being known -- backward run on the planes already resident while the
-    rest is still being copied; chi and the gradients are the device path's,
-    bit for bit.
+    the device (enqueued; nothing here synchronises the host).
     """
     if host_x.is_cuda:
         raise ValueError("soft_step_host takes a host tensor (pin it for asynchronous copies)")
@@ -728,19 +814,22 @@ def soft_step_host(module: SoftECC, host_x: torch.Tensor, upstream: torch.Tensor
             chi, *_, bwd = _stream_3d_item(_soft_tensor(host_x), module.taus, u, module.alpha, module._lam,
                                            keep, slab_planes, up)
         if grad:
-            _, dtau, G = bwd
-            Gs = G.sum(0)
-            outs, grads = [], []
-            if module.taus.requires_grad:
-                outs.append(module.taus)
-                grads.append(dtau.sum(0).to(module.taus.dtype))
-            if module.v.requires_grad:
-                outs.append(module.direction())
-                grads.append((-module.alpha.detach().to(torch.float64) * Gs).to(module.v.dtype))
-            if module.alpha.requires_grad:
-                outs.append(module.alpha)
-                grads.append((-(Gs * u.to(torch.float64)).sum()).to(module.alpha.dtype))
-            torch.autograd.backward(outs, grads)
+            _accumulate_param_grads(module, u, bwd[1], bwd[2])
+        return chi
+    params = [t for t in (module.taus, module.v, module.alpha) if t.requires_grad]
+    if (torch.is_grad_enabled() and params and dev.type == "cuda" and host_x.dim() == module.ndim + 1
+            and hasattr(_lib.lib(), "ecc_soft_backward_range_d")):
+        # a batch: item groups streamed, each group's prepare, forward and
+        # backward overlapping the next group's copy (one reduction at the end)
+        nb = module.taus.numel()
+        up = (torch.ones((n, nb), dtype=torch.float64, device=dev) if upstream is None
+              else upstream.to(dev, torch.float64, non_blocking=True).reshape(n, nb))
+        keep = 10 * host_x.numel() <= _total_memory(dev) * SoftECCFunction.RECORDS_MEMORY_FRACTION
+        with torch.no_grad():
+            u = module.direction()
+            chi, dtau, G = _stream_batch(_soft_tensor(host_x), module.ndim, module.taus, u, module.alpha,
+                                         module._lam, keep, micro, up)
+        _accumulate_param_grads(module, u, dtau, G)
         return chi
     micro = max(1, min(int(micro), n))
     cur = torch.cuda.current_stream(dev)
