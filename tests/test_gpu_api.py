@@ -254,3 +254,25 @@ def test_soft_step_host_streams_a_3d_item(slab):
     want = torch.ops.ecc_b200.soft_ecc_fwd(x.cuda(), *args)
     for k in (0, 1, 2):   # chi, coefficients, centred field
         assert torch.equal(got[k], want[k]), k
+
+
+@pytest.mark.parametrize("shape,v,group", [((5, 96, 80), [1.0, 2.0], 2), ((3, 20, 24, 32), [1.0, 2.0, -0.5], 2)])
+def test_soft_step_host_streamed_batch_bit_identical(shape, v, group):
+    """Batches (2-D, and 3-D with several items) stream in item groups over
+    the whole batch's buffers: chi and the gradients equal the device path's
+    bit for bit (units sized for a group, one reduction at the end)."""
+    B = 256
+    u = np.asarray(v) / np.linalg.norm(v)
+    span = 0.3 * np.abs(u).sum()
+    taus = np.linspace(-span, 1.0 + span, B + 1)[1:]
+    x = torch.rand(shape, generator=torch.Generator().manual_seed(5))
+    up = torch.rand((shape[0], B), dtype=torch.float64, device="cuda") + 0.5
+    ref = E.SoftECC(taus, v, alpha=0.3, lam=50.0).cuda()
+    chi_ref = ref(x.cuda())
+    (chi_ref * up).sum().backward()
+    m = E.SoftECC(taus, v, alpha=0.3, lam=50.0).cuda()
+    chi = E.soft_step_host(m, x.pin_memory(), up, micro=group)
+    torch.cuda.synchronize()
+    assert torch.equal(chi, chi_ref.detach())
+    for name in ("taus", "v", "alpha"):
+        assert torch.equal(getattr(m, name).grad, getattr(ref, name).grad), name
