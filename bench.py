@@ -656,10 +656,55 @@ def bench_c5(args, dev, world, rank, dist_on=False):
            "gpu_launches_per_step": 2,
            "roofline": {"bound": "hbm", "achieved": gbs_gpu, "peak": peak, "unit": "GB/s",
                         "frac": gbs_gpu / peak, "peak_source": peak_kind, "per": "GPU"},
-           "e2e": None,
-           "e2e_note": ("not measured for C5: a rank's slab (32 GiB at N = 1) would have to sit in pinned host "
-                        "memory; the host -> HBM path of a slab is the C2 leg's e2e (ecc_discrete_host / "
-                        "distributed.slab_curve)")}
+           "e2e": None}
+    # e2e: the rank's slab from pinned host memory through the public API
+    # every step (N = 1: ecc_discrete_host streams the 32 GiB volume through
+    # device ring buffers; N > 1: the slab copied into the padded buffer, then
+    # distributed.slab_curve), the curve back to the host.  Needs the slab in
+    # pinned host memory: skipped when the host lacks room for it.
+    if not args.no_e2e:
+        slab_bytes = 4 * P * H * W
+        try:
+            import psutil
+
+            avail = psutil.virtual_memory().available
+        except Exception:   # noqa: BLE001
+            avail = 0
+        ok_all = torch.tensor([1 if avail >= 3 * slab_bytes else 0], device=dev)
+        if dist_on:
+            dist.all_reduce(ok_all, op=dist.ReduceOp.MIN)
+        if int(ok_all.item()):
+            want_curve = curve.cpu()
+            host = torch.empty((P, H, W), dtype=torch.float32, pin_memory=True)
+            host.copy_(whole)
+            if not dist_on:
+                def e2e_step():
+                    return E.ecc_discrete_host(host, taus, chunk_planes=64).cpu()
+                api = ("paper_2510_20271_b200.ecc_discrete_host (the 32 GiB volume streamed from pinned host memory "
+                       "through device ring buffers of 64-plane chunks)")
+            else:
+                def e2e_step():
+                    padded[1:-1].copy_(host, non_blocking=True)
+                    return D.slab_curve(padded, taus, depth=Dz).cpu()
+                api = ("paper_2510_20271_b200.distributed.slab_curve (the rank's slab copied pinned host -> HBM, "
+                       "halo exchange, slab sweep, NCCL all-reduce, scan)")
+            got = e2e_step()
+            _gate(np.array_equal(got.numpy(), want_curve.numpy()), "C5 e2e curve")
+            if dist_on:
+                dist.barrier(device_ids=[dev.index])
+            t0 = time.perf_counter()
+            reps = 2
+            for _ in range(reps):
+                e2e_step()
+            torch.cuda.synchronize()
+            e_ms = _max_over_ranks([(time.perf_counter() - t0) * 1e3 / reps], dev, dist_on)[0]
+            out["e2e"] = {"value": vox / (e_ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": e_ms,
+                          "h2d_bytes_per_step": 4 * vox, "d2h_bytes_per_step": NB * 8 * world,
+                          "api": api + " (pinned host -> HBM copy inside the timed region)"}
+            del host
+        else:
+            out["e2e_note"] = (f"not measured: the host lacks room to pin this rank's {slab_bytes / 2 ** 30:.0f} GiB "
+                               "slab (3x its size must be available)")
     del padded, gen, whole
     torch.cuda.empty_cache()
     if rank == 0 and not args.no_cpu:
