@@ -849,8 +849,9 @@ def soft_step_host(module: SoftECC, host_x: torch.Tensor, upstream: torch.Tensor
         cur.wait_event(ready)
         buf.record_stream(cur)
         chi = module(buf)
-        up = torch.ones_like(chi) if upstream is None else upstream[i0:i1].to(dev, chi.dtype, non_blocking=True)
-        chi.backward(up)
+        if chi.requires_grad:   # forward only without gradients
+            up = torch.ones_like(chi) if upstream is None else upstream[i0:i1].to(dev, chi.dtype, non_blocking=True)
+            chi.backward(up)
         chis.append(chi.detach())
         done = torch.cuda.Event()
         done.record(cur)

@@ -280,3 +280,32 @@ def test_soft_step_host_streamed_batch_bit_identical(shape, v, group):
     assert torch.equal(chi, chi_ref.detach())
     for name in ("taus", "v", "alpha"):
         assert torch.equal(getattr(m, name).grad, getattr(ref, name).grad), name
+
+
+def test_soft_step_host_without_gradients():
+    """Without gradients soft_step_host runs the module over micro-batches
+    (the next one's copy overlapping the current one's forward): chi equals
+    the device path's, no gradient is touched."""
+    x = torch.rand((7, 96, 80), generator=torch.Generator().manual_seed(7))
+    m = E.SoftECC(np.linspace(-0.4, 1.4, 64), [1.0, 2.0], alpha=0.3, lam=50.0).cuda()
+    with torch.no_grad():
+        chi_ref = m(x.cuda())
+        chi = E.soft_step_host(m, x.pin_memory(), micro=3)
+    torch.cuda.synchronize()
+    assert torch.equal(chi, chi_ref)
+    assert m.taus.grad is None and m.v.grad is None and m.alpha.grad is None
+
+
+def test_soft_step_host_3d_item_without_gradients():
+    """A single 3-D item without gradients: the streamed forward alone."""
+    B, v = 256, [1.0, 2.0, -0.5]
+    u = np.asarray(v) / np.linalg.norm(v)
+    span = 0.3 * np.abs(u).sum()
+    m = E.SoftECC(np.linspace(-span, 1.0 + span, B + 1)[1:], v, alpha=0.3, lam=50.0).cuda()
+    x = torch.rand((1, 40, 48, 64), generator=torch.Generator().manual_seed(9))
+    with torch.no_grad():
+        chi_ref = m(x.cuda())
+        chi = E.soft_step_host(m, x.pin_memory(), slab_planes=8)
+    torch.cuda.synchronize()
+    assert torch.equal(chi, chi_ref)
+    assert m.taus.grad is None
